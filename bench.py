@@ -1,0 +1,369 @@
+"""M2L throughput benchmark (BASELINE.json metric: M2L cell-pair interactions/s,
+fp64, with the fraction of the FP64-tensor roofline).
+
+Workload (BASELINE config 2, the largest single-GPU config the metric is
+quoted on): N = 10^7 points uniform in the unit cube (seeded), octree height 7
+(reference depth 6, leaf level 6: 262,144 cells, all occupied), Chebyshev
+order l = 5, Laplace kernel 1/(4 pi r), symmetry-blocked full-rank M2L
+(variant nablk) over every level >= 2: 52,337,880 cell pairs per step.
+Multipoles are seeded U[-1,1] (M2L is linear; SURVEY.md §8d allows seeded
+multipoles for configs 2/4).
+
+A step = one M2L application of all levels (what the reference times with
+engine.py:212-214).  `value` is measured with device-resident expansions
+(CUDA events on the launching stream, L2 flushed between steps); `e2e` runs
+the same step through the handler with pinned HOST buffers (copies in the
+timed region).  `--impl reference` times the CPU port of the reference
+(oracle/, kind "port") on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests" / "golden"))
+
+METRIC = "M2L cell-pair interactions/sec (fp64)"
+FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak.json"
+
+CONFIGS = {
+    # name: (n_points, depth, order, geometry, variant, eps)
+    "cfg2": (10_000_000, 6, 5, "cube", "nablk", 1e-5),
+    "cfg2_ia": (10_000_000, 6, 5, "cube", "iablk", 1e-5),
+    "cfg1": (10_000, 3, 4, "cube", "nablk", 1e-5),
+    "cfg3": (8_000_000, 5, 9, "sphere", "nablk", 1e-8),
+    "cfg4": (100_000_000, 7, 7, "cube", "nablk", 1e-7),
+}
+
+
+def fp64_peak():
+    if FP64_PEAK_FILE.exists():
+        d = json.loads(FP64_PEAK_FILE.read_text())
+        return float(d["dmma_tflops"]), "measured (profiles/fp64_peak.json, DMMA m8n8k4 microbenchmark)"
+    return 37.1, "fallback (148 SM x 128 flop/clk x 1.965 GHz)"
+
+
+def level_cells(cfg):
+    """Occupied cells per level (lexicographic = reference row order)."""
+    from geometry import cube_points, sphere_points
+
+    n, depth, order, geom, _, _ = CONFIGS[cfg]
+    if geom == "cube":
+        pts = cube_points(n, seed=2)
+        low, width = np.zeros(3), 1.0
+    else:
+        pts = sphere_points(n, seed=3)
+        low, width = -np.ones(3), 2.0
+    side = 1 << depth
+    ijk = np.minimum(((pts - low) / width * side).astype(np.int64), side - 1)
+    del pts
+    key = np.unique((ijk[:, 0] << 42) | (ijk[:, 1] << 21) | ijk[:, 2])
+    del ijk
+    out = {}
+    cur = np.stack([key >> 42, (key >> 21) & 0x1FFFFF, key & 0x1FFFFF], 1)
+    out[depth] = cur
+    for lvl in range(depth - 1, 1, -1):
+        p = cur >> 1
+        k = np.unique((p[:, 0] << 42) | (p[:, 1] << 21) | p[:, 2])
+        cur = np.stack([k >> 42, (k >> 21) & 0x1FFFFF, k & 0x1FFFFF], 1)
+        out[lvl] = cur
+    widths = {lvl: width / (1 << lvl) for lvl in out}
+    return out, widths
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_port_sample(cfg, cells, widths, n_targets, threads):
+    """Time the oracle's faithful port of the reference apply (m2l.py:397-452)
+    on the first n_targets targets of the deepest level (reference row order)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import oracle as O
+
+    _, depth, order, _, variant, eps = CONFIGS[cfg]
+    lvl = depth
+    rows = np.arange(min(n_targets, len(cells[lvl])))
+    tgt, off, src, t = O.far_lists(cells[lvl], lvl, targets=rows)
+    full = O.full_far_field()
+    lt = {l: full for l in cells}
+    orc = O.OracleM2L(variant, O.laplace_profile, np.float64, order, eps, -1.0).precompute(lt, widths)
+    rng = np.random.default_rng(7)
+    mp = rng.uniform(-1, 1, (len(cells[lvl]), order**3))
+    loc = np.zeros_like(mp)
+    batch = O.csr_to_batch(tgt, off, src, t)
+    with threadpool_limits(limits=threads):
+        tic = time.perf_counter()
+        orc.apply_faithful(lvl, batch, mp, loc)
+        dt = time.perf_counter() - tic
+    pairs = int(off[-1])
+    return pairs / dt, pairs, dt
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = args.config
+    cells, widths = level_cells(cfg)
+    threads = os.cpu_count() or 1
+    n_t = args.cpu_targets
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, pairs, dt = cpu_port_sample(cfg, cells, widths, n_t, threads)
+        if i >= args.warmup:
+            vals.append((v, pairs, dt))
+    v = statistics.median(x[0] for x in vals)
+    pairs = vals[0][1]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(x[2] for x in vals),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg}: {CONFIGS[cfg]}", "sample": f"first {n_t} targets of level {max(cells)}"},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "port",
+                         "sample": f"{pairs} pairs: first {n_t} level-{max(cells)} targets, faithful port of "
+                                   f"m2l.py _apply_blocked (oracle/oracle.py), BLAS threads={threads}"},
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    cfg = args.config
+    n, depth, order, geom, variant, eps = CONFIGS[cfg]
+    variant = args.variant or variant
+    size = order**3
+    cells, widths = level_cells(cfg)
+    levels = sorted(cells)
+    full = full_far_field_vectors()
+    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps, device=local)
+    h.precompute({l: full for l in levels}, widths)
+
+    # shard target rows across ranks (contiguous ranges in lexicographic order);
+    # every rank holds the level's multipoles (replicated inputs, no exchange).
+    stats = {}
+    for lvl in levels:
+        c = cells[lvl].astype(np.int32)
+        st = h.plan_level_cells(lvl, c)
+        stats[lvl] = st
+    pairs_total = sum(st["pairs"] for st in stats.values())
+
+    gen = torch.Generator(device=dev).manual_seed(11)
+    mp = {l: torch.rand((len(cells[l]), size), dtype=torch.float64, device=dev, generator=gen) * 2 - 1 for l in levels}
+    loc = {l: torch.zeros_like(mp[l]) for l in levels}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def step():
+        launches = 0
+        for l in levels:
+            h.apply_planned(l, mp[l], loc[l])
+            launches += h.last_apply_stats()[1]
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    lvl_ev = {l: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for l in levels}
+    lvl_ms = {l: [] for l in levels}
+    launches = 0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            ev[i][0].record()
+            for l in levels:
+                lvl_ev[l][0].record()
+                h.apply_planned(l, mp[l], loc[l])
+                lvl_ev[l][1].record()
+                launches += h.last_apply_stats()[1]
+            ev[i][1].record()
+            torch.cuda.synchronize()
+            for l in levels:
+                lvl_ms[l].append(lvl_ev[l][0].elapsed_time(lvl_ev[l][1]))
+    torch.cuda.synchronize()
+    step_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    total_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = t.item()
+    value = pairs_total * args.steps / (total_ms * 1e-3)
+
+    # e2e: same step through the handler with pinned host buffers
+    h_mp = {l: torch.empty(mp[l].shape, dtype=torch.float64, pin_memory=True) for l in levels}
+    h_loc = {l: torch.zeros(mp[l].shape, dtype=torch.float64, pin_memory=True) for l in levels}
+    for l in levels:
+        h_mp[l].copy_(mp[l].cpu())
+    np_mp = {l: h_mp[l].numpy() for l in levels}
+    np_loc = {l: h_loc[l].numpy() for l in levels}
+    for _ in range(max(1, args.warmup // 2)):
+        for l in levels:
+            h.apply_planned(l, np_mp[l], np_loc[l])
+    torch.cuda.synchronize()
+    e2e_steps = max(1, args.steps)
+    tic = time.perf_counter()
+    for _ in range(e2e_steps):
+        for l in levels:
+            h.apply_planned(l, np_mp[l], np_loc[l])
+    e2e_s = (time.perf_counter() - tic) / e2e_steps
+    bytes_lvl = {l: mp[l].numel() * 8 for l in levels}
+    h2d = sum(2 * b for b in bytes_lvl.values())  # multipoles + locals (accumulated in place)
+    d2h = sum(bytes_lvl.values())
+
+    # roofline of the dominant kernel launch (deepest level, one tile_gemm launch)
+    peak, peak_src = fp64_peak()
+    deep = levels[-1]
+    deep_ms = statistics.median(lvl_ms[deep])
+    flops_pair = 2 * size * size if variant in ("na", "nasym", "nablk") else None
+    achieved = (stats[deep]["pairs"] * flops_pair / (deep_ms * 1e-3) / 1e12) if flops_pair else None
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(cfg, {}).get(variant)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        v, pairs, dt = cpu_port_sample(cfg, cells, widths, args.cpu_targets, 1)
+        cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port",
+               "sample": f"{pairs} pairs ({args.cpu_targets} level-{deep} targets, full far lists), faithful port "
+                         f"of m2l.py _apply_blocked, 1 thread, {dt:.1f} s"}
+
+    if rank == 0:
+        slots = sum(st["slots"] for st in stats.values())
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config 2: N=1e7 uniform cube, height 7 (levels 2-{deep}), l={order}, "
+                                   f"Laplace, variant {variant}", "pairs_per_step": pairs_total,
+                       "levels": {str(l): stats[l]["pairs"] for l in levels},
+                       "tile_fill": pairs_total / max(slots, 1),
+                       "l2": "flushed between steps (256 MB write)", "multipoles": "seeded U[-1,1]"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": f"tile_gemm level {deep} ({stats[deep]['pairs']} pairs x {flops_pair} flop)",
+                         "peak_source": peak_src, "dominant_ms": deep_ms,
+                         "step_tflops": (pairs_total * flops_pair / (total_ms / args.steps * 1e-3) / 1e12)
+                         if flops_pair else None},
+            "e2e": {"value": pairs_total / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                    "path": "B200M2LHandler.apply_planned with pinned host numpy buffers (C ABI, copies inside)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "level_ms": {str(l): statistics.median(lvl_ms[l]) for l in levels},
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--cpu-targets", type=int, default=1024)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,122 @@
+"""ctypes binding of the C ABI in include/chebm2l.h (libchebm2l.so, sm_100a).
+
+There is no CPU fallback: importing the product path without the built
+library, or calling it on a machine without a CUDA device, raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_NAME = "libchebm2l.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+CFM_OK = 0
+CFM_ERR_VALUE = 1
+CFM_ERR_PRECOMPUTE = 2
+CFM_ERR_BUDGET = 3
+CFM_ERR_CUDA = 4
+CFM_ERR_INTERNAL = 5
+
+VARIANT_IDS = {"na": 0, "nasym": 1, "nablk": 2, "sa": 3, "sarcmp": 4, "ia": 5, "iasym": 6, "iablk": 7}
+
+# Every symbol include/chebm2l.h declares (checked by tests/test_native_abi.py).
+EXPORTS = (
+    "cfm_last_error",
+    "cfm_abi_version",
+    "cfm_handler_create",
+    "cfm_handler_destroy",
+    "cfm_set_dense_group",
+    "cfm_set_lowrank_group",
+    "cfm_set_shared_group",
+    "cfm_set_level",
+    "cfm_apply_level_csr",
+    "cfm_plan_level_cells",
+    "cfm_plan_level_csr",
+    "cfm_apply_planned",
+    "cfm_plan_stats",
+    "cfm_classify_count",
+    "cfm_classify_fill",
+    "cfm_last_apply_stats",
+)
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+
+_SIGS = {
+    "cfm_last_error": ([], ctypes.c_char_p),
+    "cfm_abi_version": ([], _I),
+    "cfm_handler_create": ([_I, _I, _I, _I, ctypes.POINTER(_P)], _I),
+    "cfm_handler_destroy": ([_P], _I),
+    "cfm_set_dense_group": ([_P, _I, _I, _P, _I, _P, _P], _I),
+    "cfm_set_lowrank_group": ([_P, _I, _I, _P, _I, _P, _P, _P, _P], _I),
+    "cfm_set_shared_group": ([_P, _I, _I, _I, _P, _P, _I, _P, _P, _P], _I),
+    "cfm_set_level": ([_P, _I, _I, _D], _I),
+    "cfm_apply_level_csr": ([_P, _I, _I64, _P, _P, _P, _P, _I, _P, _I64, _P, _P, _P], _I),
+    "cfm_plan_level_cells": ([_P, _I, _I64, _P, _I, _P, _P], _I),
+    "cfm_plan_level_csr": ([_P, _I, _I64, _P, _P, _P, _P, _I, _I64, _P], _I),
+    "cfm_apply_planned": ([_P, _I, _P, _I64, _P, _P], _I),
+    "cfm_plan_stats": ([_P, _I, _P, _P, _P, _P, _P, _P], _I),
+    "cfm_classify_count": ([_I, _I, _I64, _P, _P, _P], _I),
+    "cfm_classify_fill": ([_I, _I, _I64, _P, _P, _P, _P, _P, _P], _I),
+    "cfm_last_apply_stats": ([_P, _P, _P], _I),
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """A CUDA/internal failure reported through the C ABI."""
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load libchebm2l.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise ImportError(
+            f"{p} is missing: build the CUDA extension first (python -c "
+            "'import __graft_entry__ as g; g.build()' or `make`)"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int, precompute_error=None, budget_error=None) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == CFM_OK:
+        return
+    msg = load().cfm_last_error().decode("utf-8", "replace")
+    if rc == CFM_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == CFM_ERR_PRECOMPUTE and precompute_error is not None:
+        raise precompute_error(msg)
+    if rc == CFM_ERR_BUDGET and budget_error is not None:
+        raise budget_error(msg)
+    raise NativeError(f"chebm2l error {rc}: {msg}")
+
+
+def ptr(a) -> int | None:
+    """Raw data pointer of a numpy array or a torch tensor (None for None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    data_ptr = getattr(a, "data_ptr", None)
+    if data_ptr is not None:
+        return int(data_ptr())
+    raise TypeError(f"unsupported buffer type {type(a)!r}")

@@ -1,0 +1,1023 @@
+// C-ABI implementation (include/chebm2l.h): operator cache on the device,
+// plan cache per level, and the per-variant launch sequences.
+//
+// Variant -> device work (reference apply paths in m2l.py):
+//   na            _apply_plain  :320-338  one tile_gemm over the |T| dense operators
+//   nasym, nablk  _apply_sym    :340-364  one tile_gemm over the 16 representatives
+//                 _apply_blocked:397-452  with row-gather (table) + column-gather (inv)
+//   ia            _apply_plain  (low-rank)      pass 1: Y = right^H P^T w   (per pair)
+//   iasym, iablk  _apply_sym/_blocked (low-rank) pass 2: acc += left[table] Y (per tile)
+//   sa, sarcmp    _apply_shared :366-395  W~ = B^H M[src] (per source), Z = sum C_t W~
+//                                         (dense or factored cores), locals += s U Z
+// The reference's own accumulation model is kept: a target's contributions are
+// summed into an accumulator and added once, scaled, into locals (m2l.py:337,
+// :363, :393); the blocked variant's per-column adds (:430-431) differ from that
+// only by floating-point reassociation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/chebm2l.h"
+#include "classify.cuh"
+#include "plan.hpp"
+#include "symmetry.hpp"
+#include "tile_gemm.cuh"
+
+namespace cfm {
+
+static thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_CHECK(x)                                                                       \
+  do {                                                                                      \
+    cudaError_t _e = (x);                                                                   \
+    if (_e != cudaSuccess)                                                                  \
+      throw Error(CFM_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e));          \
+  } while (0)
+
+// ---------------------------------------------------------------- device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b) {
+    if (b <= bytes && p) return;
+    release();
+    if (b == 0) return;
+    CUDA_CHECK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+static void upload(DevBuf& d, const std::vector<T>& h) {
+  d.alloc(std::max<size_t>(h.size() * sizeof(T), 16));
+  if (!h.empty()) CUDA_CHECK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+constexpr int kKC = 32;
+
+// ------------------------------------------------------------------ code maps
+struct CodeMap {
+  std::array<int, kNumCodes> op;
+  std::array<int, kNumCodes> rperm;
+  std::array<int, kNumCodes> cperm;
+  DevBuf d_op, d_rperm, d_cperm;
+  CodeMap() { op.fill(-1); rperm.fill(-1); cperm.fill(-1); }
+  void push() {
+    upload(d_op, std::vector<int>(op.begin(), op.end()));
+    upload(d_rperm, std::vector<int>(rperm.begin(), rperm.end()));
+    upload(d_cperm, std::vector<int>(cperm.begin(), cperm.end()));
+  }
+};
+
+// A stack of real operators laid out for tile_gemm: rows x ld (ld = cols
+// rounded up to KC, zero padded).
+struct OpStack {
+  DevBuf d;
+  int n_ops = 0, rows = 0, cols = 0, ld = 0;
+  long long stride = 0;
+  DevBuf d_rows, d_klen;  // optional per-op row / inner counts
+  bool has_rows = false, has_klen = false;
+  size_t host_bytes = 0;
+};
+
+static void realify_into(const double* src, int m, int k, bool cplx, double* dst, int ld, bool conj_t = false) {
+  // src: m x k (complex interleaved if cplx) row-major; dst: (m f) x (k f) with leading dim ld.
+  // conj_t: use conj(src)^T instead (src is k x m then).
+  if (!cplx) {
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < k; ++j) dst[(size_t)i * ld + j] = conj_t ? src[(size_t)j * m + i] : src[(size_t)i * k + j];
+    return;
+  }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < k; ++j) {
+      double re, im;
+      if (conj_t) {
+        re = src[2 * ((size_t)j * m + i)];
+        im = -src[2 * ((size_t)j * m + i) + 1];
+      } else {
+        re = src[2 * ((size_t)i * k + j)];
+        im = src[2 * ((size_t)i * k + j) + 1];
+      }
+      dst[(size_t)(2 * i) * ld + 2 * j] = re;
+      dst[(size_t)(2 * i) * ld + 2 * j + 1] = -im;
+      dst[(size_t)(2 * i + 1) * ld + 2 * j] = im;
+      dst[(size_t)(2 * i + 1) * ld + 2 * j + 1] = re;
+    }
+}
+
+// ------------------------------------------------------------------ groups
+enum GroupKind { kDense = 0, kLowRank = 1, kShared = 2 };
+
+struct Group {
+  GroupKind kind = kDense;
+  int n_ops = 0;
+  CodeMap main;       // dense / pass-2 (left) / SA dense cores
+  CodeMap pass1;      // low-rank pass 1 (right^H) / SA factored cores pass 1
+  CodeMap sa_fac2;    // SA factored cores pass 2
+  CodeMap single;     // code 0 -> op 0 (SA transforms)
+  OpStack dense;      // dense ops / SA dense cores
+  OpStack left, right_h;  // low-rank factors (also SA factored cores)
+  OpStack sa_bh, sa_u;    // SA bases
+  int r_u = 0, r_b = 0;
+  bool any_dense_core = false, any_fac_core = false;
+  std::array<int, kNumCodes> valid{};  // transfer vectors of the group
+};
+
+struct LevelPlan {
+  HostPlan hp;
+  int dc = 1;
+  DevBuf tile_col, tile_off, entry_code, entry_src;
+  DevBuf slot_ids, iota;  // low-rank: per-entry slots
+  // shared basis
+  std::vector<int64_t> sources, targets;
+  HostPlan src_plan, tgt_plan;
+  DevBuf s_tile_col, s_tile_off, s_entry_code, s_entry_src;
+  DevBuf t_tile_col, t_tile_off, t_entry_code, t_entry_src;
+  int64_t n_rows = 0;
+};
+
+}  // namespace cfm
+
+using namespace cfm;
+
+struct cfm_handler {
+  int device = 0, variant = 0, order = 0, op_complex = 0;
+  int n = 0, f = 1;
+  bool sym = false, lowrank = false, shared = false;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevBuf rowtab, invtab;  // [48][n f] int16
+  std::map<int, Group> groups;
+  std::map<int, std::pair<int, double>> levels;
+  std::map<int, LevelPlan> plans;
+  DevBuf x_stage, y_stage, ybuf, wt, z;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int64_t last_launches = 0;
+};
+
+namespace cfm {
+
+// ------------------------------------------------------------------ launching
+template <int BM, int BN, int WM, int WN>
+static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStream_t s) {
+  constexpr int STAGES = 3;
+  constexpr int smem = tile_smem_bytes<BM, BN, kKC, STAGES>();
+  auto kern = tile_gemm_kernel<BM, BN, WM, WN, kKC, STAGES>;
+  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  TileParams q = p;
+  q.tile_base = tile_base;
+  dim3 grid(n_tiles, (p.nr + BM - 1) / BM);
+  kern<<<grid, WM * WN * 32, smem, s>>>(q);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// Launch tiles [first, first + count) of the plan in p.
+static int64_t launch_range(const TileParams& p, int64_t first, int64_t count, cudaStream_t s) {
+  int64_t launches = 0;
+  const int64_t max_grid = 1 << 30;
+  for (int64_t base = first; base < first + count; base += max_grid) {
+    const int nt = int(std::min<int64_t>(max_grid, first + count - base));
+    if (nt <= 0) break;
+    if (p.nr <= 32)
+      launch_cfg<32, kBN, 1, 8>(p, nt, int(base), s);
+    else if (p.nr <= 64)
+      launch_cfg<64, kBN, 2, 4>(p, nt, int(base), s);
+    else
+      launch_cfg<128, kBN, 4, 2>(p, nt, int(base), s);
+    ++launches;
+  }
+  return launches;
+}
+
+static int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s) {
+  return launch_range(p, 0, n_tiles, s);
+}
+
+static void fill_ops(TileParams& p, const OpStack& s, const CodeMap& m) {
+  p.ops = s.d.as<double>();
+  p.op_stride = s.stride;
+  p.op_ld = s.ld;
+  p.nr = s.rows;
+  p.nk = s.cols;
+  p.op_rows = s.has_rows ? s.d_rows.as<int>() : nullptr;
+  p.op_klen = s.has_klen ? s.d_klen.as<int>() : nullptr;
+  p.code_op = m.d_op.as<int>();
+  p.code_rperm = m.d_rperm.as<int>();
+  p.code_cperm = m.d_cperm.as<int>();
+}
+
+static void fill_plan(TileParams& p, const DevBuf& col, const DevBuf& toff, const DevBuf& code, const DevBuf& src,
+                      int64_t n_tiles) {
+  p.n_tiles = int(n_tiles);
+  p.tile_col = col.as<int>();
+  p.tile_off = toff.as<int>();
+  p.entry_code = code.as<int>();
+  p.entry_src = src.as<int>();
+}
+
+static void push_plan(const HostPlan& hp, DevBuf& col, DevBuf& toff, DevBuf& code, DevBuf& src) {
+  upload(col, hp.tile_col);
+  upload(toff, hp.tile_off);
+  upload(code, hp.entry_code);
+  upload(src, hp.entry_src);
+}
+
+static bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------------ handler ops
+static void build_tables(cfm_handler* h) {
+  const int nf = h->n * h->f;
+  std::vector<int16_t> row(size_t(kNumPerms) * nf), inv(size_t(kNumPerms) * nf);
+  for (int pid = 0; pid < kNumPerms; ++pid) {
+    auto tab = permutation_table(pid, h->order);
+    auto itab = inverse_table(tab);
+    for (int i = 0; i < h->n; ++i)
+      for (int q = 0; q < h->f; ++q) {
+        row[size_t(pid) * nf + i * h->f + q] = int16_t(tab[i] * h->f + q);
+        inv[size_t(pid) * nf + i * h->f + q] = int16_t(itab[i] * h->f + q);
+      }
+  }
+  upload(h->rowtab, row);
+  upload(h->invtab, inv);
+}
+
+// Map every transfer of the group to (op index, perm) following the variant:
+// symmetric variants go through canonicalize (symmetry.py:63-75, lookup :142-144),
+// plain ones index the operator of t itself.
+static void map_transfers(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, int n_ops,
+                          const int8_t* op_t, bool rows_permuted, bool cols_permuted, CodeMap& m) {
+  std::array<int, kNumCodes> op_of_code;
+  op_of_code.fill(-1);
+  for (int i = 0; i < n_ops; ++i) {
+    const int t0 = op_t[3 * i], t1 = op_t[3 * i + 1], t2 = op_t[3 * i + 2];
+    if (t0 < -3 || t0 > 3 || t1 < -3 || t1 > 3 || t2 < -3 || t2 > 3)
+      throw Error(CFM_ERR_VALUE, "operator transfer vector outside [-3,3]^3");
+    op_of_code[tcode(t0, t1, t2)] = i;
+  }
+  for (int k = 0; k < n_transfers; ++k) {
+    const int t0 = transfers[3 * k], t1 = transfers[3 * k + 1], t2 = transfers[3 * k + 2];
+    if (t0 < -3 || t0 > 3 || t1 < -3 || t1 > 3 || t2 < -3 || t2 > 3)
+      throw Error(CFM_ERR_VALUE, "transfer vector outside [-3,3]^3");
+    const int c = tcode(t0, t1, t2);
+    g.valid[c] = 1;
+    if (h->sym) {
+      int ts[3], pid;
+      canonicalize(t0, t1, t2, ts, pid);
+      const int o = op_of_code[tcode(ts[0], ts[1], ts[2])];
+      if (o < 0) throw Error(CFM_ERR_PRECOMPUTE, "no representative operator for a transfer vector");
+      m.op[c] = o;
+      m.rperm[c] = rows_permuted ? pid : -1;
+      m.cperm[c] = cols_permuted ? pid : -1;
+    } else {
+      const int o = op_of_code[c];
+      if (o < 0) throw Error(CFM_ERR_PRECOMPUTE, "no operator for a transfer vector");
+      m.op[c] = o;
+    }
+  }
+}
+
+static void make_stack(OpStack& s, int n_ops, int rows, int cols) {
+  s.n_ops = n_ops;
+  s.rows = rows;
+  s.cols = cols;
+  s.ld = round_up(std::max(cols, 1), kKC);
+  s.stride = (long long)rows * s.ld;
+  s.d.alloc(std::max<size_t>(size_t(n_ops) * s.stride * sizeof(double), 16));
+  CUDA_CHECK(cudaMemset(s.d.p, 0, s.d.bytes));
+}
+
+static void put_stack(OpStack& s, int i, const std::vector<double>& hostblock) {
+  CUDA_CHECK(cudaMemcpy(s.d.as<double>() + (size_t)i * s.stride, hostblock.data(),
+                        hostblock.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+static void set_per_op(OpStack& s, const std::vector<int>& rows, const std::vector<int>& klen) {
+  if (!rows.empty()) {
+    upload(s.d_rows, rows);
+    s.has_rows = true;
+  }
+  if (!klen.empty()) {
+    upload(s.d_klen, klen);
+    s.has_klen = true;
+  }
+}
+
+// Low-rank factor stacks: pass 1 op = right^H (r f x n f), pass 2 op = left (n f x r f).
+static void build_lowrank_stacks(cfm_handler* h, OpStack& left, OpStack& right_h, int n_ops, const int* ranks,
+                                 const double* L, const double* R, int rows_left, int rows_right) {
+  // rows_left: rows of left (n or r_u); rows_right: rows of right (n or r_b)
+  const int f = h->f;
+  const bool cplx = h->op_complex;
+  int rmax = 0;
+  for (int i = 0; i < n_ops; ++i) rmax = std::max(rmax, ranks[i]);
+  make_stack(left, n_ops, rows_left * f, std::max(rmax * f, 1));
+  make_stack(right_h, n_ops, std::max(rmax * f, 1), rows_right * f);
+  std::vector<int> rrows(n_ops), rk(n_ops);
+  size_t offL = 0, offR = 0;
+  const int sc = cplx ? 2 : 1;
+  for (int i = 0; i < n_ops; ++i) {
+    const int r = ranks[i];
+    rrows[i] = r * f;
+    rk[i] = r * f;
+    std::vector<double> bl((size_t)left.stride, 0.0), br((size_t)right_h.stride, 0.0);
+    if (r > 0) {
+      realify_into(L + offL, rows_left, r, cplx, bl.data(), left.ld);
+      realify_into(R + offR, r, rows_right, cplx, br.data(), right_h.ld, /*conj_t=*/true);
+    }
+    put_stack(left, i, bl);
+    put_stack(right_h, i, br);
+    offL += (size_t)rows_left * r * sc;
+    offR += (size_t)rows_right * r * sc;
+    left.host_bytes += (size_t)rows_left * r * sc * 8;
+    right_h.host_bytes += (size_t)rows_right * r * sc * 8;
+  }
+  set_per_op(left, {}, rk);       // pass 2: inner length = rank
+  set_per_op(right_h, rrows, {});  // pass 1: rows = rank
+}
+
+// ------------------------------------------------------------------ planning
+static std::vector<int16_t> codes_from_t(int64_t P, const int8_t* t) {
+  std::vector<int16_t> codes(P);
+  for (int64_t q = 0; q < P; ++q) {
+    const int t0 = t[3 * q], t1 = t[3 * q + 1], t2 = t[3 * q + 2];
+    if (t0 < -3 || t0 > 3 || t1 < -3 || t1 > 3 || t2 < -3 || t2 > 3) {
+      throw Error(CFM_ERR_PRECOMPUTE, "no operator for transfer vector (" + std::to_string(t0) + ", " +
+                                          std::to_string(t1) + ", " + std::to_string(t2) + ")");
+    }
+    codes[q] = int16_t(tcode(t0, t1, t2));
+  }
+  return codes;
+}
+
+static Group& group_for_level(cfm_handler* h, int level) {
+  auto it = h->levels.find(level);
+  if (it == h->levels.end())
+    throw Error(CFM_ERR_PRECOMPUTE, "no operators precomputed for level " + std::to_string(level));
+  auto git = h->groups.find(it->second.first);
+  if (git == h->groups.end()) throw Error(CFM_ERR_PRECOMPUTE, "level group has no operators");
+  return git->second;
+}
+
+static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
+                            const int64_t* src, const int16_t* codes, int data_complex, int64_t n_rows) {
+  Group& g = group_for_level(h, level);
+  const int dc = (data_complex && !h->op_complex) ? 2 : 1;
+  if (h->op_complex && !data_complex)
+    throw Error(CFM_ERR_VALUE, "complex operators need complex128 expansions (engine.py:99)");
+  std::array<int, kNumCodes> key;
+  for (int c = 0; c < kNumCodes; ++c) key[c] = g.valid[c] ? std::max(g.main.op[c], 0) + 1 : -1;
+  if (g.kind == kShared)
+    for (int c = 0; c < kNumCodes; ++c) key[c] = g.valid[c] ? c : -1;
+  LevelPlan lp;
+  try {
+    lp.hp = build_plan_csr(n_targets, tgt, off, src, codes, dc, key, n_rows);
+  } catch (const PlanError& e) {
+    throw Error(e.code == 2 ? CFM_ERR_PRECOMPUTE : CFM_ERR_VALUE, e.what());
+  }
+  lp.dc = dc;
+  lp.n_rows = n_rows;
+  push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
+  const int64_t E = lp.hp.n_entries();
+  if (g.kind == kLowRank || (g.kind == kShared && g.any_fac_core)) {
+    std::vector<int> slots(size_t(E) * kBN), iota(E + 1);
+    for (int64_t e = 0; e < E; ++e)
+      for (int c = 0; c < kBN; ++c)
+        slots[size_t(e) * kBN + c] = lp.hp.entry_src[size_t(e) * kBN + c] >= 0 ? int(e * kBN + c) : -1;
+    std::iota(iota.begin(), iota.end(), 0);
+    upload(lp.slot_ids, slots);
+    upload(lp.iota, iota);
+  }
+  // distinct targets / sources (SA transforms and accounting)
+  {
+    std::vector<char> seen_t(n_rows, 0), seen_s(n_rows, 0);
+    for (int64_t i = 0; i < n_targets; ++i)
+      if (off[i + 1] > off[i]) {
+        seen_t[tgt[i]] = 1;
+        for (int64_t q = off[i]; q < off[i + 1]; ++q) seen_s[src[q]] = 1;
+      }
+    for (int64_t r = 0; r < n_rows; ++r) {
+      if (seen_t[r]) lp.targets.push_back(r);
+      if (seen_s[r]) lp.sources.push_back(r);
+    }
+  }
+  if (g.kind == kShared) {
+    lp.src_plan = build_identity_plan(lp.sources, dc);
+    lp.tgt_plan = build_identity_plan(lp.targets, dc);
+    push_plan(lp.src_plan, lp.s_tile_col, lp.s_tile_off, lp.s_entry_code, lp.s_entry_src);
+    push_plan(lp.tgt_plan, lp.t_tile_col, lp.t_tile_off, lp.t_entry_code, lp.t_entry_src);
+  }
+  h->plans[level] = std::move(lp);
+  return h->plans[level];
+}
+
+// ------------------------------------------------------------------ apply
+static void ensure(DevBuf& b, size_t bytes) { b.alloc(std::max<size_t>(bytes, 16)); }
+
+static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, double* d_y, cudaStream_t s) {
+  Group& g = group_for_level(h, level);
+  const double scale = h->levels[level].second;
+  const int dc = lp.dc;
+  const int nf = h->n * h->f;
+  const long long row_ld = (long long)h->n * (dc == 2 || h->op_complex ? 2 : 1);  // doubles per expansion row
+  int64_t launches = 0;
+  const int64_t E = lp.hp.n_entries();
+  if (lp.hp.n_tiles == 0) return 0;
+
+  TileParams p{};
+  p.rowtab = h->rowtab.as<short>();
+  p.invtab = h->invtab.as<short>();
+
+  if (g.kind == kDense) {
+    fill_ops(p, g.dense, g.main);
+    fill_plan(p, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src, lp.hp.n_tiles);
+    p.x = d_x; p.x_ld = row_ld; p.x_dc = dc;
+    p.y = d_y; p.y_ld = row_ld; p.y_dc = dc;
+    p.scale = scale; p.accumulate = 1;
+    launches += launch_tiles(p, lp.hp.n_tiles, s);
+    return launches;
+  }
+
+  if (g.kind == kLowRank) {
+    // chunk tiles so the per-pair intermediate stays bounded
+    const int ldy = g.right_h.rows;  // rmax * f
+    const size_t max_slots = std::max<size_t>(kBN, (size_t(1) << 30) / (sizeof(double) * std::max(ldy, 1)));
+    const std::vector<int>& toff = lp.hp.tile_off;
+    int64_t t0 = 0;
+    while (t0 < lp.hp.n_tiles) {
+      int64_t t1 = t0 + 1;
+      while (t1 < lp.hp.n_tiles && size_t(toff[t1 + 1] - toff[t0]) * kBN <= max_slots) ++t1;
+      const int64_t e0 = toff[t0], e1 = toff[t1];
+      if (e1 > e0) {
+        ensure(h->ybuf, size_t(e1 - e0) * kBN * ldy * sizeof(double));
+        double* ybase = h->ybuf.as<double>() - (long long)e0 * kBN * ldy;  // slot ids are global
+        // pass 1: Y[slot] = right^H P^T w   (tiles = entries)
+        TileParams p1 = p;
+        fill_ops(p1, g.right_h, g.pass1);
+        fill_plan(p1, lp.slot_ids, lp.iota, lp.entry_code, lp.entry_src, E);
+        p1.x = d_x; p1.x_ld = row_ld; p1.x_dc = dc;
+        p1.y = ybase; p1.y_ld = ldy; p1.y_dc = 1;
+        p1.scale = 1.0; p1.accumulate = 0;
+        launches += launch_range(p1, e0, e1 - e0, s);
+        // pass 2: acc += left[table] Y  (tiles = target tiles, sources = slots)
+        TileParams p2 = p;
+        fill_ops(p2, g.left, g.main);
+        fill_plan(p2, lp.tile_col, lp.tile_off, lp.entry_code, lp.slot_ids, lp.hp.n_tiles);
+        p2.x = ybase; p2.x_ld = ldy; p2.x_dc = 1;
+        p2.y = d_y; p2.y_ld = row_ld; p2.y_dc = dc;
+        p2.scale = scale; p2.accumulate = 1;
+        launches += launch_range(p2, t0, t1 - t0, s);
+      }
+      t0 = t1;
+    }
+    return launches;
+  }
+
+  // ---- shared basis (sa / sarcmp), m2l.py:366-395
+  const int rbf = g.sa_bh.rows;  // r_b * f (realified) rows of B^H
+  const int ruf = g.sa_u.cols;   // r_u * f
+  const long long wt_ld = (long long)rbf * (dc == 2 ? 2 : 1);
+  const long long z_ld = (long long)ruf * (dc == 2 ? 2 : 1);
+  ensure(h->wt, size_t(lp.n_rows) * wt_ld * sizeof(double));
+  ensure(h->z, size_t(lp.n_rows) * z_ld * sizeof(double));
+  CUDA_CHECK(cudaMemsetAsync(h->z.p, 0, size_t(lp.n_rows) * z_ld * sizeof(double), s));
+  // stage 1: W~[src] = B^H M[src]
+  {
+    TileParams q = p;
+    fill_ops(q, g.sa_bh, g.single);
+    fill_plan(q, lp.s_tile_col, lp.s_tile_off, lp.s_entry_code, lp.s_entry_src, lp.src_plan.n_tiles);
+    q.x = d_x; q.x_ld = row_ld; q.x_dc = dc;
+    q.y = h->wt.as<double>(); q.y_ld = wt_ld; q.y_dc = dc;
+    q.scale = 1.0; q.accumulate = 0;
+    launches += launch_tiles(q, lp.src_plan.n_tiles, s);
+  }
+  // stage 2a: dense cores Z[tgt] += C_t W~[src]
+  if (g.any_dense_core) {
+    TileParams q = p;
+    fill_ops(q, g.dense, g.main);
+    fill_plan(q, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src, lp.hp.n_tiles);
+    q.x = h->wt.as<double>(); q.x_ld = wt_ld; q.x_dc = dc;
+    q.y = h->z.as<double>(); q.y_ld = z_ld; q.y_dc = dc;
+    q.scale = 1.0; q.accumulate = 1;
+    launches += launch_tiles(q, lp.hp.n_tiles, s);
+  }
+  // stage 2b: factored cores Z[tgt] += L_t (R_t^H W~[src])
+  if (g.any_fac_core) {
+    const int ldy = g.right_h.rows;
+    ensure(h->ybuf, size_t(E) * kBN * ldy * sizeof(double));
+    TileParams p1 = p;
+    fill_ops(p1, g.right_h, g.pass1);
+    fill_plan(p1, lp.slot_ids, lp.iota, lp.entry_code, lp.entry_src, E);
+    p1.x = h->wt.as<double>(); p1.x_ld = wt_ld; p1.x_dc = dc;
+    p1.y = h->ybuf.as<double>(); p1.y_ld = ldy; p1.y_dc = 1;
+    p1.scale = 1.0; p1.accumulate = 0;
+    launches += launch_tiles(p1, E, s);
+    TileParams p2 = p;
+    fill_ops(p2, g.left, g.sa_fac2);
+    fill_plan(p2, lp.tile_col, lp.tile_off, lp.entry_code, lp.slot_ids, lp.hp.n_tiles);
+    p2.x = h->ybuf.as<double>(); p2.x_ld = ldy; p2.x_dc = 1;
+    p2.y = h->z.as<double>(); p2.y_ld = z_ld; p2.y_dc = dc;
+    p2.scale = 1.0; p2.accumulate = 1;
+    launches += launch_tiles(p2, lp.hp.n_tiles, s);
+  }
+  // stage 3: locals[tgt] += scale * U Z[tgt]
+  {
+    TileParams q = p;
+    fill_ops(q, g.sa_u, g.single);
+    fill_plan(q, lp.t_tile_col, lp.t_tile_off, lp.t_entry_code, lp.t_entry_src, lp.tgt_plan.n_tiles);
+    q.x = h->z.as<double>(); q.x_ld = z_ld; q.x_dc = dc;
+    q.y = d_y; q.y_ld = row_ld; q.y_dc = dc;
+    q.scale = scale; q.accumulate = 1;
+    launches += launch_tiles(q, lp.tgt_plan.n_tiles, s);
+  }
+  (void)nf;
+  return launches;
+}
+
+static void apply_with_buffers(cfm_handler* h, int level, LevelPlan& lp, const double* mpoles, double* locals,
+                               cudaStream_t s) {
+  const int dc = lp.dc;
+  const size_t row_d = size_t(h->n) * (dc == 2 || h->op_complex ? 2 : 1);
+  const size_t bytes = size_t(lp.n_rows) * row_d * sizeof(double);
+  const bool dev_x = is_device_ptr(mpoles), dev_y = is_device_ptr(locals);
+  const double* d_x = mpoles;
+  double* d_y = locals;
+  if (!dev_x) {
+    ensure(h->x_stage, bytes);
+    CUDA_CHECK(cudaMemcpyAsync(h->x_stage.p, mpoles, bytes, cudaMemcpyHostToDevice, s));
+    d_x = h->x_stage.as<double>();
+  }
+  if (!dev_y) {
+    ensure(h->y_stage, bytes);
+    CUDA_CHECK(cudaMemcpyAsync(h->y_stage.p, locals, bytes, cudaMemcpyHostToDevice, s));
+    d_y = h->y_stage.as<double>();
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev0, s));
+  h->last_launches = run_plan(h, level, lp, d_x, d_y, s);
+  CUDA_CHECK(cudaEventRecord(h->ev1, s));
+  if (!dev_y) CUDA_CHECK(cudaMemcpyAsync(locals, d_y, bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  h->last_ms = ms;
+}
+
+// ------------------------------------------------------------------ classifier
+struct DeviceLists {
+  DevBuf off, src, code;
+  int64_t total = 0;
+  std::vector<int64_t> h_off;
+};
+
+static void init_cone_table() {
+  static bool done = false;
+  if (done) return;
+  int8_t tab[kNumCodes];
+  std::fill(tab, tab + kNumCodes, int8_t(-1));
+  auto cone = full_cone_codes();
+  for (size_t i = 0; i < cone.size(); ++i) tab[cone[i]] = int8_t(i);
+  CUDA_CHECK(cudaMemcpyToSymbol(c_cone_index, tab, sizeof(tab)));
+  done = true;
+}
+
+static void classify_device(int level, int64_t n_cells, const int32_t* ijk, cudaStream_t s, DeviceLists& out,
+                            bool want_codes, int32_t* h_src = nullptr, int8_t* h_t = nullptr, uint8_t* h_rep = nullptr,
+                            uint8_t* h_perm = nullptr, const int64_t* given_off = nullptr) {
+  if (level < 0 || level > 9) throw Error(CFM_ERR_VALUE, "classifier supports levels 0..9");
+  init_cone_table();
+  const int S = 1 << level;
+  DevBuf d_ijk, grid, counts;
+  const int32_t* dijk = ijk;
+  if (!is_device_ptr(ijk)) {
+    d_ijk.alloc(std::max<size_t>(size_t(n_cells) * 3 * sizeof(int32_t), 16));
+    if (n_cells) CUDA_CHECK(cudaMemcpyAsync(d_ijk.p, ijk, size_t(n_cells) * 12, cudaMemcpyHostToDevice, s));
+    dijk = d_ijk.as<int32_t>();
+  }
+  // validate on host copy (bounds): cheap check on device would need a flag; do it on host data when given
+  if (!is_device_ptr(ijk)) {
+    for (int64_t i = 0; i < n_cells; ++i)
+      for (int a = 0; a < 3; ++a)
+        if (ijk[3 * i + a] < 0 || ijk[3 * i + a] >= S) throw Error(CFM_ERR_VALUE, "cell index outside the level grid");
+  }
+  grid.alloc(size_t(S) * S * S * sizeof(int));
+  CUDA_CHECK(cudaMemsetAsync(grid.p, 0xff, grid.bytes, s));
+  const int tb = 256;
+  const unsigned nb = unsigned((n_cells + tb - 1) / tb);
+  if (n_cells) k_grid_scatter<<<nb, tb, 0, s>>>(dijk, n_cells, S, grid.as<int>());
+  CUDA_CHECK(cudaGetLastError());
+  out.h_off.assign(n_cells + 1, 0);
+  if (given_off) {
+    std::copy(given_off, given_off + n_cells + 1, out.h_off.begin());
+  } else {
+    counts.alloc(std::max<size_t>(size_t(n_cells) * sizeof(int), 16));
+    if (n_cells && level >= 2)
+      k_classify<false><<<nb, tb, 0, s>>>(dijk, n_cells, S, grid.as<int>(), counts.as<int>(), nullptr, nullptr,
+                                          nullptr, nullptr, nullptr, nullptr);
+    else if (n_cells)
+      CUDA_CHECK(cudaMemsetAsync(counts.p, 0, size_t(n_cells) * sizeof(int), s));
+    CUDA_CHECK(cudaGetLastError());
+    std::vector<int> hc(n_cells);
+    if (n_cells) CUDA_CHECK(cudaMemcpyAsync(hc.data(), counts.p, size_t(n_cells) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n_cells; ++i) out.h_off[i + 1] = out.h_off[i] + hc[i];
+  }
+  out.total = out.h_off[n_cells];
+  if (!want_codes && !h_src) return;
+  upload(out.off, out.h_off);
+  out.src.alloc(std::max<size_t>(size_t(out.total) * sizeof(int), 16));
+  DevBuf d_t, d_rep, d_perm;
+  if (want_codes) out.code.alloc(std::max<size_t>(size_t(out.total) * sizeof(int16_t), 16));
+  if (h_t) d_t.alloc(std::max<size_t>(size_t(out.total) * 3, 16));
+  if (h_rep) d_rep.alloc(std::max<size_t>(size_t(out.total), 16));
+  if (h_perm) d_perm.alloc(std::max<size_t>(size_t(out.total), 16));
+  if (n_cells && level >= 2 && out.total)
+    k_classify<true><<<nb, tb, 0, s>>>(dijk, n_cells, S, grid.as<int>(), nullptr, out.off.as<long long>(),
+                                       out.src.as<int>(), want_codes ? out.code.as<int16_t>() : nullptr,
+                                       h_t ? d_t.as<int8_t>() : nullptr, h_rep ? d_rep.as<uint8_t>() : nullptr,
+                                       h_perm ? d_perm.as<uint8_t>() : nullptr);
+  CUDA_CHECK(cudaGetLastError());
+  if (h_src && out.total) CUDA_CHECK(cudaMemcpyAsync(h_src, out.src.p, size_t(out.total) * 4, cudaMemcpyDeviceToHost, s));
+  if (h_t && out.total) CUDA_CHECK(cudaMemcpyAsync(h_t, d_t.p, size_t(out.total) * 3, cudaMemcpyDeviceToHost, s));
+  if (h_rep && out.total) CUDA_CHECK(cudaMemcpyAsync(h_rep, d_rep.p, size_t(out.total), cudaMemcpyDeviceToHost, s));
+  if (h_perm && out.total) CUDA_CHECK(cudaMemcpyAsync(h_perm, d_perm.p, size_t(out.total), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+template <class F>
+static int guarded(F&& fn) {
+  try {
+    g_last_error.clear();
+    fn();
+    return CFM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return CFM_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CFM_ERR_INTERNAL;
+  }
+}
+
+static cudaStream_t pick_stream(cfm_handler* h, void* s) { return s ? static_cast<cudaStream_t>(s) : h->stream; }
+
+}  // namespace cfm
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* cfm_last_error(void) { return cfm::g_last_error.c_str(); }
+
+int cfm_abi_version(void) { return 1; }
+
+int cfm_handler_create(int device, int variant, int order, int op_complex, cfm_handler** out) {
+  return guarded([&] {
+    if (!out) throw Error(CFM_ERR_VALUE, "out is null");
+    if (variant < CFM_NA || variant > CFM_IABLK) throw Error(CFM_ERR_VALUE, "unknown M2L variant");
+    if (order < 2 || order > 12) throw Error(CFM_ERR_VALUE, "interpolation order must be in [2, 12]");
+    int ndev = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Error(CFM_ERR_VALUE, "no such CUDA device");
+    CUDA_CHECK(cudaSetDevice(device));
+    auto h = std::make_unique<cfm_handler>();
+    h->device = device;
+    h->variant = variant;
+    h->order = order;
+    h->op_complex = op_complex ? 1 : 0;
+    h->n = order * order * order;
+    h->f = op_complex ? 2 : 1;
+    h->sym = variant == CFM_NASYM || variant == CFM_NABLK || variant == CFM_IASYM || variant == CFM_IABLK;
+    h->lowrank = variant == CFM_IA || variant == CFM_IASYM || variant == CFM_IABLK;
+    h->shared = variant == CFM_SA || variant == CFM_SARCMP;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreate(&h->ev0));
+    CUDA_CHECK(cudaEventCreate(&h->ev1));
+    build_tables(h.get());
+    *out = h.release();
+  });
+}
+
+int cfm_handler_destroy(cfm_handler* h) {
+  return guarded([&] {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    cudaStreamDestroy(h->stream);
+    delete h;
+  });
+}
+
+int cfm_set_dense_group(cfm_handler* h, int key, int n_transfers, const int8_t* transfers, int n_ops,
+                        const int8_t* op_t, const double* ops) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    if (h->lowrank || h->shared) throw Error(CFM_ERR_VALUE, "dense group on a non-dense variant");
+    Group g;
+    g.kind = kDense;
+    g.n_ops = n_ops;
+    map_transfers(h, g, n_transfers, transfers, n_ops, op_t, true, true, g.main);
+    g.main.push();
+    const int nf = h->n * h->f;
+    make_stack(g.dense, n_ops, nf, nf);
+    const size_t blk = size_t(h->n) * h->n * (h->op_complex ? 2 : 1);
+    std::vector<double> tmp(g.dense.stride);
+    for (int i = 0; i < n_ops; ++i) {
+      std::fill(tmp.begin(), tmp.end(), 0.0);
+      realify_into(ops + i * blk, h->n, h->n, h->op_complex, tmp.data(), g.dense.ld);
+      put_stack(g.dense, i, tmp);
+    }
+    h->groups[key] = std::move(g);
+    h->plans.clear();
+  });
+}
+
+int cfm_set_lowrank_group(cfm_handler* h, int key, int n_transfers, const int8_t* transfers, int n_ops,
+                          const int8_t* op_t, const int32_t* ranks, const double* left, const double* right) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    if (!h->lowrank) throw Error(CFM_ERR_VALUE, "low-rank group on a non-low-rank variant");
+    Group g;
+    g.kind = kLowRank;
+    g.n_ops = n_ops;
+    map_transfers(h, g, n_transfers, transfers, n_ops, op_t, /*rows*/ true, /*cols*/ false, g.main);
+    map_transfers(h, g, n_transfers, transfers, n_ops, op_t, /*rows*/ false, /*cols*/ true, g.pass1);
+    g.main.push();
+    g.pass1.push();
+    for (int i = 0; i < n_ops; ++i)
+      if (ranks[i] < 0 || ranks[i] > h->n) throw Error(CFM_ERR_VALUE, "rank out of range");
+    build_lowrank_stacks(h, g.left, g.right_h, n_ops, ranks, left, right, h->n, h->n);
+    h->groups[key] = std::move(g);
+    h->plans.clear();
+  });
+}
+
+int cfm_set_shared_group(cfm_handler* h, int key, int r_u, int r_b, const double* u, const double* b, int n_cores,
+                         const int8_t* core_t, const int32_t* core_rank, const double* core_data) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    if (!h->shared) throw Error(CFM_ERR_VALUE, "shared group on a non-shared variant");
+    if (r_u < 0 || r_b < 0 || r_u > h->n || r_b > h->n) throw Error(CFM_ERR_VALUE, "shared rank out of range");
+    const int f = h->f;
+    const bool cplx = h->op_complex;
+    const int sc = cplx ? 2 : 1;
+    Group g;
+    g.kind = kShared;
+    g.n_ops = n_cores;
+    g.r_u = r_u;
+    g.r_b = r_b;
+    // bases: B^H (r_b f x n f) and U (n f x r_u f)
+    make_stack(g.sa_bh, 1, std::max(r_b * f, 1), h->n * f);
+    make_stack(g.sa_u, 1, h->n * f, std::max(r_u * f, 1));
+    {
+      std::vector<double> tmp(g.sa_bh.stride, 0.0);
+      if (r_b) realify_into(b, r_b, h->n, cplx, tmp.data(), g.sa_bh.ld, /*conj_t=*/true);
+      put_stack(g.sa_bh, 0, tmp);
+      std::vector<double> tu(g.sa_u.stride, 0.0);
+      if (r_u) realify_into(u, h->n, r_u, cplx, tu.data(), g.sa_u.ld);
+      put_stack(g.sa_u, 0, tu);
+    }
+    g.single.op[0] = 0;
+    g.single.push();
+    // cores
+    std::vector<int> dense_idx, fac_idx, fac_rank;
+    std::vector<size_t> off(n_cores);
+    size_t o = 0;
+    for (int i = 0; i < n_cores; ++i) {
+      off[i] = o;
+      const int t0 = core_t[3 * i], t1 = core_t[3 * i + 1], t2 = core_t[3 * i + 2];
+      if (t0 < -3 || t0 > 3 || t1 < -3 || t1 > 3 || t2 < -3 || t2 > 3)
+        throw Error(CFM_ERR_VALUE, "core transfer vector outside [-3,3]^3");
+      const int c = tcode(t0, t1, t2);
+      g.valid[c] = 1;
+      if (core_rank[i] < 0) {
+        g.main.op[c] = int(dense_idx.size());
+        dense_idx.push_back(i);
+        o += size_t(r_u) * r_b * sc;
+      } else {
+        g.pass1.op[c] = int(fac_idx.size());
+        g.sa_fac2.op[c] = int(fac_idx.size());
+        fac_idx.push_back(i);
+        fac_rank.push_back(core_rank[i]);
+        o += size_t(r_u + r_b) * core_rank[i] * sc;
+      }
+    }
+    g.any_dense_core = !dense_idx.empty();
+    g.any_fac_core = !fac_idx.empty();
+    if (g.any_dense_core) {
+      make_stack(g.dense, int(dense_idx.size()), std::max(r_u * f, 1), std::max(r_b * f, 1));
+      std::vector<double> tmp(g.dense.stride);
+      for (size_t k = 0; k < dense_idx.size(); ++k) {
+        std::fill(tmp.begin(), tmp.end(), 0.0);
+        realify_into(core_data + off[dense_idx[k]], r_u, r_b, cplx, tmp.data(), g.dense.ld);
+        put_stack(g.dense, int(k), tmp);
+      }
+    }
+    if (g.any_fac_core) {
+      // gather factored blocks contiguously: left blocks then right blocks per core
+      std::vector<double> L, R;
+      for (size_t k = 0; k < fac_idx.size(); ++k) {
+        const double* base = core_data + off[fac_idx[k]];
+        const size_t nl = size_t(r_u) * fac_rank[k] * sc, nr = size_t(r_b) * fac_rank[k] * sc;
+        L.insert(L.end(), base, base + nl);
+        R.insert(R.end(), base + nl, base + nl + nr);
+      }
+      build_lowrank_stacks(h, g.left, g.right_h, int(fac_idx.size()), fac_rank.data(), L.data(), R.data(), r_u, r_b);
+    }
+    g.main.push();
+    g.pass1.push();
+    g.sa_fac2.push();
+    h->groups[key] = std::move(g);
+    h->plans.clear();
+  });
+}
+
+int cfm_set_level(cfm_handler* h, int level, int key, double scale) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->groups.count(key)) throw Error(CFM_ERR_VALUE, "unknown group key");
+    h->levels[level] = {key, scale};
+    h->plans.erase(level);
+  });
+}
+
+int cfm_plan_level_csr(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
+                       const int64_t* src, const int8_t* t, int data_complex, int64_t n_rows, int64_t* pair_count_out) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    if (n_targets < 0 || n_rows < 0) throw Error(CFM_ERR_VALUE, "negative size");
+    const int64_t P = n_targets ? off[n_targets] : 0;
+    auto codes = codes_from_t(P, t);
+    LevelPlan& lp = make_plan(h, level, n_targets, tgt, off, src, codes.data(), data_complex, n_rows);
+    if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
+  });
+}
+
+int cfm_apply_planned(cfm_handler* h, int level, const double* mpoles, int64_t n_rows, double* locals, void* stream) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    auto it = h->plans.find(level);
+    if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(level));
+    if (it->second.n_rows != n_rows) throw Error(CFM_ERR_VALUE, "row count differs from the planned level");
+    apply_with_buffers(h, level, it->second, mpoles, locals, pick_stream(h, stream));
+  });
+}
+
+int cfm_apply_level_csr(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
+                        const int64_t* src, const int8_t* t, int data_complex, const double* mpoles, int64_t n_rows,
+                        double* locals, void* stream, int64_t* pair_count_out) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    if (n_targets < 0 || n_rows < 0) throw Error(CFM_ERR_VALUE, "negative size");
+    const int64_t P = n_targets ? off[n_targets] : 0;
+    auto codes = codes_from_t(P, t);
+    LevelPlan& lp = make_plan(h, level, n_targets, tgt, off, src, codes.data(), data_complex, n_rows);
+    if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
+    apply_with_buffers(h, level, lp, mpoles, locals, pick_stream(h, stream));
+  });
+}
+
+int cfm_plan_level_cells(cfm_handler* h, int level, int64_t n_cells, const int32_t* ijk, int data_complex,
+                         void* stream, int64_t* pair_count_out) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    cudaStream_t s = pick_stream(h, stream);
+    DeviceLists dl;
+    classify_device(level, n_cells, ijk, s, dl, /*want_codes=*/true);
+    std::vector<int32_t> hsrc(dl.total);
+    std::vector<int16_t> hcode(dl.total);
+    if (dl.total) {
+      CUDA_CHECK(cudaMemcpyAsync(hsrc.data(), dl.src.p, size_t(dl.total) * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaMemcpyAsync(hcode.data(), dl.code.p, size_t(dl.total) * 2, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    std::vector<int64_t> tgt(n_cells), src64(hsrc.begin(), hsrc.end());
+    std::iota(tgt.begin(), tgt.end(), 0);
+    LevelPlan& lp = make_plan(h, level, n_cells, tgt.data(), dl.h_off.data(), src64.data(), hcode.data(),
+                              data_complex, n_cells);
+    if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
+  });
+}
+
+int cfm_plan_stats(cfm_handler* h, int level, int64_t* n_tiles, int64_t* n_entries, int64_t* n_pairs,
+                   int64_t* n_slots, int64_t* n_targets, int64_t* n_sources) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->plans.find(level);
+    if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(level));
+    const LevelPlan& lp = it->second;
+    if (n_tiles) *n_tiles = lp.hp.n_tiles;
+    if (n_entries) *n_entries = lp.hp.n_entries();
+    if (n_pairs) *n_pairs = lp.hp.n_pairs;
+    if (n_slots) *n_slots = lp.hp.n_entries() * kBN / lp.dc;
+    if (n_targets) *n_targets = int64_t(lp.targets.size());
+    if (n_sources) *n_sources = int64_t(lp.sources.size());
+  });
+}
+
+int cfm_classify_count(int device, int level, int64_t n_cells, const int32_t* ijk, int64_t* offsets_out,
+                       int64_t* total_out) {
+  return guarded([&] {
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DeviceLists dl;
+    try {
+      classify_device(level, n_cells, ijk, s, dl, false);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaStreamDestroy(s);
+    if (offsets_out) std::copy(dl.h_off.begin(), dl.h_off.end(), offsets_out);
+    if (total_out) *total_out = dl.total;
+  });
+}
+
+int cfm_classify_fill(int device, int level, int64_t n_cells, const int32_t* ijk, const int64_t* offsets,
+                      int32_t* src_out, int8_t* t_out, uint8_t* rep_out, uint8_t* perm_out) {
+  return guarded([&] {
+    if (!offsets || !src_out) throw Error(CFM_ERR_VALUE, "offsets and src_out are required");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DeviceLists dl;
+    try {
+      classify_device(level, n_cells, ijk, s, dl, false, src_out, t_out, rep_out, perm_out, offsets);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaStreamDestroy(s);
+  });
+}
+
+int cfm_last_apply_stats(cfm_handler* h, double* ms, int64_t* launches) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    if (ms) *ms = h->last_ms;
+    if (launches) *launches = h->last_launches;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// GPU interaction-list classifier.
+//
+// Restates build_interaction_lists' far part (octree.py:148-178): for every
+// occupied target cell at level L >= 2, the candidates are the 8 children of
+// each of the 27 neighbours of its parent; a candidate is kept iff it is
+// occupied and t . t > 3 with t = ijk_target - ijk_source (octree.py:50-65).
+// The reference filters neighbours through the occupied parent set first;
+// a child can only be occupied if its parent is, so testing the child alone
+// is equivalent.  The reference sorts each list by source ijk (octree.py:176);
+// enumerating candidates with source x, then y, then z ascending produces that
+// order directly, so no sort is needed.
+//
+// Each kept pair is classified on the fly (symmetry.py:63-75): the cone
+// representative index (into the 16 sorted representatives) and the perm id.
+//
+// Occupancy lookup: a dense S^3 int32 grid of row indices (S = 2^L), built by
+// one scatter kernel; L <= 9 keeps it at <= 512 MB of the 180 GB HBM.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "symmetry.hpp"
+
+namespace cfm {
+
+__constant__ int8_t c_cone_index[kNumCodes];  // t_sym code -> index in sorted cone, -1 otherwise
+
+__global__ void k_grid_scatter(const int* __restrict__ ijk, long long n, int S, int* __restrict__ grid) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+  grid[((long long)x * S + y) * S + z] = int(i);
+}
+
+template <bool FILL>
+__global__ void k_classify(const int* __restrict__ ijk, long long n, int S, const int* __restrict__ grid,
+                           int* __restrict__ counts, const long long* __restrict__ off,
+                           int* __restrict__ src_out, int16_t* __restrict__ code_out,
+                           int8_t* __restrict__ t_out, uint8_t* __restrict__ rep_out,
+                           uint8_t* __restrict__ perm_out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+  const int bx = 2 * ((x >> 1) - 1), by = 2 * ((y >> 1) - 1), bz = 2 * ((z >> 1) - 1);
+  long long w = FILL ? off[i] : 0;
+  int cnt = 0;
+  for (int sx = bx; sx < bx + 6; ++sx) {
+    if (sx < 0 || sx >= S) continue;
+    const int t0 = x - sx;
+    for (int sy = by; sy < by + 6; ++sy) {
+      if (sy < 0 || sy >= S) continue;
+      const int t1 = y - sy;
+      const long long rowbase = ((long long)sx * S + sy) * S;
+      for (int sz = bz; sz < bz + 6; ++sz) {
+        if (sz < 0 || sz >= S) continue;
+        const int t2 = z - sz;
+        if (!is_far(t0, t1, t2)) continue;
+        const int r = grid[rowbase + sz];
+        if (r < 0) continue;
+        if (FILL) {
+          src_out[w] = r;
+          const int c = tcode(t0, t1, t2);
+          if (code_out) code_out[w] = int16_t(c);
+          if (t_out) {
+            t_out[3 * w] = int8_t(t0);
+            t_out[3 * w + 1] = int8_t(t1);
+            t_out[3 * w + 2] = int8_t(t2);
+          }
+          if (rep_out || perm_out) {
+            int ts[3], pid;
+            canonicalize(t0, t1, t2, ts, pid);
+            if (rep_out) rep_out[w] = uint8_t(c_cone_index[tcode(ts[0], ts[1], ts[2])]);
+            if (perm_out) perm_out[w] = uint8_t(pid);
+          }
+          ++w;
+        } else {
+          ++cnt;
+        }
+      }
+    }
+  }
+  if (!FILL) counts[i] = cnt;
+}
+
+}  // namespace cfm

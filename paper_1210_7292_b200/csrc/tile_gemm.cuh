@@ -1,0 +1,297 @@
+// Fused gather-permute -> FP64 DMMA -> ordered accumulate tile kernel (sm_100a).
+//
+// One CTA owns a (row block r0..r0+BM) x (tile of BN output columns) block of
+// the result and walks the tile's entries.  An entry is one (transfer vector,
+// occurrence) with one source column per output column; all columns of an
+// entry share an operator and a permutation, so the entry is one small GEMM:
+//
+//   acc[i, c] += sum_k  Op[ rowtab[i] , k ] * X[ src_c , invtab[k] ]
+//
+// which is the reference's symmetric apply (m2l.py:353-362, blocked form
+// :437-444 + :422 + :430-431):  u = w[inv]; out = K_rep @ u; acc += out[table]
+// with acc[i] += out[table[i]] = sum_k K_rep[table[i], k] * w[inv[k]].
+// The accumulator stays in registers across all entries of the tile, so the
+// inverse-permute scatter of the reference becomes a row gather of the
+// operator (rowtab) and the result is written once per tile, ordered per
+// target column with no atomics (each output column belongs to one tile).
+//
+// Staging: the operator rows (contiguous 16-B cp.async) and the gathered,
+// permuted source columns (8-B cp.async, zero-filled for empty slots) are
+// streamed through a STAGES-deep shared-memory ring in K-chunks of KC; the
+// MMA is mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4): tcgen05 has no f64 kind, and
+// DMMA runs at the chip's FP64 peak (37.1 TF/s measured, profiles/).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cfm {
+
+struct TileParams {
+  // plan
+  int n_tiles;
+  int tile_base;          // tile index of blockIdx.x == 0
+  const int* tile_col;    // [n_tiles * BN]  virtual output id or -1
+  const int* tile_off;    // [n_tiles + 1]   entry range per tile
+  const int* entry_code;  // [E]             code -> (op, row perm, col perm)
+  const int* entry_src;   // [E * BN]        virtual source id or -1
+  const int* code_op;     // [n_codes]
+  const int* code_rperm;  // [n_codes] row perm id (-1 identity)
+  const int* code_cperm;  // [n_codes] col perm id (-1 identity)
+  // operators: op o = ops + o * op_stride, row-major, leading dim op_ld,
+  // columns zero-padded up to a multiple of KC.
+  const double* ops;
+  long long op_stride;
+  int op_ld;
+  int nr;                  // output rows
+  int nk;                  // inner length
+  const int* op_rows;      // optional per-op row count
+  const int* op_klen;      // optional per-op inner length
+  const short* rowtab;     // rowtab[p * nr + i]
+  const short* invtab;     // invtab[p * nk + k]
+  // data: virtual id v -> base (v / dc) * ld + (v % dc), element stride dc
+  const double* x;
+  long long x_ld;
+  int x_dc;
+  double* y;
+  long long y_ld;
+  int y_dc;
+  double scale;
+  int accumulate;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int BM, int BN, int KC, int STAGES>
+constexpr int tile_smem_bytes() {
+  return STAGES * (BM + BN) * (KC + 4) * 8 + BN * 4;
+}
+
+// Per-entry decode shared by producer and consumer.
+struct EntryInfo {
+  int op, rperm, cperm, rows, klen, nchunks;
+};
+
+template <int BM, int KC>
+__device__ __forceinline__ EntryInfo decode_entry(const TileParams& p, int e, int r0) {
+  EntryInfo d;
+  const int code = p.entry_code[e];
+  d.op = p.code_op[code];
+  d.rperm = p.code_rperm[code];
+  d.cperm = p.code_cperm[code];
+  if (d.op < 0) {  // code handled by another launch (shared-basis dense vs factored cores)
+    d.rows = 0;
+    d.klen = 0;
+    d.nchunks = 0;
+    return d;
+  }
+  d.rows = p.op_rows ? p.op_rows[d.op] : p.nr;
+  d.klen = p.op_klen ? p.op_klen[d.op] : p.nk;
+  d.nchunks = (d.rows > r0) ? (d.klen + KC - 1) / KC : 0;
+  return d;
+}
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TileParams p) {
+  constexpr int NT = WM * WN * 32;
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int MT = WTM / 8, NTL = WTN / 8;
+  constexpr int LDA = KC + 4, LDB = KC + 4;
+  constexpr int A_PIECES = BM * (KC / 2);  // 16-B pieces per chunk
+  constexpr int A_PER_T = A_PIECES / NT;
+  constexpr int B_ELEMS = BN * KC;
+  constexpr int B_PER_T = B_ELEMS / NT;
+  static_assert(A_PIECES % NT == 0 && B_ELEMS % NT == 0, "tile/thread mismatch");
+  static_assert(NT % KC == 0, "B mapping needs NT multiple of KC");
+  static_assert(MT >= 1 && NTL >= 1, "warp tile too small");
+
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = As + STAGES * BM * LDA;
+  int* s_col = reinterpret_cast<int*>(Bs + STAGES * BN * LDB);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int wm = warp % WM, wn = warp / WM;
+  const int tile = p.tile_base + blockIdx.x;
+  const int r0 = blockIdx.y * BM;
+  const int e_begin = p.tile_off[tile], e_end = p.tile_off[tile + 1];
+
+  for (int c = tid; c < BN; c += NT) s_col[c] = p.tile_col[(long long)tile * BN + c];
+
+  // ---------------- producer state ----------------
+  int pe = e_begin, pk = 0;  // entry / chunk to issue next
+  EntryInfo pinfo;
+  if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
+  // skip entries with no chunks for this row block
+  while (pe < e_end && pinfo.nchunks == 0) {
+    ++pe;
+    if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
+  }
+  const double* a_row[A_PER_T];
+  bool a_ok[A_PER_T];
+  const double* b_col[B_PER_T];
+  int pe_loaded = -1;
+
+  auto load_entry_ptrs = [&](int e, const EntryInfo& d) {
+    const double* opbase = p.ops + (long long)d.op * p.op_stride;
+#pragma unroll
+    for (int u = 0; u < A_PER_T; ++u) {
+      const int id = tid + u * NT;
+      const int i = id / (KC / 2), kp = id % (KC / 2);
+      const int gr = r0 + i;
+      a_ok[u] = gr < d.rows;
+      int orow = gr;
+      if (a_ok[u] && d.rperm >= 0) orow = p.rowtab[(long long)d.rperm * p.nr + gr];
+      a_row[u] = opbase + (long long)(a_ok[u] ? orow : 0) * p.op_ld + 2 * kp;
+    }
+#pragma unroll
+    for (int u = 0; u < B_PER_T; ++u) {
+      const int c = tid / KC + u * (NT / KC);
+      const int v = p.entry_src[(long long)e * BN + c];
+      b_col[u] = (v >= 0) ? p.x + (long long)(v / p.x_dc) * p.x_ld + (v % p.x_dc) : nullptr;
+    }
+  };
+
+  auto issue = [&](int stage) {
+    if (pe >= e_end) {
+      cp_async_commit();
+      return;
+    }
+    if (pe_loaded != pe) {
+      load_entry_ptrs(pe, pinfo);
+      pe_loaded = pe;
+    }
+    const int k0 = pk * KC;
+    double* as = As + stage * BM * LDA;
+    double* bs = Bs + stage * BN * LDB;
+#pragma unroll
+    for (int u = 0; u < A_PER_T; ++u) {
+      const int id = tid + u * NT;
+      const int i = id / (KC / 2), kp = id % (KC / 2);
+      cp_async16(as + i * LDA + 2 * kp, a_ok[u] ? (const void*)(a_row[u] + k0) : (const void*)p.ops, a_ok[u]);
+    }
+    const int kk = tid % KC;
+    const int k = k0 + kk;
+    const bool kvalid = k < pinfo.klen;
+    int j = k;
+    if (kvalid && pinfo.cperm >= 0) j = p.invtab[(long long)pinfo.cperm * p.nk + k];
+#pragma unroll
+    for (int u = 0; u < B_PER_T; ++u) {
+      const int c = tid / KC + u * (NT / KC);
+      const bool ok = kvalid && b_col[u] != nullptr;
+      cp_async8(bs + c * LDB + kk, ok ? (const void*)(b_col[u] + (long long)p.x_dc * j) : (const void*)p.ops, ok);
+    }
+    cp_async_commit();
+    // advance producer
+    if (++pk >= pinfo.nchunks) {
+      pk = 0;
+      ++pe;
+      if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
+      while (pe < e_end && pinfo.nchunks == 0) {
+        ++pe;
+        if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
+      }
+    }
+  };
+
+  double acc[MT][NTL][2];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < NTL; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+
+  // ---------------- consumer state ----------------
+  int ce = e_begin, ck = 0;
+  EntryInfo cinfo;
+  if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
+  while (ce < e_end && cinfo.nchunks == 0) {
+    ++ce;
+    if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
+  }
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+
+  int q = 0;
+  while (ce < e_end) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue((q + STAGES - 1) % STAGES);
+    const int stage = q % STAGES;
+    const double* as = As + stage * BM * LDA + (wm * WTM + g) * LDA + tg;
+    const double* bs = Bs + stage * BN * LDB + (wn * WTN + g) * LDB + tg;
+    const int kmax = min(KC, cinfo.klen - ck * KC);
+    const int mrows = cinfo.rows - r0 - wm * WTM;  // rows of this warp tile that are live
+#pragma unroll 2
+    for (int kk = 0; kk < kmax; kk += 4) {
+      double a[MT], b[NTL];
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+      for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) {
+        if (mi * 8 < mrows) {
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        }
+      }
+    }
+    ++q;
+    if (++ck >= cinfo.nchunks) {
+      ck = 0;
+      ++ce;
+      if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
+      while (ce < e_end && cinfo.nchunks == 0) {
+        ++ce;
+        if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---------------- epilogue: ordered, atomic-free write ----------------
+  if (e_begin == e_end && p.accumulate) return;
+  __syncthreads();
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi) {
+    const int row = r0 + wm * WTM + mi * 8 + g;
+    if (row >= p.nr) continue;
+#pragma unroll
+    for (int nj = 0; nj < NTL; ++nj) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = wn * WTN + nj * 8 + 2 * tg + h;
+        const int v = s_col[c];
+        if (v < 0) continue;
+        double* dst = p.y + (long long)(v / p.y_dc) * p.y_ld + (v % p.y_dc) + (long long)p.y_dc * row;
+        const double val = p.scale * acc[mi][nj][h];
+        if (p.accumulate)
+          *dst += val;
+        else
+          *dst = val;
+      }
+    }
+  }
+}
+
+}  // namespace cfm

@@ -1,0 +1,290 @@
+"""GPU parity: the product path (C ABI -> sm_100a kernels) against the golden
+fixtures (executed reference) and the pinned oracle.
+
+Tolerances (north_star): lists / permutation ids bit-exact; fp64 locals
+relative L2 <= 1e-12 for full-rank variants and <= 1e-10 for compressed ones,
+with equal ranks and equal reference-model flop counts.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FULL = ("na", "nasym", "nablk")
+TOL = {v: (1e-12 if v in FULL else 1e-10) for v in O.VARIANTS}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return torch
+
+
+def _kernel_grid(g):
+    from paper_1210_7292_b200 import ChebyshevGrid, helmholtz_kernel, laplace_kernel
+
+    k = laplace_kernel() if str(g["kernel"]) == "laplace" else helmholtz_kernel(float(g["wavenumber"]))
+    return k, ChebyshevGrid(int(g["order"]))
+
+
+def _lt_lw(g):
+    levels = [int(l) for l in g["levels"]]
+    lt = {l: sorted({tuple(int(c) for c in t) for t in g[f"t_{l}"]}) for l in levels}
+    lw = dict(zip(levels, (float(w) for w in g["widths"])))
+    return levels, lt, lw
+
+
+def _mpoles(g, lvl, case):
+    if f"mpoles_{lvl}" in g:
+        return g[f"mpoles_{lvl}"]
+    seed = {"sphere9": 33, "sphere_lists": 44}[case]
+    n = len(g[f"cells_{lvl}"])
+    rng = np.random.default_rng(seed + lvl)
+    size = int(g["order"]) ** 3
+    m = rng.uniform(-1, 1, (n, size))
+    if str(g["kernel"]) != "laplace":
+        m = m + 1j * rng.uniform(-1, 1, (n, size))
+    return m
+
+
+def _handler(g, variant, **kw):
+    from paper_1210_7292_b200 import make_handler
+
+    kernel, grid = _kernel_grid(g)
+    levels, lt, lw = _lt_lw(g)
+    h = make_handler(variant, kernel, grid, float(g["eps"]), **kw)
+    h.precompute(lt, lw)
+    return h, levels
+
+
+CASES = [("cfg1", v) for v in O.VARIANTS] + [("helm", v) for v in O.VARIANTS] + \
+    [("lapcplx", v) for v in ("na", "nablk", "iablk", "sa")] + [("sphere_lists", "nasym")]
+
+
+@pytest.mark.parametrize("case,variant", CASES)
+def test_handler_matches_reference(torch_cuda, golden, case, variant):
+    g = golden(case)
+    h, levels = _handler(g, variant)
+    for lvl in levels:
+        mp = _mpoles(g, lvl, case)
+        tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+        batch = O.csr_to_batch(tgt, off, src, t)
+        loc = np.zeros(mp.shape, dtype=np.result_type(h.kernel.dtype, mp.dtype))
+        fl = h.apply_level(lvl, batch, mp, loc)
+        got = loc[g[f"rows_{lvl}"]] if f"rows_{lvl}" in g else loc
+        err = O.rel_l2(got, g[f"locals_{variant}_{lvl}"])
+        assert err <= TOL[variant], (case, variant, lvl, err)
+        assert fl == int(g[f"flops_{variant}_{lvl}"])
+        assert h.flops[lvl] == int(g[f"flops_{variant}_{lvl}"])
+        assert h.level_ranks(lvl) == list(g[f"ranks_{variant}_{lvl}"])
+        if h.is_shared_basis:
+            assert h.shared_rank(lvl) == int(g[f"shared_rank_{variant}_{lvl}"])
+            rt = h.recompression_table(lvl)
+            assert [(-1 if r is None else r) for _, r in rt] == list(g[f"recomp_r_{variant}_{lvl}"])
+        if h.uses_blocking:
+            assert h.block_stats[lvl]["columns"] == int(g[f"blk_columns_{variant}_{lvl}"])
+            assert len(h.block_stats[lvl]["reps_used"]) == int(g[f"blk_reps_{variant}_{lvl}"])
+    assert h.operator_count() == int(g[f"operator_count_{variant}"])
+    assert h.stored_bytes() == int(g[f"stored_bytes_{variant}"])
+    assert h.factorization_calls == int(g[f"factorization_calls_{variant}"])
+
+
+def test_sphere9_nablk_and_sa(torch_cuda, golden):
+    """l = 9 (729 nodes) on a sparse sphere tree: nablk and sa (eps 1e-8)."""
+    g = golden("sphere9")
+    for variant in ("nablk", "sa"):
+        h, levels = _handler(g, variant, budget_bytes=4_000_000_000)
+        for lvl in levels:
+            mp = _mpoles(g, lvl, "sphere9")
+            tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+            loc = np.zeros_like(mp)
+            fl = h.apply_level_csr(lvl, tgt, off, src, t, mp, loc)
+            err = O.rel_l2(loc[g[f"rows_{lvl}"]], g[f"locals_{variant}_{lvl}"])
+            assert err <= TOL[variant], (variant, lvl, err)
+            assert fl == int(g[f"flops_{variant}_{lvl}"])
+        if variant == "sa":
+            assert h.shared_rank(levels[0]) == int(g[f"shared_rank_sa_{levels[0]}"])
+
+
+@pytest.mark.parametrize("case", ["cfg1", "sphere_lists", "helm", "sphere9"])
+def test_classifier_bit_exact(torch_cuda, golden, case):
+    import ctypes
+
+    from paper_1210_7292_b200 import _native
+
+    lib = _native.load()
+    g = golden(case)
+    for lvl in g["levels"]:
+        cells = np.ascontiguousarray(g[f"cells_{lvl}"], dtype=np.int32)
+        n = len(cells)
+        offs = np.zeros(n + 1, np.int64)
+        total = ctypes.c_int64()
+        _native.check(lib.cfm_classify_count(0, int(lvl), n, cells.ctypes.data, offs.ctypes.data, ctypes.byref(total)))
+        src = np.zeros(total.value, np.int32)
+        tv = np.zeros((total.value, 3), np.int8)
+        rep = np.zeros(total.value, np.uint8)
+        perm = np.zeros(total.value, np.uint8)
+        _native.check(lib.cfm_classify_fill(0, int(lvl), n, cells.ctypes.data, offs.ctypes.data, src.ctypes.data,
+                                            tv.ctypes.data, rep.ctypes.data, perm.ctypes.data))
+        counts = np.diff(offs)
+        rows = np.nonzero(counts)[0]
+        assert np.array_equal(rows, g[f"tgt_{lvl}"])
+        assert np.array_equal(np.concatenate([[0], np.cumsum(counts[rows])]), g[f"off_{lvl}"])
+        assert np.array_equal(src, g[f"src_{lvl}"])
+        assert np.array_equal(tv, g[f"t_{lvl}"])
+        full_cone, _ = O.cone_of(O.full_far_field())
+        exp_rep, exp_perm = [], []
+        for t in tv:
+            ts, fl, od = O.canonicalize(tuple(int(c) for c in t))
+            exp_rep.append(full_cone.index(ts))
+            exp_perm.append(O.perm_id(fl, od))
+        assert np.array_equal(rep, np.asarray(exp_rep, np.uint8))
+        assert np.array_equal(perm, np.asarray(exp_perm, np.uint8))
+
+
+@pytest.mark.parametrize("variant", ["nablk", "na", "iablk", "sarcmp"])
+def test_cells_path_equals_csr_path(torch_cuda, golden, variant):
+    """Device-built lists (classifier -> plan) give the same locals as the
+    reference's host batch, bitwise (same lists, same plan)."""
+    torch = torch_cuda
+    g = golden("cfg1")
+    h, levels = _handler(g, variant)
+    for lvl in levels:
+        mp = g[f"mpoles_{lvl}"]
+        tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+        a = np.zeros_like(mp)
+        fa = h.apply_level_csr(lvl, tgt, off, src, t, mp, a)
+        h.plan_level_cells(lvl, g[f"cells_{lvl}"])
+        b = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
+        fb = h.apply_planned(lvl, torch.from_numpy(mp).cuda(), b)
+        assert fa == fb
+        assert np.array_equal(a, b.cpu().numpy())
+
+
+def test_edge_cases(torch_cuda, golden):
+    from paper_1210_7292_b200 import PrecomputeIncompleteError, make_handler
+
+    g = golden("cfg1")
+    kernel, grid = _kernel_grid(g)
+    h = make_handler("nablk", kernel, grid, 1e-5)
+    mp = g["mpoles_3"]
+    loc = np.zeros_like(mp)
+    with pytest.raises(PrecomputeIncompleteError):
+        h.apply_level(3, [(0, [(100, (3, 0, 0))])], mp, loc)
+    levels, lt, lw = _lt_lw(g)
+    h.precompute(lt, lw)
+    assert h.apply_level(3, [], mp, loc) == 0
+    with pytest.raises(PrecomputeIncompleteError):
+        h.apply_level(7, [(0, [(1, (2, 0, 0))])], mp, loc)
+    with pytest.raises(KeyError):  # PrecomputeIncompleteError is a KeyError, as in the reference
+        h.apply_level(3, [(0, [(1, (1, 0, 0))])], mp, loc)
+    assert np.all(loc == 0)
+    # empty far lists, a single pair, a duplicated target and duplicated pairs
+    batch = [(5, []), (7, [(300, (2, 1, 0))]), (9, [(40, (3, 3, 3)), (41, (-2, 0, 0))]),
+             (9, [(40, (3, 3, 3))])]
+    orc, _ = _oracle(g, "nablk")
+    ref = np.zeros_like(mp)
+    fr = orc.apply_faithful(3, batch, mp, ref)
+    fg = h.apply_level(3, batch, mp, loc)
+    assert fg == fr
+    assert O.rel_l2(loc, ref) <= 1e-13
+    assert np.all(loc[5] == 0)
+
+
+def _oracle(g, variant):
+    kname = str(g["kernel"])
+    prof, dt, deg = (O.laplace_profile, np.float64, -1.0) if kname == "laplace" else \
+        (O.helmholtz_profile(float(g["wavenumber"])), np.complex128, None)
+    levels, lt, lw = _lt_lw(g)
+    return O.OracleM2L(variant, prof, dt, int(g["order"]), float(g["eps"]), deg).precompute(lt, lw), levels
+
+
+def test_torch_tensors_in_place(torch_cuda, golden):
+    torch = torch_cuda
+    g = golden("helm")
+    h, levels = _handler(g, "iablk")
+    for lvl in levels:
+        mp = g[f"mpoles_{lvl}"]
+        tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+        loc = torch.zeros(mp.shape, dtype=torch.complex128, device="cuda")
+        h.apply_level_csr(lvl, tgt, off, src, t, torch.from_numpy(mp).cuda(), loc)
+        torch.cuda.synchronize()
+        assert O.rel_l2(loc.cpu().numpy(), g[f"locals_iablk_{lvl}"]) <= 1e-10
+
+
+def _full_level(level):
+    side = 1 << level
+    return np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3).astype(np.int32)
+
+
+@pytest.mark.parametrize("order,level,variant", [(5, 5, "nablk"), (5, 5, "iablk"), (7, 4, "nablk")])
+def test_full_level_against_oracle(torch_cuda, order, level, variant):
+    """Full cube levels (BASELINE configs 2/4 shapes at smaller depth), all
+    targets, device-built lists, against the vectorized oracle."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    eps = 1e-5
+    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: transfers}, lw)
+    st = h.plan_level_cells(level, cells)
+    assert st["pairs"] == off[-1] == (6 * 2**level - 8) ** 3 - (3 * 2**level - 2) ** 3
+    rng = np.random.default_rng(level)
+    mp = rng.uniform(-1, 1, (len(cells), order**3))
+    loc = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
+    fl = h.apply_planned(level, torch.from_numpy(mp).cuda(), loc)
+    orc = O.OracleM2L(variant, O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    ref = np.zeros_like(mp)
+    fr = orc.apply_fast(level, tgt, off, src, t, mp, ref)
+    assert fl == fr
+    assert O.rel_l2(loc.cpu().numpy(), ref) <= TOL[variant]
+
+
+def test_linearity_full_size_level(torch_cuda):
+    """Size-independent property at BASELINE config 2's deepest level (l=5,
+    262,144 cells, 46.3 M pairs): M2L(a x + b y) == a M2L(x) + b M2L(y), and a
+    sampled set of targets matches the oracle."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    level, order = 6, 5
+    cells = _full_level(level)
+    h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    full = O.full_far_field()
+    h.precompute({2: full, level: full}, {2: 0.25, level: 1.0 / 64})
+    st = h.plan_level_cells(level, cells)
+    assert st["pairs"] == 46_298_376
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.rand((len(cells), order**3), dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    y = torch.rand((len(cells), order**3), dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    outs = []
+    for m in (x, y, 0.75 * x - 1.5 * y):
+        o = torch.zeros_like(x)
+        h.apply_planned(level, m, o)
+        outs.append(o)
+    lin = 0.75 * outs[0] - 1.5 * outs[1]
+    assert (torch.linalg.norm(outs[2] - lin) / torch.linalg.norm(outs[2])).item() <= 1e-13
+    # sampled targets against the oracle (first 64 rows in reference order + a random sample)
+    rng = np.random.default_rng(3)
+    rows = np.unique(np.concatenate([np.arange(64), rng.choice(len(cells), 192, replace=False)]))
+    tgt, off, src, t = O.far_lists(cells, level, targets=rows)
+    assert np.array_equal(tgt, rows)
+    orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+        {2: full, level: full}, {2: 0.25, level: 1.0 / 64})
+    xm = x.cpu().numpy()
+    ref = np.zeros_like(xm)
+    orc.apply_fast(level, tgt, off, src, t, xm, ref)
+    assert O.rel_l2(outs[0].cpu().numpy()[rows], ref[rows]) <= 1e-12

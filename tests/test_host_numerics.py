@@ -1,0 +1,77 @@
+"""Product host-side numerics (precompute inputs) against the golden fixtures."""
+
+import numpy as np
+
+from oracle import oracle as O
+from paper_1210_7292_b200 import (
+    ChebyshevGrid,
+    assemble_for_transfer,
+    canonicalize,
+    cheb_roots,
+    full_far_field_vectors,
+    helmholtz_kernel,
+    laplace_kernel,
+    permutation_table,
+    truncated_svd,
+)
+from paper_1210_7292_b200.symmetry import SymmetryMap, inverse_permutation_table
+
+
+def test_roots_and_nodes():
+    for order in range(2, 10):
+        r = cheb_roots(order)
+        assert np.array_equal(r, O.cheb_roots(order))
+        assert np.array_equal(r, -r[::-1])
+        assert np.array_equal(ChebyshevGrid(order).nodes3d, O.nodes3d(order))
+
+
+def test_symmetry_matches_reference(golden):
+    g = golden("symmetry")
+    far = full_far_field_vectors()
+    assert np.array_equal(np.asarray(far), g["far316"])
+    for i, t in enumerate(far):
+        ts, spec = canonicalize(t)
+        assert ts == tuple(g["t_sym"][i])
+        assert spec.perm_id == g["spec_id"][i]
+    assert np.array_equal(np.asarray(SymmetryMap(far).cone), g["cone"])
+    for order in (2, 3, 4, 5, 7, 9):
+        for pid in range(48):
+            assert np.array_equal(permutation_table(pid, order), g[f"table_l{order}"][pid])
+            assert np.array_equal(inverse_permutation_table(pid, order), g[f"inv_l{order}"][pid])
+
+
+def test_operator_assembly_bitwise(golden):
+    g = golden("cfg1")
+    grid = ChebyshevGrid(4)
+    w = float(g["widths"][0])
+    for k, t in enumerate(g["K_rep_t"]):
+        K = assemble_for_transfer(laplace_kernel(), tuple(int(c) for c in t), w, grid)
+        assert np.array_equal(K, g["K_rep"][k])
+
+
+def test_operator_identity_through_permutations():
+    """K_t = P K_rep P^T for all 316 vectors, both kernels (<=1e-13)."""
+    for kernel in (laplace_kernel(), helmholtz_kernel(1.0)):
+        for order in (2, 3, 4):
+            grid = ChebyshevGrid(order)
+            reps = {}
+            for t in full_far_field_vectors():
+                ts, spec = canonicalize(t)
+                if ts not in reps:
+                    reps[ts] = assemble_for_transfer(kernel, ts, 0.5, grid)
+                K = assemble_for_transfer(kernel, t, 0.5, grid)
+                tab = permutation_table(spec.perm_id, order)
+                Kp = reps[ts][np.ix_(tab, tab)]
+                assert np.max(np.abs(K - Kp)) <= 1e-13 * np.max(np.abs(K))
+
+
+def test_lowrank_ranks_match_reference(golden):
+    g = golden("cfg1")
+    grid = ChebyshevGrid(4)
+    levels = [int(l) for l in g["levels"]]
+    w = float(g["widths"][0])
+    transfers = sorted({tuple(int(c) for c in t) for l in levels for t in g[f"t_{l}"]})
+    ranks = {t: truncated_svd(assemble_for_transfer(laplace_kernel(), t, w, grid), float(g["eps"])).rank
+             for t in transfers}
+    assert [ranks[t] for t in transfers] == list(g["ranks_ia_2"]) or \
+        [ranks[t] for t in transfers if t in set(map(tuple, g["t_2"].tolist()))] == list(g["ranks_ia_2"])

@@ -1,0 +1,170 @@
+"""Pin the oracle (oracle/oracle.py) to the golden fixtures produced by executing
+the reference (tests/golden/make_golden.py).  CPU only."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+from geometry import cube_points, sphere_points  # noqa: E402
+
+CASES = ("cfg1", "helm", "lapcplx", "sphere9", "sphere_lists")
+
+
+def test_symmetry_tables(golden):
+    g = golden("symmetry")
+    far = O.full_far_field()
+    assert len(far) == 316
+    assert np.array_equal(np.asarray(far), g["far316"])
+    for i, t in enumerate(far):
+        ts, fl, od = O.canonicalize(t)
+        assert ts == tuple(g["t_sym"][i])
+        assert fl == tuple(g["flips"][i])
+        assert od == tuple(g["axis_order"][i])
+        assert O.perm_id(fl, od) == g["spec_id"][i]
+    cone, assign = O.cone_of(far)
+    assert np.array_equal(np.asarray(cone), g["cone"]) and len(cone) == 16
+    assert [assign[tuple(t)][0] for t in far] == list(g["rep_idx"])
+    assert sorted(set(int(s) for s in g["spec_id"])) == list(range(48))
+    for order in (2, 3, 4, 5, 7, 9):
+        for pid in range(48):
+            fl = tuple(bool(pid // 6 >> a & 1) for a in range(3))
+            od = O.AXIS_ORDERS[pid % 6]
+            assert np.array_equal(O.perm_table(fl, od, order), g[f"table_l{order}"][pid])
+            assert np.array_equal(O.inv_table(fl, od, order), g[f"inv_l{order}"][pid])
+    sub_cone, sub_assign = O.cone_of([tuple(t) for t in g["sub50"]])
+    assert np.array_equal(np.asarray(sub_cone), g["sub50_cone"])
+    assert [sub_assign[tuple(int(c) for c in t)][0] for t in g["sub50"]] == list(g["sub50_rep_idx"])
+
+
+def test_spec_examples():
+    # SPEC.md symmetry examples (canonicalize)
+    assert O.canonicalize((-2, 1, 0)) == ((2, 1, 0), (True, False, False), (1, 2, 3))
+    assert O.canonicalize((1, 2, 0)) == ((2, 1, 0), (False, False, False), (2, 1, 3))
+    assert O.canonicalize((-1, 2, 0)) == ((2, 1, 0), (True, False, False), (2, 1, 3))
+    assert O.canonicalize((3, 2, 1)) == ((3, 2, 1), (False, False, False), (1, 2, 3))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_far_lists_bit_exact(golden, case):
+    g = golden(case)
+    for lvl in g["levels"]:
+        cells = g[f"cells_{lvl}"].astype(np.int64)
+        tgt, off, src, t = O.far_lists(cells, int(lvl))
+        assert np.array_equal(tgt, g[f"tgt_{lvl}"])
+        assert np.array_equal(off, g[f"off_{lvl}"])
+        assert np.array_equal(src, g[f"src_{lvl}"])
+        assert np.array_equal(t, g[f"t_{lvl}"])
+
+
+def _points(case):
+    if case == "cfg1":
+        return cube_points(10_000, 1), (0.5, 0.5, 0.5), 0.5
+    if case == "helm":
+        return sphere_points(3_000, 5), (0.0, 0.0, 0.0), 1.0
+    if case == "lapcplx":
+        return cube_points(2_000, 11), (0.5, 0.5, 0.5), 0.5
+    if case == "sphere9":
+        return sphere_points(20_000, 3), (0.0, 0.0, 0.0), 1.0
+    return sphere_points(30_000, 21), (0.0, 0.0, 0.0), 1.0
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_tree_cells(golden, case):
+    g = golden(case)
+    pts, c, hw = _points(case)
+    cells = O.level_cells_from_points(pts, c, hw, int(g["depth"]))
+    for lvl in g["levels"]:
+        assert np.array_equal(cells[int(lvl)], g[f"cells_{lvl}"].astype(np.int64))
+
+
+def full_pair_count(level):
+    s = 1 << level
+    return (6 * s - 8) ** 3 - (3 * s - 2) ** 3
+
+
+def test_full_level_pair_formula():
+    for lvl in (2, 3, 4):
+        side = 1 << lvl
+        ijk = np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3)
+        _, off, _, _ = O.far_lists(ijk, lvl)
+        assert off[-1] == full_pair_count(lvl)
+    assert [full_pair_count(L) for L in range(2, 8)] == [3096, 53352, 584136, 5398920, 46298376, 383233032]
+
+
+def _oracle_for(g, variant):
+    kname = str(g["kernel"])
+    order = int(g["order"])
+    eps = float(g["eps"])
+    if kname == "laplace":
+        prof, dt, deg = O.laplace_profile, np.float64, -1.0
+    else:
+        prof, dt, deg = O.helmholtz_profile(float(g["wavenumber"])), np.complex128, None
+    levels = [int(l) for l in g["levels"]]
+    lt = {l: sorted({tuple(int(c) for c in t) for t in g[f"t_{l}"]}) for l in levels}
+    lw = dict(zip(levels, (float(w) for w in g["widths"])))
+    return O.OracleM2L(variant, prof, dt, order, eps, deg).precompute(lt, lw), levels
+
+
+def _mpoles(g, lvl, case):
+    if f"mpoles_{lvl}" in g:
+        return g[f"mpoles_{lvl}"]
+    seed = {"sphere9": 33, "sphere_lists": 44}[case]
+    n = len(g[f"cells_{lvl}"])
+    rng = np.random.default_rng(seed + lvl)
+    size = int(g["order"]) ** 3
+    m = rng.uniform(-1, 1, (n, size))
+    if str(g["kernel"]) != "laplace":
+        m = m + 1j * rng.uniform(-1, 1, (n, size))
+    return m
+
+
+def _variants(g):
+    return sorted({k.split("_")[1] for k in g if k.startswith("locals_")})
+
+
+FAST_CASES = [("cfg1", v) for v in O.VARIANTS] + [("helm", v) for v in O.VARIANTS] + \
+    [("lapcplx", v) for v in ("na", "nablk", "iablk", "sa")] + [("sphere_lists", "nasym")]
+
+
+@pytest.mark.parametrize("case,variant", FAST_CASES)
+def test_oracle_apply_matches_reference(golden, case, variant):
+    g = golden(case)
+    orc, levels = _oracle_for(g, variant)
+    for lvl in levels:
+        mp = _mpoles(g, lvl, case)
+        ref = g[f"locals_{variant}_{lvl}"]
+        tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+        batch = O.csr_to_batch(tgt, off, src, t)
+        loc = np.zeros(mp.shape, dtype=np.result_type(orc.dtype, mp.dtype))
+        fl = orc.apply_faithful(lvl, batch, mp, loc)
+        if f"rows_{lvl}" in g:
+            loc = loc[g[f"rows_{lvl}"]]
+        assert O.rel_l2(loc, ref) <= 1e-14, (variant, lvl, O.rel_l2(loc, ref))
+        assert fl == int(g[f"flops_{variant}_{lvl}"])
+        assert orc.level_ranks(lvl) == list(g[f"ranks_{variant}_{lvl}"])
+        # the vectorized regrouping agrees with the faithful loops
+        loc2 = np.zeros(mp.shape, dtype=loc.dtype)
+        fl2 = orc.apply_fast(lvl, tgt, off, src, t, mp, loc2)
+        if f"rows_{lvl}" in g:
+            loc2 = loc2[g[f"rows_{lvl}"]]
+        assert fl2 == fl
+        assert O.rel_l2(loc2, ref) <= 1e-13
+
+
+@pytest.mark.skipif(os.environ.get("ORACLE_SLOW") != "1", reason="l=9 shared-basis precompute takes ~1 min")
+def test_oracle_sphere9(golden):
+    g = golden("sphere9")
+    for variant in ("nablk", "sa"):
+        orc, levels = _oracle_for(g, variant)
+        for lvl in levels:
+            mp = _mpoles(g, lvl, "sphere9")
+            tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+            loc = np.zeros_like(mp)
+            fl = orc.apply_fast(lvl, tgt, off, src, t, mp, loc)
+            assert O.rel_l2(loc[g[f"rows_{lvl}"]], g[f"locals_{variant}_{lvl}"]) <= 1e-13
+            assert fl == int(g[f"flops_{variant}_{lvl}"])
