@@ -135,6 +135,13 @@ int cfm_plan_level_csr(cfm_handler* h, int level, int64_t n_targets, const int64
 int cfm_apply_planned(cfm_handler* h, int level, const double* mpoles, int64_t n_rows,
                       double* locals, void* stream);
 
+/* Apply several planned levels of one M2L step together (the levels are
+ * independent, m2l.py:279 per level): dense variants run as ONE kernel launch
+ * over all levels' tiles, so small levels overlap the large one.  Arrays are
+ * indexed by position; pointers may be host or device memory. */
+int cfm_apply_levels(cfm_handler* h, int n_levels, const int* levels, const double* const* mpoles,
+                     const int64_t* n_rows, double* const* locals, void* stream);
+
 /* Plan statistics: tiles, entries (GEMM tile products), pairs, entry column
  * slots (entries * 64), distinct targets and distinct sources. */
 int cfm_plan_stats(cfm_handler* h, int level, int64_t* n_tiles, int64_t* n_entries,

@@ -38,6 +38,7 @@ EXPORTS = (
     "cfm_plan_level_cells",
     "cfm_plan_level_csr",
     "cfm_apply_planned",
+    "cfm_apply_levels",
     "cfm_plan_stats",
     "cfm_classify_count",
     "cfm_classify_fill",
@@ -62,6 +63,7 @@ _SIGS = {
     "cfm_plan_level_cells": ([_P, _I, _I64, _P, _I, _P, _P], _I),
     "cfm_plan_level_csr": ([_P, _I, _I64, _P, _P, _P, _P, _I, _I64, _P], _I),
     "cfm_apply_planned": ([_P, _I, _P, _I64, _P, _P], _I),
+    "cfm_apply_levels": ([_P, _I, _P, _P, _P, _P, _P], _I),
     "cfm_plan_stats": ([_P, _I, _P, _P, _P, _P, _P, _P], _I),
     "cfm_classify_count": ([_I, _I, _I64, _P, _P, _P], _I),
     "cfm_classify_fill": ([_I, _I, _I64, _P, _P, _P, _P, _P, _P], _I),

@@ -32,6 +32,7 @@
 #include "plan.hpp"
 #include "symmetry.hpp"
 #include "tile_gemm.cuh"
+#include "tile_gemm_ws.cuh"
 
 namespace cfm {
 
@@ -192,17 +193,102 @@ struct cfm_handler {
 namespace cfm {
 
 // ------------------------------------------------------------------ launching
+// Kernel selection (CFM_TILE_KERNEL): "ws16" warp-specialized KC=16 x 5 stages
+// (default), "ws32" KC=32 x 3 stages, "sync" the lockstep kernel.
+static int tile_kernel_kind() {
+  static int kind = [] {
+    const char* v = getenv("CFM_TILE_KERNEL");
+    if (!v) return 1;
+    if (!strcmp(v, "ws32")) return 0;
+    if (!strcmp(v, "sync")) return 2;
+    return 1;
+  }();
+  return kind;
+}
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
+static void launch_ws_multi(const MultiTileParams& mp, dim3 grid, cudaStream_t s) {
+  const TileParams& q = mp.seg[0];
+  const bool tabs = tile_perm_tabs_fit(q.nr, q.nk);
+  const int smem = ws_ring_bytes<BM, BN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, tabs);
+  auto kern = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, STAGES, SKIP>;
+  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, (WM * WN + 4) * 32, smem, s>>>(mp);
+}
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
+static void launch_ws(const TileParams& q, dim3 grid, cudaStream_t s) {
+  MultiTileParams mp{};
+  mp.n_seg = 1;
+  mp.start[0] = 0;
+  mp.start[1] = int(grid.x);
+  mp.seg[0] = q;
+  launch_ws_multi<BM, BN, WM, WN, KC, STAGES, SKIP>(mp, grid, s);
+}
+
+template <int BM, int BN, int WM, int WN, bool SKIP>
+static void launch_sync(const TileParams& q, dim3 grid, cudaStream_t s) {
+  constexpr int STAGES = 3;
+  const bool tabs = tile_perm_tabs_fit(q.nr, q.nk);
+  const int smem = tile_ring_bytes<BM, BN, kKC, STAGES>() + tile_table_bytes(q.nr, q.nk, tabs);
+  auto kern = tile_gemm_kernel<BM, BN, WM, WN, kKC, STAGES, SKIP>;
+  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, WM * WN * 32, smem, s>>>(q);
+}
+
 template <int BM, int BN, int WM, int WN>
 static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStream_t s) {
-  constexpr int STAGES = 3;
-  constexpr int smem = tile_smem_bytes<BM, BN, kKC, STAGES>();
-  auto kern = tile_gemm_kernel<BM, BN, WM, WN, kKC, STAGES>;
-  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TileParams q = p;
   q.tile_base = tile_base;
   dim3 grid(n_tiles, (p.nr + BM - 1) / BM);
-  kern<<<grid, WM * WN * 32, smem, s>>>(q);
+  const int kind = tile_kernel_kind();
+  if (p.op_rows) {
+    if (kind == 2) launch_sync<BM, BN, WM, WN, true>(q, grid, s);
+    else if (kind == 1) launch_ws<BM, BN, WM, WN, 16, 5, true>(q, grid, s);
+    else launch_ws<BM, BN, WM, WN, 32, 3, true>(q, grid, s);
+  } else {
+    if (kind == 2) launch_sync<BM, BN, WM, WN, false>(q, grid, s);
+    else if (kind == 1) launch_ws<BM, BN, WM, WN, 16, 5, false>(q, grid, s);
+    else launch_ws<BM, BN, WM, WN, 32, 3, false>(q, grid, s);
+  }
   CUDA_CHECK(cudaGetLastError());
+}
+
+// One launch over several tile lists sharing operator shapes (all levels of a
+// homogeneous dense group).  Segments are launched in the given order.
+static int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int64_t>& counts, cudaStream_t s) {
+  MultiTileParams mp{};
+  int64_t total = 0;
+  mp.n_seg = 0;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    if (counts[i] == 0) continue;
+    if (mp.n_seg == kMaxSegments) throw Error(CFM_ERR_VALUE, "too many levels in one launch");
+    mp.start[mp.n_seg] = int(total);
+    mp.seg[mp.n_seg] = segs[i];
+    mp.seg[mp.n_seg].tile_base = 0;
+    total += counts[i];
+    ++mp.n_seg;
+  }
+  if (mp.n_seg == 0) return 0;
+  if (total >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
+  mp.start[mp.n_seg] = int(total);
+  const TileParams& q = mp.seg[0];
+  const int kind = tile_kernel_kind();
+  if (q.nr <= 32) {
+    dim3 grid(unsigned(total), (q.nr + 31) / 32);
+    if (kind == 0) launch_ws_multi<32, kBN, 1, 8, 32, 3, false>(mp, grid, s);
+    else launch_ws_multi<32, kBN, 1, 8, 16, 5, false>(mp, grid, s);
+  } else if (q.nr <= 64) {
+    dim3 grid(unsigned(total), (q.nr + 63) / 64);
+    if (kind == 0) launch_ws_multi<64, kBN, 2, 4, 32, 3, false>(mp, grid, s);
+    else launch_ws_multi<64, kBN, 2, 4, 16, 5, false>(mp, grid, s);
+  } else {
+    dim3 grid(unsigned(total), (q.nr + 127) / 128);
+    if (kind == 0) launch_ws_multi<128, kBN, 4, 2, 32, 3, false>(mp, grid, s);
+    else launch_ws_multi<128, kBN, 4, 2, 16, 5, false>(mp, grid, s);
+  }
+  CUDA_CHECK(cudaGetLastError());
+  return 1;
 }
 
 // Launch tiles [first, first + count) of the plan in p.
@@ -603,6 +689,94 @@ static void apply_with_buffers(cfm_handler* h, int level, LevelPlan& lp, const d
   h->last_ms = ms;
 }
 
+// All planned levels of one step in as few launches as possible: dense groups
+// go into a single multi-segment launch (levels are independent in M2L, so
+// the long per-tile chains of the small levels overlap the big level).
+static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const double* const* mpoles,
+                              const int64_t* n_rows, double* const* locals, cudaStream_t s) {
+  struct Lv {
+    int level;
+    LevelPlan* lp;
+    const double* x;
+    double* y;
+    double* host_y;
+    size_t bytes;
+  };
+  std::vector<Lv> lv;
+  size_t stage_bytes = 0;
+  for (int i = 0; i < n_levels; ++i) {
+    auto it = h->plans.find(levels[i]);
+    if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(levels[i]));
+    if (it->second.n_rows != n_rows[i]) throw Error(CFM_ERR_VALUE, "row count differs from the planned level");
+    group_for_level(h, levels[i]);
+    const size_t row_d = size_t(h->n) * (it->second.dc == 2 || h->op_complex ? 2 : 1);
+    const size_t bytes = size_t(n_rows[i]) * row_d * sizeof(double);
+    lv.push_back({levels[i], &it->second, mpoles[i], locals[i], nullptr, bytes});
+    if (!is_device_ptr(mpoles[i])) stage_bytes += bytes;
+    if (!is_device_ptr(locals[i])) stage_bytes += bytes;
+  }
+  std::sort(lv.begin(), lv.end(), [](const Lv& a, const Lv& b) { return a.level < b.level; });
+  if (stage_bytes) ensure(h->x_stage, stage_bytes);
+  size_t off = 0;
+  for (auto& L : lv) {
+    if (!is_device_ptr(L.x)) {
+      double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
+      CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s));
+      L.x = d;
+      off += L.bytes;
+    }
+    if (!is_device_ptr(L.y)) {
+      double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
+      CUDA_CHECK(cudaMemcpyAsync(d, L.y, L.bytes, cudaMemcpyHostToDevice, s));
+      L.host_y = L.y;
+      L.y = d;
+      off += L.bytes;
+    }
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev0, s));
+  int64_t launches = 0;
+  bool all_dense = true;
+  for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
+  if (all_dense) {
+    std::vector<TileParams> segs;
+    std::vector<int64_t> counts;
+    int nr = -1;
+    bool same_shape = true;
+    for (auto& L : lv) {
+      Group& g = group_for_level(h, L.level);
+      TileParams p{};
+      p.rowtab = h->rowtab.as<short>();
+      p.invtab = h->invtab.as<short>();
+      fill_ops(p, g.dense, g.main);
+      fill_plan(p, L.lp->tile_col, L.lp->tile_off, L.lp->entry_code, L.lp->entry_src, L.lp->hp.n_tiles);
+      const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
+      p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
+      p.y = L.y; p.y_ld = row_ld; p.y_dc = L.lp->dc;
+      p.scale = h->levels[L.level].second;
+      p.accumulate = 1;
+      if (nr >= 0 && (p.nr != nr)) same_shape = false;
+      nr = p.nr;
+      segs.push_back(p);
+      counts.push_back(L.lp->hp.n_tiles);
+    }
+    if (same_shape && int(segs.size()) <= kMaxSegments) {
+      launches += launch_multi(segs, counts, s);
+    } else {
+      for (size_t i = 0; i < segs.size(); ++i) launches += launch_tiles(segs[i], counts[i], s);
+    }
+  } else {
+    for (auto& L : lv) launches += run_plan(h, L.level, *L.lp, L.x, L.y, s);
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev1, s));
+  for (auto& L : lv)
+    if (L.host_y) CUDA_CHECK(cudaMemcpyAsync(L.host_y, L.y, L.bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  h->last_ms = ms;
+  h->last_launches = launches;
+}
+
 // ------------------------------------------------------------------ classifier
 struct DeviceLists {
   DevBuf off, src, code;
@@ -955,6 +1129,18 @@ int cfm_plan_level_cells(cfm_handler* h, int level, int64_t n_cells, const int32
     LevelPlan& lp = make_plan(h, level, n_cells, tgt.data(), dl.h_off.data(), src64.data(), hcode.data(),
                               data_complex, n_cells);
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
+  });
+}
+
+int cfm_apply_levels(cfm_handler* h, int n_levels, const int* levels, const double* const* mpoles,
+                     const int64_t* n_rows, double* const* locals, void* stream) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    if (n_levels < 0 || (n_levels && (!levels || !mpoles || !n_rows || !locals)))
+      throw Error(CFM_ERR_VALUE, "bad level arrays");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    apply_levels_impl(h, n_levels, levels, mpoles, n_rows, locals, pick_stream(h, stream));
   });
 }
 

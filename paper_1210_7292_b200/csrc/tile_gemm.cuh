@@ -79,36 +79,45 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <int BM, int BN, int KC, int STAGES>
-constexpr int tile_smem_bytes() {
-  return STAGES * (BM + BN) * (KC + 4) * 8 + BN * 4;
-}
+constexpr int kMaxTileEntries = 1024;  // entry codes cached in smem per tile
 
-// Per-entry decode shared by producer and consumer.
+// Shared-memory footprint: operand ring + per-CTA lookup tables
+// (code -> op/perm, the tile's entry codes, and the 48 permutation tables
+// when they fit).
+template <int BM, int BN, int KC, int STAGES>
+constexpr int tile_ring_bytes() {
+  return STAGES * (BM + BN) * (KC + 4) * 8;
+}
+__host__ __device__ constexpr int tile_table_bytes(int nr, int nk, bool perm_tabs) {
+  return 4 * 64 /*s_col*/ + 3 * 4 * 344 + 4 * kMaxTileEntries + (perm_tabs ? 48 * 2 * (nr + nk + 8) : 0);
+}
+__host__ __device__ inline bool tile_perm_tabs_fit(int nr, int nk) { return 48 * 2 * (nr + nk) <= 48 * 1024; }
+
+// Per-entry decode shared by producer and consumer (all lookups in smem).
 struct EntryInfo {
   int op, rperm, cperm, rows, klen, nchunks;
 };
 
-template <int BM, int KC>
-__device__ __forceinline__ EntryInfo decode_entry(const TileParams& p, int e, int r0) {
+template <int KC>
+__device__ __forceinline__ EntryInfo decode_code(const TileParams& p, int code, const int* s_op, const int* s_rp,
+                                                 const int* s_cp, int r0) {
   EntryInfo d;
-  const int code = p.entry_code[e];
-  d.op = p.code_op[code];
-  d.rperm = p.code_rperm[code];
-  d.cperm = p.code_cperm[code];
+  d.op = s_op[code];
+  d.rperm = s_rp[code];
+  d.cperm = s_cp[code];
   if (d.op < 0) {  // code handled by another launch (shared-basis dense vs factored cores)
     d.rows = 0;
     d.klen = 0;
     d.nchunks = 0;
     return d;
   }
-  d.rows = p.op_rows ? p.op_rows[d.op] : p.nr;
-  d.klen = p.op_klen ? p.op_klen[d.op] : p.nk;
+  d.rows = p.op_rows ? __ldg(p.op_rows + d.op) : p.nr;
+  d.klen = p.op_klen ? __ldg(p.op_klen + d.op) : p.nk;
   d.nchunks = (d.rows > r0) ? (d.klen + KC - 1) / KC : 0;
   return d;
 }
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS>
 __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TileParams p) {
   constexpr int NT = WM * WN * 32;
   constexpr int WTM = BM / WM, WTN = BN / WN;
@@ -121,11 +130,19 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
   static_assert(A_PIECES % NT == 0 && B_ELEMS % NT == 0, "tile/thread mismatch");
   static_assert(NT % KC == 0, "B mapping needs NT multiple of KC");
   static_assert(MT >= 1 && NTL >= 1, "warp tile too small");
+  static_assert(BN <= 64, "s_col sized for 64 columns");
 
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = As + STAGES * BM * LDA;
   int* s_col = reinterpret_cast<int*>(Bs + STAGES * BN * LDB);
+  int* s_op = s_col + 64;
+  int* s_rp = s_op + 344;
+  int* s_cp = s_rp + 344;
+  int* s_ecode = s_cp + 344;
+  short* s_rowtab = reinterpret_cast<short*>(s_ecode + kMaxTileEntries);
+  const bool tabs_in_smem = tile_perm_tabs_fit(p.nr, p.nk);
+  short* s_invtab = s_rowtab + 48 * p.nr + 8;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -135,17 +152,48 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
   const int r0 = blockIdx.y * BM;
   const int e_begin = p.tile_off[tile], e_end = p.tile_off[tile + 1];
 
+  // ---------------- per-CTA tables in shared memory ----------------
   for (int c = tid; c < BN; c += NT) s_col[c] = p.tile_col[(long long)tile * BN + c];
+  for (int c = tid; c < 343; c += NT) {
+    s_op[c] = p.code_op[c];
+    s_rp[c] = p.code_rperm[c];
+    s_cp[c] = p.code_cperm[c];
+  }
+  const int n_cached = min(e_end - e_begin, kMaxTileEntries);
+  for (int i = tid; i < n_cached; i += NT) s_ecode[i] = p.entry_code[e_begin + i];
+  if (tabs_in_smem) {
+    if (p.rowtab)
+      for (int i = tid; i < 48 * p.nr; i += NT) s_rowtab[i] = p.rowtab[i];
+    if (p.invtab)
+      for (int i = tid; i < 48 * p.nk; i += NT) s_invtab[i] = p.invtab[i];
+  }
+  __syncthreads();
+  const short* rowtab = tabs_in_smem ? s_rowtab : p.rowtab;
+  const short* invtab = tabs_in_smem ? s_invtab : p.invtab;
+  auto code_of = [&](int e) -> int {
+    const int i = e - e_begin;
+    return i < kMaxTileEntries ? s_ecode[i] : __ldg(p.entry_code + e);
+  };
 
   // ---------------- producer state ----------------
   int pe = e_begin, pk = 0;  // entry / chunk to issue next
   EntryInfo pinfo;
-  if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
-  // skip entries with no chunks for this row block
-  while (pe < e_end && pinfo.nchunks == 0) {
+  pinfo.nchunks = 0;
+  while (pe < e_end) {
+    pinfo = decode_code<KC>(p, code_of(pe), s_op, s_rp, s_cp, r0);
+    if (pinfo.nchunks) break;
     ++pe;
-    if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
   }
+  // B source indices: current entry (registers) and the prefetched next entry
+  int nxt_src[B_PER_T];
+  int nxt_e = -1;
+  auto prefetch_src = [&](int e) {
+    nxt_e = e;
+    if (e < e_end) {
+#pragma unroll
+      for (int u = 0; u < B_PER_T; ++u) nxt_src[u] = __ldg(p.entry_src + (long long)e * BN + tid / KC + u * (NT / KC));
+    }
+  };
   const double* a_row[A_PER_T];
   bool a_ok[A_PER_T];
   const double* b_col[B_PER_T];
@@ -160,15 +208,16 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
       const int gr = r0 + i;
       a_ok[u] = gr < d.rows;
       int orow = gr;
-      if (a_ok[u] && d.rperm >= 0) orow = p.rowtab[(long long)d.rperm * p.nr + gr];
+      if (a_ok[u] && d.rperm >= 0) orow = rowtab[d.rperm * p.nr + gr];
       a_row[u] = opbase + (long long)(a_ok[u] ? orow : 0) * p.op_ld + 2 * kp;
     }
+    if (nxt_e != e) prefetch_src(e);
 #pragma unroll
     for (int u = 0; u < B_PER_T; ++u) {
-      const int c = tid / KC + u * (NT / KC);
-      const int v = p.entry_src[(long long)e * BN + c];
+      const int v = nxt_src[u];
       b_col[u] = (v >= 0) ? p.x + (long long)(v / p.x_dc) * p.x_ld + (v % p.x_dc) : nullptr;
     }
+    prefetch_src(e + 1);  // latency hidden behind this entry's chunks
   };
 
   auto issue = [&](int stage) {
@@ -193,7 +242,7 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
     const int k = k0 + kk;
     const bool kvalid = k < pinfo.klen;
     int j = k;
-    if (kvalid && pinfo.cperm >= 0) j = p.invtab[(long long)pinfo.cperm * p.nk + k];
+    if (kvalid && pinfo.cperm >= 0) j = invtab[pinfo.cperm * p.nk + k];
 #pragma unroll
     for (int u = 0; u < B_PER_T; ++u) {
       const int c = tid / KC + u * (NT / KC);
@@ -205,10 +254,10 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
     if (++pk >= pinfo.nchunks) {
       pk = 0;
       ++pe;
-      if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
-      while (pe < e_end && pinfo.nchunks == 0) {
+      while (pe < e_end) {
+        pinfo = decode_code<KC>(p, code_of(pe), s_op, s_rp, s_cp, r0);
+        if (pinfo.nchunks) break;
         ++pe;
-        if (pe < e_end) pinfo = decode_entry<BM, KC>(p, pe, r0);
       }
     }
   };
@@ -222,10 +271,11 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
   // ---------------- consumer state ----------------
   int ce = e_begin, ck = 0;
   EntryInfo cinfo;
-  if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
-  while (ce < e_end && cinfo.nchunks == 0) {
+  cinfo.nchunks = 0;
+  while (ce < e_end) {
+    cinfo = decode_code<KC>(p, code_of(ce), s_op, s_rp, s_cp, r0);
+    if (cinfo.nchunks) break;
     ++ce;
-    if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
   }
 
 #pragma unroll
@@ -240,30 +290,58 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
     const double* as = As + stage * BM * LDA + (wm * WTM + g) * LDA + tg;
     const double* bs = Bs + stage * BN * LDB + (wn * WTN + g) * LDB + tg;
     const int kmax = min(KC, cinfo.klen - ck * KC);
-    const int mrows = cinfo.rows - r0 - wm * WTM;  // rows of this warp tile that are live
+    if (SKIP_ROWS) {
+      const int mrows = cinfo.rows - r0 - wm * WTM;  // live rows of this warp tile
 #pragma unroll 2
-    for (int kk = 0; kk < kmax; kk += 4) {
-      double a[MT], b[NTL];
+      for (int kk = 0; kk < kmax; kk += 4) {
+        double a[MT], b[NTL];
 #pragma unroll
-      for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+        for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
 #pragma unroll
-      for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+        for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
 #pragma unroll
-      for (int mi = 0; mi < MT; ++mi) {
-        if (mi * 8 < mrows) {
+        for (int mi = 0; mi < MT; ++mi) {
+          if (mi * 8 < mrows) {
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+          }
+        }
+      }
+    } else if (kmax == KC) {
+#pragma unroll
+      for (int kk = 0; kk < KC; kk += 4) {
+        double a[MT], b[NTL];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+        for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
           for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
-        }
+      }
+    } else {
+#pragma unroll 2
+      for (int kk = 0; kk < kmax; kk += 4) {
+        double a[MT], b[NTL];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+        for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
       }
     }
     ++q;
     if (++ck >= cinfo.nchunks) {
       ck = 0;
       ++ce;
-      if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
-      while (ce < e_end && cinfo.nchunks == 0) {
+      while (ce < e_end) {
+        cinfo = decode_code<KC>(p, code_of(ce), s_op, s_rp, s_cp, r0);
+        if (cinfo.nchunks) break;
         ++ce;
-        if (ce < e_end) cinfo = decode_entry<BM, KC>(p, ce, r0);
       }
     }
   }
@@ -271,7 +349,6 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) tile_gemm_kernel(const TilePar
 
   // ---------------- epilogue: ordered, atomic-free write ----------------
   if (e_begin == e_end && p.accumulate) return;
-  __syncthreads();
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi) {
     const int row = r0 + wm * WTM + mi * 8 + g;

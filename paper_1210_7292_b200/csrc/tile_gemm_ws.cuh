@@ -1,0 +1,295 @@
+// Warp-specialized variant of tile_gemm_kernel (same math, same plan).
+//
+// 4 producer warps walk the tile's (entry, K-chunk) stream and issue the
+// cp.async gathers (operator rows by the row table, source columns by the
+// inverse table); each producer thread signals the stage's "full" mbarrier
+// with cp.async.mbarrier.arrive.noinc when its copies land.  8 consumer warps
+// wait on "full", run the LDS -> DMMA.8x8x4 loop on the stage and release it
+// on the "empty" mbarrier.  There is no CTA-wide barrier in the main loop, so
+// the consumer warps keep the FP64 tensor pipe fed while the producers run
+// STAGES-1 chunks ahead.
+#pragma once
+#include "tile_gemm.cuh"
+
+namespace cfm {
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_cp_async_arrive(uint64_t* bar) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+template <int BM, int BN, int KC, int STAGES>
+constexpr int ws_ring_bytes() {
+  return STAGES * (BM + BN) * (KC + 4) * 8 + 2 * STAGES * 8;
+}
+
+// Several independent tile lists (e.g. all octree levels of one M2L step) in
+// one launch: blockIdx.x ranges [start[s], start[s+1]) belong to segment s.
+constexpr int kMaxSegments = 12;
+struct MultiTileParams {
+  int n_seg;
+  int start[kMaxSegments + 1];
+  TileParams seg[kMaxSegments];
+};
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS>
+__global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(const __grid_constant__ MultiTileParams mp) {
+  int sidx = 0;
+  while (sidx + 1 < mp.n_seg && int(blockIdx.x) >= mp.start[sidx + 1]) ++sidx;
+  const TileParams& p = mp.seg[sidx];
+  constexpr int NC = WM * WN * 32;  // consumer threads
+  constexpr int NP = 4 * 32;        // producer threads
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int MT = WTM / 8, NTL = WTN / 8;
+  constexpr int LDA = KC + 4, LDB = KC + 4;
+  constexpr int A_PIECES = BM * (KC / 2);
+  constexpr int A_PER_T = A_PIECES / NP;
+  constexpr int B_ELEMS = BN * KC;
+  constexpr int B_PER_T = B_ELEMS / NP;
+  static_assert(A_PIECES % NP == 0 && B_ELEMS % NP == 0, "tile/thread mismatch");
+  static_assert(NP % KC == 0, "B mapping needs NP multiple of KC");
+  static_assert(BN <= 64, "s_col sized for 64 columns");
+
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = As + STAGES * BM * LDA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * BN * LDB);
+  uint64_t* empty = full + STAGES;
+  int* s_col = reinterpret_cast<int*>(empty + STAGES);
+  int* s_op = s_col + 64;
+  int* s_rp = s_op + 344;
+  int* s_cp = s_rp + 344;
+  int* s_ecode = s_cp + 344;
+  short* s_rowtab = reinterpret_cast<short*>(s_ecode + kMaxTileEntries);
+  const bool tabs_in_smem = tile_perm_tabs_fit(p.nr, p.nk);
+  short* s_invtab = s_rowtab + 48 * p.nr + 8;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int tile = p.tile_base + int(blockIdx.x) - mp.start[sidx];
+  const int r0 = blockIdx.y * BM;
+  const int e_begin = p.tile_off[tile], e_end = p.tile_off[tile + 1];
+
+  for (int c = tid; c < BN; c += NC + NP) s_col[c] = p.tile_col[(long long)tile * BN + c];
+  for (int c = tid; c < 343; c += NC + NP) {
+    s_op[c] = p.code_op[c];
+    s_rp[c] = p.code_rperm[c];
+    s_cp[c] = p.code_cperm[c];
+  }
+  const int n_cached = min(e_end - e_begin, kMaxTileEntries);
+  for (int i = tid; i < n_cached; i += NC + NP) s_ecode[i] = p.entry_code[e_begin + i];
+  if (tabs_in_smem) {
+    if (p.rowtab)
+      for (int i = tid; i < 48 * p.nr; i += NC + NP) s_rowtab[i] = p.rowtab[i];
+    if (p.invtab)
+      for (int i = tid; i < 48 * p.nk; i += NC + NP) s_invtab[i] = p.invtab[i];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, NP);
+      mbar_init(empty + s, NC / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const short* rowtab = tabs_in_smem ? s_rowtab : p.rowtab;
+  const short* invtab = tabs_in_smem ? s_invtab : p.invtab;
+  auto code_of = [&](int e) -> int {
+    const int i = e - e_begin;
+    return i < kMaxTileEntries ? s_ecode[i] : __ldg(p.entry_code + e);
+  };
+  auto next_live = [&](int e, EntryInfo& d) -> int {
+    while (e < e_end) {
+      d = decode_code<KC>(p, code_of(e), s_op, s_rp, s_cp, r0);
+      if (d.nchunks) break;
+      ++e;
+    }
+    return e;
+  };
+
+  if (tid >= NC) {
+    // ======================= producer warps =======================
+    const int pt = tid - NC;
+    EntryInfo d;
+    d.nchunks = 0;
+    int e = next_live(e_begin, d);
+    int q = 0;
+    int nxt_src[B_PER_T];
+    int nxt_e = -1;
+    auto prefetch_src = [&](int ee) {
+      nxt_e = ee;
+      if (ee < e_end) {
+#pragma unroll
+        for (int u = 0; u < B_PER_T; ++u)
+          nxt_src[u] = __ldg(p.entry_src + (long long)ee * BN + pt / KC + u * (NP / KC));
+      }
+    };
+    const double* a_row[A_PER_T];
+    bool a_ok[A_PER_T];
+    const double* b_col[B_PER_T];
+    while (e < e_end) {
+      // per-entry pointers
+      const double* opbase = p.ops + (long long)d.op * p.op_stride;
+#pragma unroll
+      for (int u = 0; u < A_PER_T; ++u) {
+        const int id = pt + u * NP;
+        const int i = id / (KC / 2), kp = id % (KC / 2);
+        const int gr = r0 + i;
+        a_ok[u] = gr < d.rows;
+        int orow = gr;
+        if (a_ok[u] && d.rperm >= 0) orow = rowtab[d.rperm * p.nr + gr];
+        a_row[u] = opbase + (long long)(a_ok[u] ? orow : 0) * p.op_ld + 2 * kp;
+      }
+      if (nxt_e != e) prefetch_src(e);
+#pragma unroll
+      for (int u = 0; u < B_PER_T; ++u) {
+        const int v = nxt_src[u];
+        b_col[u] = (v >= 0) ? p.x + (long long)(v / p.x_dc) * p.x_ld + (v % p.x_dc) : nullptr;
+      }
+      prefetch_src(e + 1);
+      for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
+        const int s = q % STAGES;
+        if (q >= STAGES) mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
+        const int k0 = kc * KC;
+        double* as = As + s * BM * LDA;
+        double* bs = Bs + s * BN * LDB;
+#pragma unroll
+        for (int u = 0; u < A_PER_T; ++u) {
+          const int id = pt + u * NP;
+          const int i = id / (KC / 2), kp = id % (KC / 2);
+          cp_async16(as + i * LDA + 2 * kp, a_ok[u] ? (const void*)(a_row[u] + k0) : (const void*)p.ops, a_ok[u]);
+        }
+        const int kk = pt % KC;
+        const int k = k0 + kk;
+        const bool kvalid = k < d.klen;
+        int j = k;
+        if (kvalid && d.cperm >= 0) j = invtab[d.cperm * p.nk + k];
+#pragma unroll
+        for (int u = 0; u < B_PER_T; ++u) {
+          const int c = pt / KC + u * (NP / KC);
+          const bool ok = kvalid && b_col[u] != nullptr;
+          cp_async8(bs + c * LDB + kk, ok ? (const void*)(b_col[u] + (long long)p.x_dc * j) : (const void*)p.ops, ok);
+        }
+        mbar_cp_async_arrive(full + s);
+      }
+      e = next_live(e + 1, d);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  const int g = lane >> 2, tg = lane & 3;
+  const int wm = warp % WM, wn = warp / WM;
+  double acc[MT][NTL][2];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < NTL; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+
+  EntryInfo d;
+  d.nchunks = 0;
+  int e = next_live(e_begin, d);
+  int q = 0;
+  while (e < e_end) {
+    const int mrows = d.rows - r0 - wm * WTM;
+    for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
+      const int s = q % STAGES;
+      mbar_wait(full + s, (q / STAGES) & 1);
+      const double* as = As + s * BM * LDA + (wm * WTM + g) * LDA + tg;
+      const double* bs = Bs + s * BN * LDB + (wn * WTN + g) * LDB + tg;
+      const int kmax = min(KC, d.klen - kc * KC);
+      if (SKIP_ROWS) {
+#pragma unroll 2
+        for (int kk = 0; kk < kmax; kk += 4) {
+          double a[MT], b[NTL];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) {
+            if (mi * 8 < mrows) {
+#pragma unroll
+              for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+            }
+          }
+        }
+      } else if (kmax == KC) {
+#pragma unroll
+        for (int kk = 0; kk < KC; kk += 4) {
+          double a[MT], b[NTL];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        }
+      } else {
+#pragma unroll 2
+        for (int kk = 0; kk < kmax; kk += 4) {
+          double a[MT], b[NTL];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+    e = next_live(e + 1, d);
+  }
+
+  // ---------------- epilogue: ordered, atomic-free write ----------------
+  if (e_begin == e_end && p.accumulate) return;
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi) {
+    const int row = r0 + wm * WTM + mi * 8 + g;
+    if (row >= p.nr) continue;
+#pragma unroll
+    for (int nj = 0; nj < NTL; ++nj) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = wn * WTN + nj * 8 + 2 * tg + h;
+        const int v = s_col[c];
+        if (v < 0) continue;
+        double* dst = p.y + (long long)(v / p.y_dc) * p.y_ld + (v % p.y_dc) + (long long)p.y_dc * row;
+        const double val = p.scale * acc[mi][nj][h];
+        if (p.accumulate)
+          *dst += val;
+        else
+          *dst = val;
+      }
+    }
+  }
+}
+
+}  // namespace cfm

@@ -506,6 +506,42 @@ class B200M2LHandler:
         self._record(level, key, st["counts"], flops)
         return flops
 
+    def apply_levels(self, arrays) -> int:
+        """Apply several planned levels of one M2L step together.
+
+        ``arrays`` maps level -> (mpoles, locals_out).  Dense variants run all
+        levels in a single kernel launch; returns the total counted flops and
+        records per-level accounting exactly as per-level calls would."""
+        levels = sorted(arrays)
+        prepared = []
+        for lvl in levels:
+            self._level_key(lvl)
+            st = self._planned.get(lvl)
+            if st is None:
+                raise PrecomputeIncompleteError(f"level {lvl} has no device plan; call plan_level_cells first")
+            x, y, wb, data_complex, n_rows = self._prepare(*arrays[lvl])
+            if bool(data_complex) != (st["complex"] or self._op_complex):
+                raise ValueError("expansion dtype differs from the one the level was planned for")
+            prepared.append((lvl, x, y, wb, n_rows, st))
+        if not prepared:
+            return 0
+        n = len(prepared)
+        lv = (ctypes.c_int * n)(*[p[0] for p in prepared])
+        xs = (ctypes.c_void_p * n)(*[_native.ptr(p[1]) for p in prepared])
+        ys = (ctypes.c_void_p * n)(*[_native.ptr(p[2]) for p in prepared])
+        rows = (ctypes.c_int64 * n)(*[int(p[4]) for p in prepared])
+        with self._lock:
+            self._check(self._lib.cfm_apply_levels(self._h, n, lv, xs, rows, ys, self._stream_of(prepared[0][1])))
+        total = 0
+        for lvl, x, y, wb, n_rows, st in prepared:
+            if wb is not None:
+                wb[...] = y
+            key = self._level_group[lvl]
+            flops = self._count_flops(key, st["counts"], st["targets"], st["sources"])
+            self._record(lvl, key, st["counts"], flops)
+            total += flops
+        return total
+
     def last_apply_stats(self) -> tuple[float, int]:
         ms = ctypes.c_double()
         n = ctypes.c_int64()

@@ -288,3 +288,30 @@ def test_linearity_full_size_level(torch_cuda):
     ref = np.zeros_like(xm)
     orc.apply_fast(level, tgt, off, src, t, xm, ref)
     assert O.rel_l2(outs[0].cpu().numpy()[rows], ref[rows]) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", ["nablk", "iablk", "sa"])
+def test_apply_levels_equals_per_level(torch_cuda, golden, variant):
+    """One multi-level launch gives bitwise the per-level results and flops."""
+    torch = torch_cuda
+    g = golden("cfg1")
+    h, levels = _handler(g, variant)
+    for lvl in levels:
+        h.plan_level_cells(lvl, g[f"cells_{lvl}"])
+    arrays, ref = {}, {}
+    fl_ref = 0
+    for lvl in levels:
+        mp = torch.from_numpy(g[f"mpoles_{lvl}"]).cuda()
+        ref[lvl] = torch.zeros_like(mp)
+        fl_ref += h.apply_planned(lvl, mp, ref[lvl])
+        arrays[lvl] = (mp, torch.zeros_like(mp))
+    fl = h.apply_levels(arrays)
+    assert fl == fl_ref
+    for lvl in levels:
+        assert torch.equal(arrays[lvl][1], ref[lvl])
+        assert O.rel_l2(arrays[lvl][1].cpu().numpy(), g[f"locals_{variant}_{lvl}"]) <= TOL[variant]
+    # host buffers through the same call
+    host = {lvl: (g[f"mpoles_{lvl}"], np.zeros_like(g[f"mpoles_{lvl}"])) for lvl in levels}
+    h.apply_levels(host)
+    for lvl in levels:
+        assert np.array_equal(host[lvl][1], ref[lvl].cpu().numpy())
