@@ -336,7 +336,8 @@ def run_b200(args):
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(cfg, {}).get(variant)
+            t = json.loads(prof.read_text()).get(cfg, {}).get(variant)
+            traffic = t["dram_bytes"] if isinstance(t, dict) else t
         except Exception:
             traffic = None
 

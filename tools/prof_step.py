@@ -1,0 +1,39 @@
+"""One bench step (all levels, one launch) for ncu: plans BASELINE config 2 and
+applies it `--reps` times with device-resident expansions."""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    n, depth, order, geom, variant, eps = bench.CONFIGS[a.config]
+    variant = a.variant or variant
+    cells, widths = bench.cached_level_cells(a.config)
+    levels = sorted(cells)
+    full = full_far_field_vectors()
+    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({l: full for l in levels}, widths)
+    for l in levels:
+        h.plan_level_cells(l, cells[l].astype("int32"))
+    mp = {l: torch.rand((len(cells[l]), order**3), dtype=torch.float64, device="cuda") for l in levels}
+    loc = {l: torch.zeros_like(mp[l]) for l in levels}
+    for _ in range(a.reps):
+        h.apply_levels({l: (mp[l], loc[l]) for l in levels})
+        torch.cuda.synchronize()
+        print("step device ms %.3f launches %d" % h.last_apply_stats())
+
+
+if __name__ == "__main__":
+    main()
