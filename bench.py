@@ -39,13 +39,16 @@ METRIC = "M2L cell-pair interactions/sec (fp64)"
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak.json"
 
 CONFIGS = {
-    # name: (n_points, depth, order, geometry, variant, eps)
+    # name: (n_points, depth, order, geometry, variant, eps)   (BASELINE.json configs; height H = depth + 1)
+    "cfg1": (10_000, 3, 4, "cube", "nablk", 1e-5),
     "cfg2": (10_000_000, 6, 5, "cube", "nablk", 1e-5),
     "cfg2_ia": (10_000_000, 6, 5, "cube", "iablk", 1e-5),
-    "cfg1": (10_000, 3, 4, "cube", "nablk", 1e-5),
     "cfg3": (8_000_000, 5, 9, "sphere", "nablk", 1e-8),
+    "cfg3_sa": (8_000_000, 5, 9, "sphere", "sa", 1e-8),
     "cfg4": (100_000_000, 7, 7, "cube", "nablk", 1e-7),
+    "cfg5": (2_000_000, 5, 5, "sphere", "iablk", 1e-4),   # Helmholtz k = 8 pi, complex128, non-directional
 }
+HELMHOLTZ = {"cfg5": 8 * np.pi}
 
 
 def fp64_peak():
@@ -60,17 +63,24 @@ def level_cells(cfg):
     from geometry import cube_points, sphere_points
 
     n, depth, order, geom, _, _ = CONFIGS[cfg]
+    side = 1 << depth
     if geom == "cube":
-        pts = cube_points(n, seed=2)
         low, width = np.zeros(3), 1.0
     else:
-        pts = sphere_points(n, seed=3)
         low, width = -np.ones(3), 2.0
-    side = 1 << depth
-    ijk = np.minimum(((pts - low) / width * side).astype(np.int64), side - 1)
-    del pts
-    key = np.unique((ijk[:, 0] << 42) | (ijk[:, 1] << 21) | ijk[:, 2])
-    del ijk
+    keys = []
+    chunk = 10_000_000
+    rng_seed = 2 if geom == "cube" else 3
+    # generated in chunks of 10^7 points (config 4 has 10^8) with per-chunk seeds
+    for i in range(0, n, chunk):
+        m = min(chunk, n - i)
+        seed = rng_seed + 1000 * (i // chunk)
+        pts = cube_points(m, seed=seed) if geom == "cube" else sphere_points(m, seed=seed)
+        ijk = np.minimum(((pts - low) / width * side).astype(np.int64), side - 1)
+        del pts
+        keys.append(np.unique((ijk[:, 0] << 42) | (ijk[:, 1] << 21) | ijk[:, 2]))
+        del ijk
+    key = np.unique(np.concatenate(keys))
     out = {}
     cur = np.stack([key >> 42, (key >> 21) & 0x1FFFFF, key & 0x1FFFFF], 1)
     out[depth] = cur
@@ -145,23 +155,44 @@ def dist_env():
     return ws, rank, local
 
 
+_PORT = {}
+
+
+def _port_setup(cfg):
+    """Oracle port of the reference handler for a config, precomputed once in the
+    parent process (forked workers share it)."""
+    from oracle import oracle as O
+
+    if cfg in _PORT:
+        return _PORT[cfg]
+    cells, widths = cached_level_cells(cfg)
+    _, depth, order, _, variant, eps = CONFIGS[cfg]
+    full = O.full_far_field()
+    if cfg in HELMHOLTZ:
+        prof, dt, deg = O.helmholtz_profile(HELMHOLTZ[cfg]), np.complex128, None
+    else:
+        prof, dt, deg = O.laplace_profile, np.float64, -1.0
+    orc = O.OracleM2L(variant, prof, dt, order, eps, deg).precompute({l: full for l in cells}, widths)
+    rng = np.random.default_rng(7)
+    mp = rng.uniform(-1, 1, (len(cells[depth]), order**3))
+    if cfg in HELMHOLTZ:
+        mp = mp + 1j * rng.uniform(-1, 1, mp.shape)
+    _PORT[cfg] = (orc, mp)
+    return _PORT[cfg]
+
+
 def _port_worker(job):
-    """One worker of the CPU port: faithful apply (m2l.py:397-452) on a chunk
+    """One worker of the CPU port: faithful apply (m2l.py:279-452) on a chunk
     of targets; returns (pairs, seconds) of the timed apply only."""
     from threadpoolctl import threadpool_limits
 
     from oracle import oracle as O
 
     cfg, rows, blas_threads = job
-    cells, widths = cached_level_cells(cfg)
-    _, depth, order, _, variant, eps = CONFIGS[cfg]
-    lvl = depth
+    cells, _ = cached_level_cells(cfg)
+    orc, mp = _port_setup(cfg)
+    lvl = CONFIGS[cfg][1]
     tgt, off, src, t = O.far_lists(cells[lvl], lvl, targets=rows)
-    full = O.full_far_field()
-    orc = O.OracleM2L(variant, O.laplace_profile, np.float64, order, eps, -1.0).precompute(
-        {l: full for l in cells}, widths)
-    rng = np.random.default_rng(7)
-    mp = rng.uniform(-1, 1, (len(cells[lvl]), order**3))
     loc = np.zeros_like(mp)
     batch = O.csr_to_batch(tgt, off, src, t)
     with threadpool_limits(limits=blas_threads):
@@ -189,6 +220,8 @@ def cpu_port_sample(cfg, n_targets, workers):
 
     _, depth, _, _, _, _ = CONFIGS[cfg]
     cached_level_cells(cfg)  # build once in the parent; forked workers share it
+    _port_setup(cfg)
+    n_targets = min(n_targets, len(_LEVEL_CACHE[cfg][0][depth]))
     rows = np.arange(n_targets)
     chunks = [c for c in np.array_split(rows, workers) if len(c)]
     if workers == 1:
@@ -221,7 +254,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(x[2] for x in vals),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128" if cfg in HELMHOLTZ else "f64", "data": "synthetic",
         "config": {"workload": f"{cfg}: {CONFIGS[cfg]}", "sample": f"first {n_t} targets of level {lvl}"},
         "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "sample": f"{pairs} pairs: first {n_t} level-{lvl} targets (full far lists), faithful "
@@ -243,7 +277,13 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+    from paper_1210_7292_b200 import (
+        ChebyshevGrid,
+        full_far_field_vectors,
+        helmholtz_kernel,
+        laplace_kernel,
+        make_handler,
+    )
 
     cfg = args.config
     n, depth, order, geom, variant, eps = CONFIGS[cfg]
@@ -252,8 +292,14 @@ def run_b200(args):
     cells, widths = cached_level_cells(cfg)
     levels = sorted(cells)
     full = full_far_field_vectors()
-    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps, device=local)
+    cplx = cfg in HELMHOLTZ
+    kernel = helmholtz_kernel(HELMHOLTZ[cfg]) if cplx else laplace_kernel()
+    dt = torch.complex128 if cplx else torch.float64
+    budget = 4_000_000_000 if variant in ("sa", "sarcmp") else 2_000_000_000
+    h = make_handler(variant, kernel, ChebyshevGrid(order), eps, device=local, budget_bytes=budget)
+    t_pre = time.perf_counter()
     h.precompute({l: full for l in levels}, widths)
+    t_pre = time.perf_counter() - t_pre
 
     # shard target rows across ranks (contiguous ranges in lexicographic order);
     # every rank holds the level's multipoles (replicated inputs, no exchange).
@@ -265,12 +311,15 @@ def run_b200(args):
     pairs_total = sum(st["pairs"] for st in stats.values())
 
     gen = torch.Generator(device=dev).manual_seed(11)
-    mp = {l: torch.rand((len(cells[l]), size), dtype=torch.float64, device=dev, generator=gen) * 2 - 1 for l in levels}
+    mp = {l: torch.rand((len(cells[l]), size), dtype=dt, device=dev, generator=gen) * 2 - (1 + 1j if cplx else 1)
+          for l in levels}
     loc = {l: torch.zeros_like(mp[l]) for l in levels}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
+    step_flops = [0]
+
     def step():
-        h.apply_levels({l: (mp[l], loc[l]) for l in levels})
+        step_flops[0] = h.apply_levels({l: (mp[l], loc[l]) for l in levels})
         return h.last_apply_stats()[1]
 
     for _ in range(args.warmup):
@@ -308,8 +357,8 @@ def run_b200(args):
     value = pairs_total * args.steps / (total_ms * 1e-3)
 
     # e2e: same step through the handler with pinned host buffers
-    h_mp = {l: torch.empty(mp[l].shape, dtype=torch.float64, pin_memory=True) for l in levels}
-    h_loc = {l: torch.zeros(mp[l].shape, dtype=torch.float64, pin_memory=True) for l in levels}
+    h_mp = {l: torch.empty(mp[l].shape, dtype=dt, pin_memory=True) for l in levels}
+    h_loc = {l: torch.zeros(mp[l].shape, dtype=dt, pin_memory=True) for l in levels}
     for l in levels:
         h_mp[l].copy_(mp[l].cpu())
     np_mp = {l: h_mp[l].numpy() for l in levels}
@@ -322,7 +371,7 @@ def run_b200(args):
     for _ in range(e2e_steps):
         h.apply_levels({l: (np_mp[l], np_loc[l]) for l in levels})
     e2e_s = (time.perf_counter() - tic) / e2e_steps
-    bytes_lvl = {l: mp[l].numel() * 8 for l in levels}
+    bytes_lvl = {l: mp[l].numel() * mp[l].element_size() for l in levels}
     h2d = sum(2 * b for b in bytes_lvl.values())  # multipoles + locals (accumulated in place)
     d2h = sum(bytes_lvl.values())
 
@@ -330,8 +379,11 @@ def run_b200(args):
     peak, peak_src = fp64_peak()
     deep = levels[-1]
     step_ms_med = statistics.median(step_ms)
-    flops_pair = 2 * size * size if variant in ("na", "nasym", "nablk") else None
-    achieved = (pairs_total * flops_pair / (step_ms_med * 1e-3) / 1e12) if flops_pair else None
+    # algorithmic flops of one step = the reference's own accounting (m2l.py:333-426),
+    # converted to real flops (x4 for complex128 operators)
+    real_flops = step_flops[0] * (4 if cplx else 1)
+    flops_pair = real_flops / pairs_total
+    achieved = real_flops / (step_ms_med * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
@@ -354,18 +406,19 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE config 2: N=1e7 uniform cube, height 7 (levels 2-{deep}), l={order}, "
-                                   f"Laplace, variant {variant}", "pairs_per_step": pairs_total,
+            "config": {"workload": f"{cfg}: N={n:.0e} {geom}, height {depth + 1} (levels {levels[0]}-{deep}), "
+                                   f"l={order}, {'Helmholtz k=8pi complex128' if cplx else 'Laplace'}, variant {variant}"
+                                   f", eps={eps:g}", "pairs_per_step": pairs_total, "precompute_s": t_pre,
                        "levels": {str(l): stats[l]["pairs"] for l in levels},
                        "tile_fill": pairs_total / max(slots, 1),
                        "l2": "flushed between steps (256 MB write)", "multipoles": "seeded U[-1,1]"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"tile_gemm_ws, one launch over levels {levels[0]}-{deep} "
-                                   f"({pairs_total} pairs x {flops_pair} flop)",
+                         "kernel": f"tile_gemm_ws over levels {levels[0]}-{deep} "
+                                   f"({pairs_total} pairs x {flops_pair:.0f} flop avg, reference accounting"
+                                   f"{' x4 complex' if cplx else ''})",
                          "peak_source": peak_src, "dominant_ms": step_ms_med,
-                         "step_tflops": (pairs_total * flops_pair / (total_ms / args.steps * 1e-3) / 1e12)
-                         if flops_pair else None},
+                         "step_tflops": real_flops / (total_ms / args.steps * 1e-3) / 1e12},
             "e2e": {"value": pairs_total / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                     "path": "B200M2LHandler.apply_levels with pinned host numpy buffers (C ABI; H2D multipoles "
