@@ -147,6 +147,12 @@ int cfm_apply_levels(cfm_handler* h, int n_levels, const int* levels, const doub
 int cfm_plan_stats(cfm_handler* h, int level, int64_t* n_tiles, int64_t* n_entries,
                    int64_t* n_pairs, int64_t* n_slots, int64_t* n_targets, int64_t* n_sources);
 
+/* Plan layout chosen for a level: mode 0 = target tiles (per-target register
+ * accumulators; dense trees), 1 = pair entries + ordered per-target reduction
+ * (sparse trees, chosen when target tiles would be < 60% full; override with
+ * CFM_PLAN_MODE=target|pair).  target_fill = pairs / target-tile slots. */
+int cfm_plan_info(cfm_handler* h, int level, int* mode, double* target_fill);
+
 /* Interaction-list classifier (octree.py:148-178 + symmetry.py:63-75) on the
  * GPU.  Cells: sorted occupied ijk of `level` (int32 triples, host or device).
  * count: per-cell far-pair counts -> offsets (n_cells+1, host int64), returns

@@ -40,6 +40,7 @@ EXPORTS = (
     "cfm_apply_planned",
     "cfm_apply_levels",
     "cfm_plan_stats",
+    "cfm_plan_info",
     "cfm_classify_count",
     "cfm_classify_fill",
     "cfm_last_apply_stats",
@@ -65,6 +66,7 @@ _SIGS = {
     "cfm_apply_planned": ([_P, _I, _P, _I64, _P, _P], _I),
     "cfm_apply_levels": ([_P, _I, _P, _P, _P, _P, _P], _I),
     "cfm_plan_stats": ([_P, _I, _P, _P, _P, _P, _P, _P], _I),
+    "cfm_plan_info": ([_P, _I, _P, _P], _I),
     "cfm_classify_count": ([_I, _I, _I64, _P, _P, _P], _I),
     "cfm_classify_fill": ([_I, _I, _I64, _P, _P, _P, _P, _P, _P], _I),
     "cfm_last_apply_stats": ([_P, _P, _P], _I),

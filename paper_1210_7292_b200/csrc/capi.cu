@@ -33,6 +33,7 @@
 #include "symmetry.hpp"
 #include "tile_gemm.cuh"
 #include "tile_gemm_ws.cuh"
+#include "pair_reduce.cuh"
 
 namespace cfm {
 
@@ -160,6 +161,10 @@ struct Group {
 struct LevelPlan {
   HostPlan hp;
   int dc = 1;
+  int mode = 0;  // 0: target tiles (accumulator per target column); 1: pair entries + ordered reduction
+  double target_fill = 1.0;
+  PairReduce red;
+  DevBuf r_tgt, r_off, r_frow;
   DevBuf tile_col, tile_off, entry_code, entry_src;
   DevBuf slot_ids, iota;  // low-rank: per-entry slots
   // shared basis
@@ -184,7 +189,7 @@ struct cfm_handler {
   std::map<int, Group> groups;
   std::map<int, std::pair<int, double>> levels;
   std::map<int, LevelPlan> plans;
-  DevBuf x_stage, y_stage, ybuf, wt, z;
+  DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
@@ -241,7 +246,7 @@ static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStre
   TileParams q = p;
   q.tile_base = tile_base;
   dim3 grid(n_tiles, (p.nr + BM - 1) / BM);
-  const int kind = tile_kernel_kind();
+  const int kind = (p.pair_out && tile_kernel_kind() == 2) ? 1 : tile_kernel_kind();
   if (p.op_rows) {
     if (kind == 2) launch_sync<BM, BN, WM, WN, true>(q, grid, s);
     else if (kind == 1) launch_ws<BM, BN, WM, WN, 16, 5, true>(q, grid, s);
@@ -499,6 +504,18 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
   LevelPlan lp;
   try {
     lp.hp = build_plan_csr(n_targets, tgt, off, src, codes, dc, key, n_rows);
+    const double slots = double(lp.hp.n_entries()) * kBN;
+    lp.target_fill = slots > 0 ? double(lp.hp.n_pairs) * dc / slots : 1.0;
+    const char* m = getenv("CFM_PLAN_MODE");
+    const bool force_pair = m && !strcmp(m, "pair");
+    const bool force_target = m && !strcmp(m, "target");
+    if (force_pair || (!force_target && lp.target_fill < 0.6)) {
+      lp.hp = build_plan_pairs(n_targets, tgt, off, src, codes, dc, key, n_rows, 16, lp.red);
+      lp.mode = 1;
+      upload(lp.r_tgt, lp.red.tgt);
+      upload(lp.r_off, lp.red.off);
+      upload(lp.r_frow, lp.red.frow);
+    }
   } catch (const PlanError& e) {
     throw Error(e.code == 2 ? CFM_ERR_PRECOMPUTE : CFM_ERR_VALUE, e.what());
   }
@@ -541,6 +558,16 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
 // ------------------------------------------------------------------ apply
 static void ensure(DevBuf& b, size_t bytes) { b.alloc(std::max<size_t>(bytes, 16)); }
 
+static int64_t launch_reduce(const LevelPlan& lp, const double* F, long long f_ld, double* y, long long y_ld, int len,
+                             double scale, cudaStream_t s) {
+  const int64_t nt = int64_t(lp.red.tgt.size());
+  if (nt == 0) return 0;
+  k_pair_reduce<<<unsigned(nt), 128, 0, s>>>(F, f_ld, lp.r_tgt.as<long long>(), lp.r_off.as<long long>(),
+                                             lp.r_frow.as<int>(), nt, y, y_ld, len, scale, 1);
+  CUDA_CHECK(cudaGetLastError());
+  return 1;
+}
+
 static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, double* d_y, cudaStream_t s) {
   Group& g = group_for_level(h, level);
   const double scale = h->levels[level].second;
@@ -559,6 +586,14 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     fill_ops(p, g.dense, g.main);
     fill_plan(p, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src, lp.hp.n_tiles);
     p.x = d_x; p.x_ld = row_ld; p.x_dc = dc;
+    if (lp.mode == 1) {
+      ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
+      p.y = h->fbuf.as<double>(); p.y_ld = row_ld; p.y_dc = dc;
+      p.scale = 1.0; p.accumulate = 0; p.pair_out = 1;
+      launches += launch_tiles(p, lp.hp.n_tiles, s);
+      launches += launch_reduce(lp, h->fbuf.as<double>(), row_ld, d_y, row_ld, int(row_ld), scale, s);
+      return launches;
+    }
     p.y = d_y; p.y_ld = row_ld; p.y_dc = dc;
     p.scale = scale; p.accumulate = 1;
     launches += launch_tiles(p, lp.hp.n_tiles, s);
@@ -570,6 +605,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     const int ldy = g.right_h.rows;  // rmax * f
     const size_t max_slots = std::max<size_t>(kBN, (size_t(1) << 30) / (sizeof(double) * std::max(ldy, 1)));
     const std::vector<int>& toff = lp.hp.tile_off;
+    if (lp.mode == 1) ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
     int64_t t0 = 0;
     while (t0 < lp.hp.n_tiles) {
       int64_t t1 = t0 + 1;
@@ -591,12 +627,18 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
         fill_ops(p2, g.left, g.main);
         fill_plan(p2, lp.tile_col, lp.tile_off, lp.entry_code, lp.slot_ids, lp.hp.n_tiles);
         p2.x = ybase; p2.x_ld = ldy; p2.x_dc = 1;
-        p2.y = d_y; p2.y_ld = row_ld; p2.y_dc = dc;
-        p2.scale = scale; p2.accumulate = 1;
+        if (lp.mode == 1) {
+          p2.y = h->fbuf.as<double>(); p2.y_ld = row_ld; p2.y_dc = dc;
+          p2.scale = 1.0; p2.accumulate = 0; p2.pair_out = 1;
+        } else {
+          p2.y = d_y; p2.y_ld = row_ld; p2.y_dc = dc;
+          p2.scale = scale; p2.accumulate = 1;
+        }
         launches += launch_range(p2, t0, t1 - t0, s);
       }
       t0 = t1;
     }
+    if (lp.mode == 1) launches += launch_reduce(lp, h->fbuf.as<double>(), row_ld, d_y, row_ld, int(row_ld), scale, s);
     return launches;
   }
 
@@ -618,14 +660,24 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     q.scale = 1.0; q.accumulate = 0;
     launches += launch_tiles(q, lp.src_plan.n_tiles, s);
   }
+  // stage 2 output: Z directly (target tiles) or per-pair rows Fz (pair mode)
+  double* z_out = h->z.as<double>();
+  int z_pair = 0, z_acc = 1;
+  if (lp.mode == 1) {
+    ensure(h->fzbuf, size_t(lp.red.n_frows) * z_ld * sizeof(double));
+    CUDA_CHECK(cudaMemsetAsync(h->fzbuf.p, 0, size_t(lp.red.n_frows) * z_ld * sizeof(double), s));
+    z_out = h->fzbuf.as<double>();
+    z_pair = 1;
+    z_acc = 0;
+  }
   // stage 2a: dense cores Z[tgt] += C_t W~[src]
   if (g.any_dense_core) {
     TileParams q = p;
     fill_ops(q, g.dense, g.main);
     fill_plan(q, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src, lp.hp.n_tiles);
     q.x = h->wt.as<double>(); q.x_ld = wt_ld; q.x_dc = dc;
-    q.y = h->z.as<double>(); q.y_ld = z_ld; q.y_dc = dc;
-    q.scale = 1.0; q.accumulate = 1;
+    q.y = z_out; q.y_ld = z_ld; q.y_dc = dc;
+    q.scale = 1.0; q.accumulate = z_acc; q.pair_out = z_pair;
     launches += launch_tiles(q, lp.hp.n_tiles, s);
   }
   // stage 2b: factored cores Z[tgt] += L_t (R_t^H W~[src])
@@ -643,10 +695,11 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     fill_ops(p2, g.left, g.sa_fac2);
     fill_plan(p2, lp.tile_col, lp.tile_off, lp.entry_code, lp.slot_ids, lp.hp.n_tiles);
     p2.x = h->ybuf.as<double>(); p2.x_ld = ldy; p2.x_dc = 1;
-    p2.y = h->z.as<double>(); p2.y_ld = z_ld; p2.y_dc = dc;
-    p2.scale = 1.0; p2.accumulate = 1;
+    p2.y = z_out; p2.y_ld = z_ld; p2.y_dc = dc;
+    p2.scale = 1.0; p2.accumulate = z_acc; p2.pair_out = z_pair;
     launches += launch_tiles(p2, lp.hp.n_tiles, s);
   }
+  if (lp.mode == 1) launches += launch_reduce(lp, z_out, z_ld, h->z.as<double>(), z_ld, int(z_ld), 1.0, s);
   // stage 3: locals[tgt] += scale * U Z[tgt]
   {
     TileParams q = p;
@@ -736,7 +789,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
   int64_t launches = 0;
   bool all_dense = true;
-  for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
+  for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense && L.lp->mode == 0;
   if (all_dense) {
     std::vector<TileParams> segs;
     std::vector<int64_t> counts;
@@ -1158,6 +1211,17 @@ int cfm_plan_stats(cfm_handler* h, int level, int64_t* n_tiles, int64_t* n_entri
     if (n_slots) *n_slots = lp.hp.n_entries() * kBN / lp.dc;
     if (n_targets) *n_targets = int64_t(lp.targets.size());
     if (n_sources) *n_sources = int64_t(lp.sources.size());
+  });
+}
+
+int cfm_plan_info(cfm_handler* h, int level, int* mode, double* target_fill) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->plans.find(level);
+    if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(level));
+    if (mode) *mode = it->second.mode;
+    if (target_fill) *target_fill = it->second.target_fill;
   });
 }
 

@@ -211,6 +211,91 @@ inline HostPlan build_plan_csr(int64_t n_targets, const int64_t* tgt, const int6
   return plan;
 }
 
+// Pair-mode plan (sparse trees): entries are runs of up to BN/dc pairs that
+// share one transfer vector, whatever their targets; `entries_per_tile`
+// consecutive entries form a tile (one CTA).  Entry e, slot s produces result
+// row e*(BN/dc)+s; red_* is the per-target CSR of those rows (rows ascending)
+// for the ordered reduction.
+struct PairReduce {
+  std::vector<int64_t> tgt, off;
+  std::vector<int> frow;
+  int64_t n_frows = 0;
+};
+
+inline HostPlan build_plan_pairs(int64_t n_targets, const int64_t* tgt, const int64_t* off, const int64_t* src,
+                                 const int16_t* codes, int dc, const std::array<int, kNumCodes>& opkey,
+                                 int64_t n_rows, int entries_per_tile, PairReduce& red) {
+  HostPlan plan;
+  plan.dc = dc;
+  const int tpt = kBN / dc;
+  struct P {
+    int key, code;
+    int64_t row, src;
+  };
+  std::vector<P> pairs;
+  for (int64_t i = 0; i < n_targets; ++i) {
+    if (tgt[i] < 0 || tgt[i] >= n_rows) throw PlanError(1, "target row out of range");
+    if (off[i + 1] < off[i]) throw PlanError(1, "offsets must be non-decreasing");
+    for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+      const int c = codes[q];
+      if (c < 0 || c >= kNumCodes) throw PlanError(1, "transfer vector outside [-3,3]^3");
+      if (opkey[c] < 0) {
+        int t0, t1, t2;
+        tcode_decode(c, t0, t1, t2);
+        throw PlanError(2, "no operator for transfer vector (" + std::to_string(t0) + ", " + std::to_string(t1) +
+                               ", " + std::to_string(t2) + ")");
+      }
+      if (src[q] < 0 || src[q] >= n_rows) throw PlanError(1, "source row out of range");
+      pairs.push_back({opkey[c], c, tgt[i], src[q]});
+      plan.code_count[c] += 1;
+    }
+  }
+  plan.n_pairs = int64_t(pairs.size());
+  std::stable_sort(pairs.begin(), pairs.end(), [](const P& a, const P& b) {
+    if (a.key != b.key) return a.key < b.key;
+    if (a.code != b.code) return a.code < b.code;
+    return a.row < b.row;
+  });
+  std::vector<std::pair<int64_t, int>> tf;  // (target row, result row)
+  tf.reserve(pairs.size());
+  for (size_t i = 0; i < pairs.size();) {
+    size_t j = i;
+    while (j < pairs.size() && pairs[j].code == pairs[i].code) ++j;
+    for (size_t a = i; a < j; a += tpt) {
+      const int64_t e = int64_t(plan.entry_code.size());
+      plan.entry_code.push_back(pairs[i].code);
+      plan.entry_src.resize(size_t(e + 1) * kBN, -1);
+      for (size_t b = a; b < std::min(j, a + tpt); ++b) {
+        const int sl = int(b - a);
+        for (int q = 0; q < dc; ++q) plan.entry_src[size_t(e) * kBN + sl * dc + q] = int(pairs[b].src * dc + q);
+        tf.emplace_back(pairs[b].row, int(e * tpt + sl));
+      }
+    }
+    i = j;
+  }
+  const int64_t E = plan.n_entries();
+  if (E * tpt > INT32_MAX) throw PlanError(1, "pair plan too large");
+  plan.n_tiles = (E + entries_per_tile - 1) / entries_per_tile;
+  plan.tile_off.resize(plan.n_tiles + 1);
+  for (int64_t t = 0; t <= plan.n_tiles; ++t) plan.tile_off[t] = int(std::min<int64_t>(t * entries_per_tile, E));
+  plan.tile_col.assign(size_t(plan.n_tiles) * kBN, -1);
+  std::sort(tf.begin(), tf.end());
+  red.n_frows = E * tpt;
+  red.tgt.clear();
+  red.off.assign(1, 0);
+  red.frow.resize(tf.size());
+  for (size_t i = 0; i < tf.size(); ++i) {
+    if (i == 0 || tf[i].first != tf[i - 1].first) {
+      if (i) red.off.push_back(int64_t(i));
+      red.tgt.push_back(tf[i].first);
+    }
+    red.frow[i] = tf[i].second;
+  }
+  red.off.push_back(int64_t(tf.size()));
+  if (tf.empty()) red.off.assign(1, 0);
+  return plan;
+}
+
 // One entry per tile over a list of virtual ids: used for the shared-basis
 // per-source (m2l.py:378) and per-target (m2l.py:393) transforms, where the
 // "source" of output column v is row v of the input.

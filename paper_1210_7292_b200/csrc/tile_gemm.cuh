@@ -57,6 +57,7 @@ struct TileParams {
   int y_dc;
   double scale;
   int accumulate;
+  int pair_out;  // 1: write each entry's result to y rows (e * BN + c) when the entry ends
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {

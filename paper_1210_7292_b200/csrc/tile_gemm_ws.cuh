@@ -265,8 +265,34 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
     }
+    if (p.pair_out) {
+      // pair mode: this entry's 64 columns are 64 distinct (target, source)
+      // pairs; write their results to rows e*BN + c (segment-reduced per target later)
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) {
+        const int row = r0 + wm * WTM + mi * 8 + g;
+#pragma unroll
+        for (int nj = 0; nj < NTL; ++nj) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = wn * WTN + nj * 8 + 2 * tg + h;
+            if (row < p.nr && __ldg(p.entry_src + (long long)e * BN + c) >= 0) {
+              const long long v = (long long)e * BN + c;
+              double* dst = p.y + (v / p.y_dc) * p.y_ld + (v % p.y_dc) + (long long)p.y_dc * row;
+              const double val = p.scale * acc[mi][nj][h];
+              if (p.accumulate)
+                *dst += val;
+              else
+                *dst = val;
+            }
+            acc[mi][nj][h] = 0.0;
+          }
+        }
+      }
+    }
     e = next_live(e + 1, d);
   }
+  if (p.pair_out) return;
 
   // ---------------- epilogue: ordered, atomic-free write ----------------
   if (e_begin == e_end && p.accumulate) return;

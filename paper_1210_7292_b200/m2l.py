@@ -486,7 +486,12 @@ class B200M2LHandler:
         vals = [ctypes.c_int64() for _ in range(6)]
         self._check(self._lib.cfm_plan_stats(self._h, int(level), *[ctypes.byref(v) for v in vals]))
         names = ("tiles", "entries", "pairs", "slots", "targets", "sources")
-        return {k: int(v.value) for k, v in zip(names, vals)}
+        out = {k: int(v.value) for k, v in zip(names, vals)}
+        mode, fill = ctypes.c_int(), ctypes.c_double()
+        self._check(self._lib.cfm_plan_info(self._h, int(level), ctypes.byref(mode), ctypes.byref(fill)))
+        out["mode"] = "pair" if mode.value == 1 else "target"
+        out["target_fill"] = fill.value
+        return out
 
     def apply_planned(self, level: int, mpoles, locals_out) -> int:
         """Apply a level planned with :meth:`plan_level_cells` (same flops/accounting)."""

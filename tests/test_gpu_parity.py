@@ -315,3 +315,33 @@ def test_apply_levels_equals_per_level(torch_cuda, golden, variant):
     h.apply_levels(host)
     for lvl in levels:
         assert np.array_equal(host[lvl][1], ref[lvl].cpu().numpy())
+
+
+PAIR_CASES = [("cfg1", v) for v in ("na", "nablk", "iablk", "sa", "sarcmp")] + \
+    [("helm", v) for v in ("nablk", "iablk", "sarcmp")] + [("lapcplx", v) for v in ("nablk", "iablk", "sa")]
+
+
+@pytest.mark.parametrize("case,variant", PAIR_CASES)
+def test_pair_mode_matches_reference(torch_cuda, golden, case, variant, monkeypatch):
+    """Pair-mode plans (per-transfer-vector entries + ordered per-target
+    reduction, used for sparse trees) give the reference locals too."""
+    monkeypatch.setenv("CFM_PLAN_MODE", "pair")
+    g = golden(case)
+    h, levels = _handler(g, variant)
+    for lvl in levels:
+        mp = _mpoles(g, lvl, case)
+        tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+        loc = np.zeros(mp.shape, dtype=np.result_type(h.kernel.dtype, mp.dtype))
+        fl = h.apply_level_csr(lvl, tgt, off, src, t, mp, loc)
+        assert h.plan_stats(lvl)["mode"] == "pair"
+        err = O.rel_l2(loc, g[f"locals_{variant}_{lvl}"])
+        assert err <= TOL[variant], (case, variant, lvl, err)
+        assert fl == int(g[f"flops_{variant}_{lvl}"])
+
+
+def test_sparse_level_picks_pair_mode(torch_cuda, golden):
+    g = golden("sphere9")
+    h, levels = _handler(g, "nablk")
+    lvl = levels[-1]
+    st = h.plan_level_cells(lvl, g[f"cells_{lvl}"])
+    assert st["mode"] == "pair" and st["target_fill"] < 0.6
