@@ -301,24 +301,48 @@ def run_b200(args):
     h.precompute({l: full for l in levels}, widths)
     t_pre = time.perf_counter() - t_pre
 
-    # shard target rows across ranks (contiguous ranges in lexicographic order);
-    # every rank holds the level's multipoles (replicated inputs, no exchange).
-    stats = {}
+    # N > 1: each rank owns a contiguous Morton range of every level's targets
+    # (paper_1210_7292_b200.distributed); the source-multipole halo is exchanged
+    # with one NCCL all_to_all per level inside every timed step.
+    stats, halos, owned = {}, {}, {}
     for lvl in levels:
         c = cells[lvl].astype(np.int32)
-        st = h.plan_level_cells(lvl, c)
+        if ws == 1:
+            stats[lvl] = h.plan_level_cells(lvl, c)
+            owned[lvl] = None
+            continue
+        from paper_1210_7292_b200.distributed import PreparedHalo, build_halo, partition_rows
+
+        parts = partition_rows(c, ws)
+        owned[lvl] = parts[rank]
+        st, srcs = h.plan_level_cells_subset(lvl, c, parts[rank])
+        gathered = [None] * ws
+        dist.all_gather_object(gathered, srcs)
+        halos[lvl] = PreparedHalo(build_halo(parts, srcs, gathered, rank), dev)
         stats[lvl] = st
-    pairs_total = sum(st["pairs"] for st in stats.values())
+    pairs_local = sum(st["pairs"] for st in stats.values())
+    pairs_total = pairs_local
+    if ws > 1:
+        t = torch.tensor([pairs_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        pairs_total = int(t.item())
 
     gen = torch.Generator(device=dev).manual_seed(11)
     mp = {l: torch.rand((len(cells[l]), size), dtype=dt, device=dev, generator=gen) * 2 - (1 + 1j if cplx else 1)
           for l in levels}
+    if ws > 1:  # a rank starts with its own rows only; the halo arrives through the exchange
+        for l in levels:
+            keep = torch.zeros(len(cells[l]), dtype=torch.bool, device=dev)
+            keep[torch.as_tensor(owned[l], device=dev)] = True
+            mp[l][~keep] = 0
     loc = {l: torch.zeros_like(mp[l]) for l in levels}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     step_flops = [0]
 
     def step():
+        for l in halos:
+            halos[l].exchange(dist, mp[l])
         step_flops[0] = h.apply_levels({l: (mp[l], loc[l]) for l in levels})
         return h.last_apply_stats()[1]
 
@@ -363,17 +387,37 @@ def run_b200(args):
         h_mp[l].copy_(mp[l].cpu())
     np_mp = {l: h_mp[l].numpy() for l in levels}
     np_loc = {l: h_loc[l].numpy() for l in levels}
+    d_mp = {l: torch.empty_like(mp[l]) for l in levels}
+
+    def e2e_step():
+        if ws == 1:
+            h.apply_levels({l: (np_mp[l], np_loc[l]) for l in levels})
+            return
+        for l in levels:  # host -> device, halo exchange, apply into host locals
+            d_mp[l].copy_(h_mp[l], non_blocking=True)
+            halos[l].exchange(dist, d_mp[l])
+        h.apply_levels({l: (d_mp[l], loc[l]) for l in levels})
+        for l in levels:
+            h_loc[l].copy_(loc[l], non_blocking=True)
+        torch.cuda.synchronize()
+
     for _ in range(max(1, args.warmup // 2)):
-        h.apply_levels({l: (np_mp[l], np_loc[l]) for l in levels})
+        e2e_step()
     torch.cuda.synchronize()
     e2e_steps = max(1, args.steps)
+    if ws > 1:
+        dist.barrier()
     tic = time.perf_counter()
     for _ in range(e2e_steps):
-        h.apply_levels({l: (np_mp[l], np_loc[l]) for l in levels})
+        e2e_step()
     e2e_s = (time.perf_counter() - tic) / e2e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
     bytes_lvl = {l: mp[l].numel() * mp[l].element_size() for l in levels}
-    h2d = sum(2 * b for b in bytes_lvl.values())  # multipoles + locals (accumulated in place)
-    d2h = sum(bytes_lvl.values())
+    h2d = sum(2 * b for b in bytes_lvl.values()) * ws  # multipoles + locals (accumulated in place), all ranks
+    d2h = sum(bytes_lvl.values()) * ws
 
     # roofline of the dominant kernel: the single multi-level tile_gemm launch of a step
     peak, peak_src = fp64_peak()
@@ -405,12 +449,15 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
             "config": {"workload": f"{cfg}: N={n:.0e} {geom}, height {depth + 1} (levels {levels[0]}-{deep}), "
                                    f"l={order}, {'Helmholtz k=8pi complex128' if cplx else 'Laplace'}, variant {variant}"
                                    f", eps={eps:g}", "pairs_per_step": pairs_total, "precompute_s": t_pre,
                        "levels": {str(l): stats[l]["pairs"] for l in levels},
-                       "tile_fill": pairs_total / max(slots, 1),
+                       "tile_fill": pairs_local / max(slots, 1),
+                       "plan_modes": {str(l): stats[l].get("mode") for l in levels},
+                       "parallelism": f"{ws} GPU(s): targets sharded by Morton range, NCCL halo all_to_all per level"
+                                      if ws > 1 else "1 GPU",
                        "l2": "flushed between steps (256 MB write)", "multipoles": "seeded U[-1,1]"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,

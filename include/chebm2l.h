@@ -132,6 +132,13 @@ int cfm_plan_level_cells(cfm_handler* h, int level, int64_t n_cells, const int32
 int cfm_plan_level_csr(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt,
                        const int64_t* off, const int64_t* src, const int8_t* t,
                        int data_complex, int64_t n_rows, int64_t* pair_count_out);
+/* As cfm_plan_level_cells, but only for the targets in target_rows (a
+ * multi-GPU rank's Morton range of the level).  Optionally returns the sorted
+ * source rows those targets read (sources_out must hold n_cells entries): the
+ * rows a rank must own or receive in the halo exchange. */
+int cfm_plan_level_cells_subset(cfm_handler* h, int level, int64_t n_cells, const int32_t* ijk, int64_t n_targets,
+                                const int64_t* target_rows, int data_complex, void* stream, int64_t* pair_count_out,
+                                int64_t* n_sources_out, int64_t* sources_out);
 int cfm_apply_planned(cfm_handler* h, int level, const double* mpoles, int64_t n_rows,
                       double* locals, void* stream);
 

@@ -37,6 +37,7 @@ EXPORTS = (
     "cfm_apply_level_csr",
     "cfm_plan_level_cells",
     "cfm_plan_level_csr",
+    "cfm_plan_level_cells_subset",
     "cfm_apply_planned",
     "cfm_apply_levels",
     "cfm_plan_stats",
@@ -63,6 +64,7 @@ _SIGS = {
     "cfm_apply_level_csr": ([_P, _I, _I64, _P, _P, _P, _P, _I, _P, _I64, _P, _P, _P], _I),
     "cfm_plan_level_cells": ([_P, _I, _I64, _P, _I, _P, _P], _I),
     "cfm_plan_level_csr": ([_P, _I, _I64, _P, _P, _P, _P, _I, _I64, _P], _I),
+    "cfm_plan_level_cells_subset": ([_P, _I, _I64, _P, _I64, _P, _I, _P, _P, _P, _P], _I),
     "cfm_apply_planned": ([_P, _I, _P, _I64, _P, _P], _I),
     "cfm_apply_levels": ([_P, _I, _P, _P, _P, _P, _P], _I),
     "cfm_plan_stats": ([_P, _I, _P, _P, _P, _P, _P, _P], _I),

@@ -1197,6 +1197,45 @@ int cfm_apply_levels(cfm_handler* h, int n_levels, const int* levels, const doub
   });
 }
 
+int cfm_plan_level_cells_subset(cfm_handler* h, int level, int64_t n_cells, const int32_t* ijk, int64_t n_targets,
+                                const int64_t* target_rows, int data_complex, void* stream, int64_t* pair_count_out,
+                                int64_t* n_sources_out, int64_t* sources_out) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    if (n_targets < 0 || (n_targets && !target_rows)) throw Error(CFM_ERR_VALUE, "bad target rows");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_CHECK(cudaSetDevice(h->device));
+    cudaStream_t s = pick_stream(h, stream);
+    DeviceLists dl;
+    classify_device(level, n_cells, ijk, s, dl, /*want_codes=*/true);
+    std::vector<int32_t> hsrc(dl.total);
+    std::vector<int16_t> hcode(dl.total);
+    if (dl.total) {
+      CUDA_CHECK(cudaMemcpyAsync(hsrc.data(), dl.src.p, size_t(dl.total) * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaMemcpyAsync(hcode.data(), dl.code.p, size_t(dl.total) * 2, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    // restrict the CSR to the requested targets (this rank's Morton range)
+    std::vector<int64_t> tgt, off(1, 0), src64;
+    std::vector<int16_t> codes;
+    for (int64_t k = 0; k < n_targets; ++k) {
+      const int64_t r = target_rows[k];
+      if (r < 0 || r >= n_cells) throw Error(CFM_ERR_VALUE, "target row out of range");
+      tgt.push_back(r);
+      for (int64_t q = dl.h_off[r]; q < dl.h_off[r + 1]; ++q) {
+        src64.push_back(hsrc[q]);
+        codes.push_back(hcode[q]);
+      }
+      off.push_back(int64_t(src64.size()));
+    }
+    LevelPlan& lp = make_plan(h, level, int64_t(tgt.size()), tgt.data(), off.data(), src64.data(), codes.data(),
+                              data_complex, n_cells);
+    if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
+    if (n_sources_out) *n_sources_out = int64_t(lp.sources.size());
+    if (sources_out) std::copy(lp.sources.begin(), lp.sources.end(), sources_out);
+  });
+}
+
 int cfm_plan_stats(cfm_handler* h, int level, int64_t* n_tiles, int64_t* n_entries, int64_t* n_pairs,
                    int64_t* n_slots, int64_t* n_targets, int64_t* n_sources) {
   return guarded([&] {

@@ -1,0 +1,161 @@
+"""Multi-GPU M2L: targets sharded by contiguous Morton ranges, NCCL halo.
+
+The reference has no distributed execution; its only
+parallelism is disjoint target chunks over threads sharing the multipole
+array (engine.py:145-155).  The B200 build scales the same way across GPUs
+(SURVEY.md §8e): every level's occupied cells are ordered by Morton key and
+split into one contiguous range per rank; a rank computes the locals of its
+own targets only (owners write them, no reduction), and the one exchange step
+per level is the source-multipole halo — rows a rank's far lists read but
+another rank owns — moved with one ``all_to_all_single`` (NCCL over NVLink on
+GPUs, gloo on CPU in the tests).  Range boundaries are aligned to sibling
+groups (multiples of 8 in Morton order) so the halo is the 2-cell shell of
+SURVEY.md §8e.
+
+One process per GPU; ``torch.distributed`` provides the plumbing.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def morton_keys(ijk) -> np.ndarray:
+    """3-D Morton (Z-order) keys, x in the most significant bit of each triple."""
+    ijk = np.asarray(ijk, dtype=np.int64).reshape(-1, 3)
+    key = np.zeros(len(ijk), dtype=np.int64)
+    for b in range(21):
+        for a in range(3):
+            key |= ((ijk[:, a] >> b) & 1) << (3 * b + (2 - a))
+    return key
+
+
+def partition_rows(cells_ijk, world: int) -> list[np.ndarray]:
+    """Split a level's rows (lexicographic order = reference row order) into
+    `world` contiguous Morton ranges of ~equal size, boundaries on sibling
+    groups.  Returns the sorted row indices owned by each rank."""
+    cells = np.asarray(cells_ijk, dtype=np.int64).reshape(-1, 3)
+    n = len(cells)
+    order = np.argsort(morton_keys(cells), kind="stable")
+    parent = morton_keys(cells[order] >> 1)
+    # candidate cut points: starts of sibling groups (parent key changes)
+    starts = np.concatenate([[0], np.nonzero(np.diff(parent))[0] + 1, [n]])
+    out = []
+    prev = 0
+    for r in range(1, world + 1):
+        target = (n * r) // world
+        if r == world:
+            cut = n
+        else:
+            cut = int(starts[np.searchsorted(starts, target)]) if n else 0
+            cut = max(cut, prev)
+        out.append(np.sort(order[prev:cut]))
+        prev = cut
+    return out
+
+
+@dataclass
+class HaloPlan:
+    """Rows this rank sends to / receives from every peer (sorted per peer)."""
+
+    send_rows: list  # per peer: np.ndarray of rows owned here, needed there
+    recv_rows: list  # per peer: np.ndarray of rows owned there, needed here
+
+    @property
+    def send_counts(self):
+        return [len(r) for r in self.send_rows]
+
+    @property
+    def recv_counts(self):
+        return [len(r) for r in self.recv_rows]
+
+
+def build_halo(owned_by_rank: list, needed_here: np.ndarray, needed_by_rank: list, rank: int) -> HaloPlan:
+    """Halo plan from every rank's owned rows and every rank's needed source rows."""
+    world = len(owned_by_rank)
+    n = max([int(o.max()) + 1 for o in owned_by_rank if len(o)] + [int(x.max()) + 1 for x in needed_by_rank if len(x)]
+            + [1])
+    owner = np.full(n, -1, dtype=np.int64)
+    for r, rows in enumerate(owned_by_rank):
+        owner[rows] = r
+    recv = []
+    need = np.asarray(needed_here, dtype=np.int64)
+    for q in range(world):
+        recv.append(np.sort(need[(owner[need] == q)]) if q != rank else np.zeros(0, np.int64))
+    send = []
+    mine = owner == rank
+    for q in range(world):
+        if q == rank:
+            send.append(np.zeros(0, np.int64))
+            continue
+        nq = np.asarray(needed_by_rank[q], dtype=np.int64)
+        send.append(np.sort(nq[mine[nq]]))
+    return HaloPlan(send, recv)
+
+
+def setup_level(dist, cells_ijk, needed_fn):
+    """Collective setup for one level.
+
+    needed_fn(owned_rows) -> sorted source rows read by those targets
+    (e.g. the handler's ``plan_level_cells_subset``).  Returns
+    (owned_rows, halo_plan)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    parts = partition_rows(cells_ijk, world)
+    owned = parts[rank]
+    needed = np.asarray(needed_fn(owned), dtype=np.int64)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, needed)
+    return owned, build_halo(parts, needed, gathered, rank)
+
+
+def exchange_halo(dist, mpoles, halo: HaloPlan, group=None):
+    """Fill the halo rows of this rank's (full-size) multipole array from
+    their owners: one all_to_all_single of packed rows (NCCL on CUDA tensors).
+    Rows owned here are left untouched."""
+    import torch
+
+    dev = mpoles.device
+    send_idx = torch.as_tensor(np.concatenate(halo.send_rows) if halo.send_rows else np.zeros(0, np.int64),
+                               device=dev)
+    recv_idx = torch.as_tensor(np.concatenate(halo.recv_rows) if halo.recv_rows else np.zeros(0, np.int64),
+                               device=dev)
+    send = mpoles.index_select(0, send_idx).contiguous()
+    recv = torch.empty((len(recv_idx),) + tuple(mpoles.shape[1:]), dtype=mpoles.dtype, device=dev)
+    if mpoles.is_complex():  # NCCL/gloo all_to_all on real views
+        dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), halo.recv_counts,
+                               halo.send_counts, group=group)
+    else:
+        dist.all_to_all_single(recv, send, halo.recv_counts, halo.send_counts, group=group)
+    if len(recv_idx):
+        mpoles.index_copy_(0, recv_idx, recv)
+    return mpoles
+
+
+class PreparedHalo:
+    """Device-resident index tensors of a HaloPlan (built once, reused every step)."""
+
+    def __init__(self, halo: HaloPlan, device):
+        import torch
+
+        self.halo = halo
+        cat = lambda rows: np.concatenate(rows) if rows else np.zeros(0, np.int64)  # noqa: E731
+        self.send_idx = torch.as_tensor(cat(halo.send_rows), device=device)
+        self.recv_idx = torch.as_tensor(cat(halo.recv_rows), device=device)
+        self.send_counts = halo.send_counts
+        self.recv_counts = halo.recv_counts
+
+    def exchange(self, dist, mpoles, group=None):
+        import torch
+
+        send = mpoles.index_select(0, self.send_idx)
+        recv = torch.empty((len(self.recv_idx),) + tuple(mpoles.shape[1:]), dtype=mpoles.dtype, device=mpoles.device)
+        if mpoles.is_complex():
+            dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), self.recv_counts,
+                                   self.send_counts, group=group)
+        else:
+            dist.all_to_all_single(recv, send, self.recv_counts, self.send_counts, group=group)
+        if len(self.recv_idx):
+            mpoles.index_copy_(0, self.recv_idx, recv)
+        return mpoles

@@ -482,6 +482,29 @@ class B200M2LHandler:
         self._planned[level] = stats
         return stats
 
+    def plan_level_cells_subset(self, level: int, cells_ijk, target_rows, complex_data: bool | None = None):
+        """Plan only ``target_rows`` of a level (a multi-GPU rank's range).
+        Returns (stats, source_rows) where source_rows are the rows the planned
+        targets read (owned rows plus the halo to receive)."""
+        self._level_key(level)
+        cells = np.ascontiguousarray(cells_ijk, dtype=np.int32).reshape(-1, 3)
+        rows = np.ascontiguousarray(target_rows, dtype=np.int64)
+        if complex_data is None:
+            complex_data = self._op_complex
+        counts = np.zeros(343, np.int64)
+        nsrc = ctypes.c_int64()
+        srcs = np.zeros(len(cells), np.int64)
+        with self._lock:
+            self._check(self._lib.cfm_plan_level_cells_subset(
+                self._h, int(level), len(cells), cells.ctypes.data, len(rows), rows.ctypes.data,
+                int(bool(complex_data)), None, counts.ctypes.data, ctypes.byref(nsrc), srcs.ctypes.data))
+        stats = self.plan_stats(level)
+        stats["counts"] = counts
+        stats["n_rows"] = len(cells)
+        stats["complex"] = bool(complex_data)
+        self._planned[level] = stats
+        return stats, srcs[: nsrc.value].copy()
+
     def plan_stats(self, level: int) -> dict:
         vals = [ctypes.c_int64() for _ in range(6)]
         self._check(self._lib.cfm_plan_stats(self._h, int(level), *[ctypes.byref(v) for v in vals]))

@@ -345,3 +345,33 @@ def test_sparse_level_picks_pair_mode(torch_cuda, golden):
     lvl = levels[-1]
     st = h.plan_level_cells(lvl, g[f"cells_{lvl}"])
     assert st["mode"] == "pair" and st["target_fill"] < 0.6
+
+
+@pytest.mark.parametrize("mode", ["target", "pair"])
+def test_sharded_plans_equal_single_gpu(torch_cuda, golden, mode, monkeypatch):
+    """Two Morton-range shards planned with plan_level_cells_subset, each
+    reading only its own rows plus its halo, reproduce the single-plan locals
+    bitwise (per-target accumulation order does not depend on the partition)."""
+    torch = torch_cuda
+    from paper_1210_7292_b200.distributed import partition_rows
+
+    monkeypatch.setenv("CFM_PLAN_MODE", mode)
+    g = golden("sphere_lists")
+    lvl = 4
+    cells = g[f"cells_{lvl}"]
+    mp = torch.from_numpy(_mpoles(g, lvl, "sphere_lists")).cuda()
+    h, _ = _handler(g, "nablk")
+    h.plan_level_cells(lvl, cells)
+    ref = torch.zeros_like(mp)
+    h.apply_planned(lvl, mp, ref)
+    out = torch.zeros_like(mp)
+    for part in partition_rows(cells, 2):
+        hs, _ = _handler(g, "nablk")
+        st, srcs = hs.plan_level_cells_subset(lvl, cells, part)
+        local = torch.zeros_like(mp)
+        local[torch.as_tensor(srcs, device="cuda")] = mp[torch.as_tensor(srcs, device="cuda")]
+        loc = torch.zeros_like(mp)
+        hs.apply_planned(lvl, local, loc)
+        rows = torch.as_tensor(part, device="cuda")
+        out[rows] = loc[rows]
+    assert torch.equal(out, ref)
