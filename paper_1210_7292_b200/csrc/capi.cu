@@ -89,6 +89,7 @@ static void upload(DevBuf& d, const std::vector<T>& h) {
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 constexpr int kKC = 32;
+constexpr int kPass1Run = 16;  // entries per CTA in low-rank pass 1 (per-entry outputs)
 
 // ------------------------------------------------------------------ code maps
 struct CodeMap {
@@ -167,6 +168,9 @@ struct LevelPlan {
   DevBuf r_tgt, r_off, r_frow;
   DevBuf tile_col, tile_off, entry_code, entry_src;
   DevBuf slot_ids, iota;  // low-rank: per-entry slots
+  DevBuf runs;            // low-rank pass 1: tiles = runs of kPass1Run consecutive entries
+  int64_t n_runs = 0;
+  std::vector<int64_t> run_start;  // per target tile: first run
   // shared basis
   std::vector<int64_t> sources, targets;
   HostPlan src_plan, tgt_plan;
@@ -531,6 +535,18 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     std::iota(iota.begin(), iota.end(), 0);
     upload(lp.slot_ids, slots);
     upload(lp.iota, iota);
+    // runs of <= kPass1Run entries that never cross a tile boundary, so a tile
+    // range [t0, t1) maps to the run range [run_start[t0], run_start[t1])
+    std::vector<int> runs;
+    lp.run_start.assign(lp.hp.n_tiles + 1, 0);
+    for (int64_t t = 0; t < lp.hp.n_tiles; ++t) {
+      lp.run_start[t] = int64_t(runs.size());
+      for (int e = lp.hp.tile_off[t]; e < lp.hp.tile_off[t + 1]; e += kPass1Run) runs.push_back(e);
+    }
+    lp.run_start[lp.hp.n_tiles] = int64_t(runs.size());
+    runs.push_back(int(E));
+    lp.n_runs = int64_t(runs.size()) - 1;
+    upload(lp.runs, runs);
   }
   // distinct targets / sources (SA transforms and accounting)
   {
@@ -621,7 +637,10 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
         p1.x = d_x; p1.x_ld = row_ld; p1.x_dc = dc;
         p1.y = ybase; p1.y_ld = ldy; p1.y_dc = 1;
         p1.scale = 1.0; p1.accumulate = 0;
-        launches += launch_range(p1, e0, e1 - e0, s);
+        // runs of up to kPass1Run entries per CTA; each entry's Y written when it ends
+        p1.tile_off = lp.runs.as<int>();
+        p1.pair_out = 1;
+        launches += launch_range(p1, lp.run_start[t0], lp.run_start[t1] - lp.run_start[t0], s);
         // pass 2: acc += left[table] Y  (tiles = target tiles, sources = slots)
         TileParams p2 = p;
         fill_ops(p2, g.left, g.main);
@@ -789,13 +808,25 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
   int64_t launches = 0;
   bool all_dense = true;
-  for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense && L.lp->mode == 0;
+  for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
   if (all_dense) {
+    // one launch: target-mode levels accumulate into locals, pair-mode levels
+    // write per-pair rows into their slice of fbuf, reduced right after
+    size_t f_total = 0;
+    std::vector<size_t> f_off(lv.size(), 0);
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (lv[i].lp->mode != 1) continue;
+      const size_t row_d = size_t(h->n) * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
+      f_off[i] = f_total;
+      f_total += size_t(lv[i].lp->red.n_frows) * row_d;
+    }
+    if (f_total) ensure(h->fbuf, f_total * sizeof(double));
     std::vector<TileParams> segs;
     std::vector<int64_t> counts;
     int nr = -1;
     bool same_shape = true;
-    for (auto& L : lv) {
+    for (size_t i = 0; i < lv.size(); ++i) {
+      auto& L = lv[i];
       Group& g = group_for_level(h, L.level);
       TileParams p{};
       p.rowtab = h->rowtab.as<short>();
@@ -804,9 +835,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       fill_plan(p, L.lp->tile_col, L.lp->tile_off, L.lp->entry_code, L.lp->entry_src, L.lp->hp.n_tiles);
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
-      p.y = L.y; p.y_ld = row_ld; p.y_dc = L.lp->dc;
-      p.scale = h->levels[L.level].second;
-      p.accumulate = 1;
+      if (L.lp->mode == 1) {
+        p.y = h->fbuf.as<double>() + f_off[i]; p.y_ld = row_ld; p.y_dc = L.lp->dc;
+        p.scale = 1.0; p.accumulate = 0; p.pair_out = 1;
+      } else {
+        p.y = L.y; p.y_ld = row_ld; p.y_dc = L.lp->dc;
+        p.scale = h->levels[L.level].second;
+        p.accumulate = 1;
+      }
       if (nr >= 0 && (p.nr != nr)) same_shape = false;
       nr = p.nr;
       segs.push_back(p);
@@ -816,6 +852,12 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       launches += launch_multi(segs, counts, s);
     } else {
       for (size_t i = 0; i < segs.size(); ++i) launches += launch_tiles(segs[i], counts[i], s);
+    }
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (lv[i].lp->mode != 1) continue;
+      const long long row_ld = (long long)h->n * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
+      launches += launch_reduce(*lv[i].lp, h->fbuf.as<double>() + f_off[i], row_ld, lv[i].y, row_ld, int(row_ld),
+                                h->levels[lv[i].level].second, s);
     }
   } else {
     for (auto& L : lv) launches += run_plan(h, L.level, *L.lp, L.x, L.y, s);
