@@ -34,6 +34,7 @@
 #include "tile_gemm.cuh"
 #include "tile_gemm_ws.cuh"
 #include "pair_reduce.cuh"
+#include "lowrank_ws.cuh"
 
 namespace cfm {
 
@@ -190,6 +191,7 @@ struct cfm_handler {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   DevBuf rowtab, invtab;  // [48][n f] int16
+  DevBuf zeros;           // zero row for bulk copies past an operator
   std::map<int, Group> groups;
   std::map<int, std::pair<int, double>> levels;
   std::map<int, LevelPlan> plans;
@@ -203,16 +205,26 @@ namespace cfm {
 
 // ------------------------------------------------------------------ launching
 // Kernel selection (CFM_TILE_KERNEL): "ws16" warp-specialized KC=16 x 5 stages
-// (default), "ws32" KC=32 x 3 stages, "sync" the lockstep kernel.
+// (default), "ws32" KC=32 x 3 stages, "sync" the lockstep kernel, "ws16w"
+// like ws16 with 16 consumer warps (32x16 warp tiles) on 128-row blocks.
 static int tile_kernel_kind() {
   static int kind = [] {
     const char* v = getenv("CFM_TILE_KERNEL");
     if (!v) return 1;
     if (!strcmp(v, "ws32")) return 0;
     if (!strcmp(v, "sync")) return 2;
+    if (!strcmp(v, "ws16w")) return 3;
     return 1;
   }();
   return kind;
+}
+
+static bool use_bulk_a() {
+  static int v = [] {
+    const char* e = getenv("CFM_BULK_A");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
 }
 
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
@@ -220,6 +232,14 @@ static void launch_ws_multi(const MultiTileParams& mp, dim3 grid, cudaStream_t s
   const TileParams& q = mp.seg[0];
   const bool tabs = tile_perm_tabs_fit(q.nr, q.nk);
   const int smem = ws_ring_bytes<BM, BN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, tabs);
+  if constexpr (BM == 128) {
+    if (use_bulk_a() && q.zero_row && q.op_ld <= 8192) {
+      auto kb = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, STAGES, SKIP, true>;
+      CUDA_CHECK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kb<<<grid, (WM * WN + 4) * 32, smem, s>>>(mp);
+      return;
+    }
+  }
   auto kern = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, STAGES, SKIP>;
   CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, (WM * WN + 4) * 32, smem, s>>>(mp);
@@ -263,6 +283,45 @@ static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStre
   CUDA_CHECK(cudaGetLastError());
 }
 
+// ---- fused low-rank kernel (phase 1 + phase 2 in one CTA)
+static bool use_fused_lowrank() {
+  static int v = [] {
+    const char* e = getenv("CFM_LOWRANK_FUSED");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+template <int RP, int STAGES>
+static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, cudaStream_t s) {
+  constexpr int KC = 16;
+  const int fixed = lr_smem_bytes<RP, KC, STAGES>() + 4 * 64 + 3 * 4 * 344 + 4 * kMaxTileEntries;
+  if (lp_.n_ops > 344 || fixed > 227 * 1024) return false;
+  const int tabs = 48 * 2 * (lp_.nr + lp_.nk + 8);
+  lp_.tabs_smem = (fixed + tabs <= 227 * 1024) ? 1 : 0;
+  const int smem = fixed + (lp_.tabs_smem ? tabs : 0);
+  auto kern = lowrank_ws_kernel<RP, KC, STAGES>;
+  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int64_t max_grid = 1 << 30;
+  for (int64_t base = first; base < first + count; base += max_grid) {
+    const int nt = int(std::min<int64_t>(max_grid, first + count - base));
+    LowRankParams q = lp_;
+    q.tile_base = int(base);
+    dim3 grid(nt, (lp_.nr + 127) / 128);
+    kern<<<grid, 12 * 32, smem, s>>>(q);
+    CUDA_CHECK(cudaGetLastError());
+  }
+  return true;
+}
+
+static bool launch_lowrank_fused(const LowRankParams& lp_, int rmax, int64_t first, int64_t count, cudaStream_t s) {
+  if (!use_fused_lowrank()) return false;
+  if (rmax <= 16) return launch_lowrank_cfg<16, 5>(lp_, first, count, s);
+  if (rmax <= 32) return launch_lowrank_cfg<32, 4>(lp_, first, count, s);
+  if (rmax <= 64) return launch_lowrank_cfg<64, 2>(lp_, first, count, s);
+  return false;
+}
+
 // One launch over several tile lists sharing operator shapes (all levels of a
 // homogeneous dense group).  Segments are launched in the given order.
 static int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int64_t>& counts, cudaStream_t s) {
@@ -294,6 +353,7 @@ static int64_t launch_multi(const std::vector<TileParams>& segs, const std::vect
   } else {
     dim3 grid(unsigned(total), (q.nr + 127) / 128);
     if (kind == 0) launch_ws_multi<128, kBN, 4, 2, 32, 3, false>(mp, grid, s);
+    else if (kind == 3) launch_ws_multi<128, kBN, 4, 4, 16, 5, false>(mp, grid, s);
     else launch_ws_multi<128, kBN, 4, 2, 16, 5, false>(mp, grid, s);
   }
   CUDA_CHECK(cudaGetLastError());
@@ -597,6 +657,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
   TileParams p{};
   p.rowtab = h->rowtab.as<short>();
   p.invtab = h->invtab.as<short>();
+  p.zero_row = h->zeros.as<double>();
 
   if (g.kind == kDense) {
     fill_ops(p, g.dense, g.main);
@@ -617,6 +678,44 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
   }
 
   if (g.kind == kLowRank) {
+    {
+      LowRankParams q{};
+      q.n_tiles = int(lp.hp.n_tiles);
+      q.tile_col = lp.tile_col.as<int>();
+      q.tile_off = lp.tile_off.as<int>();
+      q.entry_code = lp.entry_code.as<int>();
+      q.entry_src = lp.entry_src.as<int>();
+      q.code_op = g.main.d_op.as<int>();
+      q.code_rperm = g.main.d_rperm.as<int>();
+      q.code_cperm = g.pass1.d_cperm.as<int>();
+      q.vh = g.right_h.d.as<double>();
+      q.vh_stride = g.right_h.stride;
+      q.vh_ld = g.right_h.ld;
+      q.u = g.left.d.as<double>();
+      q.u_stride = g.left.stride;
+      q.u_ld = g.left.ld;
+      q.rank = g.left.d_klen.as<int>();
+      q.n_ops = g.left.n_ops;
+      q.nr = g.left.rows;
+      q.nk = g.right_h.cols;
+      q.rowtab = h->rowtab.as<short>();
+      q.invtab = h->invtab.as<short>();
+      q.x = d_x; q.x_ld = row_ld; q.x_dc = dc;
+      if (lp.mode == 1) {
+        ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
+        q.y = h->fbuf.as<double>(); q.y_ld = row_ld; q.y_dc = dc;
+        q.scale = 1.0; q.accumulate = 0; q.pair_out = 1;
+      } else {
+        q.y = d_y; q.y_ld = row_ld; q.y_dc = dc;
+        q.scale = scale; q.accumulate = 1; q.pair_out = 0;
+      }
+      if (launch_lowrank_fused(q, g.right_h.rows, 0, lp.hp.n_tiles, s)) {
+        ++launches;
+        if (lp.mode == 1)
+          launches += launch_reduce(lp, h->fbuf.as<double>(), row_ld, d_y, row_ld, int(row_ld), scale, s);
+        return launches;
+      }
+    }
     // chunk tiles so the per-pair intermediate stays bounded
     const int ldy = g.right_h.rows;  // rmax * f
     const size_t max_slots = std::max<size_t>(kBN, (size_t(1) << 30) / (sizeof(double) * std::max(ldy, 1)));
@@ -831,8 +930,21 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       TileParams p{};
       p.rowtab = h->rowtab.as<short>();
       p.invtab = h->invtab.as<short>();
+      p.zero_row = h->zeros.as<double>();
       fill_ops(p, g.dense, g.main);
       fill_plan(p, L.lp->tile_col, L.lp->tile_off, L.lp->entry_code, L.lp->entry_src, L.lp->hp.n_tiles);
+      {
+        // timing experiments only (results are wrong): CFM_EXP=norow|nocol|noperm drops permutations
+        static const char* exp = getenv("CFM_EXP");
+        static std::vector<int> neg(kNumCodes, -1);
+        static DevBuf d_neg;
+        if (exp && !d_neg.p) upload(d_neg, neg);
+        if (exp && (!strcmp(exp, "norow") || !strcmp(exp, "noperm"))) p.code_rperm = d_neg.as<int>();
+        if (exp && (!strcmp(exp, "nocol") || !strcmp(exp, "noperm"))) p.code_cperm = d_neg.as<int>();
+        if (exp && !strcmp(exp, "nowait")) p.debug = 1;
+        if (exp && !strcmp(exp, "spin")) p.debug = 2;
+        if (exp && !strcmp(exp, "nocopy")) p.debug = 4;
+      }
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
       if (L.lp->mode == 1) {
@@ -1005,6 +1117,7 @@ int cfm_handler_create(int device, int variant, int order, int op_complex, cfm_h
     CUDA_CHECK(cudaEventCreate(&h->ev0));
     CUDA_CHECK(cudaEventCreate(&h->ev1));
     build_tables(h.get());
+    upload(h->zeros, std::vector<double>(8192, 0.0));
     *out = h.release();
   });
 }

@@ -58,6 +58,8 @@ struct TileParams {
   double scale;
   int accumulate;
   int pair_out;  // 1: write each entry's result to y rows (e * BN + c) when the entry ends
+  int debug;     // timing experiments only (bit 0: consumers skip the full-barrier wait)
+  const double* zero_row;  // >= op_ld zeros (rows past an operator, bulk-copy path)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {

@@ -25,6 +25,43 @@ __device__ __forceinline__ void mbar_cp_async_arrive(uint64_t* bar) {
   unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier (bytes).
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+               "l"(gmem), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Producer-side wait with exponential nanosleep backoff: a spinning producer
+// warp would steal issue slots from the DMMA consumer warps of its SMSP.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, unsigned parity) {
+  unsigned ns = 32;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 512 ? ns * 2 : 512;
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   asm volatile(
@@ -52,7 +89,7 @@ struct MultiTileParams {
   TileParams seg[kMaxSegments];
 };
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS, bool BULK_A = false>
 __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(const __grid_constant__ MultiTileParams mp) {
   int sidx = 0;
   while (sidx + 1 < mp.n_seg && int(blockIdx.x) >= mp.start[sidx + 1]) ++sidx;
@@ -69,6 +106,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   static_assert(A_PIECES % NP == 0 && B_ELEMS % NP == 0, "tile/thread mismatch");
   static_assert(NP % KC == 0, "B mapping needs NP multiple of KC");
   static_assert(BN <= 64, "s_col sized for 64 columns");
+  static_assert(!BULK_A || BM == NP, "bulk A path: one operator row per producer thread");
 
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -106,7 +144,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, NP);
+      mbar_init(full + s, BULK_A ? NP + 1 : NP);
       mbar_init(empty + s, NC / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -146,6 +184,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     };
     const double* a_row[A_PER_T];
     bool a_ok[A_PER_T];
+    const double* a_rowb[BM / NP > 0 ? BM / NP : 1];
     const double* b_col[B_PER_T];
     while (e < e_end) {
       // per-entry pointers
@@ -160,6 +199,16 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         if (a_ok[u] && d.rperm >= 0) orow = rowtab[d.rperm * p.nr + gr];
         a_row[u] = opbase + (long long)(a_ok[u] ? orow : 0) * p.op_ld + 2 * kp;
       }
+      if (BULK_A) {
+#pragma unroll
+        for (int u = 0; u < BM / NP; ++u) {
+          const int gr = r0 + pt + u * NP;
+          const bool ok = gr < d.rows;
+          int orow = gr;
+          if (ok && d.rperm >= 0) orow = rowtab[d.rperm * p.nr + gr];
+          a_rowb[u] = ok ? opbase + (long long)orow * p.op_ld : p.zero_row;
+        }
+      }
       if (nxt_e != e) prefetch_src(e);
 #pragma unroll
       for (int u = 0; u < B_PER_T; ++u) {
@@ -169,15 +218,35 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       prefetch_src(e + 1);
       for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
         const int s = q % STAGES;
-        if (q >= STAGES) mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
+        if (q >= STAGES) {
+          if (p.debug & 2)
+            mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
+          else
+            mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
+        }
+        if (p.debug & 4) {  // timing experiment: no copies, stale stage data
+          mbar_arrive(full + s);
+          continue;
+        }
         const int k0 = kc * KC;
         double* as = As + s * BM * LDA;
         double* bs = Bs + s * BN * LDB;
+        if (BULK_A) {
+          // one bulk copy per operator row (KC doubles); rows past the operator
+          // read the zero row kept after the stack
+          if (pt == 0) mbar_arrive_expect_tx(full + s, BM * KC * 8);
 #pragma unroll
-        for (int u = 0; u < A_PER_T; ++u) {
-          const int id = pt + u * NP;
-          const int i = id / (KC / 2), kp = id % (KC / 2);
-          cp_async16(as + i * LDA + 2 * kp, a_ok[u] ? (const void*)(a_row[u] + k0) : (const void*)p.ops, a_ok[u]);
+          for (int u = 0; u < BM / NP; ++u) {
+            const int i = pt + u * NP;
+            bulk_g2s(as + i * LDA, a_rowb[u] + k0, KC * 8, full + s);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < A_PER_T; ++u) {
+            const int id = pt + u * NP;
+            const int i = id / (KC / 2), kp = id % (KC / 2);
+            cp_async16(as + i * LDA + 2 * kp, a_ok[u] ? (const void*)(a_row[u] + k0) : (const void*)p.ops, a_ok[u]);
+          }
         }
         const int kk = pt % KC;
         const int k = k0 + kk;
@@ -215,7 +284,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     const int mrows = d.rows - r0 - wm * WTM;
     for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
       const int s = q % STAGES;
-      mbar_wait(full + s, (q / STAGES) & 1);
+      if (!(p.debug & 1)) mbar_wait(full + s, (q / STAGES) & 1);
       const double* as = As + s * BM * LDA + (wm * WTM + g) * LDA + tg;
       const double* bs = Bs + s * BN * LDB + (wn * WTN + g) * LDB + tg;
       const int kmax = min(KC, d.klen - kc * KC);
