@@ -195,7 +195,7 @@ struct cfm_handler {
   std::map<int, Group> groups;
   std::map<int, std::pair<int, double>> levels;
   std::map<int, LevelPlan> plans;
-  DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf;
+  DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
@@ -960,13 +960,36 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       segs.push_back(p);
       counts.push_back(L.lp->hp.n_tiles);
     }
+    // small pair-mode segments reduce inside the launch (their last CTA)
+    std::vector<bool> reduced_inside(lv.size(), false);
     if (same_shape && int(segs.size()) <= kMaxSegments) {
+      ensure(h->counters, kMaxSegments * sizeof(unsigned));
+      CUDA_CHECK(cudaMemsetAsync(h->counters.p, 0, kMaxSegments * sizeof(unsigned), s));
+      for (size_t i = 0; i < lv.size(); ++i) {
+        const LevelPlan& P = *lv[i].lp;
+        const long long row_ld = (long long)h->n * (P.dc == 2 || h->op_complex ? 2 : 1);
+        const double work = double(P.red.frow.size()) * double(row_ld);
+        if (P.mode == 1 && work <= 1.6e7 && !P.red.tgt.empty()) {
+          TileParams& q = segs[i];
+          q.red_counter = h->counters.as<unsigned>() + i;
+          q.red_ctas = int(counts[i]) * ((q.nr + 127) / 128);
+          q.red_tgt = P.r_tgt.as<long long>();
+          q.red_off = P.r_off.as<long long>();
+          q.red_frow = P.r_frow.as<int>();
+          q.red_n_tgt = int64_t(P.red.tgt.size());
+          q.red_y = lv[i].y;
+          q.red_ld = row_ld;
+          q.red_len = int(row_ld);
+          q.red_scale = h->levels[lv[i].level].second;
+          reduced_inside[i] = true;
+        }
+      }
       launches += launch_multi(segs, counts, s);
     } else {
       for (size_t i = 0; i < segs.size(); ++i) launches += launch_tiles(segs[i], counts[i], s);
     }
     for (size_t i = 0; i < lv.size(); ++i) {
-      if (lv[i].lp->mode != 1) continue;
+      if (lv[i].lp->mode != 1 || reduced_inside[i]) continue;
       const long long row_ld = (long long)h->n * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
       launches += launch_reduce(*lv[i].lp, h->fbuf.as<double>() + f_off[i], row_ld, lv[i].y, row_ld, int(row_ld),
                                 h->levels[lv[i].level].second, s);

@@ -60,6 +60,18 @@ struct TileParams {
   int pair_out;  // 1: write each entry's result to y rows (e * BN + c) when the entry ends
   int debug;     // timing experiments only (bit 0: consumers skip the full-barrier wait)
   const double* zero_row;  // >= op_ld zeros (rows past an operator, bulk-copy path)
+  // pair mode, small segments: the last CTA of the segment reduces the per-pair
+  // rows into the targets itself (ordered, no extra launch)
+  unsigned int* red_counter;  // null: reduction launched separately
+  int red_ctas;               // CTAs in the segment (tiles x row blocks)
+  const long long* red_tgt;
+  const long long* red_off;
+  const int* red_frow;
+  long long red_n_tgt;
+  double* red_y;
+  long long red_ld;
+  int red_len;
+  double red_scale;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {

@@ -361,7 +361,33 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     }
     e = next_live(e + 1, d);
   }
-  if (p.pair_out) return;
+  if (p.pair_out) {
+    if (p.red_counter) {
+      // last CTA of the segment: ordered per-target reduction of the pair rows
+      __shared__ int s_last;
+      __threadfence();  // every consumer's pair rows are visible device-wide before the count
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+      if (tid == 0) {
+        __threadfence();
+        const unsigned old = atomicAdd(p.red_counter, 1u);
+        s_last = (old == unsigned(p.red_ctas) - 1) ? 1 : 0;
+        __threadfence();
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+      if (s_last) {
+        const long long total = p.red_n_tgt * p.red_len;
+        for (long long idx = tid; idx < total; idx += NC) {
+          const long long t = idx / p.red_len;
+          const int i = int(idx - t * p.red_len);
+          double sum = 0.0;
+          for (long long q2 = p.red_off[t]; q2 < p.red_off[t + 1]; ++q2)
+            sum += __ldcg(p.y + (long long)p.red_frow[q2] * p.red_ld + i);
+          p.red_y[p.red_tgt[t] * p.red_ld + i] += p.red_scale * sum;
+        }
+      }
+    }
+    return;
+  }
 
   // ---------------- epilogue: ordered, atomic-free write ----------------
   if (e_begin == e_end && p.accumulate) return;
