@@ -13,6 +13,7 @@
 // summed into an accumulator and added once, scaled, into locals (m2l.py:337,
 // :363, :393); the blocked variant's per-column adds (:430-431) differ from that
 // only by floating-point reassociation.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -167,6 +168,11 @@ struct LevelPlan {
   double target_fill = 1.0;
   PairReduce red;
   DevBuf r_tgt, r_off, r_frow;
+  // copy pipeline (target mode, large levels): rows split into n_slabs ranges
+  int n_slabs = 1;
+  std::vector<int64_t> slab_row0;        // n_slabs + 1 row boundaries
+  std::vector<unsigned> slab_expected;   // CTAs (tiles x row blocks) writing each slab
+  DevBuf p_need_mp, p_need_loc, p_lo, p_hi;
   DevBuf tile_col, tile_off, entry_code, entry_src;
   DevBuf slot_ids, iota;  // low-rank: per-entry slots
   DevBuf runs;            // low-rank pass 1: tiles = runs of kPass1Run consecutive entries
@@ -195,7 +201,9 @@ struct cfm_handler {
   std::map<int, Group> groups;
   std::map<int, std::pair<int, double>> levels;
   std::map<int, LevelPlan> plans;
-  DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters;
+  DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters, pipe_flags;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
@@ -284,6 +292,38 @@ static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStre
 }
 
 // ---- fused low-rank kernel (phase 1 + phase 2 in one CTA)
+// Driver stream-memory ops resolved at run time (no link-time libcuda
+// dependency, so the library still loads on machines without a driver).
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_writeValue32 p_writeValue32 = nullptr;
+static PFN_waitValue32 p_waitValue32 = nullptr;
+static bool resolve_stream_mem_ops() {
+  static int ok = [] {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &f2, cudaEnableDefault, &q2) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !f1 || !f2) {
+      cudaGetLastError();
+      return 0;
+    }
+    p_writeValue32 = reinterpret_cast<PFN_writeValue32>(f1);
+    p_waitValue32 = reinterpret_cast<PFN_waitValue32>(f2);
+    return 1;
+  }();
+  return ok != 0;
+}
+
+static bool use_copy_pipeline() {
+  static int v = [] {
+    const char* e = getenv("CFM_COPY_PIPELINE");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0 && resolve_stream_mem_ops();
+}
+
 static bool use_fused_lowrank() {
   static int v = [] {
     const char* e = getenv("CFM_LOWRANK_FUSED");
@@ -627,6 +667,75 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     push_plan(lp.src_plan, lp.s_tile_col, lp.s_tile_off, lp.s_entry_code, lp.s_entry_src);
     push_plan(lp.tgt_plan, lp.t_tile_col, lp.t_tile_off, lp.t_entry_code, lp.t_entry_src);
   }
+  if (lp.mode == 0 && lp.hp.n_tiles > 0) {
+    // dispatch order ~ row order (tiles stay class-pure; a target's entry order
+    // is unchanged, so results are bitwise identical), which lets the host
+    // copies of multipoles/locals run in row slabs alongside the kernel
+    HostPlan& hp = lp.hp;
+    const int64_t nt = hp.n_tiles;
+    std::vector<int64_t> tmin(nt, INT64_MAX);
+    for (int64_t t = 0; t < nt; ++t)
+      for (int c = 0; c < kBN; ++c) {
+        const int v = hp.tile_col[size_t(t) * kBN + c];
+        if (v >= 0) tmin[t] = std::min<int64_t>(tmin[t], v / dc);
+      }
+    std::vector<int64_t> ord(nt);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return tmin[a] < tmin[b]; });
+    HostPlan np_;
+    np_.bn = hp.bn; np_.dc = hp.dc; np_.n_tiles = nt; np_.n_pairs = hp.n_pairs; np_.code_count = hp.code_count;
+    np_.tile_col.resize(hp.tile_col.size());
+    np_.tile_off.resize(nt + 1);
+    np_.entry_code.reserve(hp.entry_code.size());
+    np_.entry_src.reserve(hp.entry_src.size());
+    for (int64_t k = 0; k < nt; ++k) {
+      const int64_t t = ord[k];
+      std::copy(hp.tile_col.begin() + t * kBN, hp.tile_col.begin() + (t + 1) * kBN, np_.tile_col.begin() + k * kBN);
+      np_.tile_off[k] = int(np_.entry_code.size());
+      for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e) {
+        np_.entry_code.push_back(hp.entry_code[e]);
+        np_.entry_src.insert(np_.entry_src.end(), hp.entry_src.begin() + size_t(e) * kBN,
+                             hp.entry_src.begin() + size_t(e + 1) * kBN);
+      }
+    }
+    np_.tile_off[nt] = int(np_.entry_code.size());
+    lp.hp = std::move(np_);
+    push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
+    // slabs of ~32K rows (at most 16)
+    const int S = int(std::min<int64_t>(16, std::max<int64_t>(1, n_rows / 32768)));
+    lp.n_slabs = S;
+    lp.slab_row0.resize(S + 1);
+    for (int k = 0; k <= S; ++k) lp.slab_row0[k] = n_rows * k / S;
+    auto slab_of = [&](int64_t row) { return int(std::min<int64_t>(S - 1, row * S / std::max<int64_t>(n_rows, 1))); };
+    std::vector<int> need_mp(nt, 0), need_loc(nt, 0), lo(nt, 0), hi(nt, -1);
+    lp.slab_expected.assign(S, 0);
+    const int nrb = (group_for_level(h, level).dense.rows + 127) / 128;
+    for (int64_t t = 0; t < nt; ++t) {
+      int l = S, hh = -1, m = 0;
+      for (int c = 0; c < kBN; ++c) {
+        const int v = lp.hp.tile_col[size_t(t) * kBN + c];
+        if (v < 0) continue;
+        const int k = slab_of(v / dc);
+        l = std::min(l, k);
+        hh = std::max(hh, k);
+      }
+      for (int e = lp.hp.tile_off[t]; e < lp.hp.tile_off[t + 1]; ++e)
+        for (int c = 0; c < kBN; ++c) {
+          const int v = lp.hp.entry_src[size_t(e) * kBN + c];
+          if (v >= 0) m = std::max(m, slab_of(v / dc) + 1);
+        }
+      if (hh < 0) { l = 0; hh = -1; }
+      need_mp[t] = m;
+      need_loc[t] = hh + 1;
+      lo[t] = l;
+      hi[t] = hh;
+      for (int k = l; k <= hh; ++k) lp.slab_expected[k] += unsigned(nrb);
+    }
+    upload(lp.p_need_mp, need_mp);
+    upload(lp.p_need_loc, need_loc);
+    upload(lp.p_lo, lo);
+    upload(lp.p_hi, hi);
+  }
   h->plans[level] = std::move(lp);
   return h->plans[level];
 }
@@ -888,20 +997,92 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   }
   std::sort(lv.begin(), lv.end(), [](const Lv& a, const Lv& b) { return a.level < b.level; });
   if (stage_bytes) ensure(h->x_stage, stage_bytes);
+  // ---- copy pipeline: large target-mode levels given as host buffers stream
+  // their rows in slabs on a copy stream while the kernel runs (flags in device
+  // memory, written with cuStreamWriteValue32, gate producers and epilogues;
+  // per-slab completion counters gate the D2H slabs via cuStreamWaitValue32)
+  bool all_dense_pre = true;
+  for (auto& L : lv) all_dense_pre = all_dense_pre && group_for_level(h, L.level).kind == kDense;
+  std::vector<int> piped(lv.size(), 0);
+  bool any_piped = false;
+  if (all_dense_pre && use_copy_pipeline() && lv.size() <= size_t(kMaxSegments)) {
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (!is_device_ptr(lv[i].x) && !is_device_ptr(lv[i].y) && lv[i].lp->mode == 0 && lv[i].lp->n_slabs >= 2) {
+        piped[i] = 1;
+        any_piped = true;
+      }
+    }
+  }
   size_t off = 0;
-  for (auto& L : lv) {
+  std::vector<const double*> host_x(lv.size(), nullptr);
+  std::vector<size_t> flag_off(lv.size(), 0);
+  cudaStream_t s_in = s;
+  if (any_piped) {
+    if (!h->s_h2d) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    if (!h->s_d2h) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    if (!h->ev_in) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+    if (!h->ev_out) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+    s_in = h->s_h2d;
+    size_t nflags = 0;
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (piped[i]) {
+        flag_off[i] = nflags;
+        nflags += 2 + size_t(lv[i].lp->n_slabs);
+      }
+    ensure(h->pipe_flags, nflags * sizeof(unsigned));
+    CUDA_CHECK(cudaMemsetAsync(h->pipe_flags.p, 0, nflags * sizeof(unsigned), s_in));
+  }
+  for (size_t i = 0; i < lv.size(); ++i) {
+    auto& L = lv[i];
     if (!is_device_ptr(L.x)) {
       double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
-      CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s));
+      host_x[i] = L.x;
+      if (!piped[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s_in));
       L.x = d;
       off += L.bytes;
     }
     if (!is_device_ptr(L.y)) {
       double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
-      CUDA_CHECK(cudaMemcpyAsync(d, L.y, L.bytes, cudaMemcpyHostToDevice, s));
+      if (!piped[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.y, L.bytes, cudaMemcpyHostToDevice, s_in));
       L.host_y = L.y;
       L.y = d;
       off += L.bytes;
+    }
+  }
+  if (any_piped) {
+    // the kernel may start once the non-pipelined levels and the zeroed flags are in
+    CUDA_CHECK(cudaEventRecord(h->ev_in, s_in));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_in, 0));
+    CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_in, 0));
+    unsigned* flags = h->pipe_flags.as<unsigned>();
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (!piped[i]) continue;
+      const LevelPlan& P = *lv[i].lp;
+      const int S = P.n_slabs;
+      const size_t row_b = lv[i].bytes / size_t(P.n_rows);
+      auto slab_copy = [&](const void* hsrc, void* ddst, int k, cudaMemcpyKind kind, cudaStream_t st) {
+        const size_t b0 = size_t(P.slab_row0[k]) * row_b, b1 = size_t(P.slab_row0[k + 1]) * row_b;
+        if (b1 > b0)
+          CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(ddst) + b0, static_cast<const char*>(hsrc) + b0, b1 - b0,
+                                     kind, st));
+      };
+      auto write_flag = [&](unsigned* f, unsigned v) {
+        CUresult r = p_writeValue32(reinterpret_cast<CUstream>(s_in), reinterpret_cast<CUdeviceptr>(f), v, 0);
+        if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuStreamWriteValue32 failed");
+      };
+      unsigned* mp_ready = flags + flag_off[i];
+      unsigned* loc_ready = mp_ready + 1;
+      // multipole slab k is needed by targets of slab k-1: keep multipoles one slab ahead
+      for (int k = 0; k < S; ++k) {
+        slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
+        write_flag(mp_ready, unsigned(k + 1));
+        if (k >= 1) {
+          slab_copy(lv[i].host_y, lv[i].y, k - 1, cudaMemcpyHostToDevice, s_in);
+          write_flag(loc_ready, unsigned(k));
+        }
+      }
+      slab_copy(lv[i].host_y, lv[i].y, S - 1, cudaMemcpyHostToDevice, s_in);
+      write_flag(loc_ready, unsigned(S));
     }
   }
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
@@ -955,6 +1136,16 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         p.scale = h->levels[L.level].second;
         p.accumulate = 1;
       }
+      if (piped[i]) {
+        unsigned* f = h->pipe_flags.as<unsigned>() + flag_off[i];
+        p.pipe_mp = f;
+        p.pipe_loc = f + 1;
+        p.pipe_done = f + 2;
+        p.pipe_need_mp = L.lp->p_need_mp.as<int>();
+        p.pipe_need_loc = L.lp->p_need_loc.as<int>();
+        p.pipe_lo = L.lp->p_lo.as<int>();
+        p.pipe_hi = L.lp->p_hi.as<int>();
+      }
       if (nr >= 0 && (p.nr != nr)) same_shape = false;
       nr = p.nr;
       segs.push_back(p);
@@ -998,8 +1189,37 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     for (auto& L : lv) launches += run_plan(h, L.level, *L.lp, L.x, L.y, s);
   }
   CUDA_CHECK(cudaEventRecord(h->ev1, s));
-  for (auto& L : lv)
-    if (L.host_y) CUDA_CHECK(cudaMemcpyAsync(L.host_y, L.y, L.bytes, cudaMemcpyDeviceToHost, s));
+  if (any_piped) {
+    unsigned* flags = h->pipe_flags.as<unsigned>();
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (!piped[i]) continue;
+      const LevelPlan& P = *lv[i].lp;
+      const size_t row_b = lv[i].bytes / size_t(P.n_rows);
+      unsigned* done = flags + flag_off[i] + 2;
+      for (int k = 0; k < P.n_slabs; ++k) {
+        if (P.slab_expected[k]) {
+          CUresult r = p_waitValue32(reinterpret_cast<CUstream>(h->s_d2h),
+                                           reinterpret_cast<CUdeviceptr>(done + k), P.slab_expected[k],
+                                           CU_STREAM_WAIT_VALUE_GEQ);
+          if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuStreamWaitValue32 failed");
+        }
+        const size_t b0 = size_t(P.slab_row0[k]) * row_b, b1 = size_t(P.slab_row0[k + 1]) * row_b;
+        if (b1 > b0)
+          CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(lv[i].host_y) + b0, reinterpret_cast<char*>(lv[i].y) + b0,
+                                     b1 - b0, cudaMemcpyDeviceToHost, h->s_d2h));
+      }
+    }
+    CUDA_CHECK(cudaEventRecord(h->ev_out, s));  // kernel (and reductions) done
+    CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_out, 0));
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (!piped[i] && lv[i].host_y)
+        CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
+    CUDA_CHECK(cudaStreamSynchronize(h->s_d2h));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  } else {
+    for (auto& L : lv)
+      if (L.host_y) CUDA_CHECK(cudaMemcpyAsync(L.host_y, L.y, L.bytes, cudaMemcpyDeviceToHost, s));
+  }
   CUDA_CHECK(cudaStreamSynchronize(s));
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
@@ -1152,6 +1372,10 @@ int cfm_handler_destroy(cfm_handler* h) {
     cudaStreamSynchronize(h->stream);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->ev_in) cudaEventDestroy(h->ev_in);
+    if (h->ev_out) cudaEventDestroy(h->ev_out);
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     cudaStreamDestroy(h->stream);
     delete h;
   });

@@ -72,7 +72,33 @@ struct TileParams {
   long long red_ld;
   int red_len;
   double red_scale;
+  // host<->device copy pipeline (target mode): per-tile slab needs and
+  // per-slab completion counters; null when the level is not pipelined
+  const unsigned* pipe_mp;   // # multipole slabs resident
+  const unsigned* pipe_loc;  // # locals slabs resident
+  unsigned* pipe_done;       // per slab: CTAs done writing its rows
+  const int* pipe_need_mp;
+  const int* pipe_need_loc;
+  const int* pipe_lo;
+  const int* pipe_hi;
 };
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Wait until a copy-stream flag reaches v (written by cuStreamWriteValue32).
+// Traps after ~4 s instead of hanging the device if a flag never arrives.
+__device__ __forceinline__ void wait_flag_geq(const unsigned* f, unsigned v) {
+  unsigned ns = 64;
+  const long long t0 = clock64();
+  while (ld_acquire_u32(f) < v) {
+    __nanosleep(ns);
+    ns = ns < 2048 ? ns * 2 : 2048;
+    if (clock64() - t0 > (1ll << 33)) __trap();
+  }
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

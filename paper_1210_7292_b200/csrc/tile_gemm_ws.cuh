@@ -168,6 +168,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   if (tid >= NC) {
     // ======================= producer warps =======================
     const int pt = tid - NC;
+    if (p.pipe_mp && e_begin < e_end) wait_flag_geq(p.pipe_mp, unsigned(p.pipe_need_mp[tile]));
     EntryInfo d;
     d.nchunks = 0;
     int e = next_live(e_begin, d);
@@ -390,7 +391,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   }
 
   // ---------------- epilogue: ordered, atomic-free write ----------------
-  if (e_begin == e_end && p.accumulate) return;
+  if (e_begin == e_end && p.accumulate && !p.pipe_done) return;
+  if (p.pipe_loc) wait_flag_geq(p.pipe_loc, unsigned(p.pipe_need_loc[tile]));
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi) {
     const int row = r0 + wm * WTM + mi * 8 + g;
@@ -410,6 +412,12 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
           *dst = val;
       }
     }
+  }
+  if (p.pipe_done) {
+    __threadfence();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+    if (tid == 0)
+      for (int k = p.pipe_lo[tile]; k <= p.pipe_hi[tile]; ++k) atomicAdd(p.pipe_done + k, 1u);
   }
 }
 
