@@ -58,28 +58,36 @@ def fp64_peak():
     return 37.1, "fallback (148 SM x 128 flop/clk x 1.965 GHz)"
 
 
-def level_cells(cfg):
-    """Occupied cells per level (lexicographic = reference row order)."""
+def bench_points(cfg):
+    """Seeded synthetic particles of a config (chunks of 10^7 with per-chunk
+    seeds) and its bounding cube (center, half width)."""
     from geometry import cube_points, sphere_points
 
     n, depth, order, geom, _, _ = CONFIGS[cfg]
-    side = 1 << depth
-    if geom == "cube":
-        low, width = np.zeros(3), 1.0
-    else:
-        low, width = -np.ones(3), 2.0
-    keys = []
     chunk = 10_000_000
-    rng_seed = 2 if geom == "cube" else 3
-    # generated in chunks of 10^7 points (config 4 has 10^8) with per-chunk seeds
+    base = 2 if geom == "cube" else 3
+    parts = []
     for i in range(0, n, chunk):
         m = min(chunk, n - i)
-        seed = rng_seed + 1000 * (i // chunk)
-        pts = cube_points(m, seed=seed) if geom == "cube" else sphere_points(m, seed=seed)
-        ijk = np.minimum(((pts - low) / width * side).astype(np.int64), side - 1)
-        del pts
+        seed = base + 1000 * (i // chunk)
+        parts.append(cube_points(m, seed=seed) if geom == "cube" else sphere_points(m, seed=seed))
+    pts = parts[0] if len(parts) == 1 else np.concatenate(parts)
+    center, half = ((0.5, 0.5, 0.5), 0.5) if geom == "cube" else ((0.0, 0.0, 0.0), 1.0)
+    return pts, center, half
+
+
+def level_cells(cfg):
+    """Occupied cells per level (lexicographic = reference row order), numpy."""
+    n, depth, order, geom, _, _ = CONFIGS[cfg]
+    pts, center, half = bench_points(cfg)
+    side = 1 << depth
+    low = np.asarray(center) - half
+    width = 2.0 * half
+    keys = []
+    for i in range(0, len(pts), 10_000_000):
+        ijk = np.minimum(((pts[i:i + 10_000_000] - low) / width * side).astype(np.int64), side - 1)
         keys.append(np.unique((ijk[:, 0] << 42) | (ijk[:, 1] << 21) | ijk[:, 2]))
-        del ijk
+    del pts
     key = np.unique(np.concatenate(keys))
     out = {}
     cur = np.stack([key >> 42, (key >> 21) & 0x1FFFFF, key & 0x1FFFFF], 1)
@@ -91,6 +99,23 @@ def level_cells(cfg):
         out[lvl] = cur
     widths = {lvl: width / (1 << lvl) for lvl in out}
     return out, widths
+
+
+def gpu_level_cells(cfg, device):
+    """Same cells from the GPU octree build (paper_1210_7292_b200.octree)."""
+    from paper_1210_7292_b200.octree import build_tree_gpu
+
+    n, depth, order, geom, _, _ = CONFIGS[cfg]
+    pts, center, half = bench_points(cfg)
+    import torch
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tree = build_tree_gpu(pts, center, half, depth, device=device)
+    cells = {l: tree.cells(l) for l in range(2, depth + 1)}
+    ms = (time.perf_counter() - t0) * 1e3
+    widths = {l: 2.0 * half / (1 << l) for l in cells}
+    return cells, widths, ms
 
 
 class ClockSampler:
@@ -289,7 +314,7 @@ def run_b200(args):
     n, depth, order, geom, variant, eps = CONFIGS[cfg]
     variant = args.variant or variant
     size = order**3
-    cells, widths = cached_level_cells(cfg)
+    cells, widths, tree_ms = gpu_level_cells(cfg, local)
     levels = sorted(cells)
     full = full_far_field_vectors()
     cplx = cfg in HELMHOLTZ
@@ -491,6 +516,7 @@ def run_b200(args):
             "config": {"workload": f"{cfg}: N={n:.0e} {geom}, height {depth + 1} (levels {levels[0]}-{deep}), "
                                    f"l={order}, {'Helmholtz k=8pi complex128' if cplx else 'Laplace'}, variant {variant}"
                                    f", eps={eps:g}", "pairs_per_step": pairs_total, "precompute_s": t_pre,
+                       "tree_build_ms": tree_ms,
                        "levels": {str(l): stats[l]["pairs"] for l in levels},
                        "tile_fill": pairs_local / max(slots, 1),
                        "plan_modes": {str(l): stats[l].get("mode") for l in levels},

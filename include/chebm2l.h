@@ -172,6 +172,20 @@ int cfm_classify_fill(int device, int level, int64_t n_cells, const int32_t* ijk
                       const int64_t* offsets, int32_t* src_out, int8_t* t_out,
                       uint8_t* rep_out, uint8_t* perm_out);
 
+/* Octree construction on the GPU (octree.py:93-127):
+ * points n x 3 (host or device), bounding cube (center, half_width), depth
+ * >= 2.  Per level: occupied cells in the reference's row order
+ * (lexicographic ijk); leaf particle lists as CSR (offsets per leaf, particle
+ * indices ascending inside a leaf).  Particles outside the cube ->
+ * CFM_ERR_VALUE ("particle outside bounding box"), like the reference. */
+typedef struct cfm_tree cfm_tree;
+int cfm_tree_build(int device, const double* points, int64_t n, const double* center, double half_width, int depth,
+                   cfm_tree** out);
+int cfm_tree_level_size(cfm_tree* t, int level, int64_t* n_cells);
+int cfm_tree_level_cells(cfm_tree* t, int level, int32_t* ijk_out);
+int cfm_tree_leaf_particles(cfm_tree* t, int64_t* offsets_out, int64_t* perm_out);
+int cfm_tree_destroy(cfm_tree* t);
+
 /* Device-side timing of the last apply (ms, CUDA events on the apply stream),
  * and the number of kernels it launched. */
 int cfm_last_apply_stats(cfm_handler* h, double* ms, int64_t* launches);

@@ -45,6 +45,11 @@ EXPORTS = (
     "cfm_classify_count",
     "cfm_classify_fill",
     "cfm_last_apply_stats",
+    "cfm_tree_build",
+    "cfm_tree_level_size",
+    "cfm_tree_level_cells",
+    "cfm_tree_leaf_particles",
+    "cfm_tree_destroy",
 )
 
 _P = ctypes.c_void_p
@@ -72,6 +77,11 @@ _SIGS = {
     "cfm_classify_count": ([_I, _I, _I64, _P, _P, _P], _I),
     "cfm_classify_fill": ([_I, _I, _I64, _P, _P, _P, _P, _P, _P], _I),
     "cfm_last_apply_stats": ([_P, _P, _P], _I),
+    "cfm_tree_build": ([_I, _P, _I64, _P, _D, _I, ctypes.POINTER(_P)], _I),
+    "cfm_tree_level_size": ([_P, _I, _P], _I),
+    "cfm_tree_level_cells": ([_P, _I, _P], _I),
+    "cfm_tree_leaf_particles": ([_P, _P, _P], _I),
+    "cfm_tree_destroy": ([_P], _I),
 }
 
 _lib = None

@@ -36,6 +36,9 @@
 #include "tile_gemm_ws.cuh"
 #include "pair_reduce.cuh"
 #include "lowrank_ws.cuh"
+#include "tree.cuh"
+
+#include <cub/cub.cuh>
 
 namespace cfm {
 
@@ -1328,6 +1331,62 @@ static int guarded(F&& fn) {
 
 static cudaStream_t pick_stream(cfm_handler* h, void* s) { return s ? static_cast<cudaStream_t>(s) : h->stream; }
 
+// ------------------------------------------------------------------ octree
+struct TreeLevel {
+  int64_t n = 0;
+  DevBuf keys;  // sorted unique lexicographic keys
+};
+
+}  // namespace cfm
+
+struct cfm_tree {
+  int device = 0, depth = 0;
+  int64_t n_points = 0;
+  std::vector<cfm::TreeLevel> levels;  // index = level
+  cfm::DevBuf leaf_off, perm;          // leaf particle CSR (int64)
+};
+
+namespace cfm {
+
+template <class F>
+static void cub_call(F&& f, cudaStream_t s) {
+  size_t tmp = 0;
+  CUDA_CHECK(f(nullptr, tmp));
+  DevBuf t;
+  t.alloc(std::max<size_t>(tmp, 16));
+  CUDA_CHECK(f(t.p, tmp));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// sorted unique keys of `in` (n keys, device) -> out (device), returns count; optional run counts
+static int64_t sort_unique(const unsigned long long* in, int64_t n, DevBuf& out, DevBuf* counts, int end_bit,
+                           cudaStream_t s) {
+  DevBuf sorted, nsel;
+  sorted.alloc(std::max<size_t>(size_t(n) * 8, 16));
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, in, sorted.as<unsigned long long>(), int64_t(n), 0, end_bit, s);
+  }, s);
+  out.alloc(std::max<size_t>(size_t(n) * 8, 16));
+  nsel.alloc(16);
+  if (counts) {
+    counts->alloc(std::max<size_t>(size_t(n) * 8, 16));
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRunLengthEncode::Encode(t, b, sorted.as<unsigned long long>(), out.as<unsigned long long>(),
+                                                counts->as<long long>(), nsel.as<long long>(), int64_t(n), s);
+    }, s);
+  } else {
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceSelect::Unique(t, b, sorted.as<unsigned long long>(), out.as<unsigned long long>(),
+                                       nsel.as<long long>(), int64_t(n), s);
+    }, s);
+  }
+  long long m = 0;
+  CUDA_CHECK(cudaMemcpy(&m, nsel.p, 8, cudaMemcpyDeviceToHost));
+  return m;
+}
+
+static int key_bits(int level) { return std::max(1, 3 * level); }
+
 }  // namespace cfm
 
 // ===================================================================== C ABI
@@ -1700,6 +1759,131 @@ int cfm_classify_fill(int device, int level, int64_t n_cells, const int32_t* ijk
       throw;
     }
     cudaStreamDestroy(s);
+  });
+}
+
+int cfm_tree_build(int device, const double* points, int64_t n, const double* center, double half_width, int depth,
+                   cfm_tree** out) {
+  return guarded([&] {
+    if (!out || !center) throw Error(CFM_ERR_VALUE, "null argument");
+    if (depth < 2) throw Error(CFM_ERR_VALUE, "octree depth must be >= 2, got " + std::to_string(depth));
+    if (depth > 20) throw Error(CFM_ERR_VALUE, "octree depth must be <= 20");
+    if (n < 0) throw Error(CFM_ERR_VALUE, "negative particle count");
+    if (!(half_width > 0)) throw Error(CFM_ERR_VALUE, "half_width must be positive");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s = nullptr;
+    auto t = std::make_unique<cfm_tree>();
+    t->device = device;
+    t->depth = depth;
+    t->n_points = n;
+    t->levels.resize(depth + 1);
+    DevBuf d_pts;
+    const double* dp = points;
+    if (n && !is_device_ptr(points)) {
+      d_pts.alloc(size_t(n) * 24);
+      CUDA_CHECK(cudaMemcpy(d_pts.p, points, size_t(n) * 24, cudaMemcpyHostToDevice));
+      dp = d_pts.as<double>();
+    }
+    DevBuf keys, idx, skeys, sidx, bad;
+    keys.alloc(std::max<size_t>(size_t(n) * 8, 16));
+    idx.alloc(std::max<size_t>(size_t(n) * 8, 16));
+    bad.alloc(16);
+    CUDA_CHECK(cudaMemset(bad.p, 0, 4));
+    const double lx = center[0] - half_width, ly = center[1] - half_width, lz = center[2] - half_width;
+    const double width = 2.0 * half_width;
+    if (n) {
+      k_leaf_keys<<<unsigned((n + 255) / 256), 256, 0, s>>>(dp, n, lx, ly, lz, width, depth,
+                                                            keys.as<unsigned long long>(), idx.as<long long>(),
+                                                            bad.as<int>());
+      CUDA_CHECK(cudaGetLastError());
+    }
+    int hb = 0;
+    CUDA_CHECK(cudaMemcpy(&hb, bad.p, 4, cudaMemcpyDeviceToHost));
+    if (hb) throw Error(CFM_ERR_VALUE, "particle outside bounding box");
+    // stable sort of (leaf key, particle index): particle indices ascend within a leaf
+    skeys.alloc(std::max<size_t>(size_t(n) * 8, 16));
+    sidx.alloc(std::max<size_t>(size_t(n) * 8, 16));
+    t->perm.alloc(std::max<size_t>(size_t(n) * 8, 16));
+    if (n) {
+      cub_call([&](void* tp, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(tp, b, keys.as<unsigned long long>(), skeys.as<unsigned long long>(),
+                                               idx.as<long long>(), t->perm.as<long long>(), int64_t(n), 0,
+                                               key_bits(depth), s);
+      }, s);
+    }
+    // leaves: unique keys and run lengths -> CSR offsets
+    DevBuf counts;
+    TreeLevel& leaf = t->levels[depth];
+    leaf.n = n ? sort_unique(skeys.as<unsigned long long>(), n, leaf.keys, &counts, key_bits(depth), s) : 0;
+    std::vector<long long> hc(leaf.n), ho(leaf.n + 1, 0);
+    if (leaf.n) CUDA_CHECK(cudaMemcpy(hc.data(), counts.p, size_t(leaf.n) * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < leaf.n; ++i) ho[i + 1] = ho[i] + hc[i];
+    upload(t->leaf_off, ho);
+    // coarser levels: sorted unique parents
+    for (int L = depth; L >= 1; --L) {
+      const TreeLevel& c = t->levels[L];
+      TreeLevel& pl = t->levels[L - 1];
+      if (c.n == 0) {
+        pl.n = 0;
+        continue;
+      }
+      DevBuf par;
+      par.alloc(size_t(c.n) * 8);
+      k_parent_keys<<<unsigned((c.n + 255) / 256), 256, 0, s>>>(c.keys.as<unsigned long long>(), c.n, 1ll << L,
+                                                                par.as<unsigned long long>());
+      CUDA_CHECK(cudaGetLastError());
+      pl.n = sort_unique(par.as<unsigned long long>(), c.n, pl.keys, nullptr, key_bits(L - 1), s);
+    }
+    *out = t.release();
+  });
+}
+
+int cfm_tree_level_size(cfm_tree* t, int level, int64_t* n_cells) {
+  return guarded([&] {
+    if (!t || !n_cells) throw Error(CFM_ERR_VALUE, "null argument");
+    if (level < 0 || level > t->depth) throw Error(CFM_ERR_VALUE, "level outside the tree");
+    *n_cells = t->levels[level].n;
+  });
+}
+
+int cfm_tree_level_cells(cfm_tree* t, int level, int32_t* ijk_out) {
+  return guarded([&] {
+    if (!t || !ijk_out) throw Error(CFM_ERR_VALUE, "null argument");
+    if (level < 0 || level > t->depth) throw Error(CFM_ERR_VALUE, "level outside the tree");
+    CUDA_CHECK(cudaSetDevice(t->device));
+    const TreeLevel& L = t->levels[level];
+    if (!L.n) return;
+    const bool dev = is_device_ptr(ijk_out);
+    DevBuf tmp;
+    int* d = ijk_out;
+    if (!dev) {
+      tmp.alloc(size_t(L.n) * 12);
+      d = tmp.as<int>();
+    }
+    k_keys_to_ijk<<<unsigned((L.n + 255) / 256), 256>>>(L.keys.as<unsigned long long>(), L.n, 1ll << level, d);
+    CUDA_CHECK(cudaGetLastError());
+    if (!dev) CUDA_CHECK(cudaMemcpy(ijk_out, d, size_t(L.n) * 12, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaDeviceSynchronize());
+  });
+}
+
+int cfm_tree_leaf_particles(cfm_tree* t, int64_t* offsets_out, int64_t* perm_out) {
+  return guarded([&] {
+    if (!t) throw Error(CFM_ERR_VALUE, "null argument");
+    CUDA_CHECK(cudaSetDevice(t->device));
+    const int64_t nl = t->levels[t->depth].n;
+    if (offsets_out)
+      CUDA_CHECK(cudaMemcpy(offsets_out, t->leaf_off.p, size_t(nl + 1) * 8, cudaMemcpyDefault));
+    if (perm_out && t->n_points)
+      CUDA_CHECK(cudaMemcpy(perm_out, t->perm.p, size_t(t->n_points) * 8, cudaMemcpyDefault));
+  });
+}
+
+int cfm_tree_destroy(cfm_tree* t) {
+  return guarded([&] {
+    if (!t) return;
+    cudaSetDevice(t->device);
+    delete t;
   });
 }
 

@@ -409,3 +409,42 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda):
         assert np.array_equal(a6, ref6.cpu().numpy())
         assert np.array_equal(a3, ref3.cpu().numpy())
     assert st["pairs"] == (6 * 64 - 8) ** 3 - (3 * 64 - 2) ** 3
+
+
+@pytest.mark.parametrize("case", ["cfg1", "helm", "lapcplx", "sphere9", "sphere_lists"])
+def test_gpu_tree_matches_reference(torch_cuda, golden, case):
+    """GPU octree (§8f rank 1): occupied cells per level equal the reference's
+    build_tree output (golden), leaf particle lists equal the oracle's."""
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from geometry import cube_points, sphere_points
+
+    from paper_1210_7292_b200.octree import build_tree_gpu
+
+    g = golden(case)
+    pts = {"cfg1": lambda: cube_points(10_000, 1), "helm": lambda: sphere_points(3_000, 5),
+           "lapcplx": lambda: cube_points(2_000, 11), "sphere9": lambda: sphere_points(20_000, 3),
+           "sphere_lists": lambda: sphere_points(30_000, 21)}[case]()
+    center, hw = tuple(g["bbox_center"]), float(g["bbox_half"])
+    tree = build_tree_gpu(pts, center, hw, int(g["depth"]))
+    for lvl in g["levels"]:
+        assert np.array_equal(tree.cells(int(lvl)), g[f"cells_{lvl}"].astype(np.int32))
+    off, perm = tree.leaf_particles()
+    depth = int(g["depth"])
+    side = 1 << depth
+    low = np.asarray(center) - hw
+    ijk = np.minimum(((pts - low) / (2 * hw) * side).astype(np.int64), side - 1)
+    key = (ijk[:, 0] * side + ijk[:, 1]) * side + ijk[:, 2]
+    order = np.lexsort((np.arange(len(pts)), key))
+    assert np.array_equal(perm, order)
+    assert off[-1] == len(pts) and len(off) - 1 == len(np.unique(key))
+
+
+def test_gpu_tree_errors(torch_cuda):
+    from paper_1210_7292_b200.octree import build_tree_gpu
+
+    with pytest.raises(ValueError):
+        build_tree_gpu(np.array([[2.0, 0.5, 0.5]]), (0.5, 0.5, 0.5), 0.5, 3)
+    with pytest.raises(ValueError):
+        build_tree_gpu(np.array([[0.2, 0.5, 0.5]]), (0.5, 0.5, 0.5), 0.5, 1)
+    t = build_tree_gpu(np.array([[1.0, 1.0, 1.0], [0.0, 0.0, 0.0]]), (0.5, 0.5, 0.5), 0.5, 2)
+    assert np.array_equal(t.cells(2), [[0, 0, 0], [3, 3, 3]])
