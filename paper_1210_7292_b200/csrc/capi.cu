@@ -215,27 +215,33 @@ struct cfm_handler {
 namespace cfm {
 
 // ------------------------------------------------------------------ launching
-// Kernel selection (CFM_TILE_KERNEL): "ws16" warp-specialized KC=16 x 5 stages
-// (default), "ws32" KC=32 x 3 stages, "sync" the lockstep kernel, "ws16w"
+// Kernel selection (CFM_TILE_KERNEL): "ws32" warp-specialized KC=32 x 3 stages
+// with TMA bulk copies of the operator rows (default, CFM_BULK_A=1), "ws16"
+// KC=16 x 5 stages, "sync" the lockstep kernel, "ws16w"
 // like ws16 with 16 consumer warps (32x16 warp tiles) on 128-row blocks.
-static int tile_kernel_kind() {
-  static int kind = [] {
+// Default by inner length (measured, profiles/r01_summary.md): KC=32 with bulk
+// operator rows up to nk = 512 (l <= 7), KC=16 with cp.async rows above (l = 9).
+static int tile_kernel_kind(int nk = 0) {
+  static int forced = [] {
     const char* v = getenv("CFM_TILE_KERNEL");
-    if (!v) return 1;
+    if (!v) return -1;
     if (!strcmp(v, "ws32")) return 0;
+    if (!strcmp(v, "ws16")) return 1;
     if (!strcmp(v, "sync")) return 2;
     if (!strcmp(v, "ws16w")) return 3;
-    return 1;
+    return -1;
   }();
-  return kind;
+  if (forced >= 0) return forced;
+  return nk > 512 ? 1 : 0;
 }
 
-static bool use_bulk_a() {
+static bool use_bulk_a(int kc) {
   static int v = [] {
     const char* e = getenv("CFM_BULK_A");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
-  return v != 0;
+  if (v >= 0) return v != 0;
+  return kc >= 32;  // 256-B row chunks: bulk copies win; 128-B: cp.async wins
 }
 
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
@@ -244,7 +250,7 @@ static void launch_ws_multi(const MultiTileParams& mp, dim3 grid, cudaStream_t s
   const bool tabs = tile_perm_tabs_fit(q.nr, q.nk);
   const int smem = ws_ring_bytes<BM, BN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, tabs);
   if constexpr (BM == 128) {
-    if (use_bulk_a() && q.zero_row && q.op_ld <= 8192) {
+    if (use_bulk_a(KC) && q.zero_row && q.op_ld <= 8192) {
       auto kb = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, STAGES, SKIP, true>;
       CUDA_CHECK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       kb<<<grid, (WM * WN + 4) * 32, smem, s>>>(mp);
@@ -281,7 +287,7 @@ static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStre
   TileParams q = p;
   q.tile_base = tile_base;
   dim3 grid(n_tiles, (p.nr + BM - 1) / BM);
-  const int kind = (p.pair_out && tile_kernel_kind() == 2) ? 1 : tile_kernel_kind();
+  const int kind = (p.pair_out && tile_kernel_kind(p.nk) == 2) ? 1 : tile_kernel_kind(p.nk);
   if (p.op_rows) {
     if (kind == 2) launch_sync<BM, BN, WM, WN, true>(q, grid, s);
     else if (kind == 1) launch_ws<BM, BN, WM, WN, 16, 5, true>(q, grid, s);
@@ -384,7 +390,7 @@ static int64_t launch_multi(const std::vector<TileParams>& segs, const std::vect
   if (total >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
   mp.start[mp.n_seg] = int(total);
   const TileParams& q = mp.seg[0];
-  const int kind = tile_kernel_kind();
+  const int kind = tile_kernel_kind(q.nk);
   if (q.nr <= 32) {
     dim3 grid(unsigned(total), (q.nr + 31) / 32);
     if (kind == 0) launch_ws_multi<32, kBN, 1, 8, 32, 3, false>(mp, grid, s);
@@ -1128,6 +1134,9 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         if (exp && !strcmp(exp, "nowait")) p.debug = 1;
         if (exp && !strcmp(exp, "spin")) p.debug = 2;
         if (exp && !strcmp(exp, "nocopy")) p.debug = 4;
+        if (exp && !strcmp(exp, "zfillA")) p.debug = 8;
+        if (exp && !strcmp(exp, "zfillB")) p.debug = 16;
+        if (exp && !strcmp(exp, "zfillAB")) p.debug = 24;
       }
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
@@ -1163,7 +1172,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         const LevelPlan& P = *lv[i].lp;
         const long long row_ld = (long long)h->n * (P.dc == 2 || h->op_complex ? 2 : 1);
         const double work = double(P.red.frow.size()) * double(row_ld);
-        if (P.mode == 1 && work <= 1.6e7 && !P.red.tgt.empty()) {
+        if (P.mode == 1 && work <= 2.0e6 && !P.red.tgt.empty()) {
           TileParams& q = segs[i];
           q.red_counter = h->counters.as<unsigned>() + i;
           q.red_ctas = int(counts[i]) * ((q.nr + 127) / 128);

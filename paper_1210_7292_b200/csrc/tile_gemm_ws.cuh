@@ -246,7 +246,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
           for (int u = 0; u < A_PER_T; ++u) {
             const int id = pt + u * NP;
             const int i = id / (KC / 2), kp = id % (KC / 2);
-            cp_async16(as + i * LDA + 2 * kp, a_ok[u] ? (const void*)(a_row[u] + k0) : (const void*)p.ops, a_ok[u]);
+            const bool ok = a_ok[u] && !(p.debug & 8);
+            cp_async16(as + i * LDA + 2 * kp, ok ? (const void*)(a_row[u] + k0) : (const void*)p.ops, ok);
           }
         }
         const int kk = pt % KC;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
 #pragma unroll
         for (int u = 0; u < B_PER_T; ++u) {
           const int c = pt / KC + u * (NP / KC);
-          const bool ok = kvalid && b_col[u] != nullptr;
+          const bool ok = kvalid && b_col[u] != nullptr && !(p.debug & 16);
           cp_async8(bs + c * LDB + kk, ok ? (const void*)(b_col[u] + (long long)p.x_dc * j) : (const void*)p.ops, ok);
         }
         mbar_cp_async_arrive(full + s);

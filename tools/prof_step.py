@@ -23,7 +23,8 @@ def main():
     cells, widths = bench.cached_level_cells(a.config)
     levels = sorted(cells)
     full = full_far_field_vectors()
-    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps)
+    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps,
+                     budget_bytes=4_000_000_000 if variant in ("sa", "sarcmp") else 2_000_000_000)
     h.precompute({l: full for l in levels}, widths)
     for l in levels:
         h.plan_level_cells(l, cells[l].astype("int32"))
