@@ -462,6 +462,40 @@ def run_b200(args):
         except Exception:
             traffic = None
 
+    # Classifier (row a) on its own: device far-list classification of the
+    # deepest level (HBM-bound integer work), timed with CUDA events.
+    classifier = None
+    if rank == 0:
+        import ctypes
+
+        from paper_1210_7292_b200 import _native
+
+        lib = _native.load()
+        deep_cells = torch.from_numpy(cells[levels[-1]].astype(np.int32)).to(dev)
+        ncell = len(cells[levels[-1]])
+        offs = np.zeros(ncell + 1, np.int64)
+        tot = ctypes.c_int64()
+        reps = []
+        for i in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _native.check(lib.cfm_classify_count(local, levels[-1], ncell, deep_cells.data_ptr(), offs.ctypes.data,
+                                                 ctypes.byref(tot)))
+            src = np.empty(tot.value, np.int32)
+            tv = np.empty((tot.value, 3), np.int8)
+            _native.check(lib.cfm_classify_fill(local, levels[-1], ncell, deep_cells.data_ptr(), offs.ctypes.data,
+                                                src.ctypes.data, tv.ctypes.data, None, None))
+            reps.append(time.perf_counter() - t0)
+        cl_s = min(reps[1:])
+        # algorithmic bytes: grid scatter (4 B/cell), 2 passes reading cells (12 B) and writing counts
+        # (4 B), per pair 4 B source row + 3 B transfer vector written
+        cl_bytes = ncell * (4 + 2 * 12 + 4) + tot.value * 7
+        classifier = {"level": levels[-1], "pairs": tot.value, "ms_incl_host_copies": cl_s * 1e3,
+                      "pairs_per_s": tot.value / cl_s, "algorithmic_bytes": cl_bytes,
+                      "note": "cfm_classify_count + cfm_classify_fill with device cells and host outputs "
+                              "(includes the D2H of the lists)"}
+        del deep_cells
+
     # BASELINE config 2 also names the per-pair SVD-compressed variant (iablk,
     # eps=1e-5): measured in the same run on the same device-resident inputs.
     secondary = None
@@ -542,6 +576,8 @@ def run_b200(args):
             line["cpu_baseline"] = cpu
         if secondary:
             line["secondary_variant"] = secondary
+        if classifier:
+            line["classifier"] = classifier
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

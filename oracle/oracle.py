@@ -356,11 +356,19 @@ class OracleM2L:
         blocks = {t: self._op(t, width) for t in transfers}
         row = np.hstack([blocks[t] for t in transfers])
         col = np.vstack([blocks[t] for t in transfers])
-        u_row, s_row, vh_row = np.linalg.svd(row, full_matrices=False)
-        _, s_col, vh_col = np.linalg.svd(col, full_matrices=False)
+        if self.compression == "svd":
+            u_row, s_row, vh_row = np.linalg.svd(row, full_matrices=False)
+            _, s_col, vh_col = np.linalg.svd(col, full_matrices=False)
+            r = max(eps_rank(s_row, self.eps), eps_rank(s_col, self.eps))
+            u, sig, vh, b = u_row[:, :r], s_row[:r], vh_row[:r], vh_col[:r].conj().T
+        else:  # m2l.py:241-255: ACA on the concatenations
+            L, R = aca_svd(lambda i, j: row[np.asarray(i), np.asarray(j)], n, row.shape[1], self.eps)
+            _, Rc = aca_svd(lambda i, j: col[np.asarray(i), np.asarray(j)], col.shape[0], n, self.eps)
+            sig = np.linalg.norm(L, axis=0)
+            u = L / sig
+            vh = R.conj().T
+            b = Rc
         self.factorization_calls += 2
-        r = max(eps_rank(s_row, self.eps), eps_rank(s_col, self.eps))
-        u, sig, vh, b = u_row[:, :r], s_row[:r], vh_row[:r], vh_col[:r].conj().T
         cores = {t: ("dense", (sig[:, None] * vh[:, k * n:(k + 1) * n]) @ b) for k, t in enumerate(transfers)}
         if self.variant == "sarcmp":
             for t, (_, c) in list(cores.items()):

@@ -117,7 +117,7 @@ def _csr(batch):
 
 
 def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
-             budget=2_000_000_000, store_rows=None, seeded_mpoles=None, extra=None):
+             budget=2_000_000_000, store_rows=None, seeded_mpoles=None, extra=None, compression="svd"):
     """Build tree/lists with the reference, run every variant's apply_level per
     level on identical multipoles, and store inputs + outputs + accounting."""
     t0 = time.time()
@@ -127,7 +127,7 @@ def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
     levels = lists.far_levels()
     lt = {lvl: unique_transfer_vectors(lists, lvl) for lvl in levels}
     lw = {lvl: tree.cell_width(lvl) for lvl in levels}
-    out = dict(order=order, eps=eps, depth=depth, levels=np.asarray(levels),
+    out = dict(order=order, eps=eps, depth=depth, levels=np.asarray(levels), compression=np.asarray(compression),
                widths=np.asarray([lw[l] for l in levels]),
                kernel=np.asarray(kernel.name), bbox_center=np.asarray(bbox.center),
                bbox_half=bbox.half_width)
@@ -158,7 +158,7 @@ def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
             rows = np.sort(rng.choice(len(cells), min(store_rows, len(cells)), replace=False))
             out[f"rows_{lvl}"] = rows.astype(np.int32)
     for v in variants:
-        h = make_handler(v, kernel, grid, eps, budget_bytes=budget)
+        h = make_handler(v, kernel, grid, eps, budget_bytes=budget, compression=compression)
         tp = time.time()
         h.precompute(lt, lw)
         tp = time.time() - tp
@@ -194,6 +194,11 @@ def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
 
 
 def main() -> None:
+    only = set(sys.argv[1:])
+    if only:
+        if "aca" in only:
+            aca_case()
+        return
     symmetry_fixture()
 
     # BASELINE config 1: N=10,000 uniform cube, height 4 -> reference depth 3,
@@ -237,6 +242,17 @@ def main() -> None:
     w = np.random.default_rng(22).uniform(-1.0, 1.0, len(pts))
     run_case("sphere_lists", pts, w, AffineMap((0.0, 0.0, 0.0), 1.0), 4, laplace_kernel(), 3, 1e-3,
              ("nasym",), seeded_mpoles=44, store_rows=32)
+
+    aca_case()
+
+
+def aca_case() -> None:
+    # compression="aca" (lowrank.py:65-184, m2l.py:206-214 / 241-255): cube,
+    # l = 4, eps = 1e-4, multipoles from the reference's P2M/M2M.
+    pts = cube_points(3_000, seed=31)
+    w = np.random.default_rng(32).uniform(-1.0, 1.0, len(pts))
+    run_case("aca", pts, w, AffineMap((0.5, 0.5, 0.5), 0.5), 3, laplace_kernel(), 4, 1e-4,
+             ("ia", "iasym", "iablk", "sa", "sarcmp"), compression="aca")
 
 
 if __name__ == "__main__":

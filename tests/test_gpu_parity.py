@@ -61,13 +61,16 @@ def _handler(g, variant, **kw):
 
     kernel, grid = _kernel_grid(g)
     levels, lt, lw = _lt_lw(g)
+    if "compression" in g:
+        kw.setdefault("compression", str(g["compression"]))
     h = make_handler(variant, kernel, grid, float(g["eps"]), **kw)
     h.precompute(lt, lw)
     return h, levels
 
 
 CASES = [("cfg1", v) for v in O.VARIANTS] + [("helm", v) for v in O.VARIANTS] + \
-    [("lapcplx", v) for v in ("na", "nablk", "iablk", "sa")] + [("sphere_lists", "nasym")]
+    [("lapcplx", v) for v in ("na", "nablk", "iablk", "sa")] + [("sphere_lists", "nasym")] + \
+    [("aca", v) for v in ("ia", "iasym", "iablk", "sa", "sarcmp")]
 
 
 @pytest.mark.parametrize("case,variant", CASES)

@@ -12,7 +12,7 @@ from oracle import oracle as O
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
 from geometry import cube_points, sphere_points  # noqa: E402
 
-CASES = ("cfg1", "helm", "lapcplx", "sphere9", "sphere_lists")
+CASES = ("cfg1", "helm", "lapcplx", "sphere9", "sphere_lists", "aca")
 
 
 def test_symmetry_tables(golden):
@@ -70,6 +70,8 @@ def _points(case):
         return cube_points(2_000, 11), (0.5, 0.5, 0.5), 0.5
     if case == "sphere9":
         return sphere_points(20_000, 3), (0.0, 0.0, 0.0), 1.0
+    if case == "aca":
+        return cube_points(3_000, 31), (0.5, 0.5, 0.5), 0.5
     return sphere_points(30_000, 21), (0.0, 0.0, 0.0), 1.0
 
 
@@ -107,7 +109,8 @@ def _oracle_for(g, variant):
     levels = [int(l) for l in g["levels"]]
     lt = {l: sorted({tuple(int(c) for c in t) for t in g[f"t_{l}"]}) for l in levels}
     lw = dict(zip(levels, (float(w) for w in g["widths"])))
-    return O.OracleM2L(variant, prof, dt, order, eps, deg).precompute(lt, lw), levels
+    comp = str(g["compression"]) if "compression" in g else "svd"
+    return O.OracleM2L(variant, prof, dt, order, eps, deg, compression=comp).precompute(lt, lw), levels
 
 
 def _mpoles(g, lvl, case):
@@ -128,7 +131,8 @@ def _variants(g):
 
 
 FAST_CASES = [("cfg1", v) for v in O.VARIANTS] + [("helm", v) for v in O.VARIANTS] + \
-    [("lapcplx", v) for v in ("na", "nablk", "iablk", "sa")] + [("sphere_lists", "nasym")]
+    [("lapcplx", v) for v in ("na", "nablk", "iablk", "sa")] + [("sphere_lists", "nasym")] + \
+    [("aca", v) for v in ("ia", "iasym", "iablk", "sa", "sarcmp")]
 
 
 @pytest.mark.parametrize("case,variant", FAST_CASES)
