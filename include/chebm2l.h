@@ -154,6 +154,14 @@ int cfm_apply_levels(cfm_handler* h, int n_levels, const int* levels, const doub
 int cfm_plan_stats(cfm_handler* h, int level, int64_t* n_tiles, int64_t* n_entries,
                    int64_t* n_pairs, int64_t* n_slots, int64_t* n_targets, int64_t* n_sources);
 
+/* Device-output classifier (all pointers device, work on `stream`):
+ * offsets_dev gets n_cells+1 int64 CSR offsets (total returned on the host);
+ * fill writes per pair the source row (int32) and t-code (int16). */
+int cfm_classify_count_device(int device, int level, int64_t n_cells, const int32_t* ijk, int64_t* offsets_dev,
+                              int64_t* total_out, void* stream);
+int cfm_classify_fill_device(int device, int level, int64_t n_cells, const int32_t* ijk, const int64_t* offsets_dev,
+                             int32_t* src_dev, int16_t* code_dev, void* stream);
+
 /* Plan layout chosen for a level: mode 0 = target tiles (per-target register
  * accumulators; dense trees), 1 = pair entries + ordered per-target reduction
  * (sparse trees, chosen when target tiles would be < 60% full; override with

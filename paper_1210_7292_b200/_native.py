@@ -44,6 +44,8 @@ EXPORTS = (
     "cfm_plan_info",
     "cfm_classify_count",
     "cfm_classify_fill",
+    "cfm_classify_count_device",
+    "cfm_classify_fill_device",
     "cfm_last_apply_stats",
     "cfm_tree_build",
     "cfm_tree_level_size",
@@ -76,6 +78,8 @@ _SIGS = {
     "cfm_plan_info": ([_P, _I, _P, _P], _I),
     "cfm_classify_count": ([_I, _I, _I64, _P, _P, _P], _I),
     "cfm_classify_fill": ([_I, _I, _I64, _P, _P, _P, _P, _P, _P], _I),
+    "cfm_classify_count_device": ([_I, _I, _I64, _P, _P, _P, _P], _I),
+    "cfm_classify_fill_device": ([_I, _I, _I64, _P, _P, _P, _P, _P], _I),
     "cfm_last_apply_stats": ([_P, _P, _P], _I),
     "cfm_tree_build": ([_I, _P, _I64, _P, _D, _I, ctypes.POINTER(_P)], _I),
     "cfm_tree_level_size": ([_P, _I, _P], _I),

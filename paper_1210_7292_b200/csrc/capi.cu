@@ -1771,6 +1771,70 @@ int cfm_classify_fill(int device, int level, int64_t n_cells, const int32_t* ijk
   });
 }
 
+// Device-output classifier: offsets/sources/codes stay on the device (for a
+// device-side pipeline and for timing the kernels alone).  ijk must be device.
+int cfm_classify_count_device(int device, int level, int64_t n_cells, const int32_t* ijk, int64_t* offsets_dev,
+                              int64_t* total_out, void* stream) {
+  return guarded([&] {
+    if (level < 2 || level > 9) throw Error(CFM_ERR_VALUE, "classifier supports levels 2..9");
+    if (!is_device_ptr(ijk) || !is_device_ptr(offsets_dev)) throw Error(CFM_ERR_VALUE, "device pointers required");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    init_cone_table();
+    const int S = 1 << level;
+    static thread_local DevBuf grid, counts;
+    grid.alloc(size_t(S) * S * S * sizeof(int));
+    counts.alloc(std::max<size_t>(size_t(n_cells + 1) * sizeof(long long), 16));
+    CUDA_CHECK(cudaMemsetAsync(grid.p, 0xff, size_t(S) * S * S * sizeof(int), s));
+    const unsigned nb = unsigned((n_cells + 255) / 256);
+    if (n_cells) {
+      k_grid_scatter<<<nb, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>());
+      const unsigned nbw = unsigned((n_cells * 32 + 255) / 256);
+      k_classify_warp<false><<<nbw, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>(), reinterpret_cast<int*>(counts.p),
+                                                 nullptr, nullptr, nullptr);
+      CUDA_CHECK(cudaGetLastError());
+    }
+    // offsets = exclusive scan of the counts (int -> int64), n+1 entries
+    CUDA_CHECK(cudaMemsetAsync(offsets_dev, 0, sizeof(int64_t), s));
+    if (n_cells) {
+      size_t tmp = 0;
+      const int* cin = reinterpret_cast<const int*>(counts.p);
+      CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cin, reinterpret_cast<long long*>(offsets_dev) + 1,
+                                               int64_t(n_cells), s));
+      DevBuf t;
+      t.alloc(std::max<size_t>(tmp, 16));
+      CUDA_CHECK(cub::DeviceScan::InclusiveSum(t.p, tmp, cin, reinterpret_cast<long long*>(offsets_dev) + 1,
+                                               int64_t(n_cells), s));
+    }
+    long long total = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&total, offsets_dev + n_cells, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (total_out) *total_out = total;
+  });
+}
+
+int cfm_classify_fill_device(int device, int level, int64_t n_cells, const int32_t* ijk, const int64_t* offsets_dev,
+                             int32_t* src_dev, int16_t* code_dev, void* stream) {
+  return guarded([&] {
+    if (level < 2 || level > 9) throw Error(CFM_ERR_VALUE, "classifier supports levels 2..9");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    init_cone_table();
+    const int S = 1 << level;
+    static thread_local DevBuf grid;
+    grid.alloc(size_t(S) * S * S * sizeof(int));
+    CUDA_CHECK(cudaMemsetAsync(grid.p, 0xff, size_t(S) * S * S * sizeof(int), s));
+    const unsigned nb = unsigned((n_cells + 255) / 256);
+    if (n_cells) {
+      k_grid_scatter<<<nb, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>());
+      const unsigned nbw = unsigned((n_cells * 32 + 255) / 256);
+      k_classify_warp<true><<<nbw, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>(), nullptr,
+                                                reinterpret_cast<const long long*>(offsets_dev), src_dev, code_dev);
+      CUDA_CHECK(cudaGetLastError());
+    }
+  });
+}
+
 int cfm_tree_build(int device, const double* points, int64_t n, const double* center, double half_width, int depth,
                    cfm_tree** out) {
   return guarded([&] {

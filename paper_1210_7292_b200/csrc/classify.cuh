@@ -82,4 +82,44 @@ __global__ void k_classify(const int* __restrict__ ijk, long long n, int S, cons
   if (!FILL) counts[i] = cnt;
 }
 
+// Warp per target: lane l handles candidates l, l+32, ... (216 in source-ijk
+// order); kept pairs are compacted in candidate order with ballot/popc, so
+// the output order is the reference's.  Counts (FILL=false) or writes (FILL).
+template <bool FILL>
+__global__ void k_classify_warp(const int* __restrict__ ijk, long long n, int S, const int* __restrict__ grid,
+                                int* __restrict__ counts, const long long* __restrict__ off,
+                                int* __restrict__ src_out, int16_t* __restrict__ code_out) {
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int x = __ldg(ijk + 3 * w), y = __ldg(ijk + 3 * w + 1), z = __ldg(ijk + 3 * w + 2);
+  const int bx = 2 * ((x >> 1) - 1), by = 2 * ((y >> 1) - 1), bz = 2 * ((z >> 1) - 1);
+  long long base = FILL ? off[w] : 0;
+  int total = 0;
+#pragma unroll
+  for (int r = 0; r < 7; ++r) {  // 7 x 32 >= 216 candidates
+    const int cidx = r * 32 + lane;
+    bool keep = false;
+    int row = -1, code = 0;
+    if (cidx < 216) {
+      const int sx = bx + cidx / 36, sy = by + (cidx / 6) % 6, sz = bz + cidx % 6;
+      const int t0 = x - sx, t1 = y - sy, t2 = z - sz;
+      if (sx >= 0 && sx < S && sy >= 0 && sy < S && sz >= 0 && sz < S && is_far(t0, t1, t2)) {
+        row = __ldg(grid + ((long long)sx * S + sy) * S + sz);
+        keep = row >= 0;
+        code = tcode(t0, t1, t2);
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (FILL && keep) {
+      const long long pos = base + __popc(m & ((1u << lane) - 1u));
+      src_out[pos] = row;
+      code_out[pos] = int16_t(code);
+    }
+    base += __popc(m);
+    total += __popc(m);
+  }
+  if (!FILL && lane == 0) counts[w] = total;
+}
+
 }  // namespace cfm

@@ -451,3 +451,33 @@ def test_gpu_tree_errors(torch_cuda):
         build_tree_gpu(np.array([[0.2, 0.5, 0.5]]), (0.5, 0.5, 0.5), 0.5, 1)
     t = build_tree_gpu(np.array([[1.0, 1.0, 1.0], [0.0, 0.0, 0.0]]), (0.5, 0.5, 0.5), 0.5, 2)
     assert np.array_equal(t.cells(2), [[0, 0, 0], [3, 3, 3]])
+
+
+@pytest.mark.parametrize("case", ["cfg1", "sphere_lists"])
+def test_device_classifier_matches_reference(torch_cuda, golden, case):
+    import ctypes
+
+    from paper_1210_7292_b200 import _native
+
+    torch = torch_cuda
+    lib = _native.load()
+    g = golden(case)
+    for lvl in g["levels"]:
+        cells = torch.from_numpy(g[f"cells_{lvl}"].astype(np.int32)).cuda()
+        n = len(cells)
+        offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        tot = ctypes.c_int64()
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _native.check(lib.cfm_classify_count_device(0, int(lvl), n, cells.data_ptr(), offs.data_ptr(),
+                                                    ctypes.byref(tot), st))
+        src = torch.empty(tot.value, dtype=torch.int32, device="cuda")
+        code = torch.empty(tot.value, dtype=torch.int16, device="cuda")
+        _native.check(lib.cfm_classify_fill_device(0, int(lvl), n, cells.data_ptr(), offs.data_ptr(), src.data_ptr(),
+                                                   code.data_ptr(), st))
+        torch.cuda.synchronize()
+        o = offs.cpu().numpy()
+        rows = np.nonzero(np.diff(o))[0]
+        assert np.array_equal(rows, g[f"tgt_{lvl}"])
+        assert np.array_equal(src.cpu().numpy(), g[f"src_{lvl}"])
+        t = g[f"t_{lvl}"].astype(np.int64)
+        assert np.array_equal(code.cpu().numpy(), (t[:, 0] + 3) * 49 + (t[:, 1] + 3) * 7 + (t[:, 2] + 3))
