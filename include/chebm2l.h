@@ -194,6 +194,25 @@ int cfm_tree_level_cells(cfm_tree* t, int level, int32_t* ijk_out);
 int cfm_tree_leaf_particles(cfm_tree* t, int64_t* offsets_out, int64_t* perm_out);
 int cfm_tree_destroy(cfm_tree* t);
 
+/* The FMM stages around M2L on the GPU, on a tree
+ * from cfm_tree_build.  shift_mats: 8 octant matrices (parent x child, n x n,
+ * octant = 4 cx + 2 cy + cz; engine.py:41-63).  All arrays are device
+ * pointers; level arrays are rows x n (x2 doubles when complex), rows in the
+ * tree's row order; potentials are in the original particle order.
+ *   p2m  engine.py:122-127   m2m engine.py:129-138 (child level -> parent, +=)
+ *   l2l  engine.py:159-168 (parent level -> child, +=)
+ *   l2p  engine.py:170-175 (+=)   p2p engine.py:177-199 (+=; kernel 0 Laplace
+ *   1/(4 pi r), 1 Helmholtz exp(ikr)/(4 pi r); coincident points skipped) */
+typedef struct cfm_fmm cfm_fmm;
+int cfm_fmm_create(cfm_tree* t, int order, const double* shift_mats, cfm_fmm** out);
+int cfm_fmm_destroy(cfm_fmm* f);
+int cfm_fmm_p2m(cfm_fmm* f, const double* weights, int data_complex, double* leaf_mpoles, void* stream);
+int cfm_fmm_m2m(cfm_fmm* f, int child_level, const double* child, double* parent, int data_complex, void* stream);
+int cfm_fmm_l2l(cfm_fmm* f, int parent_level, const double* parent, double* child, int data_complex, void* stream);
+int cfm_fmm_l2p(cfm_fmm* f, const double* leaf_locals, int data_complex, double* potentials, void* stream);
+int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights, int weights_complex,
+                double* potentials, int out_complex, void* stream);
+
 /* Device-side timing of the last apply (ms, CUDA events on the apply stream),
  * and the number of kernels it launched. */
 int cfm_last_apply_stats(cfm_handler* h, double* ms, int64_t* launches);

@@ -52,6 +52,13 @@ EXPORTS = (
     "cfm_tree_level_cells",
     "cfm_tree_leaf_particles",
     "cfm_tree_destroy",
+    "cfm_fmm_create",
+    "cfm_fmm_destroy",
+    "cfm_fmm_p2m",
+    "cfm_fmm_m2m",
+    "cfm_fmm_l2l",
+    "cfm_fmm_l2p",
+    "cfm_fmm_p2p",
 )
 
 _P = ctypes.c_void_p
@@ -86,6 +93,13 @@ _SIGS = {
     "cfm_tree_level_cells": ([_P, _I, _P], _I),
     "cfm_tree_leaf_particles": ([_P, _P, _P], _I),
     "cfm_tree_destroy": ([_P], _I),
+    "cfm_fmm_create": ([_P, _I, _P, ctypes.POINTER(_P)], _I),
+    "cfm_fmm_destroy": ([_P], _I),
+    "cfm_fmm_p2m": ([_P, _P, _I, _P, _P], _I),
+    "cfm_fmm_m2m": ([_P, _I, _P, _P, _I, _P], _I),
+    "cfm_fmm_l2l": ([_P, _I, _P, _P, _I, _P], _I),
+    "cfm_fmm_l2p": ([_P, _P, _I, _P, _P], _I),
+    "cfm_fmm_p2p": ([_P, _I, _D, _P, _I, _P, _I, _P], _I),
 }
 
 _lib = None

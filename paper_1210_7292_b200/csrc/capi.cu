@@ -37,6 +37,7 @@
 #include "pair_reduce.cuh"
 #include "lowrank_ws.cuh"
 #include "tree.cuh"
+#include "fmm.cuh"
 
 #include <cub/cub.cuh>
 
@@ -1351,8 +1352,19 @@ struct TreeLevel {
 struct cfm_tree {
   int device = 0, depth = 0;
   int64_t n_points = 0;
+  double center[3] = {0, 0, 0}, half = 1.0;
   std::vector<cfm::TreeLevel> levels;  // index = level
   cfm::DevBuf leaf_off, perm;          // leaf particle CSR (int64)
+  cfm::DevBuf points;                  // n x 3 on the device (original order)
+};
+
+struct cfm_fmm {
+  cfm_tree* tree = nullptr;
+  int order = 0, n = 0;
+  cfm::DevBuf troots, leaf_ijk, leaf_grid, leaf_of_pos;
+  cfm::OpStack m2m_ops, l2l_ops;
+  cfm::CodeMap octmap;
+  std::map<int, cfm::LevelPlan> m2m_plans, l2l_plans;  // key: child level / parent level (x dc)
 };
 
 namespace cfm {
@@ -1850,13 +1862,11 @@ int cfm_tree_build(int device, const double* points, int64_t n, const double* ce
     t->depth = depth;
     t->n_points = n;
     t->levels.resize(depth + 1);
-    DevBuf d_pts;
-    const double* dp = points;
-    if (n && !is_device_ptr(points)) {
-      d_pts.alloc(size_t(n) * 24);
-      CUDA_CHECK(cudaMemcpy(d_pts.p, points, size_t(n) * 24, cudaMemcpyHostToDevice));
-      dp = d_pts.as<double>();
-    }
+    for (int a = 0; a < 3; ++a) t->center[a] = center[a];
+    t->half = half_width;
+    t->points.alloc(std::max<size_t>(size_t(n) * 24, 16));
+    if (n) CUDA_CHECK(cudaMemcpy(t->points.p, points, size_t(n) * 24, cudaMemcpyDefault));
+    const double* dp = t->points.as<double>();
     DevBuf keys, idx, skeys, sidx, bad;
     keys.alloc(std::max<size_t>(size_t(n) * 8, 16));
     idx.alloc(std::max<size_t>(size_t(n) * 8, 16));
@@ -1957,6 +1967,246 @@ int cfm_tree_destroy(cfm_tree* t) {
     if (!t) return;
     cudaSetDevice(t->device);
     delete t;
+  });
+}
+
+// ---------------------------------------------------------------- FMM stages
+static FmmGeom fmm_geom(cfm_fmm* f) {
+  FmmGeom g{};
+  cfm_tree* t = f->tree;
+  g.pts = t->points.as<double>();
+  g.perm = t->perm.as<long long>();
+  g.leaf_off = t->leaf_off.as<long long>();
+  g.leaf_ijk = f->leaf_ijk.as<int>();
+  g.n_leaves = t->levels[t->depth].n;
+  g.depth = t->depth;
+  g.lx = t->center[0] - t->half;
+  g.ly = t->center[1] - t->half;
+  g.lz = t->center[2] - t->half;
+  g.leaf_w = 2.0 * t->half / double(1ll << t->depth);
+  g.troots = f->troots.as<double>();
+  g.order = f->order;
+  return g;
+}
+
+static std::vector<unsigned long long> host_keys(cfm_tree* t, int level) {
+  std::vector<unsigned long long> k(t->levels[level].n);
+  if (!k.empty())
+    CUDA_CHECK(cudaMemcpy(k.data(), t->levels[level].keys.p, k.size() * 8, cudaMemcpyDeviceToHost));
+  return k;
+}
+
+// M2M (child level L -> parent L-1) or L2L (parent L-1 -> child L) plan
+static LevelPlan& fmm_plan(cfm_fmm* f, int child_level, bool up, int dc) {
+  auto& plans = up ? f->m2m_plans : f->l2l_plans;
+  const int key = child_level * 4 + dc;
+  auto it = plans.find(key);
+  if (it != plans.end()) return it->second;
+  cfm_tree* t = f->tree;
+  auto ck = host_keys(t, child_level);
+  auto pk = host_keys(t, child_level - 1);
+  const long long cs = 1ll << child_level, ps = cs >> 1;
+  const int64_t nc = int64_t(ck.size()), np_ = int64_t(pk.size());
+  std::vector<int64_t> parent(nc);
+  std::vector<int16_t> oct(nc);
+  for (int64_t c = 0; c < nc; ++c) {
+    const long long z = ck[c] % cs, y = (ck[c] / cs) % cs, x = ck[c] / (cs * cs);
+    const unsigned long long pkey = (unsigned long long)(((x >> 1) * ps + (y >> 1)) * ps + (z >> 1));
+    parent[c] = int64_t(std::lower_bound(pk.begin(), pk.end(), pkey) - pk.begin());
+    oct[c] = int16_t((x & 1) * 4 + (y & 1) * 2 + (z & 1));
+  }
+  std::vector<int64_t> tgt, off(1, 0), src;
+  std::vector<int16_t> codes;
+  if (up) {  // targets = parents, pairs = their children in octant (lexicographic) order
+    std::vector<int64_t> ord(nc);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+      return parent[a] != parent[b] ? parent[a] < parent[b] : oct[a] < oct[b];
+    });
+    for (int64_t i = 0; i < nc;) {
+      int64_t j = i;
+      tgt.push_back(parent[ord[i]]);
+      while (j < nc && parent[ord[j]] == parent[ord[i]]) {
+        src.push_back(ord[j]);
+        codes.push_back(oct[ord[j]]);
+        ++j;
+      }
+      off.push_back(int64_t(src.size()));
+      i = j;
+    }
+  } else {  // targets = children, one pair each: (parent, octant)
+    for (int64_t c = 0; c < nc; ++c) {
+      tgt.push_back(c);
+      src.push_back(parent[c]);
+      codes.push_back(oct[c]);
+      off.push_back(int64_t(src.size()));
+    }
+  }
+  std::array<int, kNumCodes> opkey;
+  opkey.fill(-1);
+  for (int c = 0; c < 8; ++c) opkey[c] = c;
+  LevelPlan lp;
+  try {
+    lp.hp = build_plan_csr(int64_t(tgt.size()), tgt.data(), off.data(), src.data(), codes.data(), dc, opkey,
+                           std::max(nc, np_));
+  } catch (const PlanError& e) {
+    throw Error(CFM_ERR_VALUE, e.what());
+  }
+  lp.dc = dc;
+  lp.n_rows = std::max(nc, np_);
+  push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
+  plans[key] = std::move(lp);
+  return plans[key];
+}
+
+static void fmm_shift(cfm_fmm* f, int child_level, bool up, const double* x, double* y, int data_complex,
+                      cudaStream_t s) {
+  if (child_level < 1 || child_level > f->tree->depth) throw Error(CFM_ERR_VALUE, "level outside the tree");
+  const int dc = data_complex ? 2 : 1;
+  LevelPlan& lp = fmm_plan(f, child_level, up, dc);
+  TileParams p{};
+  fill_ops(p, up ? f->m2m_ops : f->l2l_ops, f->octmap);
+  fill_plan(p, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src, lp.hp.n_tiles);
+  const long long row_ld = (long long)f->n * dc;
+  p.x = x; p.x_ld = row_ld; p.x_dc = dc;
+  p.y = y; p.y_ld = row_ld; p.y_dc = dc;
+  p.scale = 1.0; p.accumulate = 1;
+  launch_tiles(p, lp.hp.n_tiles, s);
+}
+
+int cfm_fmm_create(cfm_tree* t, int order, const double* shift_mats, cfm_fmm** out) {
+  return guarded([&] {
+    if (!t || !out || !shift_mats) throw Error(CFM_ERR_VALUE, "null argument");
+    if (order < 2 || order > kMaxOrder) throw Error(CFM_ERR_VALUE, "order must be in [2, 12]");
+    if (t->depth > 9) throw Error(CFM_ERR_VALUE, "FMM stages support depth <= 9");
+    CUDA_CHECK(cudaSetDevice(t->device));
+    auto f = std::make_unique<cfm_fmm>();
+    f->tree = t;
+    f->order = order;
+    f->n = order * order * order;
+    const int n = f->n;
+    // T_k(root_i), k = 1..l-1 (interp.py:88-103 at the roots)
+    std::vector<double> roots(order), tr(size_t(order) * (order - 1));
+    const int half = order / 2;
+    for (int i = 1; i <= half; ++i) roots[i - 1] = std::cos((2 * i - 1) * M_PI / (2 * order));
+    if (order % 2) roots[half] = 0.0;
+    for (int i = 0; i < half; ++i) roots[order - half + i] = -roots[half - 1 - i];
+    for (int i = 0; i < order; ++i) {
+      const double x = roots[i];
+      double tm2 = 0, tm1 = 0;
+      for (int k = 0; k < order - 1; ++k) {
+        double v = (k == 0) ? x : (k == 1 ? 2.0 * x * x - 1.0 : 2.0 * x * tm1 - tm2);
+        tr[size_t(i) * (order - 1) + k] = v;
+        tm2 = tm1;
+        tm1 = v;
+      }
+    }
+    upload(f->troots, tr);
+    const int64_t nl = t->levels[t->depth].n;
+    f->leaf_ijk.alloc(std::max<size_t>(size_t(nl) * 12, 16));
+    if (nl) {
+      k_keys_to_ijk<<<unsigned((nl + 255) / 256), 256>>>(t->levels[t->depth].keys.as<unsigned long long>(), nl,
+                                                          1ll << t->depth, f->leaf_ijk.as<int>());
+      CUDA_CHECK(cudaGetLastError());
+    }
+    const long long S = 1ll << t->depth;
+    f->leaf_grid.alloc(size_t(S * S * S) * sizeof(int));
+    CUDA_CHECK(cudaMemset(f->leaf_grid.p, 0xff, f->leaf_grid.bytes));
+    if (nl) k_leaf_grid<<<unsigned((nl + 255) / 256), 256>>>(f->leaf_ijk.as<int>(), nl, int(S), f->leaf_grid.as<int>());
+    f->leaf_of_pos.alloc(std::max<size_t>(size_t(t->n_points) * 8, 16));
+    if (nl) k_leaf_of_pos<<<unsigned((nl + 255) / 256), 256>>>(t->leaf_off.as<long long>(), nl, f->leaf_of_pos.as<long long>());
+    CUDA_CHECK(cudaGetLastError());
+    // M2M operators: mat (parent x child) per octant; L2L: transposes
+    make_stack(f->m2m_ops, 8, n, n);
+    make_stack(f->l2l_ops, 8, n, n);
+    std::vector<double> blk(f->m2m_ops.stride), blt(f->l2l_ops.stride);
+    for (int o = 0; o < 8; ++o) {
+      std::fill(blk.begin(), blk.end(), 0.0);
+      std::fill(blt.begin(), blt.end(), 0.0);
+      const double* m = shift_mats + size_t(o) * n * n;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          blk[size_t(i) * f->m2m_ops.ld + j] = m[size_t(i) * n + j];
+          blt[size_t(j) * f->l2l_ops.ld + i] = m[size_t(i) * n + j];
+        }
+      put_stack(f->m2m_ops, o, blk);
+      put_stack(f->l2l_ops, o, blt);
+    }
+    for (int c = 0; c < 8; ++c) f->octmap.op[c] = c;
+    f->octmap.push();
+    CUDA_CHECK(cudaDeviceSynchronize());
+    *out = f.release();
+  });
+}
+
+int cfm_fmm_destroy(cfm_fmm* f) {
+  return guarded([&] {
+    if (!f) return;
+    cudaSetDevice(f->tree->device);
+    delete f;
+  });
+}
+
+int cfm_fmm_p2m(cfm_fmm* f, const double* weights, int data_complex, double* leaf_mpoles, void* stream) {
+  return guarded([&] {
+    if (!f) throw Error(CFM_ERR_VALUE, "null handle");
+    CUDA_CHECK(cudaSetDevice(f->tree->device));
+    const int dc = data_complex ? 2 : 1;
+    FmmGeom g = fmm_geom(f);
+    if (!g.n_leaves) return;
+    constexpr int CH = 64;
+    const int threads = f->n <= 1024 ? 128 : 256;
+    const size_t smem = size_t(3 * f->order * CH + CH * 2) * sizeof(double);
+    k_p2m<CH><<<unsigned(g.n_leaves), threads, smem, static_cast<cudaStream_t>(stream)>>>(g, weights, dc, leaf_mpoles,
+                                                                                      (long long)f->n * dc);
+    CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int cfm_fmm_m2m(cfm_fmm* f, int child_level, const double* child, double* parent, int data_complex, void* stream) {
+  return guarded([&] {
+    if (!f) throw Error(CFM_ERR_VALUE, "null handle");
+    CUDA_CHECK(cudaSetDevice(f->tree->device));
+    fmm_shift(f, child_level, true, child, parent, data_complex, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int cfm_fmm_l2l(cfm_fmm* f, int parent_level, const double* parent, double* child, int data_complex, void* stream) {
+  return guarded([&] {
+    if (!f) throw Error(CFM_ERR_VALUE, "null handle");
+    CUDA_CHECK(cudaSetDevice(f->tree->device));
+    fmm_shift(f, parent_level + 1, false, parent, child, data_complex, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int cfm_fmm_l2p(cfm_fmm* f, const double* leaf_locals, int data_complex, double* potentials, void* stream) {
+  return guarded([&] {
+    if (!f) throw Error(CFM_ERR_VALUE, "null handle");
+    CUDA_CHECK(cudaSetDevice(f->tree->device));
+    const int dc = data_complex ? 2 : 1;
+    FmmGeom g = fmm_geom(f);
+    const long long np_ = f->tree->n_points;
+    if (!np_) return;
+    k_l2p<<<unsigned((np_ + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        g, f->leaf_of_pos.as<long long>(), leaf_locals, (long long)f->n * dc, dc, potentials, np_);
+    CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights, int weights_complex,
+                double* potentials, int out_complex, void* stream) {
+  return guarded([&] {
+    if (!f) throw Error(CFM_ERR_VALUE, "null handle");
+    if (kernel != 0 && kernel != 1) throw Error(CFM_ERR_VALUE, "kernel must be 0 (Laplace) or 1 (Helmholtz)");
+    if (weights_complex && !out_complex) throw Error(CFM_ERR_VALUE, "complex weights need complex potentials");
+    if (kernel == 1 && !out_complex) throw Error(CFM_ERR_VALUE, "Helmholtz potentials are complex");
+    CUDA_CHECK(cudaSetDevice(f->tree->device));
+    FmmGeom g = fmm_geom(f);
+    if (!g.n_leaves) return;
+    k_p2p<128><<<unsigned(g.n_leaves), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        g, f->leaf_grid.as<int>(), kernel, wavenumber, weights, weights_complex ? 2 : 1, potentials,
+        out_complex ? 2 : 1);
+    CUDA_CHECK(cudaGetLastError());
   });
 }
 

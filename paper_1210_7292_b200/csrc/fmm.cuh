@@ -1,0 +1,209 @@
+// The FMM stages around M2L on the GPU:
+//   P2M  engine.py:122-127  leaf multipoles = S(x_p)^T w   (anterpolation)
+//   L2P  engine.py:170-175  potential_p   += S(x_p) . leaf locals
+//   P2P  engine.py:177-199  near field, direct sum over the 27 neighbour
+//                           leaves in source-ijk order, coincident points skipped
+// (M2M / L2L are dense 8-operator products and run on the tile-GEMM kernel.)
+//
+// S is the tensor Chebyshev interpolation weight (interp.py:106-111, 224-236):
+//   S_l(x, r_i) = 1/l + (2/l) sum_{k=1}^{l-1} T_k(x) T_k(r_i),
+//   S(x)[m] = S(x1, r_a1) S(x2, r_a2) S(x3, r_a3),  m = a1 + a2 l + a3 l^2,
+// with reference coordinates ref = (x - center) / half of the particle's leaf.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cfm {
+
+constexpr int kMaxOrder = 12;
+
+struct FmmGeom {
+  const double* pts;        // n x 3, original particle order
+  const long long* perm;    // particles sorted by leaf (row order), ascending index inside a leaf
+  const long long* leaf_off;  // n_leaves + 1
+  const int* leaf_ijk;      // n_leaves x 3
+  long long n_leaves;
+  int depth;
+  double lx, ly, lz;        // bounding-cube low corner
+  double leaf_w;            // leaf width
+  const double* troots;     // [l][l-1] T_k(root_i), k = 1..l-1
+  int order;
+};
+
+// 1-D weights S(x, r_i), i < l, written to s[i * stride]
+__device__ __forceinline__ void cheb_weights_1d(double x, int order, const double* __restrict__ troots, double* s,
+                                                int stride) {
+  double t[kMaxOrder];
+  if (order >= 2) t[0] = x;
+  for (int k = 1; k < order - 1; ++k) t[k] = (k == 1) ? 2.0 * x * x - 1.0 : 2.0 * x * t[k - 1] - t[k - 2];
+  const double inv = 1.0 / order, two = 2.0 / order;
+  for (int i = 0; i < order; ++i) {
+    double d = 0.0;
+    for (int k = 0; k < order - 1; ++k) d += t[k] * troots[i * (order - 1) + k];
+    s[i * stride] = inv + two * d;
+  }
+}
+
+__device__ __forceinline__ void leaf_frame(const FmmGeom& g, long long leaf, double c[3], double& half) {
+  const double w = g.leaf_w;
+  half = 0.5 * w;
+  const double low[3] = {g.lx, g.ly, g.lz};
+  for (int a = 0; a < 3; ++a) c[a] = low[a] + (double(g.leaf_ijk[3 * leaf + a]) + 0.5) * w;
+}
+
+// P2M: one CTA per leaf; particles staged in chunks of CH with their 3 x l
+// weights in shared memory; thread per output node (dc = 1 real, 2 complex).
+template <int CH>
+__global__ void k_p2m(const FmmGeom g, const double* __restrict__ weights, int dc, double* __restrict__ mp,
+                      long long mp_ld) {
+  extern __shared__ double sm[];
+  const int L = g.order, n = L * L * L;
+  double* sw = sm;                 // [3][L][CH]
+  double* swt = sw + 3 * L * CH;   // [CH][dc]
+  const long long leaf = blockIdx.x;
+  double c[3], half;
+  leaf_frame(g, leaf, c, half);
+  const long long p0 = g.leaf_off[leaf], p1 = g.leaf_off[leaf + 1];
+  double acc[2][8];
+  for (int u = 0; u < 8; ++u) acc[0][u] = acc[1][u] = 0.0;
+  for (long long base = p0; base < p1; base += CH) {
+    const int cnt = int(min((long long)CH, p1 - base));
+    __syncthreads();
+    for (int pp = threadIdx.x; pp < cnt; pp += blockDim.x) {
+      const long long q = g.perm[base + pp];
+      for (int a = 0; a < 3; ++a) {
+        const double ref = (g.pts[3 * q + a] - c[a]) / half;
+        cheb_weights_1d(ref, L, g.troots, sw + a * L * CH + pp, CH);
+      }
+      for (int d = 0; d < dc; ++d) swt[pp * dc + d] = weights[q * dc + d];
+    }
+    __syncthreads();
+    int u = 0;
+    for (int m = threadIdx.x; m < n; m += blockDim.x, ++u) {
+      const int a1 = m % L, a2 = (m / L) % L, a3 = m / (L * L);
+      const double* s1 = sw + a1 * CH;
+      const double* s2 = sw + (L + a2) * CH;
+      const double* s3 = sw + (2 * L + a3) * CH;
+      for (int pp = 0; pp < cnt; ++pp) {
+        const double s = s1[pp] * s2[pp] * s3[pp];
+        for (int d = 0; d < dc; ++d) acc[d][u] += s * swt[pp * dc + d];
+      }
+    }
+  }
+  int u = 0;
+  for (int m = threadIdx.x; m < n; m += blockDim.x, ++u)
+    for (int d = 0; d < dc; ++d) mp[leaf * mp_ld + (long long)m * dc + d] = acc[d][u];
+}
+
+// L2P: one thread per particle (sorted order); pot[q] += S(x_q) . locals[leaf]
+__global__ void k_l2p(const FmmGeom g, const long long* __restrict__ leaf_of_pos, const double* __restrict__ loc,
+                      long long loc_ld, int dc, double* __restrict__ pot, long long n_points) {
+  const long long pos = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (pos >= n_points) return;
+  const int L = g.order;
+  const long long leaf = leaf_of_pos[pos];
+  const long long q = g.perm[pos];
+  double c[3], half;
+  leaf_frame(g, leaf, c, half);
+  double s[3][kMaxOrder];
+  for (int a = 0; a < 3; ++a) cheb_weights_1d((g.pts[3 * q + a] - c[a]) / half, L, g.troots, s[a], 1);
+  const double* lp = loc + leaf * loc_ld;
+  double r0 = 0.0, r1 = 0.0;
+  int m = 0;
+  for (int a3 = 0; a3 < L; ++a3)
+    for (int a2 = 0; a2 < L; ++a2)
+      for (int a1 = 0; a1 < L; ++a1, ++m) {
+        const double w = s[0][a1] * s[1][a2] * s[2][a3];
+        r0 += w * lp[(long long)m * dc];
+        if (dc == 2) r1 += w * lp[(long long)m * dc + 1];
+      }
+  pot[q * dc] += r0;
+  if (dc == 2) pot[q * dc + 1] += r1;
+}
+
+// P2P: one CTA per target leaf; the 27 neighbour leaves (source-ijk order) are
+// walked leaf by leaf, their particles staged in shared memory.  kernel 0:
+// 1/(4 pi r); 1: exp(i k r)/(4 pi r).  Weights / output: wdc / odc components.
+template <int CH>
+__global__ void k_p2p(const FmmGeom g, const int* __restrict__ grid, int kernel, double wavenumber,
+                      const double* __restrict__ weights, int wdc, double* __restrict__ pot, int odc) {
+  __shared__ double sx[CH][3];
+  __shared__ double swv[CH][2];
+  const long long leaf = blockIdx.x;
+  const int S = 1 << g.depth;
+  const int x = g.leaf_ijk[3 * leaf], y = g.leaf_ijk[3 * leaf + 1], z = g.leaf_ijk[3 * leaf + 2];
+  const long long t0 = g.leaf_off[leaf], t1 = g.leaf_off[leaf + 1];
+  const double FOUR_PI = 4.0 * 3.141592653589793;
+  for (long long tb = t0; tb < t1; tb += blockDim.x) {
+    const long long tp = tb + threadIdx.x;
+    const bool active = tp < t1;
+    long long q = active ? g.perm[tp] : 0;
+    const double xt = active ? g.pts[3 * q] : 0.0, yt = active ? g.pts[3 * q + 1] : 0.0,
+                 zt = active ? g.pts[3 * q + 2] : 0.0;
+    double acc_r = 0.0, acc_i = 0.0;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          const int sx_ = x + dx, sy_ = y + dy, sz_ = z + dz;
+          if (sx_ < 0 || sx_ >= S || sy_ < 0 || sy_ >= S || sz_ < 0 || sz_ >= S) continue;
+          const int sl = grid[((long long)sx_ * S + sy_) * S + sz_];
+          if (sl < 0) continue;
+          const long long s0 = g.leaf_off[sl], s1 = g.leaf_off[sl + 1];
+          // per-source-leaf partial (the reference adds one mat @ w per source leaf)
+          double pr = 0.0, pi = 0.0;
+          for (long long sb = s0; sb < s1; sb += CH) {
+            const int cnt = int(min((long long)CH, s1 - sb));
+            __syncthreads();
+            for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+              const long long qs = g.perm[sb + k];
+              sx[k][0] = g.pts[3 * qs];
+              sx[k][1] = g.pts[3 * qs + 1];
+              sx[k][2] = g.pts[3 * qs + 2];
+              swv[k][0] = weights[qs * wdc];
+              swv[k][1] = wdc == 2 ? weights[qs * wdc + 1] : 0.0;
+            }
+            __syncthreads();
+            if (active) {
+              for (int k = 0; k < cnt; ++k) {
+                const double ddx = xt - sx[k][0], ddy = yt - sx[k][1], ddz = zt - sx[k][2];
+                const double r = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+                if (r == 0.0) continue;
+                const double den = FOUR_PI * r;
+                if (kernel == 0) {
+                  const double v = 1.0 / den;
+                  pr += v * swv[k][0];
+                  pi += v * swv[k][1];
+                } else {
+                  double sn, cs;
+                  sincos(wavenumber * r, &sn, &cs);
+                  const double vr = cs / den, vi = sn / den;
+                  pr += vr * swv[k][0] - vi * swv[k][1];
+                  pi += vr * swv[k][1] + vi * swv[k][0];
+                }
+              }
+            }
+          }
+          acc_r += pr;
+          acc_i += pi;
+        }
+    if (active) {
+      pot[q * odc] += acc_r;
+      if (odc == 2) pot[q * odc + 1] += acc_i;
+    }
+  }
+}
+
+__global__ void k_leaf_of_pos(const long long* __restrict__ leaf_off, long long n_leaves,
+                              long long* __restrict__ out) {
+  const long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (l >= n_leaves) return;
+  for (long long p = leaf_off[l]; p < leaf_off[l + 1]; ++p) out[p] = l;
+}
+
+__global__ void k_leaf_grid(const int* __restrict__ ijk, long long n, int S, int* __restrict__ grid) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  grid[((long long)ijk[3 * i] * S + ijk[3 * i + 1]) * S + ijk[3 * i + 2]] = int(i);
+}
+
+}  // namespace cfm

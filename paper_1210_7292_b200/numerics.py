@@ -297,3 +297,44 @@ def aca_plus_svd(evaluator, n_rows: int, n_cols: int, eps: float, max_rank: int 
     uc, s, vch = np.linalg.svd(ru @ rv.conj().T)
     r = eps_rank(s, eps)
     return LowRankFactors(qu @ (uc[:, :r] * s[:r]), qv @ vch[:r].conj().T)
+
+
+# ------------------------------------------------------------ interpolation (P2M/M2M/L2L/L2P)
+def cheb_polys(x, order: int) -> np.ndarray:
+    """T_k(x), k = 1..order-1, by the three-term recurrence (interp.py:88-103)."""
+    x = np.asarray(x, dtype=float)
+    t = np.empty(x.shape + (order - 1,))
+    if order >= 2:
+        t[..., 0] = x
+    for k in range(1, order - 1):
+        if k == 1:
+            t[..., 1] = 2.0 * x * x - 1.0
+        else:
+            t[..., k] = 2.0 * x * t[..., k - 1] - t[..., k - 2]
+    return t
+
+
+def weight_matrix_1d(x, order: int) -> np.ndarray:
+    """S_l(x_m, root_i) = 1/l + (2/l) sum_k T_k(x_m) T_k(root_i), shape (n, l) (interp.py:106-111)."""
+    x = np.atleast_1d(np.asarray(x, dtype=float))
+    return 1.0 / order + (2.0 / order) * (cheb_polys(x, order) @ cheb_polys(cheb_roots(order), order).T)
+
+
+@lru_cache(maxsize=None)
+def child_shift_matrix(order: int, octant: tuple) -> np.ndarray:
+    """Moment transfer child octant -> parent, (parent nodes x child nodes) (engine.py:41-63)."""
+    roots = cheb_roots(order)
+    axes = [weight_matrix_1d((0.5 if octant[i] else -0.5) + 0.5 * roots, order) for i in range(3)]
+    mat = np.kron(axes[2], np.kron(axes[1], axes[0])).T.copy()
+    mat.setflags(write=False)
+    return mat
+
+
+def octant_code(ijk) -> np.ndarray:
+    """Octant of a cell inside its parent, 4*cx + 2*cy + cz (lexicographic child order)."""
+    ijk = np.asarray(ijk, dtype=np.int64).reshape(-1, 3) & 1
+    return ijk[:, 0] * 4 + ijk[:, 1] * 2 + ijk[:, 2]
+
+
+def octant_of_code(code: int) -> tuple:
+    return ((code >> 2) & 1, (code >> 1) & 1, code & 1)

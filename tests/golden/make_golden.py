@@ -117,7 +117,8 @@ def _csr(batch):
 
 
 def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
-             budget=2_000_000_000, store_rows=None, seeded_mpoles=None, extra=None, compression="svd"):
+             budget=2_000_000_000, store_rows=None, seeded_mpoles=None, extra=None, compression="svd",
+             potentials_for=None):
     """Build tree/lists with the reference, run every variant's apply_level per
     level on identical multipoles, and store inputs + outputs + accounting."""
     t0 = time.time()
@@ -181,6 +182,17 @@ def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
                 out[f"blk_columns_{v}_{lvl}"] = bs["columns"]
                 out[f"blk_products_{v}_{lvl}"] = bs["products"]
                 out[f"blk_reps_{v}_{lvl}"] = len(bs["reps_used"])
+        if potentials_for and v in potentials_for:
+            # full reference pipeline (engine.py:201-222) with this handler
+            plan_v = FmmPlan(tree, lists, grid, kernel, h, eps, 1)
+            out[f"potentials_{v}"] = plan_v.run(weights)
+            if "leaf_mpoles" not in out:
+                lv2 = plan_v._level_data(weights)
+                plan_v._p2m(weights, lv2[depth])
+                out["leaf_mpoles"] = lv2[depth].mpoles.copy()
+                plan_v._m2m(lv2)
+                for lvl2 in levels:
+                    out[f"up_mpoles_{lvl2}"] = lv2[lvl2].mpoles.copy()
         out[f"operator_count_{v}"] = h.operator_count()
         out[f"stored_bytes_{v}"] = h.stored_bytes()
         out[f"factorization_calls_{v}"] = h.factorization_calls
@@ -198,6 +210,8 @@ def main() -> None:
     if only:
         if "aca" in only:
             aca_case()
+        if "fmm" in only:
+            fmm_cases()
         return
     symmetry_fixture()
 
@@ -244,6 +258,25 @@ def main() -> None:
              ("nasym",), seeded_mpoles=44, store_rows=32)
 
     aca_case()
+
+
+def fmm_cases() -> None:
+    """End-to-end potentials of the reference pipeline (P2M, M2M, M2L, L2L, L2P,
+    P2P; engine.py:201-222) for the GPU FMM path."""
+    pts = cube_points(6_000, seed=41)
+    w = np.random.default_rng(42).uniform(-1.0, 1.0, len(pts))
+    run_case("fmm_cube", pts, w, AffineMap((0.5, 0.5, 0.5), 0.5), 3, laplace_kernel(), 4, 1e-5,
+             ("nablk", "iablk"), potentials_for=("nablk", "iablk"))
+    pts = sphere_points(4_000, seed=43)
+    rng = np.random.default_rng(44)
+    wc = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    run_case("fmm_helm", pts, wc, AffineMap((0.0, 0.0, 0.0), 1.0), 3, helmholtz_kernel(8 * np.pi), 4, 1e-4,
+             ("nablk", "iablk"), potentials_for=("nablk", "iablk"))
+    pts = cube_points(3_000, seed=45)
+    rng = np.random.default_rng(46)
+    wc = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    run_case("fmm_lapcplx", pts, wc, AffineMap((0.5, 0.5, 0.5), 0.5), 3, laplace_kernel(), 5, 1e-5,
+             ("nablk",), potentials_for=("nablk",))
 
 
 def aca_case() -> None:

@@ -481,3 +481,42 @@ def test_device_classifier_matches_reference(torch_cuda, golden, case):
         assert np.array_equal(src.cpu().numpy(), g[f"src_{lvl}"])
         t = g[f"t_{lvl}"].astype(np.int64)
         assert np.array_equal(code.cpu().numpy(), (t[:, 0] + 3) * 49 + (t[:, 1] + 3) * 7 + (t[:, 2] + 3))
+
+
+FMM_CASES = [("fmm_cube", "nablk"), ("fmm_cube", "iablk"), ("fmm_helm", "nablk"), ("fmm_helm", "iablk"),
+             ("fmm_lapcplx", "nablk")]
+
+
+@pytest.mark.parametrize("case,variant", FMM_CASES)
+def test_gpu_fmm_pipeline_matches_reference(torch_cuda, golden, case, variant):
+    """§8f ranks 1-3: GPU tree, P2M, M2M, M2L, L2L, L2P, P2P against the
+    reference's FmmPlan.run potentials (and its upward-pass multipoles)."""
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from geometry import cube_points, sphere_points
+
+    from paper_1210_7292_b200.fmm import B200FmmPlan
+
+    g = golden(case)
+    if case == "fmm_cube":
+        pts = cube_points(6_000, 41)
+        w = np.random.default_rng(42).uniform(-1.0, 1.0, len(pts))
+    elif case == "fmm_helm":
+        pts = sphere_points(4_000, 43)
+        rng = np.random.default_rng(44)
+        w = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    else:
+        pts = cube_points(3_000, 45)
+        rng = np.random.default_rng(46)
+        w = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    kernel, _ = _kernel_grid(g)
+    plan = B200FmmPlan(pts, tuple(g["bbox_center"]), float(g["bbox_half"]), int(g["depth"]), kernel,
+                       int(g["order"]), float(g["eps"]), variant=variant)
+    pot = plan.run(w)
+    err = O.rel_l2(pot, g[f"potentials_{variant}"])
+    assert err <= 1e-12, err
+    depth = int(g["depth"])
+    mp = plan._last["mpoles"]
+    assert O.rel_l2(mp[depth].cpu().numpy(), g["leaf_mpoles"]) <= 1e-13
+    for lvl in g["levels"]:
+        assert O.rel_l2(mp[int(lvl)].cpu().numpy(), g[f"up_mpoles_{lvl}"]) <= 1e-13
+    assert plan.m2l_seconds > 0
