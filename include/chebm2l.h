@@ -37,7 +37,8 @@
  * Memory: mpoles/locals pointers may be host or device memory (detected with
  * cudaPointerGetAttributes).  Host buffers are staged through the handler's
  * device scratch; device buffers are used in place.  `stream` is a
- * cudaStream_t (NULL = the handler's own stream).  Calls on one handler are
+ * cudaStream_t (NULL = the CUDA default stream, so work is ordered with the
+ * caller's default-stream work).  Calls on one handler are
  * serialized by an internal mutex (the reference may call apply_level from
  * several threads, engine.py:145-155).
  */

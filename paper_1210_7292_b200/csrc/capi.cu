@@ -1339,7 +1339,12 @@ static int guarded(F&& fn) {
   }
 }
 
-static cudaStream_t pick_stream(cfm_handler* h, void* s) { return s ? static_cast<cudaStream_t>(s) : h->stream; }
+// NULL means the CUDA default (legacy) stream, as everywhere in CUDA: work
+// stays ordered with the caller's default-stream kernels (e.g. torch's).
+static cudaStream_t pick_stream(cfm_handler* h, void* s) {
+  (void)h;
+  return static_cast<cudaStream_t>(s);
+}
 
 // ------------------------------------------------------------------ octree
 struct TreeLevel {

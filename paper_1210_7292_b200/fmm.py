@@ -110,22 +110,29 @@ class B200FmmPlan:
         loc = {l: torch.zeros_like(mp[l]) for l in levels}
         st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         lib = self._lib
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        ev[0].record()
         _native.check(lib.cfm_fmm_p2m(self._f, wd.data_ptr(), int(cplx), mp[self.depth].data_ptr(), st))
+        ev[1].record()
         for lvl in range(self.depth, 2, -1):
             _native.check(lib.cfm_fmm_m2m(self._f, lvl, mp[lvl].data_ptr(), mp[lvl - 1].data_ptr(), int(cplx), st))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        ev[2].record()
         if self.m2l_levels:
             self.handler.apply_levels({l: (mp[l], loc[l]) for l in self.m2l_levels})
-        e1.record()
+        ev[3].record()
         for lvl in range(2, self.depth):
             _native.check(lib.cfm_fmm_l2l(self._f, lvl, loc[lvl].data_ptr(), loc[lvl + 1].data_ptr(), int(cplx), st))
+        ev[4].record()
         out = torch.zeros(self.n_points, dtype=tdt, device=dev)
         _native.check(lib.cfm_fmm_l2p(self._f, loc[self.depth].data_ptr(), int(cplx), out.data_ptr(), st))
+        ev[5].record()
         kind = 0 if getattr(self.kernel, "wavenumber", None) is None else 1
         k = float(getattr(self.kernel, "wavenumber", 0.0) or 0.0)
         _native.check(lib.cfm_fmm_p2p(self._f, kind, k, wd.data_ptr(), int(cplx), out.data_ptr(), int(cplx), st))
+        ev[6].record()
         torch.cuda.synchronize(dev)
-        self.m2l_seconds = e0.elapsed_time(e1) * 1e-3
+        names = ("p2m", "m2m", "m2l", "l2l", "l2p", "p2p")
+        self.stage_ms = {nm: ev[i].elapsed_time(ev[i + 1]) for i, nm in enumerate(names)}
+        self.m2l_seconds = self.stage_ms["m2l"] * 1e-3
         self._last = {"mpoles": mp, "locals": loc}
         return out.cpu().numpy()

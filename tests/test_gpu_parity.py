@@ -520,3 +520,30 @@ def test_gpu_fmm_pipeline_matches_reference(torch_cuda, golden, case, variant):
     for lvl in g["levels"]:
         assert O.rel_l2(mp[int(lvl)].cpu().numpy(), g[f"up_mpoles_{lvl}"]) <= 1e-13
     assert plan.m2l_seconds > 0
+
+
+def test_default_stream_ordering(torch_cuda, golden):
+    """Handler work on stream NULL is ordered after the caller's default-stream
+    kernels: a producer kernel writing the multipoles right before apply must be
+    seen by the M2L (large enough that a race would show)."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    level, order = 5, 5
+    cells = _full_level(level)
+    full = O.full_far_field()
+    h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    h.precompute({level: full}, {level: 1.0 / 32})
+    h.plan_level_cells(level, cells)
+    x = torch.zeros((len(cells), order**3), dtype=torch.float64, device="cuda")
+    ref = torch.zeros_like(x)
+    src = torch.rand_like(x)
+    h.apply_planned(level, src, ref)
+    for _ in range(3):
+        x.zero_()
+        big = torch.rand((4096, 4096), dtype=torch.float64, device="cuda")
+        big = big @ big  # keep the default stream busy
+        x.copy_(src + 0.0 * big[0, 0])
+        out = torch.zeros_like(x)
+        h.apply_planned(level, x, out)
+        assert torch.equal(out, ref)
