@@ -2160,10 +2160,23 @@ int cfm_fmm_p2m(cfm_fmm* f, const double* weights, int data_complex, double* lea
     FmmGeom g = fmm_geom(f);
     if (!g.n_leaves) return;
     constexpr int CH = 64;
-    const int threads = f->n <= 1024 ? 128 : 256;
-    const size_t smem = size_t(3 * f->order * CH + CH * 2) * sizeof(double);
-    k_p2m<CH><<<unsigned(g.n_leaves), threads, smem, static_cast<cudaStream_t>(stream)>>>(g, weights, dc, leaf_mpoles,
-                                                                                      (long long)f->n * dc);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned nb = unsigned(g.n_leaves);
+    const long long ld = (long long)f->n * dc;
+    switch (f->order) {
+      case 3: k_p2m_t<3, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      case 4: k_p2m_t<4, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      case 5: k_p2m_t<5, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      case 6: k_p2m_t<6, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      case 7: k_p2m_t<7, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      case 8: k_p2m_t<8, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      case 9: k_p2m_t<9, CH><<<nb, 128, 0, st>>>(g, weights, dc, leaf_mpoles, ld); break;
+      default: {
+        const int threads = f->n <= 1024 ? 128 : 256;
+        const size_t smem = size_t(3 * f->order * CH + CH * 2) * sizeof(double);
+        k_p2m<CH><<<nb, threads, smem, st>>>(g, weights, dc, leaf_mpoles, ld);
+      }
+    }
     CUDA_CHECK(cudaGetLastError());
   });
 }
@@ -2192,8 +2205,20 @@ int cfm_fmm_l2p(cfm_fmm* f, const double* leaf_locals, int data_complex, double*
     FmmGeom g = fmm_geom(f);
     const long long np_ = f->tree->n_points;
     if (!np_) return;
-    k_l2p<<<unsigned((np_ + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        g, f->leaf_of_pos.as<long long>(), leaf_locals, (long long)f->n * dc, dc, potentials, np_);
+    const unsigned nb = unsigned((np_ + 127) / 128);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long long* lop = f->leaf_of_pos.as<long long>();
+    const long long ld = (long long)f->n * dc;
+    switch (f->order) {
+      case 3: k_l2p_t<3><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      case 4: k_l2p_t<4><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      case 5: k_l2p_t<5><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      case 6: k_l2p_t<6><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      case 7: k_l2p_t<7><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      case 8: k_l2p_t<8><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      case 9: k_l2p_t<9><<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_); break;
+      default: k_l2p<<<nb, 128, 0, st>>>(g, lop, leaf_locals, ld, dc, potentials, np_);
+    }
     CUDA_CHECK(cudaGetLastError());
   });
 }
@@ -2208,7 +2233,7 @@ int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights
     CUDA_CHECK(cudaSetDevice(f->tree->device));
     FmmGeom g = fmm_geom(f);
     if (!g.n_leaves) return;
-    k_p2p<128><<<unsigned(g.n_leaves), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+    k_p2p<128><<<unsigned(g.n_leaves), 64, 0, static_cast<cudaStream_t>(stream)>>>(
         g, f->leaf_grid.as<int>(), kernel, wavenumber, weights, weights_complex ? 2 : 1, potentials,
         out_complex ? 2 : 1);
     CUDA_CHECK(cudaGetLastError());

@@ -95,6 +95,117 @@ __global__ void k_p2m(const FmmGeom g, const double* __restrict__ weights, int d
     for (int d = 0; d < dc; ++d) mp[leaf * mp_ld + (long long)m * dc + d] = acc[d][u];
 }
 
+// P2M specialized on the order (accumulators in registers).
+template <int L, int CH>
+__global__ void __launch_bounds__(128) k_p2m_t(const FmmGeom g, const double* __restrict__ weights, int dc,
+                                               double* __restrict__ mp, long long mp_ld) {
+  constexpr int N = L * L * L, U = (N + 127) / 128;
+  __shared__ double sw[3][L][CH];
+  __shared__ double swt[CH][2];
+  const long long leaf = blockIdx.x;
+  double c[3], half;
+  leaf_frame(g, leaf, c, half);
+  const long long p0 = g.leaf_off[leaf], p1 = g.leaf_off[leaf + 1];
+  double acc0[U], acc1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc0[u] = acc1[u] = 0.0;
+  int a1[U], a2[U], a3[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int m = threadIdx.x + 128 * u;
+    a1[u] = m % L;
+    a2[u] = (m / L) % L;
+    a3[u] = min(m / (L * L), L - 1);
+  }
+  for (long long base = p0; base < p1; base += CH) {
+    const int cnt = int(min((long long)CH, p1 - base));
+    __syncthreads();
+    for (int pp = threadIdx.x; pp < cnt; pp += blockDim.x) {
+      const long long q = g.perm[base + pp];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double x = (g.pts[3 * q + a] - c[a]) / half;
+        double t[L > 1 ? L - 1 : 1];
+        t[0] = x;
+#pragma unroll
+        for (int k = 1; k < L - 1; ++k) t[k] = (k == 1) ? 2.0 * x * x - 1.0 : 2.0 * x * t[k - 1] - t[k - 2];
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < L - 1; ++k) d += t[k] * __ldg(g.troots + i * (L - 1) + k);
+          sw[a][i][pp] = 1.0 / L + (2.0 / L) * d;
+        }
+      }
+      swt[pp][0] = weights[q * dc];
+      swt[pp][1] = dc == 2 ? weights[q * dc + 1] : 0.0;
+    }
+    __syncthreads();
+    for (int pp = 0; pp < cnt; ++pp) {
+      const double w0 = swt[pp][0], w1 = swt[pp][1];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double sv = sw[0][a1[u]][pp] * sw[1][a2[u]][pp] * sw[2][a3[u]][pp];
+        acc0[u] += sv * w0;
+        acc1[u] += sv * w1;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int m = threadIdx.x + 128 * u;
+    if (m < N) {
+      mp[leaf * mp_ld + (long long)m * dc] = acc0[u];
+      if (dc == 2) mp[leaf * mp_ld + (long long)m * dc + 1] = acc1[u];
+    }
+  }
+}
+
+// L2P specialized on the order: the 3 x L weights stay in registers.
+template <int L>
+__global__ void k_l2p_t(const FmmGeom g, const long long* __restrict__ leaf_of_pos, const double* __restrict__ loc,
+                        long long loc_ld, int dc, double* __restrict__ pot, long long n_points) {
+  const long long pos = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (pos >= n_points) return;
+  const long long leaf = leaf_of_pos[pos];
+  const long long q = g.perm[pos];
+  double c[3], half;
+  leaf_frame(g, leaf, c, half);
+  double s[3][L];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double x = (g.pts[3 * q + a] - c[a]) / half;
+    double t[L > 1 ? L - 1 : 1];
+    t[0] = x;
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) t[k] = (k == 1) ? 2.0 * x * x - 1.0 : 2.0 * x * t[k - 1] - t[k - 2];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      double d = 0.0;
+#pragma unroll
+      for (int k = 0; k < L - 1; ++k) d += t[k] * __ldg(g.troots + i * (L - 1) + k);
+      s[a][i] = 1.0 / L + (2.0 / L) * d;
+    }
+  }
+  const double* lp = loc + leaf * loc_ld;
+  double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+  for (int a3 = 0; a3 < L; ++a3)
+#pragma unroll
+    for (int a2 = 0; a2 < L; ++a2) {
+      const double w23 = s[1][a2];
+#pragma unroll
+      for (int a1 = 0; a1 < L; ++a1) {
+        const int m = a1 + L * (a2 + L * a3);
+        const double w = s[0][a1] * w23 * s[2][a3];
+        r0 += w * __ldg(lp + (long long)m * dc);
+        if (dc == 2) r1 += w * __ldg(lp + (long long)m * dc + 1);
+      }
+    }
+  pot[q * dc] += r0;
+  if (dc == 2) pot[q * dc + 1] += r1;
+}
+
 // L2P: one thread per particle (sorted order); pot[q] += S(x_q) . locals[leaf]
 __global__ void k_l2p(const FmmGeom g, const long long* __restrict__ leaf_of_pos, const double* __restrict__ loc,
                       long long loc_ld, int dc, double* __restrict__ pot, long long n_points) {
@@ -134,6 +245,7 @@ __global__ void k_p2p(const FmmGeom g, const int* __restrict__ grid, int kernel,
   const int x = g.leaf_ijk[3 * leaf], y = g.leaf_ijk[3 * leaf + 1], z = g.leaf_ijk[3 * leaf + 2];
   const long long t0 = g.leaf_off[leaf], t1 = g.leaf_off[leaf + 1];
   const double FOUR_PI = 4.0 * 3.141592653589793;
+  const double INV_FOUR_PI = 1.0 / FOUR_PI;
   for (long long tb = t0; tb < t1; tb += blockDim.x) {
     const long long tp = tb + threadIdx.x;
     const bool active = tp < t1;
@@ -166,17 +278,20 @@ __global__ void k_p2p(const FmmGeom g, const int* __restrict__ grid, int kernel,
             if (active) {
               for (int k = 0; k < cnt; ++k) {
                 const double ddx = xt - sx[k][0], ddy = yt - sx[k][1], ddz = zt - sx[k][2];
-                const double r = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
-                if (r == 0.0) continue;
-                const double den = FOUR_PI * r;
+                const double d2 = ddx * ddx + ddy * ddy + ddz * ddz;
+                if (d2 == 0.0) continue;
                 if (kernel == 0) {
-                  const double v = 1.0 / den;
+                  // 1/(4 pi r) via rsqrt (<= 1 ulp; the reference rounds sqrt and the division)
+                  const double v = rsqrt(d2) * INV_FOUR_PI;
                   pr += v * swv[k][0];
                   pi += v * swv[k][1];
                 } else {
+                  const double r = sqrt(d2);
+                  const double den = FOUR_PI * r;
                   double sn, cs;
                   sincos(wavenumber * r, &sn, &cs);
-                  const double vr = cs / den, vi = sn / den;
+                  const double inv = 1.0 / den;
+                  const double vr = cs * inv, vi = sn * inv;
                   pr += vr * swv[k][0] - vi * swv[k][1];
                   pi += vr * swv[k][1] + vi * swv[k][0];
                 }
