@@ -214,6 +214,16 @@ int cfm_fmm_l2p(cfm_fmm* f, const double* leaf_locals, int data_complex, double*
 int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights, int weights_complex,
                 double* potentials, int out_complex, void* stream);
 
+/* GPU operator assembly (replaces assemble_for_transfer, kernels.py:167-179,
+ * and Kernel.matrix, kernels.py:75-93, inside M2LHandler.precompute,
+ * m2l.py:136-273).  kernel 0 = Laplace 1/(4 pi r) (bit-identical to the host
+ * assembly), 1 = Helmholtz exp(ikr)/(4 pi r).  nodes: HOST [n][3] reference
+ * cube nodes (ChebyshevGrid.nodes3d); transfers: HOST int8 [n_t][3];
+ * out: DEVICE [n_t][n][n] row-major, double (kernel 0) or interleaved
+ * complex (kernel 1).  Enqueued on `stream` (NULL = default stream). */
+int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, const double* nodes, double width,
+                           int n_t, const int8_t* transfers, double* out, void* stream);
+
 /* Device-side timing of the last apply (ms, CUDA events on the apply stream),
  * and the number of kernels it launched. */
 int cfm_last_apply_stats(cfm_handler* h, double* ms, int64_t* launches);

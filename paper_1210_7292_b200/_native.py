@@ -59,6 +59,7 @@ EXPORTS = (
     "cfm_fmm_l2l",
     "cfm_fmm_l2p",
     "cfm_fmm_p2p",
+    "cfm_assemble_operators",
 )
 
 _P = ctypes.c_void_p
@@ -100,6 +101,7 @@ _SIGS = {
     "cfm_fmm_l2l": ([_P, _I, _P, _P, _I, _P], _I),
     "cfm_fmm_l2p": ([_P, _P, _I, _P, _P], _I),
     "cfm_fmm_p2p": ([_P, _I, _D, _P, _I, _P, _I, _P], _I),
+    "cfm_assemble_operators": ([_I, _I, _D, _I, _P, _D, _I, _P, _P, _P], _I),
 }
 
 _lib = None

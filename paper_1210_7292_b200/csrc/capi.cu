@@ -38,6 +38,7 @@
 #include "lowrank_ws.cuh"
 #include "tree.cuh"
 #include "fmm.cuh"
+#include "precompute.cuh"
 
 #include <cub/cub.cuh>
 
@@ -2237,6 +2238,34 @@ int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights
         g, f->leaf_grid.as<int>(), kernel, wavenumber, weights, weights_complex ? 2 : 1, potentials,
         out_complex ? 2 : 1);
     CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, const double* nodes, double width,
+                           int n_t, const int8_t* transfers, double* out, void* stream) {
+  return guarded([&] {
+    if (kernel != 0 && kernel != 1) throw Error(CFM_ERR_VALUE, "kernel must be 0 (Laplace) or 1 (Helmholtz)");
+    if (n <= 0 || n > 2048 || n_t < 0) throw Error(CFM_ERR_VALUE, "bad operator size");
+    if (!(width > 0.0)) throw Error(CFM_ERR_VALUE, "cell width must be positive");
+    if (n_t == 0) return;
+    if (!nodes || !transfers || !out) throw Error(CFM_ERR_VALUE, "null pointer");
+    for (int t = 0; t < n_t; ++t) {
+      const int a = transfers[3 * t], b = transfers[3 * t + 1], c = transfers[3 * t + 2];
+      if (a * a + b * b + c * c <= 3) throw Error(CFM_ERR_VALUE, "transfer vector is not admissible (|t| <= sqrt(3))");
+    }
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DevBuf dn, dt;
+    dn.alloc(size_t(n) * 3 * sizeof(double));
+    dt.alloc(size_t(n_t) * 3);
+    CUDA_CHECK(cudaMemcpyAsync(dn.p, nodes, size_t(n) * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(dt.p, transfers, size_t(n_t) * 3, cudaMemcpyHostToDevice, st));
+    const long long nn = (long long)n * n;
+    dim3 grid(unsigned((nn + 255) / 256), unsigned(n_t));
+    k_assemble<<<grid, 256, size_t(n) * 3 * sizeof(double), st>>>(kernel, wavenumber, n, dn.as<double>(), width,
+                                                                 dt.as<int8_t>(), out);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(st));  // the staging buffers are freed on return
   });
 }
 

@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import time
 
 import numpy as np
 
@@ -43,6 +44,7 @@ from .numerics import (
     node_evaluator,
     truncated_svd,
 )
+from .precompute import assemble_stack, device_kernel_kind, shared_basis, truncated_svds
 from .symmetry import SymmetryMap
 
 __all__ = [
@@ -124,7 +126,8 @@ class B200M2LHandler:
     """Precompute/apply/account interface of all eight variants, on a B200."""
 
     def __init__(self, variant: str, kernel, grid, epsilon: float, compression: str = "svd",
-                 block_size: int = 128, budget_bytes: int = DEFAULT_BUDGET_BYTES, device: int | None = None):
+                 block_size: int = 128, budget_bytes: int = DEFAULT_BUDGET_BYTES, device: int | None = None,
+                 precompute_on: str = "device"):
         if variant not in VARIANTS:
             raise ValueError(f"unknown M2L variant {variant!r}; expected one of {VARIANTS}")
         if compression not in ("svd", "aca"):
@@ -136,6 +139,11 @@ class B200M2LHandler:
         self.compression = compression
         self.block_size = int(block_size)  # accepted for API parity; the GPU tiles are 64 columns
         self.budget_bytes = int(budget_bytes)
+        if precompute_on not in ("device", "host"):
+            raise ValueError(f"precompute_on must be 'device' or 'host', got {precompute_on!r}")
+        # device assembly / SVDs (precompute.py) for the kernels the assembly kernel implements
+        self.precompute_on = precompute_on if device_kernel_kind(kernel) is not None else "host"
+        self.precompute_seconds = 0.0
 
         self.uses_symmetry = variant in ("nasym", "nablk", "iasym", "iablk")
         self.uses_blocking = variant in ("nablk", "iablk")
@@ -155,7 +163,7 @@ class B200M2LHandler:
         self.flops: dict[int, int] = {}
         self.block_stats: dict[int, dict] = {}
         self._precomputed = False
-        self._lock = threading.Lock()
+        self._lock = threading.RLock()  # FmmPlan may call apply_level from several threads (engine.py:145-155)
 
         self._lib = _native.load()
         self._op_complex = np.issubdtype(np.dtype(kernel.dtype), np.complexfloating)
@@ -197,6 +205,27 @@ class B200M2LHandler:
     # precompute (m2l.py:136-273)
     # ------------------------------------------------------------------
     def precompute(self, level_transfers, level_widths) -> "B200M2LHandler":
+        t0 = time.perf_counter()
+        try:
+            return self._precompute(level_transfers, level_widths)
+        finally:
+            self.precompute_seconds = time.perf_counter() - t0
+
+    def _operators(self, vectors, width: float):
+        """Operators for ``vectors`` at ``width``: a device tensor [T, n, n]
+        (device precompute) or a host array (assemble_for_transfer)."""
+        if self.precompute_on == "device":
+            return assemble_stack(self.kernel, vectors, width, self.grid, self._device)
+        dt = np.complex128 if self._op_complex else np.float64
+        if not vectors:
+            return np.zeros((0, self._size, self._size), dt)
+        return np.stack([assemble_for_transfer(self.kernel, t, width, self.grid) for t in vectors]).astype(dt)
+
+    @staticmethod
+    def _host(a):
+        return a if isinstance(a, np.ndarray) else a.cpu().numpy()
+
+    def _precompute(self, level_transfers, level_widths) -> "B200M2LHandler":
         levels = sorted(lvl for lvl, ts in level_transfers.items() if ts)
         if not levels:
             self._precomputed = True
@@ -260,9 +289,7 @@ class B200M2LHandler:
         dt = np.complex128 if self._op_complex else np.float64
         if self.is_dense:
             vectors = group.symmetry.cone if self.uses_symmetry else group.transfers
-            ops = np.ascontiguousarray(
-                np.stack([assemble_for_transfer(self.kernel, t, group.width, self.grid) for t in vectors]).astype(dt)
-            )
+            ops = np.ascontiguousarray(self._host(self._operators(list(vectors), group.width)), dtype=dt)
             self._dense[key] = {"vectors": list(vectors), "nbytes": [ops[0].nbytes] * len(vectors)}
             self._check(self._lib.cfm_set_dense_group(self._h, kid, len(tr), tr.ctypes.data, len(vectors),
                                                       _tarray(vectors).ctypes.data, ops.ctypes.data))
@@ -270,7 +297,11 @@ class B200M2LHandler:
             self._build_shared_basis(key, kid, group)
         else:
             vectors = group.symmetry.cone if self.uses_symmetry else group.transfers
-            facs = [self._factorize(t, group.width) for t in vectors]
+            if self.compression == "svd" and self.precompute_on == "device":
+                facs = truncated_svds(self._operators(list(vectors), group.width), self.epsilon)
+                self.factorization_calls += len(facs)
+            else:
+                facs = [self._factorize(t, group.width) for t in vectors]
             ranks = np.asarray([f.rank for f in facs], np.int32)
             left = np.concatenate([np.ascontiguousarray(f.left, dtype=dt).ravel() for f in facs]) if facs else np.zeros(0, dt)
             right = np.concatenate([np.ascontiguousarray(f.right, dtype=dt).ravel() for f in facs]) if facs else np.zeros(0, dt)
@@ -303,9 +334,19 @@ class B200M2LHandler:
         (m2l.py:216-273)."""
         size = self._size
         transfers = group.transfers
-        blocks = {t: assemble_for_transfer(self.kernel, t, group.width, self.grid) for t in transfers}
-        row = np.hstack([blocks[t] for t in transfers])
-        col = np.vstack([blocks[t] for t in transfers])
+        stack = self._operators(list(transfers), group.width)
+        cores = {}
+        if self.compression == "svd" and self.precompute_on == "device":
+            u, b, core_stack = shared_basis(stack, self.epsilon)
+            self.factorization_calls += 2
+            for k, t in enumerate(transfers):
+                cores[t] = ("dense", core_stack[k])
+            self._finish_shared_basis(key, kid, transfers, u, b, cores)
+            return
+        stack = self._host(stack)
+        row = np.hstack(list(stack))
+        col = np.vstack(list(stack))
+        del stack
         if self.compression == "svd":
             u_row, s_row, vh_row = np.linalg.svd(row, full_matrices=False)
             _, s_col, vh_col = np.linalg.svd(col, full_matrices=False)
@@ -323,9 +364,11 @@ class B200M2LHandler:
             u = row_fac.left / sigma
             vh = row_fac.right.conj().T
             b = col_fac.right
-        cores = {}
         for k, t in enumerate(transfers):
             cores[t] = ("dense", (sigma[:, None] * vh[:, k * size:(k + 1) * size]) @ b)
+        self._finish_shared_basis(key, kid, transfers, u, b, cores)
+
+    def _finish_shared_basis(self, key, kid: int, transfers, u, b, cores) -> None:
         r_u, r_b = u.shape[1], b.shape[1]
         if self.variant == "sarcmp":
             for t, (_, core) in list(cores.items()):
@@ -449,18 +492,20 @@ class B200M2LHandler:
         if off[-1] == 0:
             self._record(level, key, np.zeros(343, np.int64), 0, planned=False)
             return 0
-        x, y, wb, data_complex, n_rows = self._prepare(mpoles, locals_out)
+        n_targets_nonempty = int(np.count_nonzero(np.diff(off)))
+        n_sources = int(np.unique(src).size) if self.is_shared_basis else 0
         counts = np.zeros(343, np.int64)
+        # one critical section from the staging copy to the accounting: concurrent
+        # callers with disjoint target rows of shared arrays stay correct
         with self._lock:
+            x, y, wb, data_complex, n_rows = self._prepare(mpoles, locals_out)
             self._check(self._lib.cfm_apply_level_csr(
                 self._h, int(level), len(tgt), tgt.ctypes.data, off.ctypes.data, src.ctypes.data, t.ctypes.data,
                 data_complex, _native.ptr(x), int(n_rows), _native.ptr(y), self._stream_of(x), counts.ctypes.data))
-        if wb is not None:
-            wb[...] = y
-        n_targets_nonempty = int(np.count_nonzero(np.diff(off)))
-        n_sources = int(np.unique(src).size) if self.is_shared_basis else 0
-        flops = self._count_flops(key, counts, n_targets_nonempty, n_sources)
-        self._record(level, key, counts, flops)
+            if wb is not None:
+                wb[...] = y
+            flops = self._count_flops(key, counts, n_targets_nonempty, n_sources)
+            self._record(level, key, counts, flops)
         return flops
 
     # -------- device-built lists: classify on the GPU, plan once, apply many
@@ -522,16 +567,16 @@ class B200M2LHandler:
         st = self._planned.get(level)
         if st is None:
             raise PrecomputeIncompleteError(f"level {level} has no device plan; call plan_level_cells first")
-        x, y, wb, data_complex, n_rows = self._prepare(mpoles, locals_out)
-        if bool(data_complex) != (st["complex"] or self._op_complex):
-            raise ValueError("expansion dtype differs from the one the level was planned for")
         with self._lock:
+            x, y, wb, data_complex, n_rows = self._prepare(mpoles, locals_out)
+            if bool(data_complex) != (st["complex"] or self._op_complex):
+                raise ValueError("expansion dtype differs from the one the level was planned for")
             self._check(self._lib.cfm_apply_planned(self._h, int(level), _native.ptr(x), int(n_rows), _native.ptr(y),
                                                     self._stream_of(x)))
-        if wb is not None:
-            wb[...] = y
-        flops = self._count_flops(key, st["counts"], st["targets"], st["sources"])
-        self._record(level, key, st["counts"], flops)
+            if wb is not None:
+                wb[...] = y
+            flops = self._count_flops(key, st["counts"], st["targets"], st["sources"])
+            self._record(level, key, st["counts"], flops)
         return flops
 
     def apply_levels(self, arrays) -> int:
@@ -540,6 +585,10 @@ class B200M2LHandler:
         ``arrays`` maps level -> (mpoles, locals_out).  Dense variants run all
         levels in a single kernel launch; returns the total counted flops and
         records per-level accounting exactly as per-level calls would."""
+        with self._lock:
+            return self._apply_levels_locked(arrays)
+
+    def _apply_levels_locked(self, arrays) -> int:
         levels = sorted(arrays)
         prepared = []
         for lvl in levels:
@@ -558,8 +607,7 @@ class B200M2LHandler:
         xs = (ctypes.c_void_p * n)(*[_native.ptr(p[1]) for p in prepared])
         ys = (ctypes.c_void_p * n)(*[_native.ptr(p[2]) for p in prepared])
         rows = (ctypes.c_int64 * n)(*[int(p[4]) for p in prepared])
-        with self._lock:
-            self._check(self._lib.cfm_apply_levels(self._h, n, lv, xs, rows, ys, self._stream_of(prepared[0][1])))
+        self._check(self._lib.cfm_apply_levels(self._h, n, lv, xs, rows, ys, self._stream_of(prepared[0][1])))
         total = 0
         for lvl, x, y, wb, n_rows, st in prepared:
             if wb is not None:
