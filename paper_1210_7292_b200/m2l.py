@@ -370,10 +370,11 @@ class B200M2LHandler:
 
     def _finish_shared_basis(self, key, kid: int, transfers, u, b, cores) -> None:
         r_u, r_b = u.shape[1], b.shape[1]
-        if self.variant == "sarcmp":
-            for t, (_, core) in list(cores.items()):
-                fac = truncated_svd(core, self.epsilon)
-                self.factorization_calls += 1
+        if self.variant == "sarcmp" and cores:
+            keys = list(cores)
+            facs = truncated_svds(np.stack([cores[t][1] for t in keys]), self.epsilon)
+            self.factorization_calls += len(keys)
+            for t, fac in zip(keys, facs):
                 if fac.rank * (r_u + r_b) < r_u * r_b:
                     cores[t] = ("factored", fac)
         dt = np.complex128 if self._op_complex else np.float64

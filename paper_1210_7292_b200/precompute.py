@@ -14,9 +14,9 @@ precompute is ~60 s on the host; here:
   svd(R^H) = U S W^H gives the singular values S and left vectors U of A;
   for the column stack C = Q R, svd(R) = U S V^H gives S and V of C.  The
   cores C_t = diag(s) V_t^H B are U_r^H K_t B (same product, one batched GEMM);
-* the per-operator truncated SVDs of the IA variants run batched on the GPU
-  for l >= 7 (cuSOLVER gesvdj); for smaller operators the host LAPACK SVD of
-  the device-assembled operators is faster and is used instead.
+* the per-operator truncated SVDs of the IA variants (square, independent)
+  run as host LAPACK calls in parallel threads on the device-assembled
+  operators: cuSOLVER's per-matrix gesvdj measured slower for them.
 
 The truncation rule is the reference's (``eps_rank``: s_k > eps * s_1), so
 ranks are the reference's; the factors agree to rounding (the parity tests
@@ -31,8 +31,6 @@ import numpy as np
 
 from . import _native
 from .numerics import FOUR_PI, LowRankFactors, eps_rank, grid_nodes
-
-DEVICE_SVD_MIN_SIZE = 343  # l >= 7: batched device SVD beats the host LAPACK loop
 
 
 def device_kernel_kind(kernel):
@@ -86,30 +84,39 @@ def _check_eps(eps: float) -> None:
         raise ValueError(f"accuracy must lie in (0, 1), got {eps}")
 
 
+def _host_tsvd(a, eps):
+    u, s, vh = np.linalg.svd(a, full_matrices=False)
+    r = eps_rank(s, eps)
+    return LowRankFactors(u[:, :r] * s[:r], vh[:r].conj().T)
+
+
 def truncated_svds(stack, eps: float) -> list[LowRankFactors]:
-    """``truncated_svd`` (lowrank.py:53-62) of every operator in a device stack."""
-    import torch
+    """``truncated_svd`` (lowrank.py:53-62) of every operator in a stack.
+
+    The operators are square and independent, and cuSOLVER's per-matrix
+    gesvdj is slower than LAPACK for them (l = 9: 55 s vs 28 s for 316
+    operators, profiles/r01_precompute.json), so the SVDs run on the host,
+    one operator per thread with single-threaded BLAS."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
 
     _check_eps(eps)
-    if not bool(torch.isfinite(stack).all()):
+    host = stack if isinstance(stack, np.ndarray) else stack.cpu().numpy()
+    if not np.all(np.isfinite(host)):
         raise ValueError("matrix has non-finite entries")
-    if stack.shape[-1] >= DEVICE_SVD_MIN_SIZE:
-        u, s, vh = torch.linalg.svd(stack, full_matrices=False)
-        s_h = s.cpu().numpy()
-        out = []
-        for i in range(stack.shape[0]):
-            r = eps_rank(s_h[i], eps)
-            left = (u[i, :, :r] * s[i, :r].to(u.dtype)).cpu().numpy()
-            right = vh[i, :r].conj().T.contiguous().cpu().numpy()
-            out.append(LowRankFactors(left, right))
-        return out
-    host = stack.cpu().numpy()
-    out = []
-    for a in host:
-        u, s, vh = np.linalg.svd(a, full_matrices=False)
-        r = eps_rank(s, eps)
-        out.append(LowRankFactors(u[:, :r] * s[:r], vh[:r].conj().T))
-    return out
+    workers = max(1, min(len(host), os.cpu_count() or 1, 64))
+    if workers == 1 or host.shape[-1] < 64:
+        return [_host_tsvd(a, eps) for a in host]
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1, user_api="blas"):
+            with ThreadPoolExecutor(workers) as ex:
+                return list(ex.map(lambda a: _host_tsvd(a, eps), host))
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(lambda a: _host_tsvd(a, eps), host))
 
 
 def shared_basis(stack, eps: float):
