@@ -164,6 +164,12 @@ struct Group {
   int r_u = 0, r_b = 0;
   bool any_dense_core = false, any_fac_core = false;
   std::array<int, kNumCodes> valid{};  // transfer vectors of the group
+  // full-operator TMA mode (dense, real): one fully permuted K_t per transfer
+  bool has_full = false;
+  OpStack full;
+  int full_rows = 0;
+  CodeMap fullmap;
+  CUtensorMap full_tmap;
 };
 
 struct LevelPlan {
@@ -207,6 +213,8 @@ struct cfm_handler {
   std::map<int, std::pair<int, double>> levels;
   std::map<int, LevelPlan> plans;
   DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters, pipe_flags;
+  DevBuf xpad;                     // zero-padded source rows of full-operator levels
+  std::vector<int64_t> xpad_sig;   // layout the padding columns were zeroed for
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -251,6 +259,26 @@ static void launch_ws_multi(const MultiTileParams& mp, dim3 grid, cudaStream_t s
   const TileParams& q = mp.seg[0];
   const bool tabs = tile_perm_tabs_fit(q.nr, q.nk);
   const int smem = ws_ring_bytes<BM, BN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, tabs);
+  if constexpr (BM == 128 && KC == 32 && !SKIP) {
+    if (q.ft) {
+      static const int ft_stages = [] {
+        const char* e = getenv("CFM_FT_STAGES");
+        return e ? atoi(e) : 4;
+      }();
+      if (ft_stages == 3) {
+        const int smem_ft = ws_ring_bytes<BM, BN, KC, 3>() + tile_table_bytes(q.nr, q.nk, false);
+        auto kf = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 3, SKIP, false, true>;
+        CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
+        kf<<<grid, (WM * WN + 4) * 32, smem_ft, s>>>(mp);
+        return;
+      }
+      const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false);
+      auto kf = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, true>;
+      CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
+      kf<<<grid, (WM * WN + 4) * 32, smem_ft, s>>>(mp);
+      return;
+    }
+  }
   if constexpr (BM == 128) {
     if (use_bulk_a(KC) && q.zero_row && q.op_ld <= 8192) {
       auto kb = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, STAGES, SKIP, true>;
@@ -341,6 +369,36 @@ static bool use_fused_lowrank() {
     return e ? atoi(e) : 1;
   }();
   return v != 0;
+}
+
+// cuTensorMapEncodeTiled, resolved at run time like the stream memory ops.
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled resolve_encode_tiled() {
+  static PFN_encodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<PFN_encodeTiled>(nullptr);
+    }
+    return reinterpret_cast<PFN_encodeTiled>(f);
+  }();
+  return fn;
+}
+
+// Full-operator TMA mode (CFM_FULL_OPS=0 disables): real dense groups whose
+// operators take the 128-row KC=32 kernel (64 < n <= 512, l = 5..8).
+static bool use_full_ops(const cfm_handler* h) {
+  static int v = [] {
+    const char* e = getenv("CFM_FULL_OPS");
+    return e ? atoi(e) : 1;
+  }();
+  const int nf = h->n * h->f;
+  return v != 0 && !h->op_complex && nf > 64 && nf <= 512 && tile_kernel_kind(nf) == 0 &&
+         resolve_encode_tiled() != nullptr;
 }
 
 template <int RP, int STAGES>
@@ -522,6 +580,46 @@ static void map_transfers(cfm_handler* h, Group& g, int n_transfers, const int8_
       m.op[c] = o;
     }
   }
+}
+
+static void make_stack(OpStack& s, int n_ops, int rows, int cols);
+static void put_stack(OpStack& s, int i, const std::vector<double>& hostblock);
+
+// Full-operator stack for the TMA tile kernel: K_t[i][j] = Op[tab_r[i]][tab_c[j]]
+// for every transfer of the group (the same products the permuted apply forms,
+// acc[i] += sum_k Op[rowtab[i]][k] x[invtab[k]] with j = invtab[k]), rows padded
+// to a multiple of 8, columns to the KC multiple; plus the 2-D tensor map.
+static void build_full_ops(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, const double* ops) {
+  const int n = h->n;
+  const int rows = round_up(n, 8);
+  OpStack& fs = g.full;
+  make_stack(fs, n_transfers, rows, n);
+  g.full_rows = rows;
+  std::vector<double> blockv(fs.stride);
+  std::vector<int> ident(n);
+  std::iota(ident.begin(), ident.end(), 0);
+  for (int k = 0; k < n_transfers; ++k) {
+    const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
+    const int o = g.main.op[c], rp = g.main.rperm[c], cp = g.main.cperm[c];
+    const std::vector<int> tr = rp >= 0 ? permutation_table(rp, h->order) : ident;
+    const std::vector<int> tc = cp >= 0 ? permutation_table(cp, h->order) : ident;
+    std::fill(blockv.begin(), blockv.end(), 0.0);
+    const double* src = ops + size_t(o) * n * n;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) blockv[size_t(i) * fs.ld + j] = src[size_t(tr[i]) * n + tc[j]];
+    put_stack(fs, k, blockv);
+    g.fullmap.op[c] = k;
+  }
+  g.fullmap.push();
+  const cuuint64_t dims[2] = {cuuint64_t(fs.ld), cuuint64_t(n_transfers) * rows};
+  const cuuint64_t strides[1] = {cuuint64_t(fs.ld) * sizeof(double)};
+  const cuuint32_t box[2] = {cuuint32_t(kKC + 4), 128u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = resolve_encode_tiled()(&g.full_tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, fs.d.p, dims, strides,
+                                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for the operator stack");
+  g.has_full = true;
 }
 
 static void make_stack(OpStack& s, int n_ops, int rows, int cols) {
@@ -764,6 +862,54 @@ static int64_t launch_reduce(const LevelPlan& lp, const double* F, long long f_l
   return 1;
 }
 
+// ---- full-operator mode: sources as zero-padded rows (ld = group full.ld)
+static bool full_mode(const Group& g, const LevelPlan& lp) { return g.kind == kDense && g.has_full && lp.dc == 1; }
+
+// Reserve h->xpad for levels of (rows, ld) and return each level's offset (in
+// doubles); the padding columns are zeroed whenever the layout changes (rows
+// are only ever written in their first n columns afterwards).
+static std::vector<size_t> xpad_layout(cfm_handler* h, const std::vector<std::pair<int64_t, int>>& lay, cudaStream_t s) {
+  std::vector<size_t> off(lay.size());
+  std::vector<int64_t> sig;
+  size_t total = 0;
+  for (size_t i = 0; i < lay.size(); ++i) {
+    off[i] = total;
+    total += size_t(lay[i].first) * size_t(lay[i].second);
+    sig.push_back(lay[i].first);
+    sig.push_back(lay[i].second);
+  }
+  const size_t bytes = std::max<size_t>(total * sizeof(double), 16);
+  const bool grow = !h->xpad.p || bytes > h->xpad.bytes;
+  ensure(h->xpad, bytes);
+  if (grow || sig != h->xpad_sig) {
+    CUDA_CHECK(cudaMemsetAsync(h->xpad.p, 0, bytes, s));
+    h->xpad_sig = sig;
+  }
+  return off;
+}
+
+// rows [r0, r1) of a (rows x n) source array (host or device) into the padded layout
+static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s) {
+  if (r1 <= r0) return;
+  CUDA_CHECK(cudaMemcpy2DAsync(dst + size_t(r0) * ld, size_t(ld) * sizeof(double), src + size_t(r0) * h->n,
+                               size_t(h->n) * sizeof(double), size_t(h->n) * sizeof(double), size_t(r1 - r0),
+                               cudaMemcpyDefault, s));
+}
+
+static void fill_full(TileParams& p, const cfm_handler* h, const Group& g, const double* xpad) {
+  fill_ops(p, g.full, g.fullmap);
+  p.nr = h->n;
+  p.nk = h->n;
+  p.rowtab = nullptr;
+  p.invtab = nullptr;
+  p.ft = 1;
+  p.ft_rows = g.full_rows;
+  p.tmap_a = g.full_tmap;
+  p.x = xpad;
+  p.x_ld = g.full.ld;
+  p.x_dc = 1;
+}
+
 static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, double* d_y, cudaStream_t s) {
   Group& g = group_for_level(h, level);
   const double scale = h->levels[level].second;
@@ -783,6 +929,12 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     fill_ops(p, g.dense, g.main);
     fill_plan(p, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src, lp.hp.n_tiles);
     p.x = d_x; p.x_ld = row_ld; p.x_dc = dc;
+    if (full_mode(g, lp)) {
+      const auto off = xpad_layout(h, {{lp.n_rows, g.full.ld}}, s);
+      double* xp = h->xpad.as<double>() + off[0];
+      xpad_copy(h, xp, g.full.ld, d_x, 0, lp.n_rows, s);
+      fill_full(p, h, g, xp);
+    }
     if (lp.mode == 1) {
       ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
       p.y = h->fbuf.as<double>(); p.y_ld = row_ld; p.y_dc = dc;
@@ -1027,6 +1179,19 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   size_t off = 0;
   std::vector<const double*> host_x(lv.size(), nullptr);
   std::vector<size_t> flag_off(lv.size(), 0);
+  // full-operator levels read zero-padded source rows from h->xpad
+  std::vector<int> ftl(lv.size(), 0);
+  std::vector<std::pair<int64_t, int>> lay;
+  std::vector<size_t> lay_idx(lv.size(), 0);
+  if (all_dense_pre) {
+    for (size_t i = 0; i < lv.size(); ++i) {
+      Group& g = group_for_level(h, lv[i].level);
+      if (!full_mode(g, *lv[i].lp)) continue;
+      ftl[i] = 1;
+      lay_idx[i] = lay.size();
+      lay.push_back({lv[i].lp->n_rows, g.full.ld});
+    }
+  }
   cudaStream_t s_in = s;
   if (any_piped) {
     if (!h->s_h2d) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
@@ -1043,9 +1208,17 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     ensure(h->pipe_flags, nflags * sizeof(unsigned));
     CUDA_CHECK(cudaMemsetAsync(h->pipe_flags.p, 0, nflags * sizeof(unsigned), s_in));
   }
+  std::vector<size_t> xoff;
+  if (!lay.empty()) xoff = xpad_layout(h, lay, s_in);
   for (size_t i = 0; i < lv.size(); ++i) {
     auto& L = lv[i];
-    if (!is_device_ptr(L.x)) {
+    if (ftl[i]) {
+      double* xp = h->xpad.as<double>() + xoff[lay_idx[i]];
+      if (!is_device_ptr(L.x)) host_x[i] = L.x;
+      if (!piped[i]) xpad_copy(h, xp, lay[lay_idx[i]].second, L.x, 0, L.lp->n_rows, s_in);
+      L.x = xp;
+      if (!is_device_ptr(L.x)) off += L.bytes;  // (never: xp is device memory)
+    } else if (!is_device_ptr(L.x)) {
       double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
       host_x[i] = L.x;
       if (!piped[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s_in));
@@ -1085,7 +1258,11 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       unsigned* loc_ready = mp_ready + 1;
       // multipole slab k is needed by targets of slab k-1: keep multipoles one slab ahead
       for (int k = 0; k < S; ++k) {
-        slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
+        if (ftl[i])
+          xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, host_x[i], P.slab_row0[k],
+                    P.slab_row0[k + 1], s_in);
+        else
+          slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
         write_flag(mp_ready, unsigned(k + 1));
         if (k >= 1) {
           slab_copy(lv[i].host_y, lv[i].y, k - 1, cudaMemcpyHostToDevice, s_in);
@@ -1142,6 +1319,8 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       }
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
+      if (ftl[i]) fill_full(p, h, g, L.x);
+      if (i > 0 && ftl[i] != ftl[0]) same_shape = false;
       if (L.lp->mode == 1) {
         p.y = h->fbuf.as<double>() + f_off[i]; p.y_ld = row_ld; p.y_dc = L.lp->dc;
         p.scale = 1.0; p.accumulate = 0; p.pair_out = 1;
@@ -1488,6 +1667,7 @@ int cfm_set_dense_group(cfm_handler* h, int key, int n_transfers, const int8_t* 
       realify_into(ops + i * blk, h->n, h->n, h->op_complex, tmp.data(), g.dense.ld);
       put_stack(g.dense, i, tmp);
     }
+    if (use_full_ops(h)) build_full_ops(h, g, n_transfers, transfers, ops);
     h->groups[key] = std::move(g);
     h->plans.clear();
   });

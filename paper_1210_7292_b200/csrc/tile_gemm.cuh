@@ -22,6 +22,7 @@
 // DMMA runs at the chip's FP64 peak (37.1 TF/s measured, profiles/).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace cfm {
@@ -81,6 +82,14 @@ struct TileParams {
   const int* pipe_need_loc;
   const int* pipe_lo;
   const int* pipe_hi;
+  // full-operator TMA mode (real dense groups, 65 < nr, nk <= 512): ops is a
+  // stack of the fully permuted operators K_t (ft_rows rows each, one per
+  // transfer vector, code_* map t -> its K_t with identity permutations), read
+  // by one 2-D TMA tile copy per chunk through tmap_a; the sources are
+  // contiguous zero-padded rows (x_ld = op_ld), one bulk copy per column
+  int ft;
+  int ft_rows;
+  CUtensorMap tmap_a;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

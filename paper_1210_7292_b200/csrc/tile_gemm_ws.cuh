@@ -39,6 +39,16 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned 
                : "memory");
 }
 
+// 2-D TMA tile copy global -> shared (box from the tensor map), bytes on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(d), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b)
+      : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
   unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   unsigned ok;
@@ -89,7 +99,7 @@ struct MultiTileParams {
   TileParams seg[kMaxSegments];
 };
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS, bool BULK_A = false>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS, bool BULK_A = false, bool FT = false>
 __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(const __grid_constant__ MultiTileParams mp) {
   int sidx = 0;
   while (sidx + 1 < mp.n_seg && int(blockIdx.x) >= mp.start[sidx + 1]) ++sidx;
@@ -107,9 +117,10 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   static_assert(NP % KC == 0, "B mapping needs NP multiple of KC");
   static_assert(BN <= 64, "s_col sized for 64 columns");
   static_assert(!BULK_A || BM == NP, "bulk A path: one operator row per producer thread");
+  static_assert(!FT || (BN % 32 == 0 && !BULK_A), "full-operator path: whole B columns per lane");
 
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
+  extern __shared__ __align__(128) double smem_ws[];  // TMA tile destinations need 128-B alignment
+  double* As = smem_ws;
   double* Bs = As + STAGES * BM * LDA;
   uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * BN * LDB);
   uint64_t* empty = full + STAGES;
@@ -144,7 +155,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, BULK_A ? NP + 1 : NP);
+      mbar_init(full + s, FT ? 1 : (BULK_A ? NP + 1 : NP));
       mbar_init(empty + s, NC / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -165,6 +176,44 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     return e;
   };
 
+  if (FT && tid >= NC) {
+    // ============ producer, full-operator mode: one warp, TMA only ============
+    // per chunk: one 2-D tile copy of the operator block (BM rows x KC+4
+    // columns, landing with the LDA pitch) and one bulk copy per source column
+    if (tid >= NC + 32) return;
+    if (p.pipe_mp && e_begin < e_end) wait_flag_geq(p.pipe_mp, unsigned(p.pipe_need_mp[tile]));
+    constexpr int BPL = BN / 32;
+    constexpr unsigned STAGE_TX = unsigned((BM * LDA + BN * KC) * 8);
+    EntryInfo d;
+    d.nchunks = 0;
+    int e = next_live(e_begin, d);
+    int q = 0;
+    while (e < e_end) {
+      const double* bsrc[BPL];
+#pragma unroll
+      for (int u = 0; u < BPL; ++u) {
+        const int v = __ldg(p.entry_src + (long long)e * BN + lane + 32 * u);
+        bsrc[u] = v >= 0 ? p.x + (long long)v * p.x_ld : nullptr;
+      }
+      const int arow = d.op * p.ft_rows + r0;
+      for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
+        const int s = q % STAGES;
+        if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
+        const int k0 = kc * KC;
+        double* bs = Bs + s * BN * LDB;
+        if (lane == 0) {
+          mbar_arrive_expect_tx(full + s, STAGE_TX);
+          tma_load_2d(As + s * BM * LDA, &p.tmap_a, k0, arow, full + s);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < BPL; ++u)
+          bulk_g2s(bs + (lane + 32 * u) * LDB, bsrc[u] ? bsrc[u] + k0 : p.zero_row, KC * 8, full + s);
+      }
+      e = next_live(e + 1, d);
+    }
+    return;
+  }
   if (tid >= NC) {
     // ======================= producer warps =======================
     const int pt = tid - NC;
@@ -227,6 +276,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         }
         if (p.debug & 4) {  // timing experiment: no copies, stale stage data
           mbar_arrive(full + s);
+          if (BULK_A && pt == 0) mbar_arrive(full + s);  // the expect_tx arrival of the bulk path
           continue;
         }
         const int k0 = kc * KC;

@@ -13,6 +13,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--variant", default=None)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--gpu-tree", action="store_true", help="level cells from the GPU octree (large configs)")
     a = ap.parse_args()
     import torch
 
@@ -20,7 +21,10 @@ def main():
 
     n, depth, order, geom, variant, eps = bench.CONFIGS[a.config]
     variant = a.variant or variant
-    cells, widths = bench.cached_level_cells(a.config)
+    if a.gpu_tree:
+        cells, widths, _ = bench.gpu_level_cells(a.config, 0)
+    else:
+        cells, widths = bench.cached_level_cells(a.config)
     levels = sorted(cells)
     full = full_far_field_vectors()
     h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps,
