@@ -216,7 +216,7 @@ struct cfm_handler {
   DevBuf xpad;                     // zero-padded source rows of full-operator levels
   std::vector<int64_t> xpad_sig;   // layout the padding columns were zeroed for
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
@@ -1199,6 +1199,11 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     if (!h->ev_in) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
     if (!h->ev_out) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
     s_in = h->s_h2d;
+    // the copy stream reuses buffers (xpad, stages) that earlier calls' kernels
+    // on the caller's stream may still read: start after them
+    if (!h->ev_prev) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_prev, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(h->ev_prev, s));
+    CUDA_CHECK(cudaStreamWaitEvent(s_in, h->ev_prev, 0));
     size_t nflags = 0;
     for (size_t i = 0; i < lv.size(); ++i)
       if (piped[i]) {
@@ -1209,15 +1214,33 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     CUDA_CHECK(cudaMemsetAsync(h->pipe_flags.p, 0, nflags * sizeof(unsigned), s_in));
   }
   std::vector<size_t> xoff;
+  std::vector<const double*> staged_x(lv.size(), nullptr);
   if (!lay.empty()) xoff = xpad_layout(h, lay, s_in);
   for (size_t i = 0; i < lv.size(); ++i) {
     auto& L = lv[i];
     if (ftl[i]) {
+      // host rows go H2D contiguously into the stage (a pitched H2D copy of
+      // 1000-B rows runs at 8 GB/s), then device-to-device into xpad.  That
+      // copy is an SM kernel (tools/ce_probe.cu): it cannot run while the M2L
+      // grid holds every SM, so it is never issued on the copy stream during a
+      // launch.  Pipelined levels ("late", ftl = 2) copy their sources H2D
+      // while the other levels' launch runs and are padded between the two
+      // launches on the compute stream; only their locals stream by slab.
       double* xp = h->xpad.as<double>() + xoff[lay_idx[i]];
-      if (!is_device_ptr(L.x)) host_x[i] = L.x;
-      if (!piped[i]) xpad_copy(h, xp, lay[lay_idx[i]].second, L.x, 0, L.lp->n_rows, s_in);
+      const double* src = L.x;
+      if (!is_device_ptr(L.x)) {
+        double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
+        host_x[i] = L.x;
+        staged_x[i] = d;
+        if (!piped[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s_in));
+        src = d;
+        off += L.bytes;
+      }
+      if (piped[i])
+        ftl[i] = 2;
+      else
+        xpad_copy(h, xp, lay[lay_idx[i]].second, src, 0, L.lp->n_rows, s_in);
       L.x = xp;
-      if (!is_device_ptr(L.x)) off += L.bytes;  // (never: xp is device memory)
     } else if (!is_device_ptr(L.x)) {
       double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
       host_x[i] = L.x;
@@ -1238,6 +1261,17 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     CUDA_CHECK(cudaEventRecord(h->ev_in, s_in));
     CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_in, 0));
     CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_in, 0));
+    bool any_late = false;
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (ftl[i] == 2) {
+        CUDA_CHECK(cudaMemcpyAsync(const_cast<double*>(staged_x[i]), host_x[i], lv[i].bytes, cudaMemcpyHostToDevice,
+                                   s_in));
+        any_late = true;
+      }
+    if (any_late) {
+      if (!h->ev_x) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventRecord(h->ev_x, s_in));
+    }
     unsigned* flags = h->pipe_flags.as<unsigned>();
     for (size_t i = 0; i < lv.size(); ++i) {
       if (!piped[i]) continue;
@@ -1258,11 +1292,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       unsigned* loc_ready = mp_ready + 1;
       // multipole slab k is needed by targets of slab k-1: keep multipoles one slab ahead
       for (int k = 0; k < S; ++k) {
-        if (ftl[i])
-          xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, host_x[i], P.slab_row0[k],
-                    P.slab_row0[k + 1], s_in);
-        else
-          slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
+        if (!ftl[i]) slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
         write_flag(mp_ready, unsigned(k + 1));
         if (k >= 1) {
           slab_copy(lv[i].host_y, lv[i].y, k - 1, cudaMemcpyHostToDevice, s_in);
@@ -1320,7 +1350,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
       if (ftl[i]) fill_full(p, h, g, L.x);
-      if (i > 0 && ftl[i] != ftl[0]) same_shape = false;
+      if (i > 0 && (ftl[i] != 0) != (ftl[0] != 0)) same_shape = false;
       if (L.lp->mode == 1) {
         p.y = h->fbuf.as<double>() + f_off[i]; p.y_ld = row_ld; p.y_dc = L.lp->dc;
         p.scale = 1.0; p.accumulate = 0; p.pair_out = 1;
@@ -1331,7 +1361,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       }
       if (piped[i]) {
         unsigned* f = h->pipe_flags.as<unsigned>() + flag_off[i];
-        p.pipe_mp = f;
+        p.pipe_mp = ftl[i] ? nullptr : f;  // full-operator sources are resident before their launch
         p.pipe_loc = f + 1;
         p.pipe_done = f + 2;
         p.pipe_need_mp = L.lp->p_need_mp.as<int>();
@@ -1346,7 +1376,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     }
     // small pair-mode segments reduce inside the launch (their last CTA)
     std::vector<bool> reduced_inside(lv.size(), false);
-    if (same_shape && int(segs.size()) <= kMaxSegments) {
+    if (same_shape && int(segs.size()) <= kMaxSegments) {  // (one multi-segment launch per group below)
       ensure(h->counters, kMaxSegments * sizeof(unsigned));
       CUDA_CHECK(cudaMemsetAsync(h->counters.p, 0, kMaxSegments * sizeof(unsigned), s));
       for (size_t i = 0; i < lv.size(); ++i) {
@@ -1368,9 +1398,31 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
           reduced_inside[i] = true;
         }
       }
-      launches += launch_multi(segs, counts, s);
-    } else {
-      for (size_t i = 0; i < segs.size(); ++i) launches += launch_tiles(segs[i], counts[i], s);
+    }
+    // launch groups: all levels at once, or -- copy pipeline with late
+    // full-operator levels -- the other levels first while the late levels'
+    // sources cross PCIe, then the late ones once padded on this stream
+    std::vector<std::vector<size_t>> groups(2);
+    for (size_t i = 0; i < lv.size(); ++i) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const auto& grp = groups[gi];
+      if (grp.empty()) continue;
+      if (gi == 1) {
+        CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_x, 0));
+        for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
+                                       lv[i].lp->n_rows, s);
+      }
+      if (same_shape && int(segs.size()) <= kMaxSegments) {
+        std::vector<TileParams> sub;
+        std::vector<int64_t> sub_counts;
+        for (size_t i : grp) {
+          sub.push_back(segs[i]);
+          sub_counts.push_back(counts[i]);
+        }
+        launches += launch_multi(sub, sub_counts, s);
+      } else {
+        for (size_t i : grp) launches += launch_tiles(segs[i], counts[i], s);
+      }
     }
     for (size_t i = 0; i < lv.size(); ++i) {
       if (lv[i].lp->mode != 1 || reduced_inside[i]) continue;
@@ -1639,6 +1691,8 @@ int cfm_handler_destroy(cfm_handler* h) {
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->ev_in) cudaEventDestroy(h->ev_in);
     if (h->ev_out) cudaEventDestroy(h->ev_out);
+    if (h->ev_prev) cudaEventDestroy(h->ev_prev);
+    if (h->ev_x) cudaEventDestroy(h->ev_x);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     cudaStreamDestroy(h->stream);
