@@ -185,6 +185,7 @@ struct LevelPlan {
   std::vector<unsigned> slab_expected;   // CTAs (tiles x row blocks) writing each slab
   DevBuf p_need_mp, p_need_loc, p_lo, p_hi;
   DevBuf tile_col, tile_off, entry_code, entry_src;
+  DevBuf entry_ncols;     // pair mode: filled columns per entry (uint8)
   DevBuf slot_ids, iota;  // low-rank: per-entry slots
   DevBuf runs;            // low-rank pass 1: tiles = runs of kPass1Run consecutive entries
   int64_t n_runs = 0;
@@ -255,25 +256,34 @@ static bool use_bulk_a(int kc) {
 }
 
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
-static void launch_ws_multi(const MultiTileParams& mp, dim3 grid, cudaStream_t s) {
+static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaStream_t s) {
+  // grid_tiles = (tiles, row blocks) -> one CTA per (tile, row block), row blocks fastest
+  MultiTileParams mp = mp_in;
+  mp.nrb = int(grid_tiles.y);
+  const dim3 grid(unsigned(grid_tiles.x) * grid_tiles.y, 1);
+  if ((long long)grid_tiles.x * grid_tiles.y >= (1ll << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
   const TileParams& q = mp.seg[0];
   const bool tabs = tile_perm_tabs_fit(q.nr, q.nk);
   const int smem = ws_ring_bytes<BM, BN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, tabs);
   if constexpr (BM == 128 && KC == 32 && !SKIP) {
     if (q.ft) {
-      static const int ft_stages = [] {
-        const char* e = getenv("CFM_FT_STAGES");
-        return e ? atoi(e) : 4;
+      // tile skipping pays when a warp has no rows in the last row block or a
+      // segment is a pair plan; otherwise the plain full-operator kernel
+      static const int skip_env = [] {
+        const char* e = getenv("CFM_FT_SKIP");
+        return e ? atoi(e) : -1;
       }();
-      if (ft_stages == 3) {
-        const int smem_ft = ws_ring_bytes<BM, BN, KC, 3>() + tile_table_bytes(q.nr, q.nk, false);
-        auto kf = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 3, SKIP, false, true>;
-        CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
-        kf<<<grid, (WM * WN + 4) * 32, smem_ft, s>>>(mp);
-        return;
+      // (measured: the skipping kernel is ~1% slower when nothing is skipped)
+      long long pair_e = 0, all_e = 0;
+      for (int i = 0; i < mp.n_seg; ++i) {
+        all_e += mp.seg[i].n_entries;
+        if (mp.seg[i].entry_ncols) pair_e += mp.seg[i].n_entries;
       }
-      const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false);
-      auto kf = tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, true>;
+      bool skip = int(mp.nrb) * BM - q.nr >= 32 || 4 * pair_e >= all_e;
+      if (skip_env >= 0) skip = skip_env != 0;
+      const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
+      auto kf = skip ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
+                     : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
       CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
       kf<<<grid, (WM * WN + 4) * 32, smem_ft, s>>>(mp);
       return;
@@ -317,7 +327,7 @@ static void launch_cfg(const TileParams& p, int n_tiles, int tile_base, cudaStre
   TileParams q = p;
   q.tile_base = tile_base;
   dim3 grid(n_tiles, (p.nr + BM - 1) / BM);
-  const int kind = (p.pair_out && tile_kernel_kind(p.nk) == 2) ? 1 : tile_kernel_kind(p.nk);
+  const int kind = p.ft ? 0 : ((p.pair_out && tile_kernel_kind(p.nk) == 2) ? 1 : tile_kernel_kind(p.nk));
   if (p.op_rows) {
     if (kind == 2) launch_sync<BM, BN, WM, WN, true>(q, grid, s);
     else if (kind == 1) launch_ws<BM, BN, WM, WN, 16, 5, true>(q, grid, s);
@@ -389,16 +399,15 @@ static PFN_encodeTiled resolve_encode_tiled() {
   return fn;
 }
 
-// Full-operator TMA mode (CFM_FULL_OPS=0 disables): real dense groups whose
-// operators take the 128-row KC=32 kernel (64 < n <= 512, l = 5..8).
+// Full-operator TMA mode (CFM_FULL_OPS=0 disables): real dense groups with
+// 64 < n <= 1024 (l = 5..10); always the 128-row KC=32 kernel.
 static bool use_full_ops(const cfm_handler* h) {
   static int v = [] {
     const char* e = getenv("CFM_FULL_OPS");
     return e ? atoi(e) : 1;
   }();
   const int nf = h->n * h->f;
-  return v != 0 && !h->op_complex && nf > 64 && nf <= 512 && tile_kernel_kind(nf) == 0 &&
-         resolve_encode_tiled() != nullptr;
+  return v != 0 && !h->op_complex && nf > 64 && nf <= 1024 && resolve_encode_tiled() != nullptr;
 }
 
 template <int RP, int STAGES>
@@ -450,7 +459,7 @@ static int64_t launch_multi(const std::vector<TileParams>& segs, const std::vect
   if (total >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
   mp.start[mp.n_seg] = int(total);
   const TileParams& q = mp.seg[0];
-  const int kind = tile_kernel_kind(q.nk);
+  const int kind = q.ft ? 0 : tile_kernel_kind(q.nk);
   if (q.nr <= 32) {
     dim3 grid(unsigned(total), (q.nr + 31) / 32);
     if (kind == 0) launch_ws_multi<32, kBN, 1, 8, 32, 3, false>(mp, grid, s);
@@ -723,7 +732,16 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     const bool force_pair = m && !strcmp(m, "pair");
     const bool force_target = m && !strcmp(m, "target");
     if (force_pair || (!force_target && lp.target_fill < 0.6)) {
-      lp.hp = build_plan_pairs(n_targets, tgt, off, src, codes, dc, key, n_rows, 16, lp.red);
+      // dense: ~25 MFLOP of row-block work per CTA (l = 9: 2 entries, l = 5: 11) so
+      // sparse levels still give many waves of CTAs and a short tail
+      const int nkp = round_up(h->n * h->f, kKC);
+      static const int ept_env = [] {
+        const char* e = getenv("CFM_PAIR_EPT");
+        return e ? atoi(e) : 0;
+      }();
+      const int ept = ept_env > 0 ? ept_env
+                                  : (g.kind == kDense ? std::max(1, std::min(16, int(2.5e7 / (2.0 * 128 * kBN * nkp)))) : 16);
+      lp.hp = build_plan_pairs(n_targets, tgt, off, src, codes, dc, key, n_rows, ept, lp.red);
       lp.mode = 1;
       upload(lp.r_tgt, lp.red.tgt);
       upload(lp.r_off, lp.red.off);
@@ -736,6 +754,18 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
   lp.n_rows = n_rows;
   push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
   const int64_t E = lp.hp.n_entries();
+  if (lp.mode == 1) {
+    // filled columns per pair entry (slots are filled from column 0): the
+    // full-operator kernel skips the empty trailing 8-column tiles
+    std::vector<unsigned char> nc(std::max<int64_t>(E, 1), 0);
+    for (int64_t e = 0; e < E; ++e)
+      for (int c = kBN - 1; c >= 0; --c)
+        if (lp.hp.entry_src[size_t(e) * kBN + c] >= 0) {
+          nc[e] = static_cast<unsigned char>(c + 1);
+          break;
+        }
+    upload(lp.entry_ncols, nc);
+  }
   if (g.kind == kLowRank || (g.kind == kShared && g.any_fac_core)) {
     std::vector<int> slots(size_t(E) * kBN), iota(E + 1);
     for (int64_t e = 0; e < E; ++e)
@@ -934,6 +964,8 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
       double* xp = h->xpad.as<double>() + off[0];
       xpad_copy(h, xp, g.full.ld, d_x, 0, lp.n_rows, s);
       fill_full(p, h, g, xp);
+      if (lp.mode == 1) p.entry_ncols = lp.entry_ncols.as<unsigned char>();
+      p.n_entries = lp.hp.n_entries();
     }
     if (lp.mode == 1) {
       ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
@@ -1349,7 +1381,11 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       }
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
-      if (ftl[i]) fill_full(p, h, g, L.x);
+      if (ftl[i]) {
+        fill_full(p, h, g, L.x);
+        if (L.lp->mode == 1) p.entry_ncols = L.lp->entry_ncols.as<unsigned char>();
+        p.n_entries = L.lp->hp.n_entries();
+      }
       if (i > 0 && (ftl[i] != 0) != (ftl[0] != 0)) same_shape = false;
       if (L.lp->mode == 1) {
         p.y = h->fbuf.as<double>() + f_off[i]; p.y_ld = row_ld; p.y_dc = L.lp->dc;

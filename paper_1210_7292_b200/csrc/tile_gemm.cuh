@@ -89,6 +89,8 @@ struct TileParams {
   // contiguous zero-padded rows (x_ld = op_ld), one bulk copy per column
   int ft;
   int ft_rows;
+  const unsigned char* entry_ncols;  // pair plans: filled columns per entry (null: all BN)
+  long long n_entries;               // host-side hint: entries of the plan (kernel choice)
   CUtensorMap tmap_a;
 };
 

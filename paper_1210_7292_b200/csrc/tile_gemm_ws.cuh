@@ -9,6 +9,8 @@
 // the consumer warps keep the FP64 tensor pipe fed while the producers run
 // STAGES-1 chunks ahead.
 #pragma once
+#include <type_traits>
+
 #include "tile_gemm.cuh"
 
 namespace cfm {
@@ -91,18 +93,27 @@ constexpr int ws_ring_bytes() {
 }
 
 // Several independent tile lists (e.g. all octree levels of one M2L step) in
-// one launch: blockIdx.x ranges [start[s], start[s+1]) belong to segment s.
+// one launch: tiles [start[s], start[s+1]) of the launch belong to segment s.
+// CTA b works on tile b / nrb, row block b % nrb: the row blocks of a tile run
+// side by side and share its source columns in L2.
 constexpr int kMaxSegments = 12;
 struct MultiTileParams {
   int n_seg;
+  int nrb;  // row blocks per tile
   int start[kMaxSegments + 1];
   TileParams seg[kMaxSegments];
 };
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS, bool BULK_A = false, bool FT = false>
+// FTM: 0 = permuted-gather staging, 1 = full-operator TMA staging, 2 = full-operator
+// TMA staging with interleaved warp tiles that skip rows past the operator and
+// empty trailing columns of pair entries (used when a launch has either)
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP_ROWS, bool BULK_A = false, int FTM = 0>
 __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(const __grid_constant__ MultiTileParams mp) {
+  constexpr bool FT = FTM != 0;
+  constexpr bool IL = FTM == 2;
   int sidx = 0;
-  while (sidx + 1 < mp.n_seg && int(blockIdx.x) >= mp.start[sidx + 1]) ++sidx;
+  const int ltile = int(blockIdx.x) / mp.nrb;
+  while (sidx + 1 < mp.n_seg && ltile >= mp.start[sidx + 1]) ++sidx;
   const TileParams& p = mp.seg[sidx];
   constexpr int NC = WM * WN * 32;  // consumer threads
   constexpr int NP = 4 * 32;        // producer threads
@@ -130,13 +141,14 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   int* s_cp = s_rp + 344;
   int* s_ecode = s_cp + 344;
   short* s_rowtab = reinterpret_cast<short*>(s_ecode + kMaxTileEntries);
+  unsigned char* s_encols = reinterpret_cast<unsigned char*>(s_rowtab);  // full-operator mode (no perm tables)
   const bool tabs_in_smem = tile_perm_tabs_fit(p.nr, p.nk);
   short* s_invtab = s_rowtab + 48 * p.nr + 8;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int tile = p.tile_base + int(blockIdx.x) - mp.start[sidx];
-  const int r0 = blockIdx.y * BM;
+  const int tile = p.tile_base + ltile - mp.start[sidx];
+  const int r0 = (int(blockIdx.x) % mp.nrb) * BM;
   const int e_begin = p.tile_off[tile], e_end = p.tile_off[tile + 1];
 
   for (int c = tid; c < BN; c += NC + NP) s_col[c] = p.tile_col[(long long)tile * BN + c];
@@ -147,6 +159,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   }
   const int n_cached = min(e_end - e_begin, kMaxTileEntries);
   for (int i = tid; i < n_cached; i += NC + NP) s_ecode[i] = p.entry_code[e_begin + i];
+  if (IL && p.entry_ncols)
+    for (int i = tid; i < n_cached; i += NC + NP) s_encols[i] = p.entry_ncols[e_begin + i];
   if (tabs_in_smem) {
     if (p.rowtab)
       for (int i = tid; i < 48 * p.nr; i += NC + NP) s_rowtab[i] = p.rowtab[i];
@@ -322,6 +336,12 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   // ======================= consumer warps =======================
   const int g = lane >> 2, tg = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
+  // first row / column of m-tile mi / n-tile nj of this warp.  Full-operator
+  // mode interleaves them (warp (wm, wn) owns m-tiles mi*WM+wm, n-tiles
+  // nj*WN+wn) so that rows past the operator and empty trailing columns of a
+  // pair entry are skipped evenly by all four SM sub-partitions.
+  auto mrow = [&](int mi) { return IL ? (mi * WM + wm) * 8 : wm * WTM + mi * 8; };
+  auto ncol = [&](int nj) { return IL ? (nj * WN + wn) * 8 : wn * WTN + nj * 8; };
   double acc[MT][NTL][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
@@ -332,22 +352,90 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   d.nchunks = 0;
   int e = next_live(e_begin, d);
   int q = 0;
+  int ml = 0;  // live m-tiles of this warp (full-operator mode; fixed per CTA)
+  if (IL)
+    for (int mi = 0; mi < MT; ++mi)
+      if (r0 + mrow(mi) < p.nr) ml = mi + 1;
+  auto ft_entry = [&](auto mlc, auto nlc) {
+    constexpr int ML = decltype(mlc)::value, NL = decltype(nlc)::value;
+    for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
+      const int s = q % STAGES;
+      mbar_wait(full + s, (q / STAGES) & 1);
+      if (ML > 0 && NL > 0) {
+        const double* as = As + s * BM * LDA + (mrow(0) + g) * LDA + tg;
+        const double* bs = Bs + s * BN * LDB + (ncol(0) + g) * LDB + tg;
+        constexpr int MSTEP = IL ? WM * 8 : 8, NSTEP = IL ? WN * 8 : 8;
+        const int kmax = min(KC, d.klen - kc * KC);
+        auto step = [&](int kk) {
+          double a[ML > 0 ? ML : 1], b[NL > 0 ? NL : 1];
+#pragma unroll
+          for (int mi = 0; mi < ML; ++mi) a[mi] = as[mi * MSTEP * LDA + kk];
+#pragma unroll
+          for (int nj = 0; nj < NL; ++nj) b[nj] = bs[nj * NSTEP * LDB + kk];
+#pragma unroll
+          for (int mi = 0; mi < ML; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        };
+        if (kmax == KC) {
+#pragma unroll
+          for (int kk = 0; kk < KC; kk += 4) step(kk);
+        } else {
+#pragma unroll 2
+          for (int kk = 0; kk < kmax; kk += 4) step(kk);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+  };
+  auto ft_dispatch = [&](auto mlc, int nl) {
+    switch (nl) {
+      case 0: ft_entry(mlc, std::integral_constant<int, 0>{}); break;
+      case 1: ft_entry(mlc, std::integral_constant<int, (NTL < 1 ? NTL : 1)>{}); break;
+      case 2: ft_entry(mlc, std::integral_constant<int, (NTL < 2 ? NTL : 2)>{}); break;
+      case 3: ft_entry(mlc, std::integral_constant<int, (NTL < 3 ? NTL : 3)>{}); break;
+      default: ft_entry(mlc, std::integral_constant<int, NTL>{}); break;
+    }
+  };
   while (e < e_end) {
+    bool generic = true;  // all of this warp's tiles live: the plain loop
+    if constexpr (IL) {
+      static_assert(MT <= 4 && NTL <= 4, "full-operator dispatch covers 4 x 4 tiles per warp");
+      const int i = e - e_begin;
+      const int ncols = p.entry_ncols ? (i < kMaxTileEntries ? int(s_encols[i]) : int(__ldg(p.entry_ncols + e))) : BN;
+      int nl = 0;
+#pragma unroll
+      for (int nj = 0; nj < NTL; ++nj)
+        if (ncol(nj) < ncols) nl = nj + 1;
+      if (ml != MT || nl != NTL) {
+        generic = false;
+        switch (ml) {
+          case 0: ft_dispatch(std::integral_constant<int, 0>{}, nl); break;
+          case 1: ft_dispatch(std::integral_constant<int, (MT < 1 ? MT : 1)>{}, nl); break;
+          case 2: ft_dispatch(std::integral_constant<int, (MT < 2 ? MT : 2)>{}, nl); break;
+          case 3: ft_dispatch(std::integral_constant<int, (MT < 3 ? MT : 3)>{}, nl); break;
+          default: ft_dispatch(std::integral_constant<int, MT>{}, nl); break;
+        }
+      }
+    }
+    if (generic) {
+    constexpr int MSTEP = IL ? WM * 8 : 8, NSTEP = IL ? WN * 8 : 8;
     const int mrows = d.rows - r0 - wm * WTM;
     for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
       const int s = q % STAGES;
       if (!(p.debug & 1)) mbar_wait(full + s, (q / STAGES) & 1);
-      const double* as = As + s * BM * LDA + (wm * WTM + g) * LDA + tg;
-      const double* bs = Bs + s * BN * LDB + (wn * WTN + g) * LDB + tg;
+      const double* as = As + s * BM * LDA + (mrow(0) + g) * LDA + tg;
+      const double* bs = Bs + s * BN * LDB + (ncol(0) + g) * LDB + tg;
       const int kmax = min(KC, d.klen - kc * KC);
       if (SKIP_ROWS) {
 #pragma unroll 2
         for (int kk = 0; kk < kmax; kk += 4) {
           double a[MT], b[NTL];
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * MSTEP * LDA + kk];
 #pragma unroll
-          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * NSTEP * LDB + kk];
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi) {
             if (mi * 8 < mrows) {
@@ -361,9 +449,9 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         for (int kk = 0; kk < KC; kk += 4) {
           double a[MT], b[NTL];
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * MSTEP * LDA + kk];
 #pragma unroll
-          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * NSTEP * LDB + kk];
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
@@ -374,9 +462,9 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         for (int kk = 0; kk < kmax; kk += 4) {
           double a[MT], b[NTL];
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * MSTEP * LDA + kk];
 #pragma unroll
-          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * NSTEP * LDB + kk];
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
@@ -386,17 +474,18 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
     }
+    }
     if (p.pair_out) {
       // pair mode: this entry's 64 columns are 64 distinct (target, source)
       // pairs; write their results to rows e*BN + c (segment-reduced per target later)
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi) {
-        const int row = r0 + wm * WTM + mi * 8 + g;
+        const int row = r0 + mrow(mi) + g;
 #pragma unroll
         for (int nj = 0; nj < NTL; ++nj) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int c = wn * WTN + nj * 8 + 2 * tg + h;
+            const int c = ncol(nj) + 2 * tg + h;
             if (row < p.nr && __ldg(p.entry_src + (long long)e * BN + c) >= 0) {
               const long long v = (long long)e * BN + c;
               double* dst = p.y + (v / p.y_dc) * p.y_ld + (v % p.y_dc) + (long long)p.y_dc * row;
@@ -446,13 +535,13 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   if (p.pipe_loc) wait_flag_geq(p.pipe_loc, unsigned(p.pipe_need_loc[tile]));
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi) {
-    const int row = r0 + wm * WTM + mi * 8 + g;
+    const int row = r0 + mrow(mi) + g;
     if (row >= p.nr) continue;
 #pragma unroll
     for (int nj = 0; nj < NTL; ++nj) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = wn * WTN + nj * 8 + 2 * tg + h;
+        const int c = ncol(nj) + 2 * tg + h;
         const int v = s_col[c];
         if (v < 0) continue;
         double* dst = p.y + (long long)(v / p.y_dc) * p.y_ld + (v % p.y_dc) + (long long)p.y_dc * row;
