@@ -328,19 +328,40 @@ def run_b200(args):
 
     # N > 1: each rank owns a contiguous Morton range of every level's targets
     # (paper_1210_7292_b200.distributed); the source-multipole halo is exchanged
-    # with one NCCL all_to_all per level inside every timed step.
+    # with one NCCL all_to_all per level inside every timed step, overlapped by
+    # the interior targets (all sources owned) held by a second handler: the
+    # boundary targets run once the exchange is in (distributed.overlapped_step).
     stats, halos, owned = {}, {}, {}
+    h_int, int_levels, bnd_levels = None, [], list(levels)
+    if ws > 1:
+        from paper_1210_7292_b200.distributed import (PreparedHalo, build_halo, owner_of_rows, partition_rows,
+                                                      split_interior)
+
+        h_int = make_handler(variant, kernel, ChebyshevGrid(order), eps, device=local, budget_bytes=budget)
+        h_int.precompute({l: full for l in levels}, widths)
+        bnd_levels = []
     for lvl in levels:
         c = cells[lvl].astype(np.int32)
         if ws == 1:
             stats[lvl] = h.plan_level_cells(lvl, c)
             owned[lvl] = None
             continue
-        from paper_1210_7292_b200.distributed import PreparedHalo, build_halo, partition_rows
-
         parts = partition_rows(c, ws)
         owned[lvl] = parts[rank]
-        st, srcs = h.plan_level_cells_subset(lvl, c, parts[rank])
+        inner, bnd = split_interior(c, lvl, parts[rank], owner_of_rows(parts, len(c)))
+        st = {"pairs": 0, "slots": 0, "mode": ""}
+        srcs = [np.zeros(0, np.int64)]
+        for hh, rows, lst, tag in ((h_int, inner, int_levels, "interior"), (h, bnd, bnd_levels, "boundary")):
+            if len(rows) == 0:
+                continue
+            st_h, srcs_h = hh.plan_level_cells_subset(lvl, c, rows)
+            if st_h["pairs"]:
+                lst.append(lvl)
+                st["pairs"] += st_h["pairs"]
+                st["slots"] += st_h["slots"]
+                st["mode"] += f"{tag}:{st_h['mode']} "
+                srcs.append(srcs_h)
+        srcs = np.unique(np.concatenate(srcs))
         gathered = [None] * ws
         dist.all_gather_object(gathered, srcs)
         halos[lvl] = PreparedHalo(build_halo(parts, srcs, gathered, rank), dev)
@@ -365,11 +386,28 @@ def run_b200(args):
 
     step_flops = [0]
 
+    def apply_sharded(x, y):
+        """One M2L step on this rank: returns the launches issued."""
+        if ws == 1:
+            step_flops[0] = h.apply_levels({l: (x[l], y[l]) for l in levels})
+            return h.last_apply_stats()[1]
+        from paper_1210_7292_b200.distributed import overlapped_step
+
+        fl, nl = [0], [0]
+
+        def run(hh, lvls):
+            def go():
+                if lvls:
+                    fl[0] += hh.apply_levels({l: (x[l], y[l]) for l in lvls})
+                    nl[0] += hh.last_apply_stats()[1]
+            return go
+
+        overlapped_step(dist, x, halos, run(h_int, int_levels), run(h, bnd_levels))
+        step_flops[0] = fl[0]
+        return nl[0]
+
     def step():
-        for l in halos:
-            halos[l].exchange(dist, mp[l])
-        step_flops[0] = h.apply_levels({l: (mp[l], loc[l]) for l in levels})
-        return h.last_apply_stats()[1]
+        return apply_sharded(mp, loc)
 
     for _ in range(args.warmup):
         step()
@@ -393,7 +431,10 @@ def run_b200(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         flush.fill_(0.0)
         e0.record()
-        h.apply_planned(l, mp[l], loc[l])
+        if ws == 1 or l in bnd_levels:
+            h.apply_planned(l, mp[l], loc[l])
+        if ws > 1 and l in int_levels:
+            h_int.apply_planned(l, mp[l], loc[l])
         e1.record()
         torch.cuda.synchronize()
         lvl_ms[l] = e0.elapsed_time(e1)
@@ -418,10 +459,9 @@ def run_b200(args):
         if ws == 1:
             h.apply_levels({l: (np_mp[l], np_loc[l]) for l in levels})
             return
-        for l in levels:  # host -> device, halo exchange, apply into host locals
+        for l in levels:  # host -> device, overlapped halo exchange + apply, locals back to the host
             d_mp[l].copy_(h_mp[l], non_blocking=True)
-            halos[l].exchange(dist, d_mp[l])
-        h.apply_levels({l: (d_mp[l], loc[l]) for l in levels})
+        apply_sharded(d_mp, loc)
         for l in levels:
             h_loc[l].copy_(loc[l], non_blocking=True)
         torch.cuda.synchronize()
@@ -441,7 +481,10 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
     bytes_lvl = {l: mp[l].numel() * mp[l].element_size() for l in levels}
-    h2d = sum(2 * b for b in bytes_lvl.values()) * ws  # multipoles + locals (accumulated in place), all ranks
+    if ws == 1:
+        h2d = sum(2 * b for b in bytes_lvl.values())  # multipoles + locals (accumulated in place)
+    else:
+        h2d = sum(bytes_lvl.values()) * ws  # every rank uploads its multipole arrays; locals stay resident
     d2h = sum(bytes_lvl.values()) * ws
 
     # roofline of the dominant kernel: the single multi-level tile_gemm launch of a step
@@ -451,8 +494,12 @@ def run_b200(args):
     # algorithmic flops of one step = the reference's own accounting (m2l.py:333-426),
     # converted to real flops (x4 for complex128 operators)
     real_flops = step_flops[0] * (4 if cplx else 1)
+    if ws > 1:  # whole-job flops; the roofline is per GPU (average over ranks)
+        t = torch.tensor([real_flops], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        real_flops = t.item()
     flops_pair = real_flops / pairs_total
-    achieved = real_flops / (step_ms_med * 1e-3) / 1e12
+    achieved = real_flops / ws / (step_ms_med * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
@@ -540,6 +587,9 @@ def run_b200(args):
             t = torch.tensor([ms2], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms2 = t.item()
+            t = torch.tensor([fl2], dtype=torch.int64, device=dev)
+            dist.all_reduce(t)
+            fl2 = int(t.item())
         secondary = {"variant": "iablk", "eps": eps, "value": pairs_total / (ms2 * 1e-3), "unit": "pairs/s",
                      "ms_per_step": ms2, "flops_per_step_reference_accounting": fl2,
                      "achieved_tflops": fl2 / (ms2 * 1e-3) / 1e12,

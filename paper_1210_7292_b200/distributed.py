@@ -12,6 +12,13 @@ GPUs, gloo on CPU in the tests).  Range boundaries are aligned to sibling
 groups (multiples of 8 in Morton order) so the halo is the 2-cell shell of
 SURVEY.md §8e.
 
+Overlap: a rank's owned targets split into *interior* ones,
+whose far sources are all owned here, and *boundary* ones.  A step starts the
+halo exchange (asynchronous collective on the communicator's stream), runs the
+interior targets' M2L on the compute stream meanwhile, waits for the exchange
+and then runs the boundary targets — correct by construction (stream order
+only, no device-side waiting), so the exchange can never be starved of SMs.
+
 One process per GPU; ``torch.distributed`` provides the plumbing.
 """
 
@@ -54,6 +61,48 @@ def partition_rows(cells_ijk, world: int) -> list[np.ndarray]:
         out.append(np.sort(order[prev:cut]))
         prev = cut
     return out
+
+
+def split_interior(cells_ijk, level: int, rows, owner) -> tuple[np.ndarray, np.ndarray]:
+    """Split target `rows` of a level into (interior, boundary): interior
+    targets have every far source (octree.py:148-178: children of the parent's
+    neighbours with t.t > 3) owned by the same rank as the target.
+
+    `owner[r]` is the rank owning row r.  Exact: the 216 candidates of each
+    target are enumerated like the classifier does."""
+    cells = np.asarray(cells_ijk, dtype=np.int64).reshape(-1, 3)
+    rows = np.asarray(rows, dtype=np.int64)
+    owner = np.asarray(owner, dtype=np.int64)
+    if len(rows) == 0:
+        return rows.copy(), rows.copy()
+    side = 1 << level
+    grid = np.full((side, side, side), -1, dtype=np.int64)
+    grid[cells[:, 0], cells[:, 1], cells[:, 2]] = owner
+    t_ijk = cells[rows]
+    me = owner[rows]
+    base = 2 * ((t_ijk >> 1) - 1)
+    ok = np.ones(len(rows), dtype=bool)
+    for dx in range(6):
+        for dy in range(6):
+            for dz in range(6):
+                src = base + np.array([dx, dy, dz])
+                inside = np.all((src >= 0) & (src < side), axis=1)
+                t = t_ijk - src
+                far = (t * t).sum(axis=1) > 3
+                sel = inside & far
+                o = np.full(len(rows), -1, dtype=np.int64)
+                s_in = src[sel]
+                o[sel] = grid[s_in[:, 0], s_in[:, 1], s_in[:, 2]]
+                ok &= (o < 0) | (o == me)
+    return rows[ok], rows[~ok]
+
+
+def owner_of_rows(parts, n_rows: int) -> np.ndarray:
+    """Row -> owning rank from partition_rows' output."""
+    owner = np.full(n_rows, -1, dtype=np.int64)
+    for r, rows in enumerate(parts):
+        owner[np.asarray(rows, dtype=np.int64)] = r
+    return owner
 
 
 @dataclass
@@ -147,15 +196,41 @@ class PreparedHalo:
         self.recv_counts = halo.recv_counts
 
     def exchange(self, dist, mpoles, group=None):
+        return self.start(dist, mpoles, group=group).finish()
+
+    def start(self, dist, mpoles, group=None) -> "_PendingHalo":
+        """Launch the exchange asynchronously (the collective runs on the
+        communicator's stream after the packing on the current stream);
+        ``finish()`` makes the current stream wait and scatters the rows."""
         import torch
 
         send = mpoles.index_select(0, self.send_idx)
         recv = torch.empty((len(self.recv_idx),) + tuple(mpoles.shape[1:]), dtype=mpoles.dtype, device=mpoles.device)
         if mpoles.is_complex():
-            dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), self.recv_counts,
-                                   self.send_counts, group=group)
+            work = dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), self.recv_counts,
+                                          self.send_counts, group=group, async_op=True)
         else:
-            dist.all_to_all_single(recv, send, self.recv_counts, self.send_counts, group=group)
+            work = dist.all_to_all_single(recv, send, self.recv_counts, self.send_counts, group=group, async_op=True)
+        return _PendingHalo(work, mpoles, self.recv_idx, recv, send)
+
+
+class _PendingHalo:
+    def __init__(self, work, mpoles, recv_idx, recv, send):
+        self.work, self.mpoles, self.recv_idx, self.recv, self._send = work, mpoles, recv_idx, recv, send
+
+    def finish(self):
+        self.work.wait()
         if len(self.recv_idx):
-            mpoles.index_copy_(0, self.recv_idx, recv)
-        return mpoles
+            self.mpoles.index_copy_(0, self.recv_idx, self.recv)
+        return self.mpoles
+
+
+def overlapped_step(dist, mpoles: dict, halos: dict, apply_interior, apply_boundary, group=None):
+    """One sharded M2L step with the halo exchange overlapped by the interior
+    targets: start every level's exchange, apply the interior targets, finish
+    the exchanges, apply the boundary targets."""
+    pending = [halos[lvl].start(dist, mpoles[lvl], group=group) for lvl in sorted(halos)]
+    apply_interior()
+    for p in pending:
+        p.finish()
+    apply_boundary()

@@ -14,8 +14,11 @@ from paper_1210_7292_b200.distributed import (
     build_halo,
     exchange_halo,
     morton_keys,
+    overlapped_step,
+    owner_of_rows,
     partition_rows,
     setup_level,
+    split_interior,
 )
 
 
@@ -126,3 +129,95 @@ def test_sharded_apply_equals_single_process(world, case, golden):
     # of pairs, so compare at round-off (the GPU path is partition-independent)
     assert O.rel_l2(res, ref) <= 1e-14
     assert all(h > 0 for h in halo_sizes)
+
+
+@pytest.mark.parametrize("world,case", [(2, "cube"), (4, "cube"), (3, "sphere")])
+def test_split_interior_matches_far_lists(world, case, golden):
+    if case == "cube":
+        level = 4
+        side = 1 << level
+        cells = np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3)
+    else:
+        level = 4
+        cells = golden("sphere_lists")["cells_4"].astype(np.int64)
+    parts = partition_rows(cells, world)
+    owner = owner_of_rows(parts, len(cells))
+    for r in range(world):
+        inner, bnd = split_interior(cells, level, parts[r], owner)
+        assert np.array_equal(np.sort(np.concatenate([inner, bnd])), parts[r])
+        tgt, off, src, _ = O.far_lists(cells, level, targets=parts[r])
+        want = [int(t) for i, t in enumerate(tgt) if np.all(owner[src[off[i]:off[i + 1]]] == r)]
+        # targets without any far source are interior as well
+        want = sorted(set(want) | (set(parts[r].tolist()) - set(tgt.tolist())))
+        assert inner.tolist() == want
+        assert len(bnd) > 0
+
+
+def _overlap_worker(rank, world, port, cells, level, order, out):
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        glob = np.random.default_rng(5).uniform(-1, 1, (len(cells), order**3))
+        parts = partition_rows(cells, world)
+        owned = parts[rank]
+        owner = owner_of_rows(parts, len(cells))
+        inner, bnd = split_interior(cells, level, owned, owner)
+        _, _, src, _ = O.far_lists(cells, level, targets=owned)
+        need = np.unique(src)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, need)
+        halo = PreparedHalo(build_halo(parts, need, gathered, rank), torch.device("cpu"))
+        local = torch.zeros((len(cells), order**3), dtype=torch.float64)
+        local[torch.as_tensor(owned)] = torch.from_numpy(glob[owned])
+        orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+            {level: O.full_far_field()}, {level: 1.0 / (1 << level)})
+        loc = np.zeros_like(glob)
+
+        def apply(rows):
+            def run():
+                tgt, off, src, t = O.far_lists(cells, level, targets=rows)
+                orc.apply_fast(level, tgt, off, src, t, local.numpy().copy(), loc)
+            return run
+
+        # interior targets run while the halo rows of `local` are still zero
+        overlapped_step(dist, {level: local}, {level: halo}, apply(inner), apply(bnd))
+        parts_out = [None] * world
+        dist.all_gather_object(parts_out, (owned, loc[owned]))
+        if rank == 0:
+            res = np.zeros_like(glob)
+            for rows, vals in parts_out:
+                res[rows] = vals
+            out.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,case", [(2, "cube"), (3, "sphere")])
+def test_overlapped_step_equals_single_process(world, case, golden):
+    import multiprocessing as mp
+
+    level, order = 4, 3
+    if case == "cube":
+        side = 1 << level
+        cells = np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3)
+    else:
+        cells = golden("sphere_lists")["cells_4"].astype(np.int64)
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, cells, level, order, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    tgt, off, src, t = O.far_lists(cells, level)
+    orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+        {level: O.full_far_field()}, {level: 1.0 / (1 << level)})
+    glob = np.random.default_rng(5).uniform(-1, 1, (len(cells), order**3))
+    ref = np.zeros_like(glob)
+    orc.apply_fast(level, tgt, off, src, t, glob, ref)
+    assert O.rel_l2(res, ref) <= 1e-14

@@ -641,3 +641,60 @@ def test_host_precompute_path(torch_cuda, golden, case, variant):
     for attr in ("operator_count", "stored_bytes"):
         assert getattr(h_dev, attr)() == getattr(h_host, attr)()
     assert h_dev.factorization_calls == h_host.factorization_calls
+
+
+@pytest.mark.parametrize("mode", ["target", "pair"])
+@pytest.mark.parametrize("case", ["sphere_lists", "cube_l5"])
+def test_interior_boundary_split_equals_single_gpu(torch_cuda, golden, case, mode, monkeypatch):
+    """The overlapped multi-GPU step, one shard at a time on one GPU: interior
+    targets (distributed.split_interior) applied while the shard's halo rows
+    are still zero, boundary targets after they are filled -- two handlers,
+    as bench.py uses them -- reproduce the single-plan locals bitwise (with the
+    plan mode fixed: target and pair plans sum a target's pairs in different
+    orders, so a subset whose fill picks the other mode agrees to ~1e-15)."""
+    torch = torch_cuda
+    monkeypatch.setenv("CFM_PLAN_MODE", mode)
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+    from paper_1210_7292_b200.distributed import owner_of_rows, partition_rows, split_interior
+
+    if case == "sphere_lists":
+        g = golden("sphere_lists")
+        lvl = 4
+        cells = g[f"cells_{lvl}"]
+        mp = torch.from_numpy(_mpoles(g, lvl, "sphere_lists")).cuda()
+        mk = lambda: _handler(g, "nablk")[0]  # noqa: E731
+    else:  # l = 5: full-operator TMA path
+        lvl, order = 4, 5
+        side = 1 << lvl
+        cells = np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3).astype(np.int32)
+        mp = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (len(cells), order**3))).cuda()
+
+        def mk():
+            h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+            h.precompute({lvl: full_far_field_vectors()}, {lvl: 1.0 / side})
+            return h
+    h = mk()
+    h.plan_level_cells(lvl, cells)
+    ref = torch.zeros_like(mp)
+    h.apply_planned(lvl, mp, ref)
+    out = torch.zeros_like(mp)
+    parts = partition_rows(cells, 3)
+    owner = owner_of_rows(parts, len(cells))
+    for r, part in enumerate(parts):
+        inner, bnd = split_interior(cells, lvl, part, owner)
+        assert len(bnd) > 0
+        local = torch.zeros_like(mp)
+        rows = torch.as_tensor(part, device="cuda")
+        local[rows] = mp[rows]
+        loc = torch.zeros_like(mp)
+        if len(inner):
+            hi = mk()
+            hi.plan_level_cells_subset(lvl, cells, inner)
+            hi.apply_planned(lvl, local, loc)  # halo rows still zero
+        hb = mk()
+        _, srcs = hb.plan_level_cells_subset(lvl, cells, bnd)
+        idx = torch.as_tensor(srcs, device="cuda")
+        local[idx] = mp[idx]  # the exchange
+        hb.apply_planned(lvl, local, loc)
+        out[rows] = loc[rows]
+    assert torch.equal(out, ref)
