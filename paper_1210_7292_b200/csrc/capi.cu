@@ -1638,6 +1638,9 @@ struct cfm_fmm {
   cfm::OpStack m2m_ops, l2l_ops;
   cfm::CodeMap octmap;
   std::map<int, cfm::LevelPlan> m2m_plans, l2l_plans;  // key: child level / parent level (x dc)
+  // P2P: leaf-sorted positions (built on first use), sorted weights, leaf lists by size class
+  cfm::DevBuf px, py, pz, sw, small_leaves, large_leaves;
+  int64_t n_small = -1, n_large = 0;
 };
 
 namespace cfm {
@@ -2504,10 +2507,53 @@ int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights
     CUDA_CHECK(cudaSetDevice(f->tree->device));
     FmmGeom g = fmm_geom(f);
     if (!g.n_leaves) return;
-    k_p2p<128><<<unsigned(g.n_leaves), 64, 0, static_cast<cudaStream_t>(stream)>>>(
-        g, f->leaf_grid.as<int>(), kernel, wavenumber, weights, weights_complex ? 2 : 1, potentials,
-        out_complex ? 2 : 1);
-    CUDA_CHECK(cudaGetLastError());
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long long np_ = f->tree->n_points;
+    const unsigned nb = unsigned((np_ + 255) / 256);
+    if (f->n_small < 0) {
+      // leaf-sorted positions and the two leaf-size classes (<= 64 particles, more)
+      f->px.alloc(std::max<size_t>(size_t(np_) * 8, 16));
+      f->py.alloc(std::max<size_t>(size_t(np_) * 8, 16));
+      f->pz.alloc(std::max<size_t>(size_t(np_) * 8, 16));
+      if (np_) k_p2p_sort_pos<<<nb, 256, 0, st>>>(g.pts, g.perm, np_, f->px.as<double>(), f->py.as<double>(),
+                                                    f->pz.as<double>());
+      CUDA_CHECK(cudaGetLastError());
+      std::vector<long long> off(size_t(g.n_leaves) + 1);
+      CUDA_CHECK(cudaMemcpy(off.data(), g.leaf_off, off.size() * 8, cudaMemcpyDeviceToHost));
+      std::vector<long long> sm, lg;
+      for (long long l = 0; l < g.n_leaves; ++l) (off[l + 1] - off[l] <= 64 ? sm : lg).push_back(l);
+      upload(f->small_leaves, sm);
+      upload(f->large_leaves, lg);
+      f->n_small = int64_t(sm.size());
+      f->n_large = int64_t(lg.size());
+    }
+    const int wdc = weights_complex ? 2 : 1;
+    f->sw.alloc(std::max<size_t>(size_t(np_) * wdc * 8, 16));
+    if (np_) {
+      if (wdc == 2) k_p2p_sort_w<2><<<nb, 256, 0, st>>>(weights, g.perm, np_, f->sw.as<double>());
+      else k_p2p_sort_w<1><<<nb, 256, 0, st>>>(weights, g.perm, np_, f->sw.as<double>());
+      CUDA_CHECK(cudaGetLastError());
+    }
+    P2PGeom pg{g.leaf_off, g.leaf_ijk, f->leaf_grid.as<int>(), 1 << g.depth, f->px.as<double>(), f->py.as<double>(),
+               f->pz.as<double>(), g.perm};
+    auto run = [&](auto ker, auto wd, auto od) {
+      constexpr int K = decltype(ker)::value, W = decltype(wd)::value, O = decltype(od)::value;
+      if (f->n_small)
+        k_p2p_small<K, W, O><<<unsigned(f->n_small), 128, 0, st>>>(pg, f->small_leaves.as<long long>(),
+                                                                  f->sw.as<double>(), wavenumber, potentials);
+      if (f->n_large)
+        k_p2p_large<K, W, O><<<unsigned(f->n_large), 128, 0, st>>>(pg, f->large_leaves.as<long long>(),
+                                                                  f->sw.as<double>(), wavenumber, potentials);
+      CUDA_CHECK(cudaGetLastError());
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    if (kernel == 0 && wdc == 1 && !out_complex) run(I0{}, I1{}, I1{});
+    else if (kernel == 0 && wdc == 1) run(I0{}, I1{}, I2{});
+    else if (kernel == 0) run(I0{}, I2{}, I2{});
+    else if (wdc == 1) run(I1{}, I1{}, I2{});
+    else run(I1{}, I2{}, I2{});
   });
 }
 

@@ -110,6 +110,7 @@ class B200FmmPlan:
         loc = {l: torch.zeros_like(mp[l]) for l in levels}
         st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         lib = self._lib
+        out = torch.zeros(self.n_points, dtype=tdt, device=dev)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         ev[0].record()
         _native.check(lib.cfm_fmm_p2m(self._f, wd.data_ptr(), int(cplx), mp[self.depth].data_ptr(), st))
@@ -123,7 +124,6 @@ class B200FmmPlan:
         for lvl in range(2, self.depth):
             _native.check(lib.cfm_fmm_l2l(self._f, lvl, loc[lvl].data_ptr(), loc[lvl + 1].data_ptr(), int(cplx), st))
         ev[4].record()
-        out = torch.zeros(self.n_points, dtype=tdt, device=dev)
         _native.check(lib.cfm_fmm_l2p(self._f, loc[self.depth].data_ptr(), int(cplx), out.data_ptr(), st))
         ev[5].record()
         kind = 0 if getattr(self.kernel, "wavenumber", None) is None else 1
