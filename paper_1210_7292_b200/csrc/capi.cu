@@ -170,6 +170,10 @@ struct Group {
   int full_rows = 0;
   CodeMap fullmap;
   CUtensorMap full_tmap;
+  // low-rank counterpart: per-transfer permuted factors (U_t rows and V_t^H
+  // columns permuted once), read with contiguous copies from padded sources
+  bool has_lrfull = false;
+  OpStack lrf_left, lrf_right_h;
 };
 
 struct LevelPlan {
@@ -410,7 +414,7 @@ static bool use_full_ops(const cfm_handler* h) {
   return v != 0 && !h->op_complex && nf > 64 && nf <= 1024 && resolve_encode_tiled() != nullptr;
 }
 
-template <int RP, int STAGES>
+template <int RP, int STAGES, bool VB>
 static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, cudaStream_t s) {
   constexpr int KC = 16;
   const int fixed = lr_smem_bytes<RP, KC, STAGES>() + 4 * 64 + 3 * 4 * 344 + 4 * kMaxTileEntries;
@@ -418,7 +422,7 @@ static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, 
   const int tabs = 48 * 2 * (lp_.nr + lp_.nk + 8);
   lp_.tabs_smem = (fixed + tabs <= 227 * 1024) ? 1 : 0;
   const int smem = fixed + (lp_.tabs_smem ? tabs : 0);
-  auto kern = lowrank_ws_kernel<RP, KC, STAGES>;
+  auto kern = lowrank_ws_kernel<RP, KC, STAGES, VB>;
   CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int64_t max_grid = 1 << 30;
   for (int64_t base = first; base < first + count; base += max_grid) {
@@ -432,11 +436,18 @@ static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, 
   return true;
 }
 
-static bool launch_lowrank_fused(const LowRankParams& lp_, int rmax, int64_t first, int64_t count, cudaStream_t s) {
+static bool launch_lowrank_fused(const LowRankParams& lp_, int rmax, int64_t first, int64_t count, cudaStream_t s,
+                                 bool vb = false) {
   if (!use_fused_lowrank()) return false;
-  if (rmax <= 16) return launch_lowrank_cfg<16, 5>(lp_, first, count, s);
-  if (rmax <= 32) return launch_lowrank_cfg<32, 4>(lp_, first, count, s);
-  if (rmax <= 64) return launch_lowrank_cfg<64, 2>(lp_, first, count, s);
+  if (vb) {
+    if (rmax <= 16) return launch_lowrank_cfg<16, 5, true>(lp_, first, count, s);
+    if (rmax <= 32) return launch_lowrank_cfg<32, 4, true>(lp_, first, count, s);
+    if (rmax <= 64) return launch_lowrank_cfg<64, 2, true>(lp_, first, count, s);
+    return false;
+  }
+  if (rmax <= 16) return launch_lowrank_cfg<16, 5, false>(lp_, first, count, s);
+  if (rmax <= 32) return launch_lowrank_cfg<32, 4, false>(lp_, first, count, s);
+  if (rmax <= 64) return launch_lowrank_cfg<64, 2, false>(lp_, first, count, s);
   return false;
 }
 
@@ -690,6 +701,46 @@ static void build_lowrank_stacks(cfm_handler* h, OpStack& left, OpStack& right_h
   set_per_op(right_h, rrows, {});  // pass 1: rows = rank
 }
 
+// Per-transfer low-rank factors for real operators: U_t[i][a] = left_o[tab_r[i]][a],
+// V_t^H[a][j] = right_o[tab_c[j]][a] (the products the permuted apply forms:
+// Y[a] = sum_k right^H[a][k] x[inv[k]] = sum_j right^H[a][tab[j]] x[j]).
+static void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, int n_ops,
+                               const int* ranks, const double* L, const double* R) {
+  const int n = h->n;
+  int rmax = 0;
+  for (int i = 0; i < n_ops; ++i) rmax = std::max(rmax, ranks[i]);
+  std::vector<size_t> off(n_ops + 1, 0);
+  for (int i = 0; i < n_ops; ++i) off[i + 1] = off[i] + size_t(n) * ranks[i];
+  make_stack(g.lrf_left, n_transfers, n, std::max(rmax, 1));
+  make_stack(g.lrf_right_h, n_transfers, std::max(rmax, 1), n);
+  std::vector<int> ident(n), rk(n_transfers);
+  std::iota(ident.begin(), ident.end(), 0);
+  std::vector<double> bl(g.lrf_left.stride), br(g.lrf_right_h.stride);
+  for (int k = 0; k < n_transfers; ++k) {
+    const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
+    const int o = g.main.op[c];
+    const std::vector<int> tr = g.main.rperm[c] >= 0 ? permutation_table(g.main.rperm[c], h->order) : ident;
+    const std::vector<int> tc = g.pass1.cperm[c] >= 0 ? permutation_table(g.pass1.cperm[c], h->order) : ident;
+    const int r = ranks[o];
+    rk[k] = r;
+    std::fill(bl.begin(), bl.end(), 0.0);
+    std::fill(br.begin(), br.end(), 0.0);
+    const double* Lo = L + off[o];
+    const double* Ro = R + off[o];
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < r; ++a) bl[size_t(i) * g.lrf_left.ld + a] = Lo[size_t(tr[i]) * r + a];
+    for (int a = 0; a < r; ++a)
+      for (int j = 0; j < n; ++j) br[size_t(a) * g.lrf_right_h.ld + j] = Ro[size_t(tc[j]) * r + a];
+    put_stack(g.lrf_left, k, bl);
+    put_stack(g.lrf_right_h, k, br);
+    g.fullmap.op[c] = k;
+  }
+  g.fullmap.push();
+  set_per_op(g.lrf_left, {}, rk);
+  set_per_op(g.lrf_right_h, rk, {});
+  g.has_lrfull = true;
+}
+
 // ------------------------------------------------------------------ planning
 static std::vector<int16_t> codes_from_t(int64_t P, const int8_t* t) {
   std::vector<int16_t> codes(P);
@@ -739,8 +790,13 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
         const char* e = getenv("CFM_PAIR_EPT");
         return e ? atoi(e) : 0;
       }();
-      const int ept = ept_env > 0 ? ept_env
-                                  : (g.kind == kDense ? std::max(1, std::min(16, int(2.5e7 / (2.0 * 128 * kBN * nkp)))) : 16);
+      // ... and at least ~2 CTAs per SM where the level has the entries for it
+      // (a small level in few long CTAs is latency-bound)
+      const int64_t e_est = lp.hp.n_pairs * dc / kBN + 1;
+      const int ept_occ = int(std::max<int64_t>(1, e_est / (2 * 148)));
+      int ept = g.kind == kDense ? std::max(1, std::min(16, int(2.5e7 / (2.0 * 128 * kBN * nkp)))) : 16;
+      ept = std::min(ept, ept_occ);
+      if (ept_env > 0) ept = ept_env;
       lp.hp = build_plan_pairs(n_targets, tgt, off, src, codes, dc, key, n_rows, ept, lp.red);
       lp.mode = 1;
       upload(lp.r_tgt, lp.red.tgt);
@@ -1005,6 +1061,27 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
       q.rowtab = h->rowtab.as<short>();
       q.invtab = h->invtab.as<short>();
       q.x = d_x; q.x_ld = row_ld; q.x_dc = dc;
+      const bool vb = g.has_lrfull && dc == 1;
+      if (vb) {
+        // per-transfer factors, identity permutations, zero-padded source rows
+        const int ldx = g.lrf_right_h.ld;
+        const auto xo = xpad_layout(h, {{lp.n_rows, ldx}}, s);
+        double* xp = h->xpad.as<double>() + xo[0];
+        xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
+        q.code_op = g.fullmap.d_op.as<int>();
+        q.code_rperm = g.fullmap.d_rperm.as<int>();
+        q.code_cperm = g.fullmap.d_cperm.as<int>();
+        q.vh = g.lrf_right_h.d.as<double>();
+        q.vh_stride = g.lrf_right_h.stride;
+        q.vh_ld = g.lrf_right_h.ld;
+        q.u = g.lrf_left.d.as<double>();
+        q.u_stride = g.lrf_left.stride;
+        q.u_ld = g.lrf_left.ld;
+        q.rank = g.lrf_left.d_klen.as<int>();
+        q.n_ops = g.lrf_left.n_ops;
+        q.x = xp;
+        q.x_ld = ldx;
+      }
       if (lp.mode == 1) {
         ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
         q.y = h->fbuf.as<double>(); q.y_ld = row_ld; q.y_dc = dc;
@@ -1013,7 +1090,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
         q.y = d_y; q.y_ld = row_ld; q.y_dc = dc;
         q.scale = scale; q.accumulate = 1; q.pair_out = 0;
       }
-      if (launch_lowrank_fused(q, g.right_h.rows, 0, lp.hp.n_tiles, s)) {
+      if (launch_lowrank_fused(q, vb ? g.lrf_right_h.rows : g.right_h.rows, 0, lp.hp.n_tiles, s, vb)) {
         ++launches;
         if (lp.mode == 1)
           launches += launch_reduce(lp, h->fbuf.as<double>(), row_ld, d_y, row_ld, int(row_ld), scale, s);
@@ -1783,6 +1860,7 @@ int cfm_set_lowrank_group(cfm_handler* h, int key, int n_transfers, const int8_t
     for (int i = 0; i < n_ops; ++i)
       if (ranks[i] < 0 || ranks[i] > h->n) throw Error(CFM_ERR_VALUE, "rank out of range");
     build_lowrank_stacks(h, g.left, g.right_h, n_ops, ranks, left, right, h->n, h->n);
+    if (use_full_ops(h)) build_lowrank_full(h, g, n_transfers, transfers, n_ops, ranks, left, right);
     h->groups[key] = std::move(g);
     h->plans.clear();
   });

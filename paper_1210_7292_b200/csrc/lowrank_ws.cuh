@@ -59,7 +59,10 @@ constexpr int lr_smem_bytes() {
   return STAGES * (128 + 64) * (KC + 4) * 8 + 4 * 64 * (RP + 4) * 8 + 2 * STAGES * 8 + 4 * 344;
 }
 
-template <int RP, int KC, int STAGES>
+// VB: sources are contiguous zero-padded rows and the factors are the
+// per-transfer permuted ones (no permutation in the copies): B is staged with
+// 16-B cp.async pieces instead of 8-B element gathers.
+template <int RP, int KC, int STAGES, bool VB = false>
 __global__ void __launch_bounds__(12 * 32, 1) lowrank_ws_kernel(const __grid_constant__ LowRankParams p) {
   constexpr int BM = 128, BN = 64, WM = 4, WN = 2;
   constexpr int NC = 8 * 32, NP = 4 * 32;
@@ -68,7 +71,8 @@ __global__ void __launch_bounds__(12 * 32, 1) lowrank_ws_kernel(const __grid_con
   constexpr int MT1 = RP / 8;                  // phase-1 m-tiles (each warp: all RP rows x 8 columns)
   constexpr int LDA = KC + 4, LDB = KC + 4, LDY = RP + 4;
   constexpr int A1_PIECES = RP * (KC / 2), A2_PIECES = BM * (KC / 2);
-  constexpr int B_PER_T = BN * KC / NP;
+  constexpr int B_PER_T = VB ? BN * KC / 2 / NP : BN * KC / NP;  // 16-B pieces (VB) or 8-B elements per thread
+  constexpr int B_TPC = VB ? KC / 2 : KC;                          // threads per column
   static_assert(A1_PIECES % NP == 0 && A2_PIECES % NP == 0 && (BN * KC) % NP == 0, "mapping");
   static_assert(NP % KC == 0, "B mapping");
   static_assert(RP % 8 == 0 && RP <= 64, "rank pad");
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(12 * 32, 1) lowrank_ws_kernel(const __grid_con
     auto fetch_src = [&](int ee) {
 #pragma unroll
       for (int u = 0; u < B_PER_T; ++u)
-        nsrc[u] = ee < e_end ? __ldg(p.entry_src + (long long)ee * BN + pt / KC + u * (NP / KC)) : -1;
+        nsrc[u] = ee < e_end ? __ldg(p.entry_src + (long long)ee * BN + pt / B_TPC + u * (NP / B_TPC)) : -1;
     };
     fetch_src(e);
     while (e < e_end) {
@@ -186,16 +190,27 @@ __global__ void __launch_bounds__(12 * 32, 1) lowrank_ws_kernel(const __grid_con
           cp_async16(as + a * LDA + 2 * kp, ok ? (const void*)(vbase + (long long)a * p.vh_ld + k0 + 2 * kp)
                                                : (const void*)p.vh, ok);
         }
-        const int kk = pt % KC;
-        const int k = k0 + kk;
-        const bool kvalid = k < p.nk;
-        int j = k;
-        if (kvalid && d.cperm >= 0) j = invtab[d.cperm * p.nk + k];
+        if (VB) {
+          const int kp = pt % B_TPC;
+          const bool kvalid = k0 + 2 * kp < p.nk;  // (the pair past n reads a zero pad element)
 #pragma unroll
-        for (int u = 0; u < B_PER_T; ++u) {
-          const int c = pt / KC + u * (NP / KC);
-          const bool ok = kvalid && bcol[u] != nullptr;
-          cp_async8(bs + c * LDB + kk, ok ? (const void*)(bcol[u] + (long long)p.x_dc * j) : (const void*)p.vh, ok);
+          for (int u = 0; u < B_PER_T; ++u) {
+            const int c = pt / B_TPC + u * (NP / B_TPC);
+            const bool ok = kvalid && bcol[u] != nullptr;
+            cp_async16(bs + c * LDB + 2 * kp, ok ? (const void*)(bcol[u] + k0 + 2 * kp) : (const void*)p.vh, ok);
+          }
+        } else {
+          const int kk = pt % KC;
+          const int k = k0 + kk;
+          const bool kvalid = k < p.nk;
+          int j = k;
+          if (kvalid && d.cperm >= 0) j = invtab[d.cperm * p.nk + k];
+#pragma unroll
+          for (int u = 0; u < B_PER_T; ++u) {
+            const int c = pt / KC + u * (NP / KC);
+            const bool ok = kvalid && bcol[u] != nullptr;
+            cp_async8(bs + c * LDB + kk, ok ? (const void*)(bcol[u] + (long long)p.x_dc * j) : (const void*)p.vh, ok);
+          }
         }
         mbar_cp_async_arrive(full + s);
       }
