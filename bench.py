@@ -260,6 +260,13 @@ def cpu_port_sample(cfg, n_targets, workers):
     return pairs / dt, pairs, dt
 
 
+def workload_name(cfg, variant=None):
+    """The workload string both arms print in config.workload."""
+    n, depth, order, geom, v0, eps = CONFIGS[cfg]
+    return (f"{cfg}: N={n:.0e} {geom}, height {depth + 1} (levels 2-{depth}), l={order}, "
+            f"{'Helmholtz k=8pi complex128' if cfg in HELMHOLTZ else 'Laplace'}, variant {variant or v0}, eps={eps:g}")
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -279,9 +286,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(x[2] for x in vals),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c128" if cfg in HELMHOLTZ else "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg}: {CONFIGS[cfg]}", "sample": f"first {n_t} targets of level {lvl}"},
+        "config": {"workload": workload_name(cfg, args.variant), "sample": f"first {n_t} targets of level {lvl}"},
         "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "sample": f"{pairs} pairs: first {n_t} level-{lvl} targets (full far lists), faithful "
                                    f"port of m2l.py _apply_blocked (oracle/oracle.py), {threads} processes x 1 "
@@ -609,9 +616,7 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg}: N={n:.0e} {geom}, height {depth + 1} (levels {levels[0]}-{deep}), "
-                                   f"l={order}, {'Helmholtz k=8pi complex128' if cplx else 'Laplace'}, variant {variant}"
-                                   f", eps={eps:g}", "pairs_per_step": pairs_total, "precompute_s": t_pre,
+            "config": {"workload": workload_name(cfg, variant), "pairs_per_step": pairs_total, "precompute_s": t_pre,
                        "tree_build_ms": tree_ms,
                        "levels": {str(l): stats[l]["pairs"] for l in levels},
                        "tile_fill": pairs_local / max(slots, 1),
