@@ -222,6 +222,9 @@ struct cfm_handler {
   std::vector<int64_t> xpad_sig;   // layout the padding columns were zeroed for
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
+  cudaEvent_t ev_last = nullptr;  // end of the previous apply's work
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
@@ -1686,9 +1689,19 @@ static int guarded(F&& fn) {
 
 // NULL means the CUDA default (legacy) stream, as everywhere in CUDA: work
 // stays ordered with the caller's default-stream kernels (e.g. torch's).
+// The handler's scratch (padded sources, stages, pair rows) is reused by every
+// apply, so an apply on a different stream than the previous one first waits
+// for that one's work (calls on one stream are ordered anyway).
 static cudaStream_t pick_stream(cfm_handler* h, void* s) {
-  (void)h;
-  return static_cast<cudaStream_t>(s);
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  if (h->have_last && h->last_stream != st) CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_last, 0));
+  return st;
+}
+static void mark_stream(cfm_handler* h, cudaStream_t st) {
+  if (!h->ev_last) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_last, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventRecord(h->ev_last, st));
+  h->last_stream = st;
+  h->have_last = true;
 }
 
 // ------------------------------------------------------------------ octree
@@ -1809,6 +1822,7 @@ int cfm_handler_destroy(cfm_handler* h) {
     if (h->ev_out) cudaEventDestroy(h->ev_out);
     if (h->ev_prev) cudaEventDestroy(h->ev_prev);
     if (h->ev_x) cudaEventDestroy(h->ev_x);
+    if (h->ev_last) cudaEventDestroy(h->ev_last);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     cudaStreamDestroy(h->stream);
@@ -1980,7 +1994,11 @@ int cfm_apply_planned(cfm_handler* h, int level, const double* mpoles, int64_t n
     auto it = h->plans.find(level);
     if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(level));
     if (it->second.n_rows != n_rows) throw Error(CFM_ERR_VALUE, "row count differs from the planned level");
-    apply_with_buffers(h, level, it->second, mpoles, locals, pick_stream(h, stream));
+    {
+      cudaStream_t st = pick_stream(h, stream);
+      apply_with_buffers(h, level, it->second, mpoles, locals, st);
+      mark_stream(h, st);
+    }
   });
 }
 
@@ -1996,7 +2014,11 @@ int cfm_apply_level_csr(cfm_handler* h, int level, int64_t n_targets, const int6
     auto codes = codes_from_t(P, t);
     LevelPlan& lp = make_plan(h, level, n_targets, tgt, off, src, codes.data(), data_complex, n_rows);
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
-    apply_with_buffers(h, level, lp, mpoles, locals, pick_stream(h, stream));
+    {
+      cudaStream_t st = pick_stream(h, stream);
+      apply_with_buffers(h, level, lp, mpoles, locals, st);
+      mark_stream(h, st);
+    }
   });
 }
 
@@ -2032,7 +2054,11 @@ int cfm_apply_levels(cfm_handler* h, int n_levels, const int* levels, const doub
       throw Error(CFM_ERR_VALUE, "bad level arrays");
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_CHECK(cudaSetDevice(h->device));
-    apply_levels_impl(h, n_levels, levels, mpoles, n_rows, locals, pick_stream(h, stream));
+    {
+      cudaStream_t st = pick_stream(h, stream);
+      apply_levels_impl(h, n_levels, levels, mpoles, n_rows, locals, st);
+      mark_stream(h, st);
+    }
   });
 }
 

@@ -698,3 +698,34 @@ def test_interior_boundary_split_equals_single_gpu(torch_cuda, golden, case, mod
         hb.apply_planned(lvl, local, loc)
         out[rows] = loc[rows]
     assert torch.equal(out, ref)
+
+
+def test_applies_on_different_streams(torch_cuda):
+    """Back-to-back applies from two CUDA streams share the handler's scratch
+    (padded sources, pair rows): the second waits for the first."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    lvl, order = 4, 5
+    side = 1 << lvl
+    cells = np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3).astype(np.int32)
+    h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    h.precompute({lvl: full_far_field_vectors()}, {lvl: 1.0 / side})
+    h.plan_level_cells(lvl, cells)
+    rng = np.random.default_rng(9)
+    mps = [torch.from_numpy(rng.uniform(-1, 1, (len(cells), order**3))).cuda() for _ in range(4)]
+    ref = []
+    for m in mps:
+        y = torch.zeros_like(m)
+        h.apply_levels({lvl: (m, y)})
+        ref.append(y)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.zeros_like(m) for m in mps]
+    torch.cuda.synchronize()
+    for i, m in enumerate(mps):
+        with torch.cuda.stream(streams[i % 2]):
+            h.apply_levels({lvl: (m, outs[i])})
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
