@@ -200,6 +200,24 @@ struct LevelPlan {
   DevBuf s_tile_col, s_tile_off, s_entry_code, s_entry_src;
   DevBuf t_tile_col, t_tile_off, t_entry_code, t_entry_src;
   int64_t n_rows = 0;
+  uint64_t gen = 0;  // unique per built plan (merged plans remember what they were built from)
+};
+
+// Pair-mode levels of one homogeneous full-operator group merged into one
+// plan: pairs with the same transfer vector from different levels share 64-
+// column entries (their operators differ only by the level scale, which the
+// per-level reductions apply), so small sparse levels stop streaming a whole
+// operator per nearly empty entry.  Per pair the product is computed exactly
+// as in the level's own plan and every target sums its pairs in the same
+// order, so results are bitwise those of the per-level plans.
+struct MergedPairPlan {
+  std::vector<int> levels;
+  std::vector<uint64_t> gens;
+  std::vector<int64_t> row_off;  // source row offset of each level in the padded buffer
+  HostPlan hp;
+  DevBuf tile_col, tile_off, entry_code, entry_src, entry_ncols;
+  std::vector<PairReduce> red;  // per level: frows into the merged per-pair rows
+  std::vector<DevBuf> r_tgt, r_off, r_frow;
 };
 
 }  // namespace cfm
@@ -219,6 +237,7 @@ struct cfm_handler {
   std::map<int, LevelPlan> plans;
   DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters, pipe_flags;
   DevBuf xpad;                     // zero-padded source rows of full-operator levels
+  std::unique_ptr<MergedPairPlan> merged;
   std::vector<int64_t> xpad_sig;   // layout the padding columns were zeroed for
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
@@ -934,6 +953,8 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     upload(lp.p_lo, lo);
     upload(lp.p_hi, hi);
   }
+  static uint64_t plan_gen = 0;
+  lp.gen = ++plan_gen;
   h->plans[level] = std::move(lp);
   return h->plans[level];
 }
@@ -1244,6 +1265,105 @@ static void apply_with_buffers(cfm_handler* h, int level, LevelPlan& lp, const d
   h->last_ms = ms;
 }
 
+static bool use_merged_pairs() {
+  static int v = [] {
+    const char* e = getenv("CFM_MERGE_PAIRS");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+// Build (or reuse) the merged pair plan of the given pair-mode levels.
+static MergedPairPlan& merged_pair_plan(cfm_handler* h, const Group& g, const std::vector<int>& levels,
+                                        const std::vector<LevelPlan*>& plans, const std::vector<int64_t>& row_off) {
+  std::vector<uint64_t> gens;
+  for (auto* P : plans) gens.push_back(P->gen);
+  if (h->merged && h->merged->levels == levels && h->merged->gens == gens && h->merged->row_off == row_off)
+    return *h->merged;
+  auto m = std::make_unique<MergedPairPlan>();
+  m->levels = levels;
+  m->gens = gens;
+  m->row_off = row_off;
+  struct Pr {
+    int key, code, lvl;
+    int src;
+    int64_t old_frow;
+  };
+  std::vector<Pr> pairs;
+  std::vector<std::vector<int64_t>> tgt_of(plans.size());
+  for (size_t i = 0; i < plans.size(); ++i) {
+    const LevelPlan& P = *plans[i];
+    const int64_t E = P.hp.n_entries();
+    for (int64_t e = 0; e < E; ++e) {
+      const int c = P.hp.entry_code[e];
+      const int key = std::max(g.main.op[c], 0) + 1;  // the per-level plans' order (build_plan_pairs)
+      for (int j = 0; j < kBN; ++j) {
+        const int v = P.hp.entry_src[size_t(e) * kBN + j];
+        if (v >= 0) pairs.push_back({key, c, int(i), int(v + row_off[i]), e * kBN + j});
+      }
+    }
+  }
+  std::stable_sort(pairs.begin(), pairs.end(), [](const Pr& a, const Pr& b) {
+    if (a.key != b.key) return a.key < b.key;
+    return a.code < b.code;
+  });
+  std::vector<std::vector<int>> new_frow(plans.size());
+  for (size_t i = 0; i < plans.size(); ++i) new_frow[i].assign(size_t(plans[i]->hp.n_entries()) * kBN, -1);
+  HostPlan& hp = m->hp;
+  hp.dc = 1;
+  for (size_t a = 0; a < pairs.size();) {
+    size_t b = a;
+    while (b < pairs.size() && pairs[b].code == pairs[a].code && pairs[b].key == pairs[a].key) ++b;
+    for (size_t q = a; q < b; q += kBN) {
+      const int64_t e = hp.n_entries();
+      hp.entry_code.push_back(pairs[a].code);
+      hp.entry_src.resize(size_t(e + 1) * kBN, -1);
+      for (size_t r = q; r < std::min(b, q + kBN); ++r) {
+        const int sl = int(r - q);
+        hp.entry_src[size_t(e) * kBN + sl] = pairs[r].src;
+        new_frow[pairs[r].lvl][pairs[r].old_frow] = int(e * kBN + sl);
+      }
+    }
+    a = b;
+  }
+  hp.n_pairs = int64_t(pairs.size());
+  const int64_t E = hp.n_entries();
+  const int nkp = round_up(h->n * h->f, kKC);
+  int ept = std::max(1, std::min(16, int(2.5e7 / (2.0 * 128 * kBN * nkp))));
+  ept = std::min<int64_t>(ept, std::max<int64_t>(1, E / (2 * 148)));
+  hp.n_tiles = (E + ept - 1) / ept;
+  hp.tile_off.resize(hp.n_tiles + 1);
+  for (int64_t t = 0; t <= hp.n_tiles; ++t) hp.tile_off[t] = int(std::min<int64_t>(t * ept, E));
+  hp.tile_col.assign(size_t(hp.n_tiles) * kBN, -1);
+  push_plan(hp, m->tile_col, m->tile_off, m->entry_code, m->entry_src);
+  std::vector<unsigned char> nc(std::max<int64_t>(E, 1), 0);
+  for (int64_t e = 0; e < E; ++e)
+    for (int c = kBN - 1; c >= 0; --c)
+      if (hp.entry_src[size_t(e) * kBN + c] >= 0) {
+        nc[e] = static_cast<unsigned char>(c + 1);
+        break;
+      }
+  upload(m->entry_ncols, nc);
+  m->red.resize(plans.size());
+  m->r_tgt.resize(plans.size());
+  m->r_off.resize(plans.size());
+  m->r_frow.resize(plans.size());
+  for (size_t i = 0; i < plans.size(); ++i) {
+    const PairReduce& r0 = plans[i]->red;
+    PairReduce& r = m->red[i];
+    r.tgt = r0.tgt;
+    r.off = r0.off;
+    r.frow.resize(r0.frow.size());
+    for (size_t q = 0; q < r0.frow.size(); ++q) r.frow[q] = new_frow[i][r0.frow[q]];
+    r.n_frows = E * kBN;
+    upload(m->r_tgt[i], r.tgt);
+    upload(m->r_off[i], r.off);
+    upload(m->r_frow[i], r.frow);
+  }
+  h->merged = std::move(m);
+  return *h->merged;
+}
+
 // All planned levels of one step in as few launches as possible: dense groups
 // go into a single multi-segment launch (levels are independent in M2L, so
 // the long per-tile chains of the small levels overlap the big level).
@@ -1422,10 +1542,35 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   if (all_dense) {
     // one launch: target-mode levels accumulate into locals, pair-mode levels
     // write per-pair rows into their slice of fbuf, reduced right after
+    // full-operator pair-mode levels of one group share one merged plan
+    std::vector<size_t> mlv;
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (ftl[i] == 1 && lv[i].lp->mode == 1) mlv.push_back(i);
+    MergedPairPlan* mp_plan = nullptr;
+    if (use_merged_pairs() && mlv.size() >= 2) {
+      const Group* g0 = &group_for_level(h, lv[mlv[0]].level);
+      bool one_group = true;
+      for (size_t i : mlv) one_group = one_group && &group_for_level(h, lv[i].level) == g0;
+      if (one_group) {
+        std::vector<int> ml;
+        std::vector<LevelPlan*> mp_;
+        std::vector<int64_t> roff;
+        for (size_t i : mlv) {
+          ml.push_back(lv[i].level);
+          mp_.push_back(lv[i].lp);
+          roff.push_back(int64_t(xoff[lay_idx[i]] / size_t(lay[lay_idx[i]].second)));
+        }
+        mp_plan = &merged_pair_plan(h, *g0, ml, mp_, roff);
+      }
+    }
+    std::vector<char> merged_lv(lv.size(), 0);
+    if (mp_plan)
+      for (size_t i : mlv) merged_lv[i] = 1;
     size_t f_total = 0;
     std::vector<size_t> f_off(lv.size(), 0);
+    if (mp_plan) f_total = size_t(mp_plan->hp.n_entries()) * kBN * size_t(h->n);
     for (size_t i = 0; i < lv.size(); ++i) {
-      if (lv[i].lp->mode != 1) continue;
+      if (lv[i].lp->mode != 1 || merged_lv[i]) continue;
       const size_t row_d = size_t(h->n) * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
       f_off[i] = f_total;
       f_total += size_t(lv[i].lp->red.n_frows) * row_d;
@@ -1488,7 +1633,24 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       if (nr >= 0 && (p.nr != nr)) same_shape = false;
       nr = p.nr;
       segs.push_back(p);
-      counts.push_back(L.lp->hp.n_tiles);
+      counts.push_back(merged_lv[i] ? 0 : L.lp->hp.n_tiles);  // merged levels run in the merged segment
+    }
+    const size_t merged_seg = segs.size();
+    if (mp_plan) {
+      const size_t i0 = mlv[0];
+      Group& g = group_for_level(h, lv[i0].level);
+      TileParams p{};
+      p.zero_row = h->zeros.as<double>();
+      fill_plan(p, mp_plan->tile_col, mp_plan->tile_off, mp_plan->entry_code, mp_plan->entry_src,
+                mp_plan->hp.n_tiles);
+      fill_full(p, h, g, h->xpad.as<double>());  // global padded source rows
+      p.entry_ncols = mp_plan->entry_ncols.as<unsigned char>();
+      p.n_entries = mp_plan->hp.n_entries();
+      p.y = h->fbuf.as<double>(); p.y_ld = h->n; p.y_dc = 1;
+      p.scale = 1.0; p.accumulate = 0; p.pair_out = 1;
+      if (p.nr != nr) same_shape = false;
+      segs.push_back(p);
+      counts.push_back(mp_plan->hp.n_tiles);
     }
     // small pair-mode segments reduce inside the launch (their last CTA)
     std::vector<bool> reduced_inside(lv.size(), false);
@@ -1499,7 +1661,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         const LevelPlan& P = *lv[i].lp;
         const long long row_ld = (long long)h->n * (P.dc == 2 || h->op_complex ? 2 : 1);
         const double work = double(P.red.frow.size()) * double(row_ld);
-        if (P.mode == 1 && work <= 2.0e6 && !P.red.tgt.empty()) {
+        if (P.mode == 1 && !merged_lv[i] && work <= 2.0e6 && !P.red.tgt.empty()) {
           TileParams& q = segs[i];
           q.red_counter = h->counters.as<unsigned>() + i;
           q.red_ctas = int(counts[i]) * ((q.nr + 127) / 128);
@@ -1519,7 +1681,9 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     // full-operator levels -- the other levels first while the late levels'
     // sources cross PCIe, then the late ones once padded on this stream
     std::vector<std::vector<size_t>> groups(2);
-    for (size_t i = 0; i < lv.size(); ++i) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
+    if (mp_plan) groups[0].push_back(merged_seg);
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (counts[i]) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       const auto& grp = groups[gi];
       if (grp.empty()) continue;
@@ -1543,6 +1707,19 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     for (size_t i = 0; i < lv.size(); ++i) {
       if (lv[i].lp->mode != 1 || reduced_inside[i]) continue;
       const long long row_ld = (long long)h->n * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
+      if (merged_lv[i]) {
+        const size_t k = size_t(std::find(mlv.begin(), mlv.end(), i) - mlv.begin());
+        const int64_t nt = int64_t(mp_plan->red[k].tgt.size());
+        if (nt) {
+          k_pair_reduce<<<unsigned(nt), 128, 0, s>>>(h->fbuf.as<double>(), row_ld, mp_plan->r_tgt[k].as<long long>(),
+                                                      mp_plan->r_off[k].as<long long>(), mp_plan->r_frow[k].as<int>(),
+                                                      nt, lv[i].y, row_ld, int(row_ld), h->levels[lv[i].level].second,
+                                                      1);
+          CUDA_CHECK(cudaGetLastError());
+          ++launches;
+        }
+        continue;
+      }
       launches += launch_reduce(*lv[i].lp, h->fbuf.as<double>() + f_off[i], row_ld, lv[i].y, row_ld, int(row_ld),
                                 h->levels[lv[i].level].second, s);
     }

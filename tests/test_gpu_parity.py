@@ -729,3 +729,46 @@ def test_applies_on_different_streams(torch_cuda):
     torch.cuda.synchronize()
     for a, b in zip(outs, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("order", [5, 7])
+def test_merged_pair_levels_bitwise(torch_cuda, order, monkeypatch):
+    """Sparse (sphere) levels in pair mode on the full-operator path: the
+    merged multi-level pair plan of apply_levels gives bitwise the per-level
+    results (same per-pair products, same per-target summation order), and
+    matches the oracle."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_PLAN_MODE", "pair")
+    rng = np.random.default_rng(21)
+    pts = rng.normal(size=(20000, 3))
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+    depth = 5
+    side = 1 << depth
+    leaf = np.unique(np.minimum(((pts + 1.0) / 2.0 * side).astype(np.int64), side - 1), axis=0)
+    cells = {depth: leaf}
+    for lvl in range(depth - 1, 1, -1):
+        cells[lvl] = np.unique(cells[lvl + 1] >> 1, axis=0)
+    levels = sorted(cells)
+    h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    h.precompute({l: full_far_field_vectors() for l in levels}, {l: 2.0 / (1 << l) for l in levels})
+    arrays, ref = {}, {}
+    for lvl in levels:
+        st = h.plan_level_cells(lvl, cells[lvl].astype(np.int32))
+        assert st["mode"] == "pair"
+        mp = torch.from_numpy(rng.uniform(-1, 1, (len(cells[lvl]), order**3))).cuda()
+        ref[lvl] = torch.zeros_like(mp)
+        h.apply_planned(lvl, mp, ref[lvl])
+        arrays[lvl] = (mp, torch.zeros_like(mp))
+    h.apply_levels(arrays)
+    h.apply_levels(arrays)  # the cached merged plan is reused
+    for lvl in levels:
+        assert torch.equal(arrays[lvl][1], 2 * ref[lvl])
+    lvl = levels[1]
+    tgt, off, src, t = O.far_lists(cells[lvl], lvl)
+    orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+        {lvl: O.full_far_field()}, {lvl: 2.0 / (1 << lvl)})
+    want = np.zeros((len(cells[lvl]), order**3))
+    orc.apply_fast(lvl, tgt, off, src, t, arrays[lvl][0].cpu().numpy(), want)
+    assert O.rel_l2(ref[lvl].cpu().numpy(), want) <= 1e-12
