@@ -1329,8 +1329,11 @@ static MergedPairPlan& merged_pair_plan(cfm_handler* h, const Group& g, const st
   hp.n_pairs = int64_t(pairs.size());
   const int64_t E = hp.n_entries();
   const int nkp = round_up(h->n * h->f, kKC);
-  int ept = std::max(1, std::min(16, int(2.5e7 / (2.0 * 128 * kBN * nkp))));
+  // ~50 MFLOP of row-block work per CTA (measured at l = 9: 2 -> 4 entries per
+  // CTA -1.7%), >= 2 CTAs per SM
+  int ept = std::max(1, std::min(16, int(5.0e7 / (2.0 * 128 * kBN * nkp))));
   ept = std::min<int64_t>(ept, std::max<int64_t>(1, E / (2 * 148)));
+  if (const char* e = getenv("CFM_PAIR_EPT")) ept = std::max(1, atoi(e));
   hp.n_tiles = (E + ept - 1) / ept;
   hp.tile_off.resize(hp.n_tiles + 1);
   for (int64_t t = 0; t <= hp.n_tiles; ++t) hp.tile_off[t] = int(std::min<int64_t>(t * ept, E));
