@@ -1664,7 +1664,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         const LevelPlan& P = *lv[i].lp;
         const long long row_ld = (long long)h->n * (P.dc == 2 || h->op_complex ? 2 : 1);
         const double work = double(P.red.frow.size()) * double(row_ld);
-        if (P.mode == 1 && !merged_lv[i] && work <= 2.0e6 && !P.red.tgt.empty()) {
+        // opt-in (CFM_REDUCE_INSIDE_MAX = elements): a single CTA reducing a
+        // level serially measured slower than the separate parallel launch
+        // (config 1: 0.92 vs 0.76 ms per step)
+        static const double inside_max = [] {
+          const char* e = getenv("CFM_REDUCE_INSIDE_MAX");
+          return e ? atof(e) : 0.0;
+        }();
+        if (P.mode == 1 && !merged_lv[i] && work <= inside_max && !P.red.tgt.empty()) {
           TileParams& q = segs[i];
           q.red_counter = h->counters.as<unsigned>() + i;
           q.red_ctas = int(counts[i]) * ((q.nr + 127) / 128);
