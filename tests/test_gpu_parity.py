@@ -772,3 +772,46 @@ def test_merged_pair_levels_bitwise(torch_cuda, order, monkeypatch):
     want = np.zeros((len(cells[lvl]), order**3))
     orc.apply_fast(lvl, tgt, off, src, t, arrays[lvl][0].cpu().numpy(), want)
     assert O.rel_l2(ref[lvl].cpu().numpy(), want) <= 1e-12
+
+
+def test_full_operator_edge_cases(torch_cuda, monkeypatch):
+    """Full-operator path edge cases: a level with no far pairs, a one-cell
+    level, odd row counts, merged pair plan with an empty level, repeated and
+    interleaved apply_levels / apply_planned calls."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    order = 5
+    cells = {2: np.array([[1, 1, 1]]),                      # one cell: no far pairs
+             3: np.array([[0, 0, 0], [7, 7, 7], [0, 7, 3]]),  # three scattered cells
+             4: np.array([[0, 0, 0], [15, 15, 15], [3, 9, 12], [8, 1, 5], [14, 0, 7]])}
+    levels = sorted(cells)
+    h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    h.precompute({l: full_far_field_vectors() for l in levels}, {l: 1.0 / (1 << l) for l in levels})
+    rng = np.random.default_rng(2)
+    arrays, ref = {}, {}
+    for lvl in levels:
+        st = h.plan_level_cells(lvl, cells[lvl].astype(np.int32))
+        mp = torch.from_numpy(rng.uniform(-1, 1, (len(cells[lvl]), order**3))).cuda()
+        ref[lvl] = torch.zeros_like(mp)
+        h.apply_planned(lvl, mp, ref[lvl])
+        arrays[lvl] = (mp, torch.zeros_like(mp))
+        tgt, off, src, t = O.far_lists(cells[lvl], lvl)
+        assert st["pairs"] == len(src)
+        if len(src):
+            orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+                {lvl: O.full_far_field()}, {lvl: 1.0 / (1 << lvl)})
+            want = np.zeros((len(cells[lvl]), order**3))
+            orc.apply_fast(lvl, tgt, off, src, t, mp.cpu().numpy(), want)
+            assert O.rel_l2(ref[lvl].cpu().numpy(), want) <= 1e-12
+        else:
+            assert not torch.any(ref[lvl])
+    for _ in range(2):
+        h.apply_levels(arrays)
+    for lvl in levels:
+        assert torch.equal(arrays[lvl][1], 2 * ref[lvl])
+    # host buffers through the same path
+    host = {lvl: (arrays[lvl][0].cpu().numpy(), np.zeros((len(cells[lvl]), order**3))) for lvl in levels}
+    h.apply_levels(host)
+    for lvl in levels:
+        assert np.array_equal(host[lvl][1], ref[lvl].cpu().numpy())
