@@ -436,9 +436,8 @@ static bool use_full_ops(const cfm_handler* h) {
   return v != 0 && !h->op_complex && nf > 64 && nf <= 1024 && resolve_encode_tiled() != nullptr;
 }
 
-template <int RP, int STAGES, bool VB>
+template <int RP, int STAGES, bool VB, int KC = 16>
 static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, cudaStream_t s) {
-  constexpr int KC = 16;
   const int fixed = lr_smem_bytes<RP, KC, STAGES>() + 4 * 64 + 3 * 4 * 344 + 4 * kMaxTileEntries;
   if (lp_.n_ops > 344 || fixed > 227 * 1024) return false;
   const int tabs = 48 * 2 * (lp_.nr + lp_.nk + 8);
@@ -461,7 +460,15 @@ static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, 
 static bool launch_lowrank_fused(const LowRankParams& lp_, int rmax, int64_t first, int64_t count, cudaStream_t s,
                                  bool vb = false) {
   if (!use_fused_lowrank()) return false;
+  static const int kc_env = [] {
+    const char* e = getenv("CFM_LR_KC");
+    return e ? atoi(e) : 16;
+  }();
   if (vb) {
+    if (kc_env == 32) {
+      if (rmax <= 16) return launch_lowrank_cfg<16, 3, true, 32>(lp_, first, count, s);
+      if (rmax <= 32) return launch_lowrank_cfg<32, 2, true, 32>(lp_, first, count, s);
+    }
     if (rmax <= 16) return launch_lowrank_cfg<16, 5, true>(lp_, first, count, s);
     if (rmax <= 32) return launch_lowrank_cfg<32, 4, true>(lp_, first, count, s);
     if (rmax <= 64) return launch_lowrank_cfg<64, 2, true>(lp_, first, count, s);
