@@ -237,6 +237,7 @@ struct cfm_handler {
   std::map<int, LevelPlan> plans;
   DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters, pipe_flags;
   DevBuf xpad;                     // zero-padded source rows of full-operator levels
+  long long wt_ld_zeroed = -1;     // SA: leading dimension the W~ padding was zeroed for
   std::unique_ptr<MergedPairPlan> merged;
   std::vector<int64_t> xpad_sig;   // layout the padding columns were zeroed for
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
@@ -1175,9 +1176,20 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
   // ---- shared basis (sa / sarcmp), m2l.py:366-395
   const int rbf = g.sa_bh.rows;  // r_b * f (realified) rows of B^H
   const int ruf = g.sa_u.cols;   // r_u * f
-  const long long wt_ld = (long long)rbf * (dc == 2 ? 2 : 1);
+  // full-operator stage 2 reads W~ rows with bulk copies: rows padded to the
+  // cores' leading dimension, padding zeroed when the buffer is (re)allocated
+  const bool sa_full = g.has_full && g.any_dense_core && dc == 1;
+  const long long wt_ld = sa_full ? (long long)g.dense.ld : (long long)rbf * (dc == 2 ? 2 : 1);
   const long long z_ld = (long long)ruf * (dc == 2 ? 2 : 1);
-  ensure(h->wt, size_t(lp.n_rows) * wt_ld * sizeof(double));
+  {
+    const size_t need = std::max<size_t>(size_t(lp.n_rows) * wt_ld * sizeof(double), 16);
+    const bool grow = !h->wt.p || need > h->wt.bytes;
+    ensure(h->wt, need);
+    if (sa_full && (grow || h->wt_ld_zeroed != wt_ld)) {
+      CUDA_CHECK(cudaMemsetAsync(h->wt.p, 0, h->wt.bytes, s));
+      h->wt_ld_zeroed = wt_ld;
+    }
+  }
   ensure(h->z, size_t(lp.n_rows) * z_ld * sizeof(double));
   CUDA_CHECK(cudaMemsetAsync(h->z.p, 0, size_t(lp.n_rows) * z_ld * sizeof(double), s));
   // stage 1: W~[src] = B^H M[src]
@@ -1208,6 +1220,15 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     q.x = h->wt.as<double>(); q.x_ld = wt_ld; q.x_dc = dc;
     q.y = z_out; q.y_ld = z_ld; q.y_dc = dc;
     q.scale = 1.0; q.accumulate = z_acc; q.pair_out = z_pair;
+    if (sa_full) {
+      q.ft = 1;
+      q.ft_rows = g.full_rows;
+      q.tmap_a = g.full_tmap;
+      q.rowtab = nullptr;
+      q.invtab = nullptr;
+      q.n_entries = lp.hp.n_entries();
+      if (lp.mode == 1) q.entry_ncols = lp.entry_ncols.as<unsigned char>();
+    }
     launches += launch_tiles(q, lp.hp.n_tiles, s);
   }
   // stage 2b: factored cores Z[tgt] += L_t (R_t^H W~[src])
@@ -2135,6 +2156,25 @@ int cfm_set_shared_group(cfm_handler* h, int key, int r_u, int r_b, const double
         std::fill(tmp.begin(), tmp.end(), 0.0);
         realify_into(core_data + off[dense_idx[k]], r_u, r_b, cplx, tmp.data(), g.dense.ld);
         put_stack(g.dense, int(k), tmp);
+      }
+      // the cores are already one (unpermuted) operator per transfer vector:
+      // the full-operator TMA kernel reads them directly (stage 2 of sa / sarcmp)
+      static const int full_env = [] {
+        const char* e = getenv("CFM_FULL_OPS");
+        return e ? atoi(e) : 1;
+      }();
+      if (full_env && !cplx && r_u > 64 && r_b <= 1024 && resolve_encode_tiled()) {
+        const cuuint64_t dims[2] = {cuuint64_t(g.dense.ld), cuuint64_t(g.dense.n_ops) * g.dense.rows};
+        const cuuint64_t strides[1] = {cuuint64_t(g.dense.ld) * sizeof(double)};
+        const cuuint32_t box[2] = {cuuint32_t(kKC + 4), 128u};
+        const cuuint32_t estr[2] = {1u, 1u};
+        const CUresult r = resolve_encode_tiled()(&g.full_tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, g.dense.d.p, dims,
+                                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for the SA cores");
+        g.has_full = true;
+        g.full_rows = g.dense.rows;
       }
     }
     if (g.any_fac_core) {
