@@ -224,6 +224,15 @@ struct MergedPairPlan {
 
 using namespace cfm;
 
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t done = nullptr;
+};
+struct LevelScratch {  // per-level scratch of concurrently applied levels
+  DevBuf fbuf, xpad, ybuf;
+  std::vector<int64_t> xpad_sig;
+};
+
 struct cfm_handler {
   int device = 0, variant = 0, order = 0, op_complex = 0;
   int n = 0, f = 1;
@@ -243,6 +252,9 @@ struct cfm_handler {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
   cudaEvent_t ev_last = nullptr;  // end of the previous apply's work
+  cudaEvent_t ev_fork = nullptr;
+  std::vector<AuxStream> aux;
+  std::vector<LevelScratch> lvl_scratch;
   cudaStream_t last_stream = nullptr;
   bool have_last = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -398,6 +410,14 @@ static bool use_copy_pipeline() {
     return e ? atoi(e) : 1;
   }();
   return v != 0 && resolve_stream_mem_ops();
+}
+
+static bool use_concurrent_levels() {
+  static int v = [] {
+    const char* e = getenv("CFM_CONCURRENT_LEVELS");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
 }
 
 static bool use_fused_lowrank() {
@@ -1762,7 +1782,50 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
                                 h->levels[lv[i].level].second, s);
     }
   } else {
-    for (auto& L : lv) launches += run_plan(h, L.level, *L.lp, L.x, L.y, s);
+    bool all_lr = lv.size() > 1 && use_concurrent_levels();
+    for (auto& L : lv) all_lr = all_lr && group_for_level(h, L.level).kind == kLowRank;
+    if (!all_lr) {
+      for (auto& L : lv) launches += run_plan(h, L.level, *L.lp, L.x, L.y, s);
+    } else {
+      // low-rank levels are independent and each is a separate launch chain:
+      // run them side by side on forked streams, each with its own scratch
+      // (per-pair rows, padded sources), so small latency-bound levels overlap
+      const size_t nl = lv.size();
+      if (h->aux.size() < nl) {
+        h->aux.resize(nl);
+        h->lvl_scratch.resize(nl);
+      }
+      if (!h->ev_fork) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+      for (size_t k = 0; k < nl; ++k) {
+        AuxStream& a = h->aux[k];
+        if (!a.s) {
+          CUDA_CHECK(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+          CUDA_CHECK(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
+        }
+        CUDA_CHECK(cudaStreamWaitEvent(a.s, h->ev_fork, 0));
+        LevelScratch& sc = h->lvl_scratch[k];
+        std::swap(h->fbuf, sc.fbuf);
+        std::swap(h->xpad, sc.xpad);
+        std::swap(h->xpad_sig, sc.xpad_sig);
+        std::swap(h->ybuf, sc.ybuf);
+        try {
+          launches += run_plan(h, lv[k].level, *lv[k].lp, lv[k].x, lv[k].y, a.s);
+        } catch (...) {
+          std::swap(h->fbuf, sc.fbuf);
+          std::swap(h->xpad, sc.xpad);
+          std::swap(h->xpad_sig, sc.xpad_sig);
+          std::swap(h->ybuf, sc.ybuf);
+          throw;
+        }
+        std::swap(h->fbuf, sc.fbuf);
+        std::swap(h->xpad, sc.xpad);
+        std::swap(h->xpad_sig, sc.xpad_sig);
+        std::swap(h->ybuf, sc.ybuf);
+        CUDA_CHECK(cudaEventRecord(a.done, a.s));
+        CUDA_CHECK(cudaStreamWaitEvent(s, a.done, 0));
+      }
+    }
   }
   CUDA_CHECK(cudaEventRecord(h->ev1, s));
   if (any_piped) {
@@ -2038,6 +2101,11 @@ int cfm_handler_destroy(cfm_handler* h) {
     if (h->ev_prev) cudaEventDestroy(h->ev_prev);
     if (h->ev_x) cudaEventDestroy(h->ev_x);
     if (h->ev_last) cudaEventDestroy(h->ev_last);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    for (auto& a : h->aux) {
+      if (a.done) cudaEventDestroy(a.done);
+      if (a.s) cudaStreamDestroy(a.s);
+    }
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     cudaStreamDestroy(h->stream);
