@@ -294,6 +294,40 @@ static bool use_bulk_a(int kc) {
   return kc >= 32;  // 256-B row chunks: bulk copies win; 128-B: cp.async wins
 }
 
+// cuTensorMapEncodeTiled, resolved at run time like the stream memory ops.
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled resolve_encode_tiled() {
+  static PFN_encodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<PFN_encodeTiled>(nullptr);
+    }
+    return reinterpret_cast<PFN_encodeTiled>(f);
+  }();
+  return fn;
+}
+
+// Full-operator mode: the 2-D map over a segment's padded source rows
+// (x_ld doubles x x_rows rows) read by tile::gather4 copies, box (KC + 4) x 1
+// so each gathered row lands with the stage's LDB pitch; columns past x_ld and
+// rows < 0 (empty plan slots) are out of bounds and arrive as zeros.
+static void encode_source_map(TileParams& q, int kc) {
+  const cuuint64_t dims[2] = {cuuint64_t(q.x_ld), cuuint64_t(std::max<long long>(q.x_rows, 1))};
+  const cuuint64_t strides[1] = {cuuint64_t(q.x_ld) * sizeof(double)};
+  const cuuint32_t box[2] = {cuuint32_t(kc + 4), 1u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = resolve_encode_tiled()(&q.tmap_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(q.x),
+                                            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for the source rows");
+}
+
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
 static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaStream_t s) {
   // grid_tiles = (tiles, row blocks) -> one CTA per (tile, row block), row blocks fastest
@@ -321,6 +355,7 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
       bool skip = int(mp.nrb) * BM - q.nr >= 32 || 4 * pair_e >= all_e;
       if (skip_env >= 0) skip = skip_env != 0;
       const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
+      for (int i = 0; i < mp.n_seg; ++i) encode_source_map(mp.seg[i], KC);
       auto kf = skip ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
                      : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
       CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
@@ -428,23 +463,6 @@ static bool use_fused_lowrank() {
   return v != 0;
 }
 
-// cuTensorMapEncodeTiled, resolved at run time like the stream memory ops.
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static PFN_encodeTiled resolve_encode_tiled() {
-  static PFN_encodeTiled fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess) {
-      cudaGetLastError();
-      return static_cast<PFN_encodeTiled>(nullptr);
-    }
-    return reinterpret_cast<PFN_encodeTiled>(f);
-  }();
-  return fn;
-}
 
 // Full-operator TMA mode (CFM_FULL_OPS=0 disables): real dense groups with
 // 64 < n <= 1024 (l = 5..10); always the 128-row KC=32 kernel.
@@ -1034,7 +1052,7 @@ static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, in
                                cudaMemcpyDefault, s));
 }
 
-static void fill_full(TileParams& p, const cfm_handler* h, const Group& g, const double* xpad) {
+static void fill_full(TileParams& p, const cfm_handler* h, const Group& g, const double* xpad, int64_t x_rows) {
   fill_ops(p, g.full, g.fullmap);
   p.nr = h->n;
   p.nk = h->n;
@@ -1046,6 +1064,7 @@ static void fill_full(TileParams& p, const cfm_handler* h, const Group& g, const
   p.x = xpad;
   p.x_ld = g.full.ld;
   p.x_dc = 1;
+  p.x_rows = x_rows;
 }
 
 static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, double* d_y, cudaStream_t s) {
@@ -1071,7 +1090,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
       const auto off = xpad_layout(h, {{lp.n_rows, g.full.ld}}, s);
       double* xp = h->xpad.as<double>() + off[0];
       xpad_copy(h, xp, g.full.ld, d_x, 0, lp.n_rows, s);
-      fill_full(p, h, g, xp);
+      fill_full(p, h, g, xp, lp.n_rows);
       if (lp.mode == 1) p.entry_ncols = lp.entry_ncols.as<unsigned char>();
       p.n_entries = lp.hp.n_entries();
     }
@@ -1244,6 +1263,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
       q.ft = 1;
       q.ft_rows = g.full_rows;
       q.tmap_a = g.full_tmap;
+      q.x_rows = lp.n_rows;
       q.rowtab = nullptr;
       q.invtab = nullptr;
       q.n_entries = lp.hp.n_entries();
@@ -1658,7 +1678,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
       if (ftl[i]) {
-        fill_full(p, h, g, L.x);
+        fill_full(p, h, g, L.x, L.lp->n_rows);
         if (L.lp->mode == 1) p.entry_ncols = L.lp->entry_ncols.as<unsigned char>();
         p.n_entries = L.lp->hp.n_entries();
       }
@@ -1694,7 +1714,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       p.zero_row = h->zeros.as<double>();
       fill_plan(p, mp_plan->tile_col, mp_plan->tile_off, mp_plan->entry_code, mp_plan->entry_src,
                 mp_plan->hp.n_tiles);
-      fill_full(p, h, g, h->xpad.as<double>());  // global padded source rows
+      fill_full(p, h, g, h->xpad.as<double>(), int64_t(h->xpad.bytes / (sizeof(double) * g.full.ld)));  // global padded source rows
       p.entry_ncols = mp_plan->entry_ncols.as<unsigned char>();
       p.n_entries = mp_plan->hp.n_entries();
       p.y = h->fbuf.as<double>(); p.y_ld = h->n; p.y_dc = 1;

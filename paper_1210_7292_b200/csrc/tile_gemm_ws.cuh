@@ -51,6 +51,18 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, 
       : "memory");
 }
 
+// 2-D TMA tile::gather4: rows r.x..r.w of the map, columns [c0, c0 + box), landing
+// back to back in shared memory (4 x box doubles), bytes on an mbarrier.
+__device__ __forceinline__ void tma_gather4(void* smem, const CUtensorMap* map, int c0, int4 r, uint64_t* bar) {
+  unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(b)
+      : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
   unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   unsigned ok;
@@ -193,36 +205,34 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   if (FT && tid >= NC) {
     // ============ producer, full-operator mode: one warp, TMA only ============
     // per chunk: one 2-D tile copy of the operator block (BM rows x KC+4
-    // columns, landing with the LDA pitch) and one bulk copy per source column
+    // columns, landing with the LDA pitch) and BN/4 tile::gather4 copies of
+    // the source rows (4 rows x KC+4 columns each, landing with the LDB pitch;
+    // empty slots carry row -1, out of bounds, and arrive as zeros).  Lane 0
+    // issues everything; the entry's source rows are read once per entry.
     if (tid >= NC + 32) return;
     if (p.pipe_mp && e_begin < e_end) wait_flag_geq(p.pipe_mp, unsigned(p.pipe_need_mp[tile]));
-    constexpr int BPL = BN / 32;
-    constexpr unsigned STAGE_TX = unsigned((BM * LDA + BN * KC) * 8);
+    if (lane != 0) return;
+    static_assert(BN % 4 == 0 && LDA == LDB, "gather4 rows land with the A pitch");
+    constexpr unsigned STAGE_TX = unsigned((BM * LDA + BN * LDB) * 8);
     EntryInfo d;
     d.nchunks = 0;
     int e = next_live(e_begin, d);
     int q = 0;
     while (e < e_end) {
-      const double* bsrc[BPL];
+      int4 rows[BN / 4];
+      const int4* srow = reinterpret_cast<const int4*>(p.entry_src + (long long)e * BN);
 #pragma unroll
-      for (int u = 0; u < BPL; ++u) {
-        const int v = __ldg(p.entry_src + (long long)e * BN + lane + 32 * u);
-        bsrc[u] = v >= 0 ? p.x + (long long)v * p.x_ld : nullptr;
-      }
+      for (int j = 0; j < BN / 4; ++j) rows[j] = __ldg(srow + j);
       const int arow = d.op * p.ft_rows + r0;
       for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
         const int s = q % STAGES;
         if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
         const int k0 = kc * KC;
         double* bs = Bs + s * BN * LDB;
-        if (lane == 0) {
-          mbar_arrive_expect_tx(full + s, STAGE_TX);
-          tma_load_2d(As + s * BM * LDA, &p.tmap_a, k0, arow, full + s);
-        }
-        __syncwarp();
+        mbar_arrive_expect_tx(full + s, STAGE_TX);
+        tma_load_2d(As + s * BM * LDA, &p.tmap_a, k0, arow, full + s);
 #pragma unroll
-        for (int u = 0; u < BPL; ++u)
-          bulk_g2s(bs + (lane + 32 * u) * LDB, bsrc[u] ? bsrc[u] + k0 : p.zero_row, KC * 8, full + s);
+        for (int j = 0; j < BN / 4; ++j) tma_gather4(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s);
       }
       e = next_live(e + 1, d);
     }
