@@ -27,6 +27,7 @@
 #include <numeric>
 #include <string>
 #include <vector>
+#include <chrono>
 
 #include "../../include/chebm2l.h"
 #include "classify.cuh"
@@ -355,7 +356,17 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
       bool skip = int(mp.nrb) * BM - q.nr >= 32 || 4 * pair_e >= all_e;
       if (skip_env >= 0) skip = skip_env != 0;
       const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
-      for (int i = 0; i < mp.n_seg; ++i) encode_source_map(mp.seg[i], KC);
+      // the flat pipelined consumer loop runs whole KC-chunks: only when the last
+      // chunk of an operator has KC/4 k-steps anyway (l = 5: 125 = 3 x 32 + 29)
+      static const int pipe_env = [] {
+        const char* e = getenv("CFM_FT_PIPE");
+        return e ? atoi(e) : 1;
+      }();
+      for (int i = 0; i < mp.n_seg; ++i) {
+        encode_source_map(mp.seg[i], KC);
+        const int rem = mp.seg[i].nk % KC;
+        mp.seg[i].ft_pipe = pipe_env && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
+      }
       auto kf = skip ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
                      : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
       CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
@@ -1044,9 +1055,34 @@ static std::vector<size_t> xpad_layout(cfm_handler* h, const std::vector<std::pa
   return off;
 }
 
+// Zero-padded copy of rows: dst[r][k] = k < n ? src[r][k] : 0 for k < ld, whole
+// destination rows written (coalesced on both sides, memory-bound).  Replaces a
+// pitched device-to-device cudaMemcpy2D, measured at ~1.5 ms for config 2's
+// 262 MB level 6 (this kernel: ~0.1 ms).
+constexpr int kPadRowsPerBlock = 16;
+__global__ void __launch_bounds__(256) k_pad_rows(double* __restrict__ dst, int ld, const double* __restrict__ src,
+                                                  int n, long long rows) {
+  const long long r0 = (long long)blockIdx.x * kPadRowsPerBlock;
+  const int nr = int(rows - r0 < kPadRowsPerBlock ? rows - r0 : kPadRowsPerBlock);
+  const double* sb = src + r0 * n;
+  double* db = dst + r0 * ld;
+  for (int j = threadIdx.x; j < nr * ld; j += blockDim.x) {
+    const int r = j / ld, k = j - r * ld;
+    db[j] = k < n ? __ldcs(sb + (long long)r * n + k) : 0.0;
+  }
+}
+
 // rows [r0, r1) of a (rows x n) source array (host or device) into the padded layout
 static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s) {
   if (r1 <= r0) return;
+  if (is_device_ptr(src)) {
+    const long long rows = r1 - r0;
+    const long long blocks = (rows + kPadRowsPerBlock - 1) / kPadRowsPerBlock;
+    if (blocks >= (1ll << 31)) throw Error(CFM_ERR_VALUE, "too many rows to pad");
+    k_pad_rows<<<unsigned(blocks), 256, 0, s>>>(dst + size_t(r0) * ld, ld, src + size_t(r0) * h->n, h->n, rows);
+    CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   CUDA_CHECK(cudaMemcpy2DAsync(dst + size_t(r0) * ld, size_t(ld) * sizeof(double), src + size_t(r0) * h->n,
                                size_t(h->n) * sizeof(double), size_t(h->n) * sizeof(double), size_t(r1 - r0),
                                cudaMemcpyDefault, s));
@@ -1450,6 +1486,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   };
   std::vector<Lv> lv;
   size_t stage_bytes = 0;
+  // CFM_TRACE=1: host preparation time and device time before the first launch, to stderr
+  static const bool trace = getenv("CFM_TRACE") && atoi(getenv("CFM_TRACE"));
+  static cudaEvent_t ev_t = nullptr;
+  const auto t_host0 = std::chrono::steady_clock::now();
+  if (trace) {
+    if (!ev_t) CUDA_CHECK(cudaEventCreate(&ev_t));
+    CUDA_CHECK(cudaEventRecord(ev_t, s));
+  }
   for (int i = 0; i < n_levels; ++i) {
     auto it = h->plans.find(levels[i]);
     if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(levels[i]));
@@ -1607,6 +1651,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     }
   }
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
+  const auto t_host1 = std::chrono::steady_clock::now();
   int64_t launches = 0;
   bool all_dense = true;
   for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
@@ -1884,6 +1929,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   h->last_ms = ms;
   h->last_launches = launches;
+  if (trace) {
+    float pre = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&pre, ev_t, h->ev0));
+    const double prep = std::chrono::duration<double, std::milli>(t_host1 - t_host0).count();
+    const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    fprintf(stderr, "[cfm trace] host prep %.3f ms, device before launch %.3f ms, launches %.3f ms, call %.3f ms\n",
+            prep, pre, ms, tot);
+  }
 }
 
 // ------------------------------------------------------------------ classifier

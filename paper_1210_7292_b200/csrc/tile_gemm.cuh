@@ -92,6 +92,7 @@ struct TileParams {
   const unsigned char* entry_ncols;  // pair plans: filled columns per entry (null: all BN)
   long long n_entries;               // host-side hint: entries of the plan (kernel choice)
   long long x_rows;                  // full-operator mode: rows of the padded source array x
+  int ft_pipe;                       // full-operator target tiles: flat pipelined consumer loop
   CUtensorMap tmap_a;
   // full-operator mode: 2-D map over the padded sources (x_ld x x_rows), box
   // (KC + 4) x 1, read by tile::gather4 copies (4 source rows per instruction)

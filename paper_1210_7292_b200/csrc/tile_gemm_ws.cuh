@@ -408,6 +408,57 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       default: ft_entry(mlc, std::integral_constant<int, NTL>{}); break;
     }
   };
+  if constexpr (FTM == 1) {
+    if (!p.pair_out && p.ft_pipe) {
+      // Full-operator target tiles whose every chunk is KC/4 whole k-steps
+      // (host-checked): one flat chunk stream, software-pipelined across chunk
+      // and entry boundaries -- the next chunk's full barrier is waited for and
+      // its first fragments loaded before the current chunk's last k-step, so
+      // the two consumer warps of an SM sub-partition do not stall together
+      // at every boundary.
+      int total = 0;
+      for (int ee = e_begin; ee < e_end; ++ee) total += decode_code<KC>(p, code_of(ee), s_op, s_rp, s_cp, r0).nchunks;
+      if (total > 0) {
+        const int aoff = (mrow(0) + g) * LDA + tg, boff = (ncol(0) + g) * LDB + tg;
+        double a0[MT], b0[NTL], a1[MT], b1[NTL];
+        auto load = [&](double* a, double* b, int s, int kk) {
+          const double* as = As + s * BM * LDA + aoff;
+          const double* bs = Bs + s * BN * LDB + boff;
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LDA + kk];
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LDB + kk];
+        };
+        auto mma = [&](const double* a, const double* b) {
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        };
+        mbar_wait(full, 0);
+        load(a0, b0, 0, 0);
+        for (int qq = 0; qq < total; ++qq) {
+          const int s = qq % STAGES;
+#pragma unroll
+          for (int kk = 0; kk < KC; kk += 8) {
+            load(a1, b1, s, kk + 4);
+            mma(a0, b0);
+            if (kk + 8 < KC) {
+              load(a0, b0, s, kk + 8);
+            } else if (qq + 1 < total) {
+              const int s1 = (qq + 1) % STAGES;
+              mbar_wait(full + s1, ((qq + 1) / STAGES) & 1);
+              load(a0, b0, s1, 0);
+            }
+            mma(a1, b1);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+        }
+      }
+      e = e_end;
+    }
+  }
   while (e < e_end) {
     bool generic = true;  // all of this warp's tiles live: the plain loop
     if constexpr (IL) {

@@ -175,6 +175,7 @@ class B200M2LHandler:
                                                    int(self._op_complex), ctypes.byref(h)))
         self._h = h
         self._planned: dict[int, dict] = {}
+        self._acct: dict[int, tuple] = {}  # level -> (plan stats, group key, flops, block summary)
 
     @staticmethod
     def _pick_device(device):
@@ -259,6 +260,7 @@ class B200M2LHandler:
             key = self._group_key_id[self._level_group[lvl]]
             self._check(self._lib.cfm_set_level(self._h, int(lvl), key, float(self._level_scale[lvl])))
         self._planned.clear()
+        self._acct.clear()
         self._precomputed = True
         return self
 
@@ -576,9 +578,19 @@ class B200M2LHandler:
                                                     self._stream_of(x)))
             if wb is not None:
                 wb[...] = y
-            flops = self._count_flops(key, st["counts"], st["targets"], st["sources"])
-            self._record(level, key, st["counts"], flops)
+            flops, summary = self._planned_acct(level, key, st)
+            self._record(level, key, st["counts"], flops, summary=summary)
         return flops
+
+    def _planned_acct(self, level, key, st):
+        """Flops and block statistics of one apply of a planned level: fixed by the
+        plan, so computed once per plan (a per-call Python pass over the 316
+        transfer vectors of every level cost ~1.4 ms per step)."""
+        cached = self._acct.get(level)
+        if cached is None or cached[0] is not st or cached[1] != key:
+            flops = self._count_flops(key, st["counts"], st["targets"], st["sources"])
+            cached = self._acct[level] = (st, key, flops, self._record_summary(level, key, st["counts"]))
+        return cached[2], cached[3]
 
     def apply_levels(self, arrays) -> int:
         """Apply several planned levels of one M2L step together.
@@ -614,8 +626,8 @@ class B200M2LHandler:
             if wb is not None:
                 wb[...] = y
             key = self._level_group[lvl]
-            flops = self._count_flops(key, st["counts"], st["targets"], st["sources"])
-            self._record(lvl, key, st["counts"], flops)
+            flops, summary = self._planned_acct(lvl, key, st)
+            self._record(lvl, key, st["counts"], flops, summary=summary)
             total += flops
         return total
 
@@ -653,24 +665,32 @@ class B200M2LHandler:
             total += 2 * self._size * sa["r_b"] * int(n_sources) + 2 * self._size * sa["r_u"] * int(n_targets)
         return int(total)
 
-    def _record(self, level, key, counts, flops, planned: bool = True) -> None:
+    def _record_summary(self, level, key, counts, planned: bool = True):
+        """Per-call block statistics of a counts vector: (columns, products, [(rep, columns)])."""
+        if not self.uses_blocking:
+            return None
+        group = self._groups[key]
+        per_rep: dict = {}
+        for code in np.nonzero(counts)[0]:
+            c = int(code)
+            t = (c // 49 - 3, (c // 7) % 7 - 3, c % 7 - 3)
+            rep = group.symmetry.lookup(t)[0]
+            per_rep[rep] = per_rep.get(rep, 0) + int(counts[c])
+        products = self.plan_stats(level)["entries"] if planned else 0
+        return int(counts.sum()), products, [(rep, per_rep[rep]) for rep in sorted(per_rep)]
+
+    def _record(self, level, key, counts, flops, planned: bool = True, summary=None) -> None:
         self.flops[level] = self.flops.get(level, 0) + flops
         if self.uses_blocking:
-            group = self._groups[key]
+            if summary is None:
+                summary = self._record_summary(level, key, counts, planned)
+            pairs, products, flushes = summary
             st = self.block_stats.setdefault(level, {"columns": 0, "products": 0, "reps_used": set(), "flushes": []})
-            pairs = int(counts.sum())
             st["columns"] += pairs
-            if planned:  # GPU tile products (one per tile entry) instead of 128-column flushes
-                st["products"] += self.plan_stats(level)["entries"]
-            per_rep: dict = {}
-            for code in np.nonzero(counts)[0]:
-                c = int(code)
-                t = (c // 49 - 3, (c // 7) % 7 - 3, c % 7 - 3)
-                rep = group.symmetry.lookup(t)[0]
-                per_rep[rep] = per_rep.get(rep, 0) + int(counts[c])
-            for rep in sorted(per_rep):
+            st["products"] += products
+            for rep, cols in flushes:
                 st["reps_used"].add(rep)
-                st["flushes"].append((rep, per_rep[rep]))
+                st["flushes"].append((rep, cols))
 
     # ------------------------------------------------------------------
     # accounting (m2l.py:458-536)

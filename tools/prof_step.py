@@ -2,6 +2,7 @@
 applies it `--reps` times with device-resident expansions."""
 import argparse
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -14,6 +15,8 @@ def main():
     ap.add_argument("--variant", default=None)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--gpu-tree", action="store_true", help="level cells from the GPU octree (large configs)")
+    ap.add_argument("--signed", action="store_true", help="multipoles U[-1,1] (as bench.py) instead of U[0,1]")
+    ap.add_argument("--flush", action="store_true", help="write 256 MB (> L2) and synchronize before each step")
     a = ap.parse_args()
     import torch
 
@@ -33,11 +36,19 @@ def main():
     for l in levels:
         h.plan_level_cells(l, cells[l].astype("int32"))
     mp = {l: torch.rand((len(cells[l]), order**3), dtype=torch.float64, device="cuda") for l in levels}
+    if a.signed:
+        mp = {l: v * 2 - 1 for l, v in mp.items()}
     loc = {l: torch.zeros_like(mp[l]) for l in levels}
-    for _ in range(a.reps):
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda") if a.flush else None
+    for i in range(a.reps):
+        if flush is not None:
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
         h.apply_levels({l: (mp[l], loc[l]) for l in levels})
+        t1 = time.perf_counter()
         torch.cuda.synchronize()
-        print("step device ms %.3f launches %d" % h.last_apply_stats())
+        print("step device ms %.3f launches %d" % h.last_apply_stats(), "host call ms %.3f" % ((t1 - t0) * 1e3))
 
 
 if __name__ == "__main__":
