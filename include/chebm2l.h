@@ -169,6 +169,13 @@ int cfm_classify_fill_device(int device, int level, int64_t n_cells, const int32
  * CFM_PLAN_MODE=target|pair).  target_fill = pairs / target-tile slots. */
 int cfm_plan_info(cfm_handler* h, int level, int* mode, double* target_fill);
 
+/* 1 when a low-rank level (ia / iasym / iablk, real operators, target tiles)
+ * runs as two stages: Y = V_t^H x for every (source, transfer of its class) as
+ * a dense GEMM, then locals += U_t Y per target tile (m2l.py:425 split at the
+ * rank-r intermediate); 0 for the fused single-kernel path.  CFM_LR_TWOSTAGE=0
+ * at precompute disables it. */
+int cfm_plan_two_stage(cfm_handler* h, int level, int* two_stage);
+
 /* Interaction-list classifier (octree.py:148-178 + symmetry.py:63-75) on the
  * GPU.  Cells: sorted occupied ijk of `level` (int32 triples, host or device).
  * count: per-cell far-pair counts -> offsets (n_cells+1, host int64), returns

@@ -42,6 +42,7 @@ EXPORTS = (
     "cfm_apply_levels",
     "cfm_plan_stats",
     "cfm_plan_info",
+    "cfm_plan_two_stage",
     "cfm_classify_count",
     "cfm_classify_fill",
     "cfm_classify_count_device",
@@ -84,6 +85,7 @@ _SIGS = {
     "cfm_apply_levels": ([_P, _I, _P, _P, _P, _P, _P], _I),
     "cfm_plan_stats": ([_P, _I, _P, _P, _P, _P, _P, _P], _I),
     "cfm_plan_info": ([_P, _I, _P, _P], _I),
+    "cfm_plan_two_stage": ([_P, _I, _P], _I),
     "cfm_classify_count": ([_I, _I, _I64, _P, _P, _P], _I),
     "cfm_classify_fill": ([_I, _I, _I64, _P, _P, _P, _P, _P, _P], _I),
     "cfm_classify_count_device": ([_I, _I, _I64, _P, _P, _P, _P], _I),

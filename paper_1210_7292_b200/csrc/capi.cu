@@ -175,6 +175,19 @@ struct Group {
   // columns permuted once), read with contiguous copies from padded sources
   bool has_lrfull = false;
   OpStack lrf_left, lrf_right_h;
+  // two-stage low-rank mode (real, dense levels): stage 1 Y = V_t^H x per
+  // (source, transfer) for the whole transfer set of the source's class, as a
+  // dense GEMM against a per-class stack of V_t^H rows; stage 2 sums U_t Y per
+  // target tile.  Classes: per axis the transfer components lie in [-3, 2]
+  // (bit 0) or [-2, 3] (bit 1), which holds for every source of an octree
+  // level (octree.py:157-175).  Ranks are cut in 16-wide segments (<= 2).
+  bool has_ts = false;
+  int ts_nb = 0;                 // 128-row blocks per class stack
+  std::vector<int> ts_rank;      // per transfer index
+  std::vector<int> ts_slot;      // [8][n_transfers][2] segment slot in the class stack, -1 if absent
+  int ts_ntr = 0;
+  OpStack ts_v;                  // 8 * ts_nb blocks of 128 rows x n
+  CUtensorMap ts_vmap, ts_umap;  // box 36 x 128 over ts_v; box 20 x 128 over lrf_left
 };
 
 struct LevelPlan {
@@ -202,6 +215,12 @@ struct LevelPlan {
   DevBuf t_tile_col, t_tile_off, t_entry_code, t_entry_src;
   int64_t n_rows = 0;
   uint64_t gen = 0;  // unique per built plan (merged plans remember what they were built from)
+  // two-stage low-rank plans (Group::has_ts): stage 1 over source tiles, stage 2 over target tiles
+  bool ts = false;
+  HostPlan ts1, ts2;
+  DevBuf ts1_col, ts1_off, ts1_code, ts1_src, ts2_col, ts2_off, ts2_code, ts2_src;
+  int64_t ts_segs = 0;  // stage-2 B rows (entries x 64): the stage-1 output in stage-2 order, 20 doubles each (4 zero)
+  DevBuf ts_y, ts_map;  // ts_map: stage-1 segment -> its row in ts_y (-1: no pair needs it)
 };
 
 // Pair-mode levels of one homogeneous full-operator group merged into one
@@ -320,13 +339,21 @@ static PFN_encodeTiled resolve_encode_tiled() {
 static void encode_source_map(TileParams& q, int kc) {
   const cuuint64_t dims[2] = {cuuint64_t(q.x_ld), cuuint64_t(std::max<long long>(q.x_rows, 1))};
   const cuuint64_t strides[1] = {cuuint64_t(q.x_ld) * sizeof(double)};
-  const cuuint32_t box[2] = {cuuint32_t(kc + 4), 1u};
+  const cuuint32_t box[2] = {cuuint32_t(kc + 4), q.b_block ? cuuint32_t(kBN) : 1u};  // b_block: one entry's rows
   const cuuint32_t estr[2] = {1u, 1u};
   const CUresult r = resolve_encode_tiled()(&q.tmap_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(q.x),
                                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for the source rows");
+}
+
+static bool ft_pipe_enabled() {
+  static const int v = [] {
+    const char* e = getenv("CFM_FT_PIPE");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
 }
 
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
@@ -358,14 +385,10 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
       const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
       // the flat pipelined consumer loop runs whole KC-chunks: only when the last
       // chunk of an operator has KC/4 k-steps anyway (l = 5: 125 = 3 x 32 + 29)
-      static const int pipe_env = [] {
-        const char* e = getenv("CFM_FT_PIPE");
-        return e ? atoi(e) : 1;
-      }();
       for (int i = 0; i < mp.n_seg; ++i) {
         encode_source_map(mp.seg[i], KC);
         const int rem = mp.seg[i].nk % KC;
-        mp.seg[i].ft_pipe = pipe_env && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
+        mp.seg[i].ft_pipe = ft_pipe_enabled() && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
       }
       auto kf = skip ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
                      : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
@@ -590,6 +613,29 @@ static int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s
   return launch_range(p, 0, n_tiles, s);
 }
 
+// Full-operator kernel with 16-wide K chunks (two-stage low-rank stage 2: one
+// chunk per rank segment), one segment, pipelined consumer loop.
+static int64_t launch_ft16(TileParams q, int64_t n_tiles, cudaStream_t s) {
+  constexpr int KC = 16, STAGES = 6;
+  if (n_tiles <= 0) return 0;
+  if (n_tiles >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
+  MultiTileParams mp{};
+  mp.n_seg = 1;
+  mp.nrb = 1;
+  mp.start[0] = 0;
+  mp.start[1] = int(n_tiles);
+  q.tile_base = 0;
+  encode_source_map(q, KC);
+  q.ft_pipe = ft_pipe_enabled() && q.nk % KC == 0;
+  mp.seg[0] = q;
+  auto kf = tile_gemm_ws_kernel<128, kBN, 4, 2, KC, STAGES, false, false, 1>;
+  const int smem = ws_ring_bytes<128, kBN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
+  CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kf<<<unsigned(n_tiles), (4 * 2 + 4) * 32, smem, s>>>(mp);
+  CUDA_CHECK(cudaGetLastError());
+  return 1;
+}
+
 static void fill_ops(TileParams& p, const OpStack& s, const CodeMap& m) {
   p.ops = s.d.as<double>();
   p.op_stride = s.stride;
@@ -780,6 +826,72 @@ static void build_lowrank_stacks(cfm_handler* h, OpStack& left, OpStack& right_h
   set_per_op(right_h, rrows, {});  // pass 1: rows = rank
 }
 
+static bool use_two_stage() {  // read at every precompute (tests switch it)
+  const char* e = getenv("CFM_LR_TWOSTAGE");
+  return !e || atoi(e) != 0;
+}
+
+// Two-stage low-rank operators (see Group::has_ts): per class the V_t^H rows
+// of its transfers in 16-row segments, and the tensor maps of both stages.
+static void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers,
+                            const std::vector<int>& rk, const std::vector<double>& all_v) {
+  g.has_ts = false;
+  if (!use_two_stage()) return;
+  const int n = h->n;
+  int rmax = 0;
+  for (int r : rk) rmax = std::max(rmax, r);
+  if (rmax == 0 || rmax > 32 || g.lrf_left.ld != 32) return;
+  g.ts_ntr = n_transfers;
+  g.ts_rank = rk;
+  g.ts_slot.assign(size_t(8) * n_transfers * 2, -1);
+  int max_slots = 0;
+  for (int cls = 0; cls < 8; ++cls) {
+    int ns = 0;
+    for (int k = 0; k < n_transfers; ++k) {
+      bool in = rk[k] > 0;
+      for (int a = 0; a < 3 && in; ++a) {
+        const int t = transfers[3 * k + a], bit = (cls >> a) & 1;
+        in = t >= (bit ? -2 : -3) && t <= (bit ? 3 : 2);
+      }
+      if (!in) continue;
+      for (int j = 0; j * 16 < rk[k]; ++j) g.ts_slot[(size_t(cls) * n_transfers + k) * 2 + j] = ns++;
+    }
+    max_slots = std::max(max_slots, ns);
+  }
+  const int nb = (max_slots * 16 + 127) / 128;
+  g.ts_nb = nb;
+  make_stack(g.ts_v, 8 * nb, 128, n);
+  const int vld = g.lrf_right_h.ld;
+  const size_t vstride = size_t(g.lrf_right_h.stride);
+  std::vector<double> blk(size_t(g.ts_v.stride));
+  for (int cls = 0; cls < 8; ++cls)
+    for (int b = 0; b < nb; ++b) {
+      std::fill(blk.begin(), blk.end(), 0.0);
+      for (int k = 0; k < n_transfers; ++k)
+        for (int j = 0; j < 2; ++j) {
+          const int sl = g.ts_slot[(size_t(cls) * n_transfers + k) * 2 + j];
+          if (sl < 0 || sl / 8 != b) continue;
+          for (int a = 0; a < 16 && 16 * j + a < rk[k]; ++a)
+            std::copy_n(all_v.begin() + size_t(k) * vstride + size_t(16 * j + a) * vld, n,
+                        blk.begin() + size_t((sl % 8) * 16 + a) * g.ts_v.ld);
+        }
+      put_stack(g.ts_v, cls * nb + b, blk);
+    }
+  auto encode = [](CUtensorMap* m, const OpStack& st, long long rows, unsigned box0) {
+    const cuuint64_t dims[2] = {cuuint64_t(st.ld), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(st.ld) * sizeof(double)};
+    const cuuint32_t box[2] = {box0, 128u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = resolve_encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, st.d.p, dims, strides, box, estr,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for a two-stage stack");
+  };
+  encode(&g.ts_vmap, g.ts_v, (long long)8 * nb * 128, kKC + 4);
+  encode(&g.ts_umap, g.lrf_left, (long long)n_transfers * n, 16 + 4);
+  g.has_ts = true;
+}
+
 // Per-transfer low-rank factors for real operators: U_t[i][a] = left_o[tab_r[i]][a],
 // V_t^H[a][j] = right_o[tab_c[j]][a] (the products the permuted apply forms:
 // Y[a] = sum_k right^H[a][k] x[inv[k]] = sum_j right^H[a][tab[j]] x[j]).
@@ -795,6 +907,7 @@ static void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const 
   std::vector<int> ident(n), rk(n_transfers);
   std::iota(ident.begin(), ident.end(), 0);
   std::vector<double> bl(g.lrf_left.stride), br(g.lrf_right_h.stride);
+  std::vector<double> all_v(size_t(n_transfers) * g.lrf_right_h.stride);
   for (int k = 0; k < n_transfers; ++k) {
     const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
     const int o = g.main.op[c];
@@ -812,12 +925,14 @@ static void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const 
       for (int j = 0; j < n; ++j) br[size_t(a) * g.lrf_right_h.ld + j] = Ro[size_t(tc[j]) * r + a];
     put_stack(g.lrf_left, k, bl);
     put_stack(g.lrf_right_h, k, br);
+    std::copy(br.begin(), br.end(), all_v.begin() + size_t(k) * br.size());
     g.fullmap.op[c] = k;
   }
   g.fullmap.push();
   set_per_op(g.lrf_left, {}, rk);
   set_per_op(g.lrf_right_h, rk, {});
   g.has_lrfull = true;
+  build_two_stage(h, g, n_transfers, transfers, rk, all_v);
 }
 
 // ------------------------------------------------------------------ planning
@@ -841,6 +956,120 @@ static Group& group_for_level(cfm_handler* h, int level) {
   auto git = h->groups.find(it->second.first);
   if (git == h->groups.end()) throw Error(CFM_ERR_PRECOMPUTE, "level group has no operators");
   return git->second;
+}
+
+// Two-stage low-rank plans from a level's target-tile plan (Group::has_ts).
+// Stage 1: source tiles (64 sources of one class) x ts_nb entries (one per
+// 128-row block of the class stack), pair-mode output rows v = e * 64 + c
+// written as 8 segments of 16 at a 20-double pitch.  Stage 2: the target tiles
+// with every entry (t, 64 sources) split into its rank segments j, operator id
+// 2 k + j (k = transfer index), source ids = stage-1 segment rows.  Taken only
+// when stage 1 computes at most ~1.7x the segments the pairs need and the
+// stage-1 output fits CFM_LR_TWOSTAGE_GB (default 24 GB).
+static void build_two_stage_plan(const Group& g, LevelPlan& lp) {
+  const HostPlan& hp = lp.hp;
+  const int64_t n_rows = lp.n_rows;
+  const int ntr = g.ts_ntr, nb = g.ts_nb;
+  std::vector<int8_t> mn(size_t(n_rows) * 3, 127), mx(size_t(n_rows) * 3, -128);
+  std::vector<char> used(n_rows, 0);
+  int64_t need_segs = 0;
+  const int64_t E = hp.n_entries();
+  for (int64_t e = 0; e < E; ++e) {
+    const int c = hp.entry_code[e];
+    const int k = g.fullmap.op[c];
+    if (k < 0 || k >= ntr || g.ts_rank[k] <= 0) return;
+    int t[3];
+    tcode_decode(c, t[0], t[1], t[2]);
+    const int nseg = (g.ts_rank[k] + 15) / 16;
+    for (int col = 0; col < kBN; ++col) {
+      const int v = hp.entry_src[size_t(e) * kBN + col];
+      if (v < 0) continue;
+      used[v] = 1;
+      need_segs += nseg;
+      for (int a = 0; a < 3; ++a) {
+        mn[size_t(v) * 3 + a] = std::min<int8_t>(mn[size_t(v) * 3 + a], int8_t(t[a]));
+        mx[size_t(v) * 3 + a] = std::max<int8_t>(mx[size_t(v) * 3 + a], int8_t(t[a]));
+      }
+    }
+  }
+  std::vector<int8_t> cls(n_rows, -1);
+  std::vector<std::vector<int64_t>> by_cls(8);
+  for (int64_t v = 0; v < n_rows; ++v) {
+    if (!used[v]) continue;
+    int b = 0;
+    for (int a = 0; a < 3; ++a) {
+      if (mx[size_t(v) * 3 + a] <= 2) continue;        // fits [-3, 2]
+      if (mn[size_t(v) * 3 + a] >= -2) b |= 1 << a;     // fits [-2, 3]
+      else return;                                      // not an octree far list
+    }
+    cls[v] = int8_t(b);
+    by_cls[b].push_back(v);
+  }
+  // stage 1 plan
+  HostPlan p1;
+  std::vector<int> tile1(n_rows, -1), col1(n_rows, -1);
+  for (int b = 0; b < 8; ++b)
+    for (size_t i = 0; i < by_cls[b].size(); i += kBN) {
+      const int64_t t = p1.n_tiles++;
+      p1.tile_off.push_back(int(p1.entry_code.size()));
+      std::vector<int> cols(kBN, -1);
+      for (int c = 0; c < kBN && i + c < by_cls[b].size(); ++c) {
+        const int64_t v = by_cls[b][i + c];
+        cols[c] = int(v);
+        tile1[v] = int(t);
+        col1[v] = c;
+      }
+      p1.tile_col.insert(p1.tile_col.end(), cols.begin(), cols.end());
+      for (int blk = 0; blk < nb; ++blk) {
+        p1.entry_code.push_back(b * nb + blk);
+        p1.entry_src.insert(p1.entry_src.end(), cols.begin(), cols.end());
+      }
+    }
+  p1.tile_off.push_back(int(p1.entry_code.size()));
+  const int64_t segs1 = p1.n_entries() * kBN * 8;
+  static const double budget_gb = [] {
+    const char* e = getenv("CFM_LR_TWOSTAGE_GB");
+    return e ? atof(e) : 24.0;
+  }();
+  if (segs1 >= (int64_t(1) << 31) || double(need_segs) * 1.2 * 20 * 8 > budget_gb * 1e9) return;
+  if (double(p1.n_tiles) * kBN * nb * 8 > 1.7 * double(need_segs)) return;  // sparse level: fused kernel
+  // stage 2 plan; its B rows (entry e2, column c) = the stage-1 segment of that pair
+  std::vector<int> ymap(size_t(segs1), -1);
+  HostPlan p2;
+  p2.n_tiles = hp.n_tiles;
+  p2.tile_col = hp.tile_col;
+  p2.tile_off.reserve(hp.n_tiles + 1);
+  for (int64_t t = 0; t < hp.n_tiles; ++t) {
+    p2.tile_off.push_back(int(p2.entry_code.size()));
+    for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e) {
+      const int c = hp.entry_code[e];
+      const int k = g.fullmap.op[c];
+      for (int j = 0; j * 16 < g.ts_rank[k]; ++j) {
+        p2.entry_code.push_back(2 * k + j);
+        for (int col = 0; col < kBN; ++col) {
+          const int v = hp.entry_src[size_t(e) * kBN + col];
+          int id = -1;
+          if (v >= 0) {
+            const int sl = g.ts_slot[(size_t(cls[v]) * ntr + k) * 2 + j];
+            if (sl < 0) return;
+            id = int(((int64_t(tile1[v]) * nb + sl / 8) * kBN + col1[v]) * 8 + sl % 8);
+            const int64_t row2 = int64_t(p2.entry_code.size() - 1) * kBN + col;
+            if (row2 >= (int64_t(1) << 31)) return;
+            ymap[size_t(id)] = int(row2);
+          }
+          p2.entry_src.push_back(id);
+        }
+      }
+    }
+  }
+  p2.tile_off.push_back(int(p2.entry_code.size()));
+  lp.ts1 = std::move(p1);
+  lp.ts2 = std::move(p2);
+  push_plan(lp.ts1, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src);
+  push_plan(lp.ts2, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src);
+  upload(lp.ts_map, ymap);
+  lp.ts_segs = lp.ts2.n_entries() * kBN;
+  lp.ts = true;
 }
 
 static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
@@ -1010,6 +1239,7 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     upload(lp.p_lo, lo);
     upload(lp.p_hi, hi);
   }
+  if (g.kind == kLowRank && g.has_ts && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) build_two_stage_plan(g, lp);
   static uint64_t plan_gen = 0;
   lp.gen = ++plan_gen;
   h->plans[level] = std::move(lp);
@@ -1141,6 +1371,56 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     p.y = d_y; p.y_ld = row_ld; p.y_dc = dc;
     p.scale = scale; p.accumulate = 1;
     launches += launch_tiles(p, lp.hp.n_tiles, s);
+    return launches;
+  }
+
+  if (g.kind == kLowRank && lp.ts) {
+    // two-stage low-rank: stage 1 Y = V^H x per (source, class segment), stage 2
+    // locals += scale * sum U_t Y per target tile (both on the full-operator kernel)
+    const int ldx = g.ts_v.ld;
+    const auto xo = xpad_layout(h, {{lp.n_rows, ldx}}, s);
+    double* xp = h->xpad.as<double>() + xo[0];
+    xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
+    if (!lp.ts_y.p) {
+      lp.ts_y.alloc(size_t(lp.ts_segs) * 20 * sizeof(double));
+      CUDA_CHECK(cudaMemsetAsync(lp.ts_y.p, 0, lp.ts_y.bytes, s));  // segment pads stay zero
+    }
+    TileParams a{};
+    fill_ops(a, g.ts_v, g.main);
+    fill_plan(a, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src, lp.ts1.n_tiles);
+    a.op_rows = nullptr;
+    a.op_klen = nullptr;
+    a.nr = 128;
+    a.nk = h->n;
+    a.code_is_op = 1;
+    a.ft = 1;
+    a.ft_rows = 128;
+    a.tmap_a = g.ts_vmap;
+    a.x = xp; a.x_ld = ldx; a.x_dc = 1; a.x_rows = lp.n_rows;
+    a.y = lp.ts_y.as<double>(); a.y_ld = 8 * 20; a.y_dc = 1; a.y_seg = 20; a.y_map = lp.ts_map.as<int>();
+    a.scale = 1.0; a.accumulate = 0; a.pair_out = 1;
+    a.zero_row = h->zeros.as<double>();
+    a.n_entries = lp.ts1.n_entries();
+    launches += launch_tiles(a, lp.ts1.n_tiles, s);
+    TileParams b{};
+    fill_ops(b, g.lrf_left, g.main);
+    fill_plan(b, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src, lp.ts2.n_tiles);
+    b.op_rows = nullptr;
+    b.op_klen = nullptr;
+    b.nr = h->n;
+    b.nk = 16;
+    b.code_is_op = 1;
+    b.ft = 1;
+    b.ft_rows = h->n;
+    b.ft_opshift = 1;
+    b.ft_colseg = 16;
+    b.tmap_a = g.ts_umap;
+    b.x = lp.ts_y.as<double>(); b.x_ld = 20; b.x_dc = 1; b.x_rows = lp.ts_segs; b.b_block = 1;
+    b.y = d_y; b.y_ld = row_ld; b.y_dc = 1;
+    b.scale = scale; b.accumulate = 1; b.pair_out = 0;
+    b.zero_row = h->zeros.as<double>();
+    b.n_entries = lp.ts2.n_entries();
+    launches += launch_ft16(b, lp.ts2.n_tiles, s);
     return launches;
   }
 
@@ -2501,6 +2781,16 @@ int cfm_plan_info(cfm_handler* h, int level, int* mode, double* target_fill) {
     if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(level));
     if (mode) *mode = it->second.mode;
     if (target_fill) *target_fill = it->second.target_fill;
+  });
+}
+
+int cfm_plan_two_stage(cfm_handler* h, int level, int* two_stage) {
+  return guarded([&] {
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->plans.find(level);
+    if (it == h->plans.end()) throw Error(CFM_ERR_PRECOMPUTE, "no plan for level " + std::to_string(level));
+    if (two_stage) *two_stage = it->second.ts ? 1 : 0;
   });
 }
 

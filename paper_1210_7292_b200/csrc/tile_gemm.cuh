@@ -93,6 +93,13 @@ struct TileParams {
   long long n_entries;               // host-side hint: entries of the plan (kernel choice)
   long long x_rows;                  // full-operator mode: rows of the padded source array x
   int ft_pipe;                       // full-operator target tiles: flat pipelined consumer loop
+  // two-stage low-rank mode (full-operator kernels):
+  int code_is_op;   // entry codes are operator ids (no code tables, identity permutations)
+  int ft_opshift;   // operator id o -> A block row (o >> ft_opshift) * ft_rows, column (o & mask) * ft_colseg
+  int ft_colseg;
+  int y_seg;        // pair-mode output rows written as 16-row segments at this pitch (0: contiguous rows)
+  const int* y_map; // with y_seg: segment (v * 8 + row / 16) -> destination segment index (-1: not needed)
+  int b_block;      // B of entry e = rows [e * BN, e * BN + BN) of tmap_b (one 2-D box; no gathers)
   CUtensorMap tmap_a;
   // full-operator mode: 2-D map over the padded sources (x_ld x x_rows), box
   // (KC + 4) x 1, read by tile::gather4 copies (4 source rows per instruction)
@@ -159,6 +166,14 @@ template <int KC>
 __device__ __forceinline__ EntryInfo decode_code(const TileParams& p, int code, const int* s_op, const int* s_rp,
                                                  const int* s_cp, int r0) {
   EntryInfo d;
+  if (p.code_is_op) {
+    d.op = code;
+    d.rperm = d.cperm = -1;
+    d.rows = p.nr;
+    d.klen = p.nk;
+    d.nchunks = (d.rows > r0) ? (d.klen + KC - 1) / KC : 0;
+    return d;
+  }
   d.op = s_op[code];
   d.rperm = s_rp[code];
   d.cperm = s_cp[code];

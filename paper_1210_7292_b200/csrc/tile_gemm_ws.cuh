@@ -221,18 +221,25 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     while (e < e_end) {
       int4 rows[BN / 4];
       const int4* srow = reinterpret_cast<const int4*>(p.entry_src + (long long)e * BN);
+      if (!p.b_block) {
 #pragma unroll
-      for (int j = 0; j < BN / 4; ++j) rows[j] = __ldg(srow + j);
-      const int arow = d.op * p.ft_rows + r0;
+        for (int j = 0; j < BN / 4; ++j) rows[j] = __ldg(srow + j);
+      }
+      const int arow = (d.op >> p.ft_opshift) * p.ft_rows + r0;
+      const int acol = (d.op & ((1 << p.ft_opshift) - 1)) * p.ft_colseg;
       for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
         const int s = q % STAGES;
         if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
         const int k0 = kc * KC;
         double* bs = Bs + s * BN * LDB;
         mbar_arrive_expect_tx(full + s, STAGE_TX);
-        tma_load_2d(As + s * BM * LDA, &p.tmap_a, k0, arow, full + s);
+        tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
+        if (p.b_block) {
+          tma_load_2d(bs, &p.tmap_b, k0, e * BN, full + s);
+        } else {
 #pragma unroll
-        for (int j = 0; j < BN / 4; ++j) tma_gather4(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s);
+          for (int j = 0; j < BN / 4; ++j) tma_gather4(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s);
+        }
       }
       e = next_live(e + 1, d);
     }
@@ -409,7 +416,11 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     }
   };
   if constexpr (FTM == 1) {
-    if (!p.pair_out && p.ft_pipe) {
+    // pair-mode stage-1 tiles (y_seg, operator-id codes: every entry has the
+    // same chunk count and the tile's columns) also run the flat loop, writing
+    // each entry's rows when its last chunk is done
+    const bool seg_out = p.pair_out && p.y_seg && p.code_is_op;
+    if ((!p.pair_out || seg_out) && p.ft_pipe) {
       // Full-operator target tiles whose every chunk is KC/4 whole k-steps
       // (host-checked): one flat chunk stream, software-pipelined across chunk
       // and entry boundaries -- the next chunk's full barrier is waited for and
@@ -418,6 +429,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       // at every boundary.
       int total = 0;
       for (int ee = e_begin; ee < e_end; ++ee) total += decode_code<KC>(p, code_of(ee), s_op, s_rp, s_cp, r0).nchunks;
+      const int nch = (p.nk + KC - 1) / KC;  // chunks per entry (seg_out: uniform)
       if (total > 0) {
         const int aoff = (mrow(0) + g) * LDA + tg, boff = (ncol(0) + g) * LDB + tg;
         double a0[MT], b0[NTL], a1[MT], b1[NTL];
@@ -437,8 +449,21 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         };
         mbar_wait(full, 0);
         load(a0, b0, 0, 0);
+        // seg_out with a destination map: each thread's 2 segments x 8 columns,
+        // looked up at the start of an entry's last chunk (latency under its MMAs)
+        int dmap[2][NTL][2];
         for (int qq = 0; qq < total; ++qq) {
           const int s = qq % STAGES;
+          if (seg_out && p.y_map && (qq + 1) % nch == 0) {
+            const long long ve = (long long)(e_begin + qq / nch) * BN;
+#pragma unroll
+            for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+              for (int nj = 0; nj < NTL; ++nj)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  dmap[sg][nj][h] = __ldg(p.y_map + (ve + ncol(nj) + 2 * tg + h) * 8 + ((r0 + mrow(2 * sg)) >> 4));
+          }
 #pragma unroll
           for (int kk = 0; kk < KC; kk += 8) {
             load(a1, b1, s, kk + 4);
@@ -454,9 +479,47 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + s);
+          if (seg_out && p.y_map && (qq + 1) % nch == 0) {
+            // each (column, 16-row segment) is held by the 8 lanes of one tg
+            // (rows g and g + 8): shuffle so lane g holds rows 2g, 2g + 1 and
+            // store 16 B per lane -- one warp store writes 4 whole 128-B segments
+            static_assert(MT % 2 == 0, "segments are pairs of m-tiles");
+#pragma unroll
+            for (int sg = 0; sg < MT / 2; ++sg)
+#pragma unroll
+              for (int nj = 0; nj < NTL; ++nj)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const double vlo = acc[2 * sg][nj][h], vhi = acc[2 * sg + 1][nj][h];
+                  const int s0 = ((2 * g) & 7) * 4 + tg, s1 = ((2 * g + 1) & 7) * 4 + tg;
+                  const double a0 = __shfl_sync(0xffffffffu, vlo, s0), b0 = __shfl_sync(0xffffffffu, vhi, s0);
+                  const double a1 = __shfl_sync(0xffffffffu, vlo, s1), b1 = __shfl_sync(0xffffffffu, vhi, s1);
+                  const int d = dmap[sg][nj][h];
+                  if (d >= 0)
+                    *reinterpret_cast<double2*>(p.y + (long long)d * p.y_seg + 2 * g) =
+                        g < 4 ? make_double2(a0, a1) : make_double2(b0, b1);
+                  acc[2 * sg][nj][h] = acc[2 * sg + 1][nj][h] = 0.0;
+                }
+          } else if (seg_out && (qq + 1) % nch == 0) {
+            const long long ve = (long long)(e_begin + qq / nch) * BN;
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi) {
+              const int row = r0 + mrow(mi) + g;
+              const long long ro = (long long)(row >> 4) * p.y_seg + (row & 15);
+#pragma unroll
+              for (int nj = 0; nj < NTL; ++nj)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int c = ncol(nj) + 2 * tg + h;
+                  if (row < p.nr && s_col[c] >= 0) p.y[(ve + c) * p.y_ld + ro] = acc[mi][nj][h];
+                  acc[mi][nj][h] = 0.0;
+                }
+            }
+          }
         }
       }
       e = e_end;
+      if (seg_out) return;
     }
   }
   while (e < e_end) {
@@ -549,7 +612,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
             const int c = ncol(nj) + 2 * tg + h;
             if (row < p.nr && __ldg(p.entry_src + (long long)e * BN + c) >= 0) {
               const long long v = (long long)e * BN + c;
-              double* dst = p.y + (v / p.y_dc) * p.y_ld + (v % p.y_dc) + (long long)p.y_dc * row;
+              const long long ro = p.y_seg ? (long long)(row >> 4) * p.y_seg + (row & 15) : (long long)p.y_dc * row;
+              double* dst = p.y + (v / p.y_dc) * p.y_ld + (v % p.y_dc) + ro;
               const double val = p.scale * acc[mi][nj][h];
               if (p.accumulate)
                 *dst += val;

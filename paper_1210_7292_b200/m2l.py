@@ -562,6 +562,9 @@ class B200M2LHandler:
         self._check(self._lib.cfm_plan_info(self._h, int(level), ctypes.byref(mode), ctypes.byref(fill)))
         out["mode"] = "pair" if mode.value == 1 else "target"
         out["target_fill"] = fill.value
+        ts = ctypes.c_int()
+        self._check(self._lib.cfm_plan_two_stage(self._h, int(level), ctypes.byref(ts)))
+        out["two_stage"] = bool(ts.value)
         return out
 
     def apply_planned(self, level: int, mpoles, locals_out) -> int:

@@ -256,6 +256,63 @@ def test_full_level_against_oracle(torch_cuda, order, level, variant):
     assert O.rel_l2(loc.cpu().numpy(), ref) <= TOL[variant]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["iablk", "iasym", "ia"])
+def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeypatch):
+    """Dense low-rank levels run as two stages (Y = V_t^H x per source and class
+    transfer, then U_t Y per target tile).  Full level 5 at l = 5 (32,768 cells):
+    the two-stage path is taken, matches the oracle (<= 1e-10) and the fused
+    single-kernel path (CFM_LR_TWOSTAGE=0) to rounding, with equal flops."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    order, level, eps = 5, 5, 1e-5
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    rng = np.random.default_rng(7)
+    mp = torch.from_numpy(rng.uniform(-1, 1, (len(cells), order**3))).cuda()
+    out, flops = {}, {}
+    for ts in ("1", "0"):
+        monkeypatch.setenv("CFM_LR_TWOSTAGE", ts)
+        h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps)
+        h.precompute({level: transfers}, lw)
+        h.plan_level_cells(level, cells)
+        assert h.plan_stats(level)["two_stage"] == (ts == "1")
+        loc = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
+        flops[ts] = h.apply_planned(level, mp, loc)
+        loc2 = torch.zeros_like(loc)
+        h.apply_planned(level, mp, loc2)  # repeated applies reuse the stage buffers
+        assert torch.equal(loc, loc2)
+        out[ts] = loc.cpu().numpy()
+    orc = O.OracleM2L(variant, O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    ref = np.zeros(mp.shape)
+    fr = orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert flops["1"] == flops["0"] == fr
+    assert O.rel_l2(out["1"], ref) <= 1e-10
+    assert O.rel_l2(out["1"], out["0"]) <= 1e-13
+
+
+@pytest.mark.gpu
+def test_two_stage_skips_sparse_levels(torch_cuda, monkeypatch):
+    """A sparse (sphere) level in target tiles keeps the fused low-rank kernel:
+    the two-stage source GEMM would compute mostly unneeded class segments."""
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_PLAN_MODE", "target")
+    rng = np.random.default_rng(3)
+    pts = rng.normal(size=(20000, 3))
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+    level = 5
+    side = 1 << level
+    cells = np.unique(np.minimum(((pts + 1.0) / 2.0 * side).astype(np.int64), side - 1), axis=0).astype(np.int32)
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(5), 1e-5)
+    h.precompute({level: full_far_field_vectors()}, {level: 2.0 / side})
+    st = h.plan_level_cells(level, cells)
+    assert st["mode"] == "target" and not h.plan_stats(level)["two_stage"]
+
+
 def test_linearity_full_size_level(torch_cuda):
     """Size-independent property at BASELINE config 2's deepest level (l=5,
     262,144 cells, 46.3 M pairs): M2L(a x + b y) == a M2L(x) + b M2L(y), and a
