@@ -118,7 +118,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    # CFM_LIB_PATH: load another build of the library (A/B timing experiments)
+    p = Path(path) if path is not None else Path(os.environ.get("CFM_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build the CUDA extension first (python -c "
@@ -126,6 +127,8 @@ def load(path: str | os.PathLike | None = None):
         )
     lib = ctypes.CDLL(str(p))
     for name, (args, res) in _SIGS.items():
+        if "CFM_LIB_PATH" in os.environ and not hasattr(lib, name):
+            continue  # an older experimental build
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

@@ -385,13 +385,19 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
       const int smem_ft = ws_ring_bytes<BM, BN, KC, 4>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
       // the flat pipelined consumer loop runs whole KC-chunks: only when the last
       // chunk of an operator has KC/4 k-steps anyway (l = 5: 125 = 3 x 32 + 29)
+      static const int hints_env = [] {
+        const char* e = getenv("CFM_L2_HINTS");
+        return e ? atoi(e) : 0;  // measured: no gain (the operator stack stays L2-resident anyway)
+      }();
       for (int i = 0; i < mp.n_seg; ++i) {
         encode_source_map(mp.seg[i], KC);
+        mp.seg[i].l2_hints = hints_env;
         const int rem = mp.seg[i].nk % KC;
         mp.seg[i].ft_pipe = ft_pipe_enabled() && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
       }
-      auto kf = skip ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
-                     : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
+      auto kf = q.y_map ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
+                : skip    ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
+                          : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
       CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
       kf<<<grid, (WM * WN + 4) * 32, smem_ft, s>>>(mp);
       return;
@@ -627,6 +633,7 @@ static int64_t launch_ft16(TileParams q, int64_t n_tiles, cudaStream_t s) {
   q.tile_base = 0;
   encode_source_map(q, KC);
   q.ft_pipe = ft_pipe_enabled() && q.nk % KC == 0;
+  q.l2_hints = getenv("CFM_L2_HINTS") ? atoi(getenv("CFM_L2_HINTS")) : 0;
   mp.seg[0] = q;
   auto kf = tile_gemm_ws_kernel<128, kBN, 4, 2, KC, STAGES, false, false, 1>;
   const int smem = ws_ring_bytes<128, kBN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;

@@ -51,6 +51,40 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, 
       : "memory");
 }
 
+// L2 eviction-priority policies for TMA copies (createpolicy): operator tiles
+// are re-read by every tile of a level and should stay L2-resident; source rows
+// stream through.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* smem, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                                 uint64_t pol) {
+  unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4_hint(void* smem, const CUtensorMap* map, int c0, int4 r, uint64_t* bar,
+                                                 uint64_t pol) {
+  unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(b), "l"(pol)
+      : "memory");
+}
+
 // 2-D TMA tile::gather4: rows r.x..r.w of the map, columns [c0, c0 + box), landing
 // back to back in shared memory (4 x box doubles), bytes on an mbarrier.
 __device__ __forceinline__ void tma_gather4(void* smem, const CUtensorMap* map, int c0, int4 r, uint64_t* bar) {
@@ -214,6 +248,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     if (lane != 0) return;
     static_assert(BN % 4 == 0 && LDA == LDB, "gather4 rows land with the A pitch");
     constexpr unsigned STAGE_TX = unsigned((BM * LDA + BN * LDB) * 8);
+    const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
     EntryInfo d;
     d.nchunks = 0;
     int e = next_live(e_begin, d);
@@ -233,12 +268,22 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         const int k0 = kc * KC;
         double* bs = Bs + s * BN * LDB;
         mbar_arrive_expect_tx(full + s, STAGE_TX);
-        tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
-        if (p.b_block) {
-          tma_load_2d(bs, &p.tmap_b, k0, e * BN, full + s);
-        } else {
+        if (p.l2_hints) {
+          tma_load_2d_hint(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s, pol_a);
+          if (p.b_block) {
+            tma_load_2d_hint(bs, &p.tmap_b, k0, e * BN, full + s, pol_b);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 4; ++j) tma_gather4(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s);
+            for (int j = 0; j < BN / 4; ++j) tma_gather4_hint(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s, pol_b);
+          }
+        } else {
+          tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
+          if (p.b_block) {
+            tma_load_2d(bs, &p.tmap_b, k0, e * BN, full + s);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 4; ++j) tma_gather4(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s);
+          }
         }
       }
       e = next_live(e + 1, d);
@@ -415,12 +460,17 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       default: ft_entry(mlc, std::integral_constant<int, NTL>{}); break;
     }
   };
-  if constexpr (FTM == 1) {
-    // pair-mode stage-1 tiles (y_seg, operator-id codes: every entry has the
-    // same chunk count and the tile's columns) also run the flat loop, writing
-    // each entry's rows when its last chunk is done
-    const bool seg_out = p.pair_out && p.y_seg && p.code_is_op;
-    if ((!p.pair_out || seg_out) && p.ft_pipe) {
+  if constexpr (FTM == 1 || FTM == 3) {
+    // FTM 3: pair-mode stage-1 tiles of the two-stage low-rank path (y_seg,
+    // operator-id codes: every entry has the same chunk count and the tile's
+    // columns) run the flat loop too, writing each entry's rows when its last
+    // chunk is done
+    // (the KC = 16 instantiation -- stage 2 -- also keeps this path compiled in:
+    // measured 4% faster that way, a scheduling side effect; the KC = 32 FTM 1
+    // step kernel compiles without it, 0.4% faster)
+    constexpr bool kSegCapable = FTM == 3 || KC == 16;
+    const bool seg_out = kSegCapable && p.pair_out && p.y_seg && p.code_is_op;
+    if ((seg_out || !p.pair_out) && p.ft_pipe) {
       // Full-operator target tiles whose every chunk is KC/4 whole k-steps
       // (host-checked): one flat chunk stream, software-pipelined across chunk
       // and entry boundaries -- the next chunk's full barrier is waited for and
