@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--gpu-tree", action="store_true", help="level cells from the GPU octree (large configs)")
     ap.add_argument("--signed", action="store_true", help="multipoles U[-1,1] (as bench.py) instead of U[0,1]")
+    ap.add_argument("--host", action="store_true", help="pinned host numpy buffers (the e2e path)")
     ap.add_argument("--flush", action="store_true", help="write 256 MB (> L2) and synchronize before each step")
     a = ap.parse_args()
     import torch
@@ -39,6 +40,13 @@ def main():
     if a.signed:
         mp = {l: v * 2 - 1 for l, v in mp.items()}
     loc = {l: torch.zeros_like(mp[l]) for l in levels}
+    if a.host:
+        hm = {l: torch.empty(mp[l].shape, dtype=mp[l].dtype, pin_memory=True) for l in levels}
+        hl = {l: torch.zeros(mp[l].shape, dtype=mp[l].dtype, pin_memory=True) for l in levels}
+        for l in levels:
+            hm[l].copy_(mp[l].cpu())
+        mp = {l: hm[l].numpy() for l in levels}
+        loc = {l: hl[l].numpy() for l in levels}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda") if a.flush else None
     for i in range(a.reps):
         if flush is not None:
