@@ -269,8 +269,9 @@ struct cfm_handler {
   long long wt_ld_zeroed = -1;     // SA: leading dimension the W~ padding was zeroed for
   std::unique_ptr<MergedPairPlan> merged;
   std::vector<int64_t> xpad_sig;   // layout the padding columns were zeroed for
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_late = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
+  cudaEvent_t ev_late0 = nullptr, ev_late1 = nullptr;
   cudaEvent_t ev_last = nullptr;  // end of the previous apply's work
   cudaEvent_t ev_fork = nullptr;
   std::vector<AuxStream> aux;
@@ -1939,6 +1940,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   }
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
   const auto t_host1 = std::chrono::steady_clock::now();
+  std::vector<char> copied_early(lv.size(), 0);  // device->host copies already queued
   int64_t launches = 0;
   bool all_dense = true;
   for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
@@ -2090,30 +2092,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     // launch groups: all levels at once, or -- copy pipeline with late
     // full-operator levels -- the other levels first while the late levels'
     // sources cross PCIe, then the late ones once padded on this stream
-    std::vector<std::vector<size_t>> groups(2);
-    if (mp_plan) groups[0].push_back(merged_seg);
-    for (size_t i = 0; i < lv.size(); ++i)
-      if (counts[i]) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-      const auto& grp = groups[gi];
-      if (grp.empty()) continue;
-      if (gi == 1) {
-        CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_x, 0));
-        for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
-                                       lv[i].lp->n_rows, s);
-      }
-      if (same_shape && int(segs.size()) <= kMaxSegments) {
-        std::vector<TileParams> sub;
-        std::vector<int64_t> sub_counts;
-        for (size_t i : grp) {
-          sub.push_back(segs[i]);
-          sub_counts.push_back(counts[i]);
-        }
-        launches += launch_multi(sub, sub_counts, s);
-      } else {
-        for (size_t i : grp) launches += launch_tiles(segs[i], counts[i], s);
-      }
-    }
+    auto reduce_pairs = [&](cudaStream_t rs) {
     for (size_t i = 0; i < lv.size(); ++i) {
       if (lv[i].lp->mode != 1 || reduced_inside[i]) continue;
       const long long row_ld = (long long)h->n * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
@@ -2121,7 +2100,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         const size_t k = size_t(std::find(mlv.begin(), mlv.end(), i) - mlv.begin());
         const int64_t nt = int64_t(mp_plan->red[k].tgt.size());
         if (nt) {
-          k_pair_reduce<<<unsigned(nt), 128, 0, s>>>(h->fbuf.as<double>(), row_ld, mp_plan->r_tgt[k].as<long long>(),
+          k_pair_reduce<<<unsigned(nt), 128, 0, rs>>>(h->fbuf.as<double>(), row_ld, mp_plan->r_tgt[k].as<long long>(),
                                                       mp_plan->r_off[k].as<long long>(), mp_plan->r_frow[k].as<int>(),
                                                       nt, lv[i].y, row_ld, int(row_ld), h->levels[lv[i].level].second,
                                                       1);
@@ -2131,8 +2110,74 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         continue;
       }
       launches += launch_reduce(*lv[i].lp, h->fbuf.as<double>() + f_off[i], row_ld, lv[i].y, row_ld, int(row_ld),
-                                h->levels[lv[i].level].second, s);
+                                h->levels[lv[i].level].second, rs);
     }
+    };
+    bool reduced_early = false;
+    // The late group runs on a side stream: it starts (pad, then launch) as
+    // soon as its sources are in and its CTAs fill the SMs that the first
+    // group's tail leaves idle (levels are independent in M2L); the caller's
+    // stream joins it after the launches.
+    std::vector<std::vector<size_t>> groups(2);
+    if (mp_plan) groups[0].push_back(merged_seg);
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (counts[i]) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
+    static const bool late_side = [] {
+      const char* e = getenv("CFM_LATE_STREAM");
+      return !e || atoi(e) != 0;
+    }();
+    const bool side = late_side && !groups[0].empty() && !groups[1].empty();
+    if (side) {
+      if (!h->s_late) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_late, cudaStreamNonBlocking));
+      if (!h->ev_late0) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_late0, cudaEventDisableTiming));
+      if (!h->ev_late1) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_late1, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventRecord(h->ev_late0, s));  // everything this call (and earlier ones) queued so far
+      CUDA_CHECK(cudaStreamWaitEvent(h->s_late, h->ev_late0, 0));
+    }
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const auto& grp = groups[gi];
+      if (grp.empty()) continue;
+      cudaStream_t sg = s;
+      if (gi == 1) {
+        if (side) sg = h->s_late;
+        CUDA_CHECK(cudaStreamWaitEvent(sg, h->ev_x, 0));
+        for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
+                                       lv[i].lp->n_rows, sg);
+      }
+      if (same_shape && int(segs.size()) <= kMaxSegments) {
+        std::vector<TileParams> sub;
+        std::vector<int64_t> sub_counts;
+        for (size_t i : grp) {
+          sub.push_back(segs[i]);
+          sub_counts.push_back(counts[i]);
+        }
+        launches += launch_multi(sub, sub_counts, sg);
+      } else {
+        for (size_t i : grp) launches += launch_tiles(segs[i], counts[i], sg);
+      }
+      static const bool early_d2h = [] {
+        const char* e = getenv("CFM_EARLY_D2H");
+        return e && atoi(e) != 0;  // measured slower (e2e 54.1 -> 57.5 ms): off
+      }();
+      if (gi == 0 && side && early_d2h) {
+        // the first group's pair reductions and device->host copies go out
+        // while the late group still runs
+        reduce_pairs(s);
+        reduced_early = true;
+        CUDA_CHECK(cudaEventRecord(h->ev_out, s));
+        CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_out, 0));
+        for (size_t i = 0; i < lv.size(); ++i)
+          if (!piped[i] && lv[i].host_y) {
+            CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
+            copied_early[i] = 1;
+          }
+      }
+      if (gi == 1 && side) {
+        CUDA_CHECK(cudaEventRecord(h->ev_late1, sg));
+        CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_late1, 0));
+      }
+    }
+    if (!reduced_early) reduce_pairs(s);
   } else {
     bool all_lr = lv.size() > 1 && use_concurrent_levels();
     for (auto& L : lv) all_lr = all_lr && group_for_level(h, L.level).kind == kLowRank;
@@ -2203,7 +2248,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     CUDA_CHECK(cudaEventRecord(h->ev_out, s));  // kernel (and reductions) done
     CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_out, 0));
     for (size_t i = 0; i < lv.size(); ++i)
-      if (!piped[i] && lv[i].host_y)
+      if (!piped[i] && lv[i].host_y && !copied_early[i])
         CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
     CUDA_CHECK(cudaStreamSynchronize(h->s_d2h));
     CUDA_CHECK(cudaStreamSynchronize(s));
@@ -2468,6 +2513,9 @@ int cfm_handler_destroy(cfm_handler* h) {
     }
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    if (h->s_late) cudaStreamDestroy(h->s_late);
+    if (h->ev_late0) cudaEventDestroy(h->ev_late0);
+    if (h->ev_late1) cudaEventDestroy(h->ev_late1);
     cudaStreamDestroy(h->stream);
     delete h;
   });
