@@ -34,6 +34,7 @@
 #include "plan.hpp"
 #include "symmetry.hpp"
 #include "tile_gemm.cuh"
+#include "seg_gemm.cuh"
 #include "tile_gemm_ws.cuh"
 #include "pair_reduce.cuh"
 #include "lowrank_ws.cuh"
@@ -618,6 +619,21 @@ static int64_t launch_range(const TileParams& p, int64_t first, int64_t count, c
 
 static int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s) {
   return launch_range(p, 0, n_tiles, s);
+}
+
+// Two-stage low-rank stage 2 on seg_pair_gemm_kernel (two 16-wide rank
+// segments per pipeline stage); CFM_SEG_PAIR=0 runs the KC = 16 full-operator
+// kernel instead.
+static int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s) {
+  if (n_tiles <= 0) return 0;
+  if (n_tiles >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
+  q.tile_base = 0;
+  encode_source_map(q, 16);
+  const int smem = seg_pair_smem_bytes();
+  CUDA_CHECK(cudaFuncSetAttribute(seg_pair_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  seg_pair_gemm_kernel<<<unsigned(n_tiles), 12 * 32, smem, s>>>(q);
+  CUDA_CHECK(cudaGetLastError());
+  return 1;
 }
 
 // Full-operator kernel with 16-wide K chunks (two-stage low-rank stage 2: one
@@ -1428,7 +1444,11 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     b.scale = scale; b.accumulate = 1; b.pair_out = 0;
     b.zero_row = h->zeros.as<double>();
     b.n_entries = lp.ts2.n_entries();
-    launches += launch_ft16(b, lp.ts2.n_tiles, s);
+    static const bool seg_pair = [] {
+      const char* e = getenv("CFM_SEG_PAIR");
+      return !e || atoi(e) != 0;
+    }();
+    launches += seg_pair ? launch_seg_pair(b, lp.ts2.n_tiles, s) : launch_ft16(b, lp.ts2.n_tiles, s);
     return launches;
   }
 
