@@ -273,6 +273,8 @@ struct cfm_handler {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_late = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
   cudaEvent_t ev_late0 = nullptr, ev_late1 = nullptr;
+  cudaStream_t s_pad = nullptr;  // pads pipelined full-operator slabs beside the running grid
+  cudaEvent_t ev_slab[16] = {}, ev_pad_done = nullptr;
   cudaEvent_t ev_last = nullptr;  // end of the previous apply's work
   cudaEvent_t ev_fork = nullptr;
   std::vector<AuxStream> aux;
@@ -1327,13 +1329,14 @@ __global__ void __launch_bounds__(256) k_pad_rows(double* __restrict__ dst, int 
 }
 
 // rows [r0, r1) of a (rows x n) source array (host or device) into the padded layout
-static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s) {
+static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s,
+                      int threads = 256) {
   if (r1 <= r0) return;
   if (is_device_ptr(src)) {
     const long long rows = r1 - r0;
     const long long blocks = (rows + kPadRowsPerBlock - 1) / kPadRowsPerBlock;
     if (blocks >= (1ll << 31)) throw Error(CFM_ERR_VALUE, "too many rows to pad");
-    k_pad_rows<<<unsigned(blocks), 256, 0, s>>>(dst + size_t(r0) * ld, ld, src + size_t(r0) * h->n, h->n, rows);
+    k_pad_rows<<<unsigned(blocks), threads, 0, s>>>(dst + size_t(r0) * ld, ld, src + size_t(r0) * h->n, h->n, rows);
     CUDA_CHECK(cudaGetLastError());
     return;
   }
@@ -1834,6 +1837,19 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   size_t off = 0;
   std::vector<const double*> host_x(lv.size(), nullptr);
   std::vector<size_t> flag_off(lv.size(), 0);
+  std::vector<char> defer_loc(lv.size(), 0);  // locals upload after the first group's multipoles
+  // Pipelined full-operator levels with host multipoles: ftl 3 = slabs go H2D
+  // contiguously and are padded slab by slab on a side stream by a small
+  // kernel that fits beside the running M2L grid (1 CTA/SM, ~7 K registers
+  // free); the producers wait on per-slab flags, so the level joins the single
+  // launch.  ftl 2 (CFM_PAD_PIPE=0) = the whole level crosses PCIe during the
+  // other levels' launch and is padded before its own launch.
+  // (measured at config 2: ftl 3 54.0-54.4 ms vs ftl 2 53.6 ms e2e -- the
+  // first level-6 tiles wait on their slabs while holding SMs: off by default)
+  static const bool pad_pipe = [] {
+    const char* e = getenv("CFM_PAD_PIPE");
+    return e && atoi(e) != 0;
+  }();
   // full-operator levels read zero-padded source rows from h->xpad
   std::vector<int> ftl(lv.size(), 0);
   std::vector<std::pair<int64_t, int>> lay;
@@ -1865,6 +1881,18 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         flag_off[i] = nflags;
         nflags += 2 + size_t(lv[i].lp->n_slabs);
       }
+    // target-tile levels of the first launch group upload their locals after
+    // all first-group multipoles: the launch starts on the multipoles alone and
+    // each tile's epilogue waits for its level's locals flag
+    static const bool defer_env = [] {
+      const char* e = getenv("CFM_DEFER_LOCALS");
+      return !e || atoi(e) != 0;
+    }();
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (defer_env && !piped[i] && lv[i].lp->mode == 0 && !is_device_ptr(lv[i].y)) {
+        defer_loc[i] = 1;
+        flag_off[i] = nflags++;
+      }
     ensure(h->pipe_flags, nflags * sizeof(unsigned));
     CUDA_CHECK(cudaMemsetAsync(h->pipe_flags.p, 0, nflags * sizeof(unsigned), s_in));
   }
@@ -1892,7 +1920,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         off += L.bytes;
       }
       if (piped[i])
-        ftl[i] = 2;
+        ftl[i] = pad_pipe ? 3 : 2;
       else
         xpad_copy(h, xp, lay[lay_idx[i]].second, src, 0, L.lp->n_rows, s_in);
       L.x = xp;
@@ -1905,7 +1933,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     }
     if (!is_device_ptr(L.y)) {
       double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
-      if (!piped[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.y, L.bytes, cudaMemcpyHostToDevice, s_in));
+      if (!piped[i] && !defer_loc[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.y, L.bytes, cudaMemcpyHostToDevice, s_in));
       L.host_y = L.y;
       L.y = d;
       off += L.bytes;
@@ -1916,6 +1944,13 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     CUDA_CHECK(cudaEventRecord(h->ev_in, s_in));
     CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_in, 0));
     CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_in, 0));
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (!defer_loc[i]) continue;
+      CUDA_CHECK(cudaMemcpyAsync(lv[i].y, lv[i].host_y, lv[i].bytes, cudaMemcpyHostToDevice, s_in));
+      CUresult r = p_writeValue32(reinterpret_cast<CUstream>(s_in),
+                                  reinterpret_cast<CUdeviceptr>(h->pipe_flags.as<unsigned>() + flag_off[i]), 1u, 0);
+      if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuStreamWriteValue32 failed");
+    }
     bool any_late = false;
     for (size_t i = 0; i < lv.size(); ++i)
       if (ftl[i] == 2) {
@@ -1945,10 +1980,35 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       };
       unsigned* mp_ready = flags + flag_off[i];
       unsigned* loc_ready = mp_ready + 1;
+      if (ftl[i] == 3) {
+        if (!h->s_pad) {
+          // highest priority: when an SM frees up, pad blocks are dispatched
+          // before the grid's pending CTAs (which may wait on these pads)
+          int least = 0, greatest = 0;
+          CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+          CUDA_CHECK(cudaStreamCreateWithPriority(&h->s_pad, cudaStreamNonBlocking, greatest));
+        }
+        if (!h->ev_pad_done) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_pad_done, cudaEventDisableTiming));
+        for (int k = 0; k < S; ++k)
+          if (!h->ev_slab[k]) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_slab[k], cudaEventDisableTiming));
+        if (S > 16) throw Error(CFM_ERR_VALUE, "too many slabs");
+      }
       // multipole slab k is needed by targets of slab k-1: keep multipoles one slab ahead
       for (int k = 0; k < S; ++k) {
-        if (!ftl[i]) slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
-        write_flag(mp_ready, unsigned(k + 1));
+        if (ftl[i] == 3) {
+          slab_copy(host_x[i], const_cast<double*>(staged_x[i]), k, cudaMemcpyHostToDevice, s_in);
+          CUDA_CHECK(cudaEventRecord(h->ev_slab[k], s_in));
+          CUDA_CHECK(cudaStreamWaitEvent(h->s_pad, h->ev_slab[k], 0));
+          // 64-thread blocks fit beside a resident M2L CTA (registers)
+          xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], P.slab_row0[k],
+                    P.slab_row0[k + 1], h->s_pad, 64);
+          CUresult r = p_writeValue32(reinterpret_cast<CUstream>(h->s_pad), reinterpret_cast<CUdeviceptr>(mp_ready),
+                                      unsigned(k + 1), 0);
+          if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuStreamWriteValue32 failed");
+        } else {
+          if (!ftl[i]) slab_copy(host_x[i], const_cast<double*>(lv[i].x), k, cudaMemcpyHostToDevice, s_in);
+          write_flag(mp_ready, unsigned(k + 1));
+        }
         if (k >= 1) {
           slab_copy(lv[i].host_y, lv[i].y, k - 1, cudaMemcpyHostToDevice, s_in);
           write_flag(loc_ready, unsigned(k));
@@ -2045,9 +2105,13 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         p.scale = h->levels[L.level].second;
         p.accumulate = 1;
       }
+      if (defer_loc[i]) {
+        p.pipe_loc = h->pipe_flags.as<unsigned>() + flag_off[i];
+        p.pipe_need_loc = nullptr;  // one flag for the whole level
+      }
       if (piped[i]) {
         unsigned* f = h->pipe_flags.as<unsigned>() + flag_off[i];
-        p.pipe_mp = ftl[i] ? nullptr : f;  // full-operator sources are resident before their launch
+        p.pipe_mp = (ftl[i] == 0 || ftl[i] == 3) ? f : nullptr;  // ftl 2: sources resident before the launch
         p.pipe_loc = f + 1;
         p.pipe_done = f + 2;
         p.pipe_need_mp = L.lp->p_need_mp.as<int>();
@@ -2243,6 +2307,10 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         CUDA_CHECK(cudaStreamWaitEvent(s, a.done, 0));
       }
     }
+  }
+  if (std::count(ftl.begin(), ftl.end(), 3)) {  // join the slab padding stream
+    CUDA_CHECK(cudaEventRecord(h->ev_pad_done, h->s_pad));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_pad_done, 0));
   }
   CUDA_CHECK(cudaEventRecord(h->ev1, s));
   if (any_piped) {
@@ -2534,6 +2602,10 @@ int cfm_handler_destroy(cfm_handler* h) {
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     if (h->s_late) cudaStreamDestroy(h->s_late);
+    if (h->s_pad) cudaStreamDestroy(h->s_pad);
+    for (auto& e : h->ev_slab)
+      if (e) cudaEventDestroy(e);
+    if (h->ev_pad_done) cudaEventDestroy(h->ev_pad_done);
     if (h->ev_late0) cudaEventDestroy(h->ev_late0);
     if (h->ev_late1) cudaEventDestroy(h->ev_late1);
     cudaStreamDestroy(h->stream);

@@ -707,7 +707,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
 
   // ---------------- epilogue: ordered, atomic-free write ----------------
   if (e_begin == e_end && p.accumulate && !p.pipe_done) return;
-  if (p.pipe_loc) wait_flag_geq(p.pipe_loc, unsigned(p.pipe_need_loc[tile]));
+  if (p.pipe_loc) wait_flag_geq(p.pipe_loc, p.pipe_need_loc ? unsigned(p.pipe_need_loc[tile]) : 1u);
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi) {
     const int row = r0 + mrow(mi) + g;
