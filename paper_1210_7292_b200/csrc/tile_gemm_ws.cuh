@@ -248,7 +248,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     if (lane != 0) return;
     static_assert(BN % 4 == 0 && LDA == LDB, "gather4 rows land with the A pitch");
     constexpr unsigned STAGE_TX = unsigned((BM * LDA + BN * LDB) * 8);
-    const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
+    const uint64_t pol_a = l2_policy_evict_last();
+    const uint64_t pol_b = (p.l2_hints & 4) ? l2_policy_evict_last() : l2_policy_evict_first();
     EntryInfo d;
     d.nchunks = 0;
     int e = next_live(e_begin, d);
@@ -268,8 +269,13 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         const int k0 = kc * KC;
         double* bs = Bs + s * BN * LDB;
         mbar_arrive_expect_tx(full + s, STAGE_TX);
-        if (p.l2_hints) {
+        // l2_hints bit 0: operator tiles evict_last; bit 1: sources evict_first;
+        // bit 2: sources evict_last (experiments; 0 = no policy)
+        if (p.l2_hints & 1)
           tma_load_2d_hint(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s, pol_a);
+        else
+          tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
+        if (p.l2_hints & 6) {
           if (p.b_block) {
             tma_load_2d_hint(bs, &p.tmap_b, k0, e * BN, full + s, pol_b);
           } else {
@@ -277,7 +283,6 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
             for (int j = 0; j < BN / 4; ++j) tma_gather4_hint(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s, pol_b);
           }
         } else {
-          tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
           if (p.b_block) {
             tma_load_2d(bs, &p.tmap_b, k0, e * BN, full + s);
           } else {
