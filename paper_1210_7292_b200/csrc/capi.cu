@@ -191,6 +191,7 @@ struct Group {
   CUtensorMap ts_vmap, ts_umap;  // box 36 x 128 over ts_v; box 20 x 128 over lrf_left
 };
 
+struct HybridPlan;
 struct LevelPlan {
   HostPlan hp;
   int dc = 1;
@@ -222,6 +223,17 @@ struct LevelPlan {
   DevBuf ts1_col, ts1_off, ts1_code, ts1_src, ts2_col, ts2_off, ts2_code, ts2_src;
   int64_t ts_segs = 0;  // stage-2 B rows (entries x 64): the stage-1 output in stage-2 order, 20 doubles each (4 zero)
   DevBuf ts_y, ts_map;  // ts_map: stage-1 segment -> its row in ts_y (-1: no pair needs it)
+  // hybrid (dense full-operator target tiles): the tiles that are less than
+  // half full -- the partial last tile of each boundary class of targets --
+  // go to a pair-mode sub-plan; device-resident applies run the remaining
+  // tiles + the sub-plan, host-pipelined applies the full tile plan
+  std::shared_ptr<HybridPlan> hyb;
+};
+
+struct HybridPlan {
+  HostPlan main;  // the kept target tiles
+  DevBuf tile_col, tile_off, entry_code, entry_src;
+  LevelPlan aux;  // pair-mode plan of the leftover targets
 };
 
 // Pair-mode levels of one homogeneous full-operator group merged into one
@@ -1098,6 +1110,101 @@ static void build_two_stage_plan(const Group& g, LevelPlan& lp) {
   lp.ts = true;
 }
 
+static bool full_mode(const Group& g, const LevelPlan& lp) { return g.kind == kDense && g.has_full && lp.dc == 1; }
+
+// Hybrid plans are opt-in (CFM_HYBRID=1): measured at config 2 the step
+// kernel drops 50.56 -> 50.28 ms but the extra per-level reductions take
+// 0.18 ms, net -0.1 ms.  Read at every plan build; a forced CFM_PLAN_MODE
+// disables it.
+static bool use_hybrid() {
+  const char* e = getenv("CFM_HYBRID");
+  return e && atoi(e) != 0 && !getenv("CFM_PLAN_MODE");
+}
+
+// Upload a pair-mode plan's device arrays (entries, reduction, filled columns).
+static void push_pair_plan(LevelPlan& lp) {
+  push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
+  upload(lp.r_tgt, lp.red.tgt);
+  upload(lp.r_off, lp.red.off);
+  upload(lp.r_frow, lp.red.frow);
+  const int64_t E = lp.hp.n_entries();
+  std::vector<unsigned char> nc(std::max<int64_t>(E, 1), 0);
+  for (int64_t e = 0; e < E; ++e)
+    for (int c = kBN - 1; c >= 0; --c)
+      if (lp.hp.entry_src[size_t(e) * kBN + c] >= 0) {
+        nc[e] = static_cast<unsigned char>(c + 1);
+        break;
+      }
+  upload(lp.entry_ncols, nc);
+}
+
+// Hybrid split of a dense full-operator target-tile plan (LevelPlan::hyb).
+static void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, const int64_t* tgt,
+                              const int64_t* off, const int64_t* src, const int16_t* codes,
+                              const std::array<int, kNumCodes>& key) {
+  const HostPlan& hp = lp.hp;
+  std::vector<char> leftover_tile(hp.n_tiles, 0);
+  std::vector<char> leftover_row(lp.n_rows, 0);
+  int64_t n_left = 0;
+  for (int64_t t = 0; t < hp.n_tiles; ++t) {
+    int64_t valid = 0;
+    const int64_t slots = int64_t(hp.tile_off[t + 1] - hp.tile_off[t]) * kBN;
+    for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e)
+      for (int c = 0; c < kBN; ++c) valid += hp.entry_src[size_t(e) * kBN + c] >= 0;
+    if (slots == 0 || 2 * valid >= slots) continue;
+    leftover_tile[t] = 1;
+    ++n_left;
+    for (int c = 0; c < kBN; ++c) {
+      const int v = hp.tile_col[size_t(t) * kBN + c];
+      if (v >= 0) leftover_row[v] = 1;
+    }
+  }
+  if (n_left == 0 || n_left == hp.n_tiles) return;
+  auto hy = std::make_shared<HybridPlan>();
+  HostPlan& mn = hy->main;
+  mn.bn = hp.bn;
+  mn.dc = hp.dc;
+  for (int64_t t = 0; t < hp.n_tiles; ++t) {
+    if (leftover_tile[t]) continue;
+    mn.tile_col.insert(mn.tile_col.end(), hp.tile_col.begin() + t * kBN, hp.tile_col.begin() + (t + 1) * kBN);
+    mn.tile_off.push_back(int(mn.entry_code.size()));
+    for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e) {
+      mn.entry_code.push_back(hp.entry_code[e]);
+      mn.entry_src.insert(mn.entry_src.end(), hp.entry_src.begin() + size_t(e) * kBN,
+                          hp.entry_src.begin() + size_t(e + 1) * kBN);
+    }
+    ++mn.n_tiles;
+  }
+  mn.tile_off.push_back(int(mn.entry_code.size()));
+  // leftover targets' far lists (CSR order kept) -> pair entries
+  std::vector<int64_t> t2, o2{0}, s2;
+  std::vector<int16_t> c2;
+  for (int64_t i = 0; i < n_targets; ++i) {
+    if (off[i + 1] <= off[i] || !leftover_row[tgt[i]]) continue;
+    t2.push_back(tgt[i]);
+    for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+      s2.push_back(src[q]);
+      c2.push_back(codes[q]);
+    }
+    o2.push_back(int64_t(s2.size()));
+  }
+  LevelPlan& ax = hy->aux;
+  const int nkp = round_up(h->n * h->f, kKC);
+  const int64_t e_est = int64_t(s2.size()) / kBN + 1;
+  int ept = std::max(1, std::min(16, int(2.5e7 / (2.0 * 128 * kBN * nkp))));
+  ept = std::min<int>(ept, int(std::max<int64_t>(1, e_est / (2 * 148))));
+  ax.hp = build_plan_pairs(int64_t(t2.size()), t2.data(), o2.data(), s2.data(), c2.data(), 1, key, lp.n_rows, ept,
+                           ax.red);
+  ax.mode = 1;
+  ax.dc = 1;
+  ax.n_rows = lp.n_rows;
+  push_pair_plan(ax);
+  static uint64_t hyb_gen = uint64_t(1) << 62;
+  ax.gen = ++hyb_gen;
+  push_plan(mn, hy->tile_col, hy->tile_off, hy->entry_code, hy->entry_src);
+  lp.hyb = std::move(hy);
+}
+
 static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
                             const int64_t* src, const int16_t* codes, int data_complex, int64_t n_rows) {
   Group& g = group_for_level(h, level);
@@ -1266,6 +1373,13 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     upload(lp.p_hi, hi);
   }
   if (g.kind == kLowRank && g.has_ts && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) build_two_stage_plan(g, lp);
+  if (use_hybrid() && full_mode(g, lp) && lp.mode == 0 && lp.hp.n_tiles > 0) {
+    try {
+      build_hybrid_plan(h, lp, n_targets, tgt, off, src, codes, key);
+    } catch (const PlanError& e) {
+      throw Error(e.code == 2 ? CFM_ERR_PRECOMPUTE : CFM_ERR_VALUE, e.what());
+    }
+  }
   static uint64_t plan_gen = 0;
   lp.gen = ++plan_gen;
   h->plans[level] = std::move(lp);
@@ -1286,7 +1400,6 @@ static int64_t launch_reduce(const LevelPlan& lp, const double* F, long long f_l
 }
 
 // ---- full-operator mode: sources as zero-padded rows (ld = group full.ld)
-static bool full_mode(const Group& g, const LevelPlan& lp) { return g.kind == kDense && g.has_full && lp.dc == 1; }
 
 // Reserve h->xpad for levels of (rows, ld) and return each level's offset (in
 // doubles); the padding columns are zeroed whenever the layout changes (rows
@@ -1397,6 +1510,24 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     }
     p.y = d_y; p.y_ld = row_ld; p.y_dc = dc;
     p.scale = scale; p.accumulate = 1;
+    if (lp.hyb && full_mode(g, lp)) {
+      // hybrid: the kept target tiles, then the leftover targets in pair mode
+      const HybridPlan& hy = *lp.hyb;
+      fill_plan(p, hy.tile_col, hy.tile_off, hy.entry_code, hy.entry_src, hy.main.n_tiles);
+      p.n_entries = hy.main.n_entries();
+      launches += launch_tiles(p, hy.main.n_tiles, s);
+      const LevelPlan& ax = hy.aux;
+      TileParams q = p;
+      fill_plan(q, ax.tile_col, ax.tile_off, ax.entry_code, ax.entry_src, ax.hp.n_tiles);
+      q.entry_ncols = ax.entry_ncols.as<unsigned char>();
+      q.n_entries = ax.hp.n_entries();
+      ensure(h->fbuf, size_t(ax.red.n_frows) * row_ld * sizeof(double));
+      q.y = h->fbuf.as<double>(); q.y_ld = row_ld; q.y_dc = dc;
+      q.scale = 1.0; q.accumulate = 0; q.pair_out = 1;
+      launches += launch_tiles(q, ax.hp.n_tiles, s);
+      launches += launch_reduce(ax, h->fbuf.as<double>(), row_ld, d_y, row_ld, int(row_ld), scale, s);
+      return launches;
+    }
     launches += launch_tiles(p, lp.hp.n_tiles, s);
     return launches;
   }
@@ -2025,6 +2156,32 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   bool all_dense = true;
   for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
   if (all_dense) {
+    // hybrid levels (LevelPlan::hyb, not host-pipelined): the kept tiles run as
+    // the level's segment, the leftover targets as an extra pair-mode "level"
+    // sharing the level's padded sources and locals (merged with the other
+    // pair-mode levels below)
+    std::vector<char> use_hyb(lv.size(), 0);
+    {
+      const size_t n_real = lv.size();
+      for (size_t i = 0; i < n_real; ++i) {
+        if (!lv[i].lp->hyb || ftl[i] != 1 || piped[i]) continue;
+        use_hyb[i] = 1;
+        Lv ax = lv[i];
+        ax.lp = &lv[i].lp->hyb->aux;
+        ax.host_y = nullptr;
+        ax.bytes = 0;
+        lv.push_back(ax);
+        ftl.push_back(1);
+        piped.push_back(0);
+        lay_idx.push_back(lay_idx[i]);
+        flag_off.push_back(0);
+        defer_loc.push_back(0);
+        copied_early.push_back(0);
+        staged_x.push_back(nullptr);
+        host_x.push_back(nullptr);
+        use_hyb.push_back(0);
+      }
+    }
     // one launch: target-mode levels accumulate into locals, pair-mode levels
     // write per-pair rows into their slice of fbuf, reduced right after
     // full-operator pair-mode levels of one group share one merged plan
@@ -2073,7 +2230,11 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       p.invtab = h->invtab.as<short>();
       p.zero_row = h->zeros.as<double>();
       fill_ops(p, g.dense, g.main);
-      fill_plan(p, L.lp->tile_col, L.lp->tile_off, L.lp->entry_code, L.lp->entry_src, L.lp->hp.n_tiles);
+      if (use_hyb[i])
+        fill_plan(p, L.lp->hyb->tile_col, L.lp->hyb->tile_off, L.lp->hyb->entry_code, L.lp->hyb->entry_src,
+                  L.lp->hyb->main.n_tiles);
+      else
+        fill_plan(p, L.lp->tile_col, L.lp->tile_off, L.lp->entry_code, L.lp->entry_src, L.lp->hp.n_tiles);
       {
         // timing experiments only (results are wrong): CFM_EXP=norow|nocol|noperm drops permutations
         static const char* exp = getenv("CFM_EXP");
@@ -2094,7 +2255,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       if (ftl[i]) {
         fill_full(p, h, g, L.x, L.lp->n_rows);
         if (L.lp->mode == 1) p.entry_ncols = L.lp->entry_ncols.as<unsigned char>();
-        p.n_entries = L.lp->hp.n_entries();
+        p.n_entries = use_hyb[i] ? L.lp->hyb->main.n_entries() : L.lp->hp.n_entries();
       }
       if (i > 0 && (ftl[i] != 0) != (ftl[0] != 0)) same_shape = false;
       if (L.lp->mode == 1) {
@@ -2122,7 +2283,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       if (nr >= 0 && (p.nr != nr)) same_shape = false;
       nr = p.nr;
       segs.push_back(p);
-      counts.push_back(merged_lv[i] ? 0 : L.lp->hp.n_tiles);  // merged levels run in the merged segment
+      counts.push_back(merged_lv[i] ? 0 : use_hyb[i] ? L.lp->hyb->main.n_tiles : L.lp->hp.n_tiles);  // merged levels run in the merged segment
     }
     const size_t merged_seg = segs.size();
     if (mp_plan) {

@@ -295,6 +295,43 @@ def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeyp
 
 
 @pytest.mark.gpu
+def test_hybrid_plan_matches_target_tiles(torch_cuda, monkeypatch):
+    """Opt-in hybrid plans (CFM_HYBRID=1): the less-than-half-full target tiles
+    of a full cube level go to a pair-mode sub-plan.  Per level (apply_planned)
+    and through apply_levels, the locals match the plain target-tile plan to
+    rounding and the oracle to <= 1e-12."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    order = 5
+    levels = [3, 4]
+    cells = {l: _full_level(l) for l in levels}
+    rng = np.random.default_rng(17)
+    mp = {l: torch.from_numpy(rng.uniform(-1, 1, (len(cells[l]), order**3))).cuda() for l in levels}
+    out = {}
+    for hyb in ("1", "0"):
+        monkeypatch.setenv("CFM_HYBRID", hyb)
+        h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+        h.precompute({l: full_far_field_vectors() for l in levels}, {l: 1.0 / (1 << l) for l in levels})
+        for l in levels:
+            h.plan_level_cells(l, cells[l])
+        loc = {l: torch.zeros_like(mp[l]) for l in levels}
+        h.apply_levels({l: (mp[l], loc[l]) for l in levels})
+        single = torch.zeros_like(mp[4])
+        h.apply_planned(4, mp[4], single)
+        assert torch.equal(single, loc[4])
+        out[hyb] = {l: loc[l].cpu().numpy() for l in levels}
+    for l in levels:
+        tgt, off, src, t = O.far_lists(cells[l], l)
+        orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+            {l: sorted({tuple(int(c) for c in v) for v in t})}, {l: 1.0 / (1 << l)})
+        ref = np.zeros(mp[l].shape)
+        orc.apply_fast(l, tgt, off, src, t, mp[l].cpu().numpy(), ref)
+        assert O.rel_l2(out["1"][l], ref) <= 1e-12
+        assert O.rel_l2(out["1"][l], out["0"][l]) <= 1e-14
+
+
+@pytest.mark.gpu
 def test_two_stage_skips_sparse_levels(torch_cuda, monkeypatch):
     """A sparse (sphere) level in target tiles keeps the fused low-rank kernel:
     the two-stage source GEMM would compute mostly unneeded class segments."""
