@@ -1112,13 +1112,13 @@ static void build_two_stage_plan(const Group& g, LevelPlan& lp) {
 
 static bool full_mode(const Group& g, const LevelPlan& lp) { return g.kind == kDense && g.has_full && lp.dc == 1; }
 
-// Hybrid plans are opt-in (CFM_HYBRID=1): measured at config 2 the step
-// kernel drops 50.56 -> 50.28 ms but the extra per-level reductions take
-// 0.18 ms, net -0.1 ms.  Read at every plan build; a forced CFM_PLAN_MODE
-// disables it.
+// Hybrid plans (CFM_HYBRID=0 disables): measured at config 2 the step kernel
+// drops 50.56 -> 50.28 ms; with all reductions of a step in one launch the
+// step goes 50.60 -> 50.41 ms.  Read at every plan build; a forced
+// CFM_PLAN_MODE disables it.
 static bool use_hybrid() {
   const char* e = getenv("CFM_HYBRID");
-  return e && atoi(e) != 0 && !getenv("CFM_PLAN_MODE");
+  return (!e || atoi(e) != 0) && !getenv("CFM_PLAN_MODE");
 }
 
 // Upload a pair-mode plan's device arrays (entries, reduction, filled columns).
@@ -2337,26 +2337,50 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     // launch groups: all levels at once, or -- copy pipeline with late
     // full-operator levels -- the other levels first while the late levels'
     // sources cross PCIe, then the late ones once padded on this stream
+    // all pair-mode reductions of the step in one launch (disjoint targets)
     auto reduce_pairs = [&](cudaStream_t rs) {
-    for (size_t i = 0; i < lv.size(); ++i) {
-      if (lv[i].lp->mode != 1 || reduced_inside[i]) continue;
-      const long long row_ld = (long long)h->n * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
-      if (merged_lv[i]) {
-        const size_t k = size_t(std::find(mlv.begin(), mlv.end(), i) - mlv.begin());
-        const int64_t nt = int64_t(mp_plan->red[k].tgt.size());
-        if (nt) {
-          k_pair_reduce<<<unsigned(nt), 128, 0, rs>>>(h->fbuf.as<double>(), row_ld, mp_plan->r_tgt[k].as<long long>(),
-                                                      mp_plan->r_off[k].as<long long>(), mp_plan->r_frow[k].as<int>(),
-                                                      nt, lv[i].y, row_ld, int(row_ld), h->levels[lv[i].level].second,
-                                                      1);
-          CUDA_CHECK(cudaGetLastError());
-          ++launches;
+      MultiReduce mr{};
+      long long blocks = 0;
+      auto flush = [&] {
+        if (mr.n == 0) return;
+        mr.start[mr.n] = blocks;
+        k_pair_reduce_multi<<<unsigned(blocks), 128, 0, rs>>>(mr);
+        CUDA_CHECK(cudaGetLastError());
+        ++launches;
+        mr = MultiReduce{};
+        blocks = 0;
+      };
+      for (size_t i = 0; i < lv.size(); ++i) {
+        if (lv[i].lp->mode != 1 || reduced_inside[i]) continue;
+        const long long row_ld = (long long)h->n * (lv[i].lp->dc == 2 || h->op_complex ? 2 : 1);
+        ReduceSeg r{};
+        if (merged_lv[i]) {
+          const size_t k = size_t(std::find(mlv.begin(), mlv.end(), i) - mlv.begin());
+          r.F = h->fbuf.as<double>();
+          r.tgt = mp_plan->r_tgt[k].as<long long>();
+          r.off = mp_plan->r_off[k].as<long long>();
+          r.frow = mp_plan->r_frow[k].as<int>();
+          r.n_tgt = int64_t(mp_plan->red[k].tgt.size());
+        } else {
+          const LevelPlan& P = *lv[i].lp;
+          r.F = h->fbuf.as<double>() + f_off[i];
+          r.tgt = P.r_tgt.as<long long>();
+          r.off = P.r_off.as<long long>();
+          r.frow = P.r_frow.as<int>();
+          r.n_tgt = int64_t(P.red.tgt.size());
         }
-        continue;
+        if (r.n_tgt == 0) continue;
+        r.f_ld = row_ld;
+        r.y = lv[i].y;
+        r.y_ld = row_ld;
+        r.len = int(row_ld);
+        r.scale = h->levels[lv[i].level].second;
+        if (mr.n == kMaxReduceSegs || blocks + r.n_tgt >= (1ll << 31)) flush();
+        mr.start[mr.n] = blocks;
+        mr.seg[mr.n++] = r;
+        blocks += r.n_tgt;
       }
-      launches += launch_reduce(*lv[i].lp, h->fbuf.as<double>() + f_off[i], row_ld, lv[i].y, row_ld, int(row_ld),
-                                h->levels[lv[i].level].second, rs);
-    }
+      flush();
     };
     bool reduced_early = false;
     // The late group runs on a side stream: it starts (pad, then launch) as

@@ -296,7 +296,7 @@ def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeyp
 
 @pytest.mark.gpu
 def test_hybrid_plan_matches_target_tiles(torch_cuda, monkeypatch):
-    """Opt-in hybrid plans (CFM_HYBRID=1): the less-than-half-full target tiles
+    """Hybrid plans (default; CFM_HYBRID=0 disables): the less-than-half-full target tiles
     of a full cube level go to a pair-mode sub-plan.  Per level (apply_planned)
     and through apply_levels, the locals match the plain target-tile plan to
     rounding and the oracle to <= 1e-12."""
