@@ -1164,8 +1164,16 @@ static void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, 
   HostPlan& mn = hy->main;
   mn.bn = hp.bn;
   mn.dc = hp.dc;
-  for (int64_t t = 0; t < hp.n_tiles; ++t) {
-    if (leftover_tile[t]) continue;
+  // kept tiles longest first (row order kept among equally long tiles): the
+  // shorter boundary-class tiles run last and fill the launch's tail (this
+  // plan only serves device-resident applies, which need no row order)
+  std::vector<int64_t> kept;
+  for (int64_t t = 0; t < hp.n_tiles; ++t)
+    if (!leftover_tile[t]) kept.push_back(t);
+  std::stable_sort(kept.begin(), kept.end(), [&](int64_t a, int64_t b) {
+    return hp.tile_off[a + 1] - hp.tile_off[a] > hp.tile_off[b + 1] - hp.tile_off[b];
+  });
+  for (int64_t t : kept) {
     mn.tile_col.insert(mn.tile_col.end(), hp.tile_col.begin() + t * kBN, hp.tile_col.begin() + (t + 1) * kBN);
     mn.tile_off.push_back(int(mn.entry_code.size()));
     for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e) {
