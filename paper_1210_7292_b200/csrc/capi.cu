@@ -231,7 +231,8 @@ struct LevelPlan {
 };
 
 struct HybridPlan {
-  HostPlan main;  // the kept target tiles
+  HostPlan main;  // the kept target tiles, longest first
+  int64_t n_long = 0;  // leading tiles with the most entries (the rest run at the end of a launch)
   DevBuf tile_col, tile_off, entry_code, entry_src;
   LevelPlan aux;  // pair-mode plan of the leftover targets
 };
@@ -585,8 +586,7 @@ static int64_t launch_multi(const std::vector<TileParams>& segs, const std::vect
     if (counts[i] == 0) continue;
     if (mp.n_seg == kMaxSegments) throw Error(CFM_ERR_VALUE, "too many levels in one launch");
     mp.start[mp.n_seg] = int(total);
-    mp.seg[mp.n_seg] = segs[i];
-    mp.seg[mp.n_seg].tile_base = 0;
+    mp.seg[mp.n_seg] = segs[i];  // (tile_base: first tile of the segment in its plan)
     total += counts[i];
     ++mp.n_seg;
   }
@@ -1173,6 +1173,8 @@ static void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, 
   std::stable_sort(kept.begin(), kept.end(), [&](int64_t a, int64_t b) {
     return hp.tile_off[a + 1] - hp.tile_off[a] > hp.tile_off[b + 1] - hp.tile_off[b];
   });
+  const int max_e = kept.empty() ? 0 : hp.tile_off[kept[0] + 1] - hp.tile_off[kept[0]];
+  for (int64_t t : kept) hy->n_long += (hp.tile_off[t + 1] - hp.tile_off[t]) * 10 >= max_e * 9;
   for (int64_t t : kept) {
     mn.tile_col.insert(mn.tile_col.end(), hp.tile_col.begin() + t * kBN, hp.tile_col.begin() + (t + 1) * kBN);
     mn.tile_off.push_back(int(mn.entry_code.size()));
@@ -2291,7 +2293,20 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       if (nr >= 0 && (p.nr != nr)) same_shape = false;
       nr = p.nr;
       segs.push_back(p);
-      counts.push_back(merged_lv[i] ? 0 : use_hyb[i] ? L.lp->hyb->main.n_tiles : L.lp->hp.n_tiles);  // merged levels run in the merged segment
+      counts.push_back(merged_lv[i] ? 0 : use_hyb[i] ? L.lp->hyb->n_long : L.lp->hp.n_tiles);  // merged levels run in the merged segment
+    }
+    // the shorter tiles of hybrid levels: extra segments launched after all
+    // levels' long tiles (longest-processing-time order fills the launch tail)
+    std::vector<size_t> short_segs;
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (!use_hyb[i]) continue;
+      const int64_t n_short = lv[i].lp->hyb->main.n_tiles - lv[i].lp->hyb->n_long;
+      if (n_short <= 0) continue;
+      TileParams p = segs[i];
+      p.tile_base = int(lv[i].lp->hyb->n_long);
+      short_segs.push_back(segs.size());
+      segs.push_back(p);
+      counts.push_back(n_short);
     }
     const size_t merged_seg = segs.size();
     if (mp_plan) {
@@ -2396,9 +2411,10 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     // group's tail leaves idle (levels are independent in M2L); the caller's
     // stream joins it after the launches.
     std::vector<std::vector<size_t>> groups(2);
-    if (mp_plan) groups[0].push_back(merged_seg);
     for (size_t i = 0; i < lv.size(); ++i)
       if (counts[i]) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
+    for (size_t k : short_segs) groups[0].push_back(k);
+    if (mp_plan) groups[0].push_back(merged_seg);
     static const bool late_side = [] {
       const char* e = getenv("CFM_LATE_STREAM");
       return !e || atoi(e) != 0;
@@ -2430,7 +2446,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         }
         launches += launch_multi(sub, sub_counts, sg);
       } else {
-        for (size_t i : grp) launches += launch_tiles(segs[i], counts[i], sg);
+        for (size_t i : grp) launches += launch_range(segs[i], segs[i].tile_base, counts[i], sg);
       }
       static const bool early_d2h = [] {
         const char* e = getenv("CFM_EARLY_D2H");
