@@ -373,6 +373,15 @@ static bool ft_pipe_enabled() {
   return v != 0;
 }
 
+// CFM_KTAIL=0: the last k-step of l = 5 operators as a DMMA over zero padding (A/B)
+static bool ktail_enabled() {
+  static const int v = [] {
+    const char* e = getenv("CFM_KTAIL");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
 static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaStream_t s) {
   // grid_tiles = (tiles, row blocks) -> one CTA per (tile, row block), row blocks fastest
@@ -411,6 +420,7 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
         mp.seg[i].l2_hints = hints_env;
         const int rem = mp.seg[i].nk % KC;
         mp.seg[i].ft_pipe = ft_pipe_enabled() && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
+        mp.seg[i].ft_ktail = mp.seg[i].ft_pipe && rem == KC - 3 && !mp.seg[i].op_rows && ktail_enabled();
       }
       auto kf = q.y_map ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
                 : skip    ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>

@@ -93,6 +93,7 @@ struct TileParams {
   long long n_entries;               // host-side hint: entries of the plan (kernel choice)
   long long x_rows;                  // full-operator mode: rows of the padded source array x
   int ft_pipe;                       // full-operator target tiles: flat pipelined consumer loop
+  int ft_ktail;                      // flat loop: an entry's last k-step has one real column (DFMA rank-1)
   // two-stage low-rank mode (full-operator kernels):
   int code_is_op;   // entry codes are operator ids (no code tables, identity permutations)
   int ft_opshift;   // operator id o -> A block row (o >> ft_opshift) * ft_rows, column (o & mask) * ft_colseg

@@ -519,9 +519,27 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
                 for (int h = 0; h < 2; ++h)
                   dmap[sg][nj][h] = __ldg(p.y_map + (ve + ncol(nj) + 2 * tg + h) * 8 + ((r0 + mrow(2 * sg)) >> 4));
           }
+          // an entry's last k-step with one real column (p.ft_ktail: nk % KC ==
+          // KC - 3, e.g. l = 5) runs as a rank-1 DFMA update instead of a DMMA
+          // over 3 zero columns: DMMA and DFMA share the FP64 pipe
+          // (tools/fp64_mix.cu), so this drops 3/4 of that step's pipe time
+          const bool ktail = p.ft_ktail && (qq + 1) % nch == 0;
 #pragma unroll
           for (int kk = 0; kk < KC; kk += 8) {
-            load(a1, b1, s, kk + 4);
+            double bt[NTL];
+            if (kk + 8 == KC && ktail) {
+              const double* as = As + s * BM * LDA + g * LDA + kk + 4;
+              const double* bs = Bs + s * BN * LDB + 2 * tg * LDB + kk + 4;
+#pragma unroll
+              for (int mi = 0; mi < MT; ++mi) a1[mi] = as[mrow(mi) * LDA];
+#pragma unroll
+              for (int nj = 0; nj < NTL; ++nj) {
+                b1[nj] = bs[ncol(nj) * LDB];
+                bt[nj] = bs[(ncol(nj) + 1) * LDB];
+              }
+            } else {
+              load(a1, b1, s, kk + 4);
+            }
             mma(a0, b0);
             if (kk + 8 < KC) {
               load(a0, b0, s, kk + 8);
@@ -530,7 +548,17 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
               mbar_wait(full + s1, ((qq + 1) / STAGES) & 1);
               load(a0, b0, s1, 0);
             }
-            mma(a1, b1);
+            if (kk + 8 == KC && ktail) {
+#pragma unroll
+              for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+                for (int nj = 0; nj < NTL; ++nj) {
+                  acc[mi][nj][0] = fma(a1[mi], b1[nj], acc[mi][nj][0]);
+                  acc[mi][nj][1] = fma(a1[mi], bt[nj], acc[mi][nj][1]);
+                }
+            } else {
+              mma(a1, b1);
+            }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + s);
