@@ -374,12 +374,10 @@ static bool ft_pipe_enabled() {
 }
 
 // CFM_KTAIL=0: the last k-step of l = 5 operators as a DMMA over zero padding (A/B)
+// (read at every launch, so a test can compare both in one process)
 static bool ktail_enabled() {
-  static const int v = [] {
-    const char* e = getenv("CFM_KTAIL");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
+  const char* e = getenv("CFM_KTAIL");
+  return !e || atoi(e) != 0;
 }
 
 template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SKIP>
@@ -1357,8 +1355,16 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     np_.tile_off[nt] = int(np_.entry_code.size());
     lp.hp = std::move(np_);
     push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
-    // slabs of ~32K rows (at most 16)
-    const int S = int(std::min<int64_t>(16, std::max<int64_t>(1, n_rows / 32768)));
+    // slabs of ~32K rows (at most 16); CFM_SLAB_ROWS / CFM_MAX_SLABS for experiments
+    static const int64_t slab_rows = [] {
+      const char* e = getenv("CFM_SLAB_ROWS");
+      return e ? std::max<int64_t>(1024, atoll(e)) : int64_t(32768);
+    }();
+    static const int64_t max_slabs = [] {
+      const char* e = getenv("CFM_MAX_SLABS");
+      return e ? std::max<int64_t>(2, atoll(e)) : int64_t(16);
+    }();
+    const int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
     lp.n_slabs = S;
     lp.slab_row0.resize(S + 1);
     for (int k = 0; k <= S; ++k) lp.slab_row0[k] = n_rows * k / S;
@@ -2140,9 +2146,9 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
           CUDA_CHECK(cudaStreamCreateWithPriority(&h->s_pad, cudaStreamNonBlocking, greatest));
         }
         if (!h->ev_pad_done) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_pad_done, cudaEventDisableTiming));
+        if (S > 16) throw Error(CFM_ERR_VALUE, "too many slabs");
         for (int k = 0; k < S; ++k)
           if (!h->ev_slab[k]) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_slab[k], cudaEventDisableTiming));
-        if (S > 16) throw Error(CFM_ERR_VALUE, "too many slabs");
       }
       // multipole slab k is needed by targets of slab k-1: keep multipoles one slab ahead
       for (int k = 0; k < S; ++k) {
@@ -3215,7 +3221,7 @@ int cfm_classify_count_device(int device, int level, int64_t n_cells, const int3
     const unsigned nb = unsigned((n_cells + 255) / 256);
     if (n_cells) {
       k_grid_scatter<<<nb, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>());
-      const unsigned nbw = unsigned((n_cells * 32 + 255) / 256);
+      const unsigned nbw = classify_warp_blocks<false>(n_cells, device);
       k_classify_warp<false><<<nbw, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>(), reinterpret_cast<int*>(counts.p),
                                                  nullptr, nullptr, nullptr);
       CUDA_CHECK(cudaGetLastError());
@@ -3253,7 +3259,7 @@ int cfm_classify_fill_device(int device, int level, int64_t n_cells, const int32
     const unsigned nb = unsigned((n_cells + 255) / 256);
     if (n_cells) {
       k_grid_scatter<<<nb, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>());
-      const unsigned nbw = unsigned((n_cells * 32 + 255) / 256);
+      const unsigned nbw = classify_warp_blocks<true>(n_cells, device);
       k_classify_warp<true><<<nbw, 256, 0, s>>>(ijk, n_cells, S, grid.as<int>(), nullptr,
                                                 reinterpret_cast<const long long*>(offsets_dev), src_dev, code_dev);
       CUDA_CHECK(cudaGetLastError());

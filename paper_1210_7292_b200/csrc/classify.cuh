@@ -85,41 +85,90 @@ __global__ void k_classify(const int* __restrict__ ijk, long long n, int S, cons
 // Warp per target: lane l handles candidates l, l+32, ... (216 in source-ijk
 // order); kept pairs are compacted in candidate order with ballot/popc, so
 // the output order is the reference's.  Counts (FILL=false) or writes (FILL).
+//
+// t = ijk_target - ijk_source depends only on the target's parity class
+// ((x&1, y&1, z&1): x - bx = (x&1) + 2) and the candidate index, so the far
+// test and the t-code come from a per-CTA shared table (8 classes x 216) and
+// the occupancy-grid offset of a candidate from a second one; the CTAs are
+// persistent (grid-stride over targets) so the tables are built once per CTA.
+// Interior targets (whole 6^3 candidate box inside the level) skip the bounds
+// tests.  All 7 rounds' grid loads are issued before the first ballot.
+constexpr int kCandPad = 224;  // 7 x 32 lanes >= 216 candidates
+
 template <bool FILL>
-__global__ void k_classify_warp(const int* __restrict__ ijk, long long n, int S, const int* __restrict__ grid,
-                                int* __restrict__ counts, const long long* __restrict__ off,
-                                int* __restrict__ src_out, int16_t* __restrict__ code_out) {
-  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(256) k_classify_warp(const int* __restrict__ ijk, long long n, int S,
+                                                       const int* __restrict__ grid, int* __restrict__ counts,
+                                                       const long long* __restrict__ off, int* __restrict__ src_out,
+                                                       int16_t* __restrict__ code_out) {
+  __shared__ int16_t s_code[8 * kCandPad];  // -1: near (or padding)
+  __shared__ int s_goff[kCandPad];          // (dx * S + dy) * S + dz
+  __shared__ int s_dxyz[kCandPad];          // dx | dy << 8 | dz << 16
+  for (int i = threadIdx.x; i < 8 * kCandPad; i += blockDim.x) {
+    const int p = i / kCandPad, c = i % kCandPad;
+    int16_t v = -1;
+    if (c < 216) {
+      const int t0 = ((p >> 2) & 1) + 2 - c / 36, t1 = ((p >> 1) & 1) + 2 - (c / 6) % 6, t2 = (p & 1) + 2 - c % 6;
+      if (is_far(t0, t1, t2)) v = int16_t(tcode(t0, t1, t2));
+    }
+    s_code[i] = v;
+  }
+  for (int c = threadIdx.x; c < kCandPad; c += blockDim.x) {
+    const int dx = c < 216 ? c / 36 : 0, dy = c < 216 ? (c / 6) % 6 : 0, dz = c < 216 ? c % 6 : 0;
+    s_goff[c] = (dx * S + dy) * S + dz;
+    s_dxyz[c] = dx | dy << 8 | dz << 16;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  if (w >= n) return;
-  const int x = __ldg(ijk + 3 * w), y = __ldg(ijk + 3 * w + 1), z = __ldg(ijk + 3 * w + 2);
-  const int bx = 2 * ((x >> 1) - 1), by = 2 * ((y >> 1) - 1), bz = 2 * ((z >> 1) - 1);
-  long long base = FILL ? off[w] : 0;
-  int total = 0;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
+    const int x = __ldg(ijk + 3 * w), y = __ldg(ijk + 3 * w + 1), z = __ldg(ijk + 3 * w + 2);
+    const int bx = 2 * ((x >> 1) - 1), by = 2 * ((y >> 1) - 1), bz = 2 * ((z >> 1) - 1);
+    const int16_t* codes = s_code + ((x & 1) << 2 | (y & 1) << 1 | (z & 1)) * kCandPad;
+    const bool interior = bx >= 0 && by >= 0 && bz >= 0 && bx + 6 <= S && by + 6 <= S && bz + 6 <= S;
+    const long long pbase = ((long long)bx * S + by) * S + bz;
+    int rows[7], cds[7];
 #pragma unroll
-  for (int r = 0; r < 7; ++r) {  // 7 x 32 >= 216 candidates
-    const int cidx = r * 32 + lane;
-    bool keep = false;
-    int row = -1, code = 0;
-    if (cidx < 216) {
-      const int sx = bx + cidx / 36, sy = by + (cidx / 6) % 6, sz = bz + cidx % 6;
-      const int t0 = x - sx, t1 = y - sy, t2 = z - sz;
-      if (sx >= 0 && sx < S && sy >= 0 && sy < S && sz >= 0 && sz < S && is_far(t0, t1, t2)) {
-        row = __ldg(grid + ((long long)sx * S + sy) * S + sz);
-        keep = row >= 0;
-        code = tcode(t0, t1, t2);
+    for (int r = 0; r < 7; ++r) {
+      const int c = r * 32 + lane;
+      cds[r] = codes[c];
+      rows[r] = -1;
+      if (cds[r] >= 0) {
+        bool ok = true;
+        if (!interior) {
+          const int d = s_dxyz[c];
+          const int sx = bx + (d & 255), sy = by + ((d >> 8) & 255), sz = bz + (d >> 16);
+          ok = sx >= 0 && sx < S && sy >= 0 && sy < S && sz >= 0 && sz < S;
+        }
+        if (ok) rows[r] = __ldg(grid + pbase + s_goff[c]);
       }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (FILL && keep) {
-      const long long pos = base + __popc(m & ((1u << lane) - 1u));
-      src_out[pos] = row;
-      code_out[pos] = int16_t(code);
+    long long base = FILL ? __ldg(off + w) : 0;
+    int total = 0;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+      const bool keep = rows[r] >= 0;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (FILL && keep) {
+        const long long pos = base + __popc(m & ((1u << lane) - 1u));
+        src_out[pos] = rows[r];
+        code_out[pos] = int16_t(cds[r]);
+      }
+      base += __popc(m);
+      total += __popc(m);
     }
-    base += __popc(m);
-    total += __popc(m);
+    if (!FILL && lane == 0) counts[w] = total;
   }
-  if (!FILL && lane == 0) counts[w] = total;
+}
+
+// Persistent grid for k_classify_warp: one wave of resident CTAs (by the
+// occupancy calculator; the fill kernel's 44 registers allow 5 x 256 threads/SM).
+template <bool FILL>
+inline unsigned classify_warp_blocks(long long n_cells, int device) {
+  int sms = 148, per_sm = 4;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_classify_warp<FILL>, 256, 0);
+  const long long need = (n_cells + 7) / 8, cap = (long long)sms * (per_sm > 0 ? per_sm : 1);
+  return unsigned(need < cap ? need : cap);
 }
 
 }  // namespace cfm

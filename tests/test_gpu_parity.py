@@ -257,6 +257,37 @@ def test_full_level_against_oracle(torch_cuda, order, level, variant):
 
 
 @pytest.mark.gpu
+def test_rank1_ktail_matches_padded_dmma(torch_cuda, monkeypatch):
+    """l = 5 (125 = 3 x 32 + 29 inner columns): the last k-step of every entry
+    runs as a rank-1 DFMA update (default) instead of a DMMA over three zero
+    columns (CFM_KTAIL=0).  Full level 5: both agree to rounding and match the
+    oracle at the full-rank tolerance."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    order, level = 5, 5
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    h.precompute({level: transfers}, lw)
+    h.plan_level_cells(level, cells)
+    mp = torch.from_numpy(np.random.default_rng(11).uniform(-1, 1, (len(cells), order**3))).cuda()
+    out = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("CFM_KTAIL", v)
+        loc = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
+        h.apply_planned(level, mp, loc)
+        out[v] = loc.cpu().numpy()
+    orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute({level: transfers}, lw)
+    ref = np.zeros(mp.shape)
+    orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert O.rel_l2(out["1"], out["0"]) <= 1e-14
+    assert O.rel_l2(out["1"], ref) <= TOL["nablk"]
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("variant", ["iablk", "iasym", "ia"])
 def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeypatch):
     """Dense low-rank levels run as two stages (Y = V_t^H x per source and class
