@@ -1365,15 +1365,32 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
       return e ? std::max<int64_t>(2, atoll(e)) : int64_t(16);
     }();
     const int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
-    lp.n_slabs = S;
-    lp.slab_row0.resize(S + 1);
-    for (int k = 0; k <= S; ++k) lp.slab_row0[k] = n_rows * k / S;
-    auto slab_of = [&](int64_t row) { return int(std::min<int64_t>(S - 1, row * S / std::max<int64_t>(n_rows, 1))); };
+    // the last slab's download cannot start before the kernel's last wave
+    // ends: split it into halves, quarters, eighths (CFM_SLAB_TAIL=0: uniform)
+    static const bool slab_tail = [] {
+      const char* e = getenv("CFM_SLAB_TAIL");
+      return !e || atoi(e) != 0;
+    }();
+    lp.slab_row0.clear();
+    for (int k = 0; k < S; ++k) lp.slab_row0.push_back(n_rows * k / S);
+    if (slab_tail && S >= 2 && S + 3 <= 16 && n_rows / S >= 8 * 1024) {
+      const int64_t a = n_rows * (S - 1) / S, len = n_rows - a;
+      lp.slab_row0.push_back(a + len / 2);
+      lp.slab_row0.push_back(a + len / 2 + len / 4);
+      lp.slab_row0.push_back(a + len / 2 + len / 4 + len / 8);
+    }
+    lp.slab_row0.push_back(n_rows);
+    const int S_all = int(lp.slab_row0.size()) - 1;
+    lp.n_slabs = S_all;
+    auto slab_of = [&](int64_t row) {
+      const auto it = std::upper_bound(lp.slab_row0.begin(), lp.slab_row0.end(), row);
+      return int(std::min<int64_t>(S_all - 1, std::max<int64_t>(0, (it - lp.slab_row0.begin()) - 1)));
+    };
     std::vector<int> need_mp(nt, 0), need_loc(nt, 0), lo(nt, 0), hi(nt, -1);
-    lp.slab_expected.assign(S, 0);
+    lp.slab_expected.assign(S_all, 0);
     const int nrb = (group_for_level(h, level).dense.rows + 127) / 128;
     for (int64_t t = 0; t < nt; ++t) {
-      int l = S, hh = -1, m = 0;
+      int l = S_all, hh = -1, m = 0;
       for (int c = 0; c < kBN; ++c) {
         const int v = lp.hp.tile_col[size_t(t) * kBN + c];
         if (v < 0) continue;

@@ -505,15 +505,20 @@ def test_sharded_plans_equal_single_gpu(torch_cuda, golden, mode, monkeypatch):
     assert torch.equal(out, ref)
 
 
-def test_copy_pipeline_host_buffers_bitwise(torch_cuda):
+@pytest.mark.parametrize("order", [4, 5])
+def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, monkeypatch):
     """Host buffers on a large level go through the slab copy pipeline
     (multipole/locals slabs streamed while the kernel runs, gated by device
-    flags); the result must equal the device-resident path bitwise, including
-    accumulation into non-zero host locals."""
+    flags; l = 4 streams both, l = 5 -- full-operator mode -- streams the
+    locals, with the last slab split in halves/quarters/eighths); the result
+    must equal the device-resident path bitwise, including accumulation into
+    non-zero host locals.  (Hybrid plans off: the device-resident reference
+    then runs the same row-ordered tile plan as the pipelined call.)"""
     torch = torch_cuda
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
-    level, order = 6, 4
+    monkeypatch.setenv("CFM_HYBRID", "0")
+    level = 6
     cells = _full_level(level)
     full = O.full_far_field()
     h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
