@@ -1367,17 +1367,19 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
     const int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
     // the last slab's download cannot start before the kernel's last wave
     // ends: split it into halves, quarters, eighths (CFM_SLAB_TAIL=0: uniform)
-    static const bool slab_tail = [] {
+    static const int slab_tail = [] {
       const char* e = getenv("CFM_SLAB_TAIL");
-      return !e || atoi(e) != 0;
+      return e ? std::max(0, atoi(e)) : 3;
     }();
     lp.slab_row0.clear();
     for (int k = 0; k < S; ++k) lp.slab_row0.push_back(n_rows * k / S);
-    if (slab_tail && S >= 2 && S + 3 <= 16 && n_rows / S >= 8 * 1024) {
+    if (S >= 2) {
       const int64_t a = n_rows * (S - 1) / S, len = n_rows - a;
-      lp.slab_row0.push_back(a + len / 2);
-      lp.slab_row0.push_back(a + len / 2 + len / 4);
-      lp.slab_row0.push_back(a + len / 2 + len / 4 + len / 8);
+      int64_t r = a;
+      for (int d = 1; d <= slab_tail && S + d <= 16 && (len >> d) >= 1024; ++d) {
+        r += len >> d;
+        lp.slab_row0.push_back(r);
+      }
     }
     lp.slab_row0.push_back(n_rows);
     const int S_all = int(lp.slab_row0.size()) - 1;
