@@ -189,6 +189,7 @@ struct Group {
   int ts_ntr = 0;
   OpStack ts_v;                  // 8 * ts_nb blocks of 128 rows x n
   CUtensorMap ts_vmap, ts_umap;  // box 36 x 128 over ts_v; box 20 x 128 over lrf_left
+  DevBuf ts_ksteps;              // per stage-2 entry code 2k + j: k-steps holding rank columns (ceil(w / 4))
 };
 
 struct HybridPlan;
@@ -935,6 +936,15 @@ static void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int
   };
   encode(&g.ts_vmap, g.ts_v, (long long)8 * nb * 128, kKC + 4);
   encode(&g.ts_umap, g.lrf_left, (long long)n_transfers * n, 16 + 4);
+  // stage 2 skips the k-steps of a 16-wide rank segment past the rank: their
+  // U_t columns and Y rows are exact zeros, so the sums are unchanged
+  std::vector<int> ks(size_t(2) * n_transfers, 0);
+  for (int k = 0; k < n_transfers; ++k)
+    for (int j = 0; j < 2; ++j) {
+      const int w = std::min(16, std::max(0, rk[k] - 16 * j));
+      ks[size_t(2) * k + j] = (w + 3) / 4;
+    }
+  upload(g.ts_ksteps, ks);
   g.has_ts = true;
 }
 
@@ -1623,6 +1633,10 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     b.scale = scale; b.accumulate = 1; b.pair_out = 0;
     b.zero_row = h->zeros.as<double>();
     b.n_entries = lp.ts2.n_entries();
+    {
+      const char* e = getenv("CFM_SEG_KSKIP");  // 0: run all 4 k-steps of every segment (A/B)
+      b.seg_ksteps = (!e || atoi(e) != 0) ? g.ts_ksteps.as<int>() : nullptr;
+    }
     static const bool seg_pair = [] {
       const char* e = getenv("CFM_SEG_PAIR");
       return !e || atoi(e) != 0;

@@ -98,15 +98,32 @@ __global__ void __launch_bounds__(12 * 32, 1) seg_pair_gemm_kernel(const __grid_
 #pragma unroll
       for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
   };
+  // live k-steps of a stage (bit 4h + j: k-step j of its entry h): a rank
+  // segment narrower than 16 leaves exact zeros in its last k-steps, and the
+  // odd last entry pairs with an all-zero sub-tile -- those DMMAs are skipped
+  auto stage_mask = [&](int q) -> unsigned {
+    unsigned m = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = e_begin + 2 * q + h;
+      if (e < e_end) {
+        const int ks = p.seg_ksteps ? __ldg(p.seg_ksteps + __ldg(p.entry_code + e)) : 4;
+        m |= ((1u << ks) - 1u) << (4 * h);
+      }
+    }
+    return m;
+  };
   if (n_pairs > 0) {
     mbar_wait(full, 0);
     load(a0, b0, 0, 0);
+    unsigned msk = stage_mask(0);
     for (int q = 0; q < n_pairs; ++q) {
       const int s = q % STAGES;
+      const unsigned msk_next = q + 1 < n_pairs ? stage_mask(q + 1) : 0u;
 #pragma unroll
       for (int kk = 0; kk < 32; kk += 8) {
         load(a1, b1, s, kk + 4);
-        mma(a0, b0);
+        if ((msk >> (kk >> 2)) & 1u) mma(a0, b0);
         if (kk + 8 < 32) {
           load(a0, b0, s, kk + 8);
         } else if (q + 1 < n_pairs) {
@@ -114,8 +131,9 @@ __global__ void __launch_bounds__(12 * 32, 1) seg_pair_gemm_kernel(const __grid_
           mbar_wait(full + s1, ((q + 1) / STAGES) & 1);
           load(a0, b0, s1, 0);
         }
-        mma(a1, b1);
+        if ((msk >> ((kk + 4) >> 2)) & 1u) mma(a1, b1);
       }
+      msk = msk_next;
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
     }

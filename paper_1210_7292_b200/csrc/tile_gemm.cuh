@@ -101,6 +101,7 @@ struct TileParams {
   int y_seg;        // pair-mode output rows written as 16-row segments at this pitch (0: contiguous rows)
   const int* y_map; // with y_seg: segment (v * 8 + row / 16) -> destination segment index (-1: not needed)
   int b_block;      // B of entry e = rows [e * BN, e * BN + BN) of tmap_b (one 2-D box; no gathers)
+  const int* seg_ksteps;  // seg_pair_gemm_kernel: live k-steps (0..4) per entry code (null: all 4)
   int l2_hints;     // TMA copies with L2 policies: operators evict_last, sources evict_first
   CUtensorMap tmap_a;
   // full-operator mode: 2-D map over the padded sources (x_ld x x_rows), box

@@ -326,6 +326,37 @@ def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeyp
 
 
 @pytest.mark.gpu
+def test_two_stage_kstep_skip_bitwise(torch_cuda, monkeypatch):
+    """Stage 2 skips the k-steps of a rank segment past the rank (their U_t
+    columns and Y rows are exact zeros): bitwise equal to running all four
+    k-steps of every segment (CFM_SEG_KSKIP=0), and within 1e-10 of the oracle."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    order, level, eps = 5, 5, 1e-5
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: transfers}, lw)
+    h.plan_level_cells(level, cells)
+    assert h.plan_stats(level)["two_stage"]
+    mp = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, (len(cells), order**3))).cuda()
+    out = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("CFM_SEG_KSKIP", v)
+        loc = torch.full(mp.shape, 0.25, dtype=torch.float64, device="cuda")
+        h.apply_planned(level, mp, loc)
+        out[v] = loc
+    assert torch.equal(out["1"], out["0"])
+    orc = O.OracleM2L("iablk", O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    ref = np.full(mp.shape, 0.25)
+    orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert O.rel_l2(out["1"].cpu().numpy(), ref) <= 1e-10
+
+
+@pytest.mark.gpu
 def test_hybrid_plan_matches_target_tiles(torch_cuda, monkeypatch):
     """Hybrid plans (default; CFM_HYBRID=0 disables): the less-than-half-full target tiles
     of a full cube level go to a pair-mode sub-plan.  Per level (apply_planned)
