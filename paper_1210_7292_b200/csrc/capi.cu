@@ -2308,6 +2308,8 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         if (exp && !strcmp(exp, "zfillA")) p.debug = 8;
         if (exp && !strcmp(exp, "zfillB")) p.debug = 16;
         if (exp && !strcmp(exp, "zfillAB")) p.debug = 24;
+        if (exp && !strcmp(exp, "noB")) p.debug = 32;
+        if (exp && !strcmp(exp, "noA")) p.debug = 64;
       }
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;

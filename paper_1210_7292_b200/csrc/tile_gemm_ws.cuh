@@ -268,6 +268,21 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
         const int k0 = kc * KC;
         double* bs = Bs + s * BN * LDB;
+        if (p.debug & (4 | 32 | 64)) {
+          // timing experiments only (stale stage data): debug 4 no copies,
+          // 32 no source gathers, 64 no operator tile
+          if (p.debug & 4) {
+            mbar_arrive(full + s);
+          } else if (p.debug & 32) {
+            mbar_arrive_expect_tx(full + s, unsigned(BM * LDA * 8));
+            tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
+          } else {
+            mbar_arrive_expect_tx(full + s, unsigned(BN * LDB * 8));
+#pragma unroll
+            for (int j = 0; j < BN / 4; ++j) tma_gather4(bs + 4 * j * LDB, &p.tmap_b, k0, rows[j], full + s);
+          }
+          continue;
+        }
         mbar_arrive_expect_tx(full + s, STAGE_TX);
         // l2_hints bit 0: operator tiles evict_last; bit 1: sources evict_first;
         // bit 2: sources evict_last (experiments; 0 = no policy)
