@@ -1374,7 +1374,12 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
       const char* e = getenv("CFM_MAX_SLABS");
       return e ? std::max<int64_t>(2, atoll(e)) : int64_t(16);
     }();
-    const int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
+    static const int64_t min_rows = [] {  // levels with fewer rows are not host-pipelined
+      const char* e = getenv("CFM_PIPE_MIN_ROWS");
+      return e ? atoll(e) : int64_t(0);
+    }();
+    int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
+    if (min_rows > 0) S = n_rows >= min_rows ? std::max(S, 2) : 1;
     // the last slab's download cannot start before the kernel's last wave
     // ends: split it into halves, quarters, eighths (CFM_SLAB_TAIL=0: uniform)
     static const int slab_tail = [] {
