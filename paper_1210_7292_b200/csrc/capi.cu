@@ -374,6 +374,15 @@ static bool ft_pipe_enabled() {
   return v != 0;
 }
 
+// CFM_EARLY_TGT_D2H=0: first-group target-tile levels download after the whole call
+static bool early_tgt_d2h() {
+  static const bool v = [] {
+    const char* e = getenv("CFM_EARLY_TGT_D2H");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+
 // CFM_KTAIL=0: the last k-step of l = 5 operators as a DMMA over zero padding (A/B)
 // (read at every launch, so a test can compare both in one process)
 static bool ktail_enabled() {
@@ -2229,6 +2238,10 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       const size_t n_real = lv.size();
       for (size_t i = 0; i < n_real; ++i) {
         if (!lv[i].lp->hyb || ftl[i] != 1 || piped[i]) continue;
+        // host locals next to a host-pipelined level: the plain tile plan, so
+        // the level's locals are final when the first launch ends and go back
+        // while the late group runs (no pair reduction after the launch)
+        if (any_piped && lv[i].host_y && early_tgt_d2h()) continue;
         use_hyb[i] = 1;
         Lv ax = lv[i];
         ax.lp = &lv[i].lp->hyb->aux;
@@ -2520,6 +2533,22 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
             CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
             copied_early[i] = 1;
           }
+      }
+      if (gi == 0 && side && !early_d2h && early_tgt_d2h()) {
+        // target-tile levels of the first group (no pair reduction pending):
+        // their locals download while the late group runs
+        bool any = false;
+        for (size_t i = 0; i < lv.size(); ++i)
+          any = any || (!piped[i] && lv[i].host_y && lv[i].lp->mode == 0 && !use_hyb[i]);
+        if (any) {
+          CUDA_CHECK(cudaEventRecord(h->ev_out, s));
+          CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_out, 0));
+          for (size_t i = 0; i < lv.size(); ++i)
+            if (!piped[i] && lv[i].host_y && lv[i].lp->mode == 0 && !use_hyb[i]) {
+              CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
+              copied_early[i] = 1;
+            }
+        }
       }
       if (gi == 1 && side) {
         CUDA_CHECK(cudaEventRecord(h->ev_late1, sg));

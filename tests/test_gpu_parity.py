@@ -541,38 +541,34 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, monkeypatch):
     """Host buffers on a large level go through the slab copy pipeline
     (multipole/locals slabs streamed while the kernel runs, gated by device
     flags; l = 4 streams both, l = 5 -- full-operator mode -- streams the
-    locals, with the last slab split in halves/quarters/eighths); the result
-    must equal the device-resident path bitwise, including accumulation into
-    non-zero host locals.  (Hybrid plans off: the device-resident reference
-    then runs the same row-ordered tile plan as the pipelined call.)"""
+    locals, with the last slab split in halves/quarters/eighths, and the
+    first launch group's target-tile level 4 downloads while level 6 still
+    runs); the result must equal the device-resident path bitwise, including
+    accumulation into non-zero host locals.  (Hybrid plans off: the
+    device-resident reference then runs the same row-ordered tile plans as the
+    pipelined call.)"""
     torch = torch_cuda
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
     monkeypatch.setenv("CFM_HYBRID", "0")
-    level = 6
-    cells = _full_level(level)
+    lv = (3, 4, 6)
+    cells = {l: _full_level(l) for l in lv}
     full = O.full_far_field()
     h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
-    h.precompute({3: full, level: full}, {3: 1.0 / 8, level: 1.0 / 64})
-    st = h.plan_level_cells(level, cells)
-    small = _full_level(3)
-    h.plan_level_cells(3, small)
+    h.precompute({l: full for l in lv}, {l: 1.0 / (1 << l) for l in lv})
+    st = {l: h.plan_level_cells(l, cells[l]) for l in lv}
     rng = np.random.default_rng(9)
-    mp6 = rng.uniform(-1, 1, (len(cells), order**3))
-    loc6 = rng.uniform(-1, 1, mp6.shape)
-    mp3 = rng.uniform(-1, 1, (len(small), order**3))
-    loc3 = rng.uniform(-1, 1, mp3.shape)
-    ref6 = torch.from_numpy(loc6.copy()).cuda()
-    ref3 = torch.from_numpy(loc3.copy()).cuda()
-    h.apply_levels({level: (torch.from_numpy(mp6).cuda(), ref6), 3: (torch.from_numpy(mp3).cuda(), ref3)})
-    pin6 = torch.from_numpy(loc6.copy()).pin_memory()
-    pin3 = torch.from_numpy(loc3.copy()).pin_memory()
+    mp = {l: rng.uniform(-1, 1, (len(cells[l]), order**3)) for l in lv}
+    loc = {l: rng.uniform(-1, 1, mp[l].shape) for l in lv}
+    ref = {l: torch.from_numpy(loc[l].copy()).cuda() for l in lv}
+    h.apply_levels({l: (torch.from_numpy(mp[l]).cuda(), ref[l]) for l in lv})
+    pin = {l: torch.from_numpy(loc[l].copy()).pin_memory() for l in lv}
     for _ in range(2):  # twice: flags and counters must reset between calls
-        a6, a3 = pin6.numpy().copy(), pin3.numpy().copy()
-        h.apply_levels({level: (mp6, a6), 3: (mp3, a3)})
-        assert np.array_equal(a6, ref6.cpu().numpy())
-        assert np.array_equal(a3, ref3.cpu().numpy())
-    assert st["pairs"] == (6 * 64 - 8) ** 3 - (3 * 64 - 2) ** 3
+        a = {l: pin[l].numpy().copy() for l in lv}
+        h.apply_levels({l: (mp[l], a[l]) for l in lv})
+        for l in lv:
+            assert np.array_equal(a[l], ref[l].cpu().numpy()), l
+    assert st[6]["pairs"] == (6 * 64 - 8) ** 3 - (3 * 64 - 2) ** 3
 
 
 @pytest.mark.parametrize("case", ["cfg1", "helm", "lapcplx", "sphere9", "sphere_lists"])
