@@ -92,7 +92,11 @@ __global__ void k_classify(const int* __restrict__ ijk, long long n, int S, cons
 // the occupancy-grid offset of a candidate from a second one; the CTAs are
 // persistent (grid-stride over targets) so the tables are built once per CTA.
 // Interior targets (whole 6^3 candidate box inside the level) skip the bounds
-// tests.  All 7 rounds' grid loads are issued before the first ballot.
+// tests.  The 8 children of a parent share the candidate box: the first
+// occupied sibling's warp reads the box's occupancy once (7 loads per lane)
+// and emits the lists of every occupied sibling; the other siblings' warps
+// stop after one 8-lane lookup.  Output positions come from each target's own
+// offset, so the lists are the same as per-target enumeration.
 constexpr int kCandPad = 224;  // 7 x 32 lanes >= 216 candidates
 
 template <bool FILL>
@@ -122,17 +126,27 @@ __global__ void __launch_bounds__(256) k_classify_warp(const int* __restrict__ i
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
     const int x = __ldg(ijk + 3 * w), y = __ldg(ijk + 3 * w + 1), z = __ldg(ijk + 3 * w + 2);
-    const int bx = 2 * ((x >> 1) - 1), by = 2 * ((y >> 1) - 1), bz = 2 * ((z >> 1) - 1);
-    const int16_t* codes = s_code + ((x & 1) << 2 | (y & 1) << 1 | (z & 1)) * kCandPad;
+    // the 8 siblings share the parent's 6^3 candidate box: the occupied
+    // sibling with the lowest child index (x&1, y&1, z&1) handles all of them
+    // and reads the candidates' occupancy once
+    const int px = x >> 1, py = y >> 1, pz = z >> 1;
+    int sib = -1;
+    if (lane < 8) {
+      const int cx = 2 * px + (lane >> 2), cy = 2 * py + ((lane >> 1) & 1), cz = 2 * pz + (lane & 1);
+      if (cx < S && cy < S && cz < S) sib = __ldg(grid + ((long long)cx * S + cy) * S + cz);
+    }
+    const unsigned occ = __ballot_sync(0xffffffffu, sib >= 0) & 0xffu;
+    const int me = (x & 1) << 2 | (y & 1) << 1 | (z & 1);
+    if (occ & ((1u << me) - 1u)) continue;
+    const int bx = 2 * (px - 1), by = 2 * (py - 1), bz = 2 * (pz - 1);
     const bool interior = bx >= 0 && by >= 0 && bz >= 0 && bx + 6 <= S && by + 6 <= S && bz + 6 <= S;
     const long long pbase = ((long long)bx * S + by) * S + bz;
-    int rows[7], cds[7];
+    int rows[7];
 #pragma unroll
     for (int r = 0; r < 7; ++r) {
       const int c = r * 32 + lane;
-      cds[r] = codes[c];
       rows[r] = -1;
-      if (cds[r] >= 0) {
+      if (c < 216) {
         bool ok = true;
         if (!interior) {
           const int d = s_dxyz[c];
@@ -142,21 +156,27 @@ __global__ void __launch_bounds__(256) k_classify_warp(const int* __restrict__ i
         if (ok) rows[r] = __ldg(grid + pbase + s_goff[c]);
       }
     }
-    long long base = FILL ? __ldg(off + w) : 0;
-    int total = 0;
+    for (unsigned m = occ; m; m &= m - 1u) {
+      const int l = __ffs(m) - 1;
+      const int trow = __shfl_sync(0xffffffffu, sib, l);
+      const int16_t* codes = s_code + l * kCandPad;
+      long long base = FILL ? __ldg(off + trow) : 0;
+      int total = 0;
 #pragma unroll
-    for (int r = 0; r < 7; ++r) {
-      const bool keep = rows[r] >= 0;
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (FILL && keep) {
-        const long long pos = base + __popc(m & ((1u << lane) - 1u));
-        src_out[pos] = rows[r];
-        code_out[pos] = int16_t(cds[r]);
+      for (int r = 0; r < 7; ++r) {
+        const int cd = codes[r * 32 + lane];
+        const bool keep = cd >= 0 && rows[r] >= 0;
+        const unsigned bm = __ballot_sync(0xffffffffu, keep);
+        if (FILL && keep) {
+          const long long pos = base + __popc(bm & ((1u << lane) - 1u));
+          src_out[pos] = rows[r];
+          code_out[pos] = int16_t(cd);
+        }
+        base += __popc(bm);
+        total += __popc(bm);
       }
-      base += __popc(m);
-      total += __popc(m);
+      if (!FILL && lane == 0) counts[trow] = total;
     }
-    if (!FILL && lane == 0) counts[w] = total;
   }
 }
 

@@ -972,3 +972,60 @@ def test_full_operator_edge_cases(torch_cuda, monkeypatch):
     h.apply_levels(host)
     for lvl in levels:
         assert np.array_equal(host[lvl][1], ref[lvl].cpu().numpy())
+
+
+def _shell_cells(level):
+    side = 1 << level
+    c = _full_level(level).astype(np.float64)
+    r = np.linalg.norm((c + 0.5) / side - 0.5, axis=1)
+    return _full_level(level)[np.abs(r - 0.4) < 1.5 / side]
+
+
+@pytest.mark.parametrize("case", ["cube4", "sparse5", "shell6"])
+def test_device_classifier_bit_exact(torch_cuda, case):
+    """cfm_classify_count_device / cfm_classify_fill_device (the device far
+    lists of B200FmmPlan and the bench's classifier line; one warp per
+    occupied sibling group) against the oracle's restatement of
+    build_interaction_lists: per target the same source rows in the same
+    order and the same t codes, bit for bit; empty lists included."""
+    import ctypes
+
+    torch = torch_cuda
+    from paper_1210_7292_b200 import _native
+
+    if case == "cube4":
+        level, cells = 4, _full_level(4)
+    elif case == "sparse5":
+        level = 5
+        cells = _full_level(5)
+        cells = cells[np.random.default_rng(3).random(len(cells)) < 0.25]
+    else:
+        level, cells = 6, _shell_cells(6)
+    cells = np.ascontiguousarray(cells.astype(np.int32))
+    n = len(cells)
+    lib = _native.load()
+    d = torch.from_numpy(cells).cuda()
+    offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    tot = ctypes.c_int64()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _native.check(lib.cfm_classify_count_device(0, level, n, d.data_ptr(), offs.data_ptr(), ctypes.byref(tot), st))
+    src = torch.empty(max(tot.value, 1), dtype=torch.int32, device="cuda")
+    code = torch.empty(max(tot.value, 1), dtype=torch.int16, device="cuda")
+    _native.check(lib.cfm_classify_fill_device(0, level, n, d.data_ptr(), offs.data_ptr(), src.data_ptr(),
+                                               code.data_ptr(), st))
+    torch.cuda.synchronize()
+    offs, src, code = offs.cpu().numpy(), src.cpu().numpy()[: tot.value], code.cpu().numpy()[: tot.value]
+    tgt, o_off, o_src, o_t = O.far_lists(cells, level)
+    counts = np.zeros(n, np.int64)
+    counts[tgt] = np.diff(o_off)
+    assert tot.value == o_off[-1]
+    assert np.array_equal(np.diff(offs), counts)
+    ref_src = np.zeros(tot.value, np.int64)
+    ref_code = np.zeros(tot.value, np.int64)
+    for k, i in enumerate(tgt):
+        a, b = offs[i], offs[i + 1]
+        ref_src[a:b] = o_src[o_off[k]:o_off[k + 1]]
+        tt = o_t[o_off[k]:o_off[k + 1]]
+        ref_code[a:b] = (tt[:, 0] + 3) * 49 + (tt[:, 1] + 3) * 7 + (tt[:, 2] + 3)
+    assert np.array_equal(src.astype(np.int64), ref_src)
+    assert np.array_equal(code.astype(np.int64), ref_code)
