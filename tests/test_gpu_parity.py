@@ -536,8 +536,8 @@ def test_sharded_plans_equal_single_gpu(torch_cuda, golden, mode, monkeypatch):
     assert torch.equal(out, ref)
 
 
-@pytest.mark.parametrize("order", [4, 5])
-def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, monkeypatch):
+@pytest.mark.parametrize("order,hybrid", [(4, "0"), (5, "0"), (5, "1")])
+def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, hybrid, monkeypatch):
     """Host buffers on a large level go through the slab copy pipeline
     (multipole/locals slabs streamed while the kernel runs, gated by device
     flags; l = 4 streams both, l = 5 -- full-operator mode -- streams the
@@ -546,11 +546,13 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, monkeypatch):
     runs); the result must equal the device-resident path bitwise, including
     accumulation into non-zero host locals.  (Hybrid plans off: the
     device-resident reference then runs the same row-ordered tile plans as the
-    pipelined call.)"""
+    pipelined call.  With hybrid plans on -- the bench's e2e setting -- the
+    device-resident reference runs hybrid plans for levels 4 and 6, so the
+    pipelined result agrees to rounding instead.)"""
     torch = torch_cuda
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
-    monkeypatch.setenv("CFM_HYBRID", "0")
+    monkeypatch.setenv("CFM_HYBRID", hybrid)
     lv = (3, 4, 6)
     cells = {l: _full_level(l) for l in lv}
     full = O.full_far_field()
@@ -567,7 +569,11 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, monkeypatch):
         a = {l: pin[l].numpy().copy() for l in lv}
         h.apply_levels({l: (mp[l], a[l]) for l in lv})
         for l in lv:
-            assert np.array_equal(a[l], ref[l].cpu().numpy()), l
+            r = ref[l].cpu().numpy()
+            if hybrid == "0":
+                assert np.array_equal(a[l], r), l
+            else:
+                assert O.rel_l2(a[l], r) <= 1e-14, l
     assert st[6]["pairs"] == (6 * 64 - 8) ** 3 - (3 * 64 - 2) ** 3
 
 
