@@ -1498,28 +1498,63 @@ static std::vector<size_t> xpad_layout(cfm_handler* h, const std::vector<std::pa
 // pitched device-to-device cudaMemcpy2D, measured at ~1.5 ms for config 2's
 // 262 MB level 6 (this kernel: ~0.1 ms).
 constexpr int kPadRowsPerBlock = 16;
-__global__ void __launch_bounds__(256) k_pad_rows(double* __restrict__ dst, int ld, const double* __restrict__ src,
-                                                  int n, long long rows) {
-  const long long r0 = (long long)blockIdx.x * kPadRowsPerBlock;
-  const int nr = int(rows - r0 < kPadRowsPerBlock ? rows - r0 : kPadRowsPerBlock);
-  const double* sb = src + r0 * n;
-  double* db = dst + r0 * ld;
-  for (int j = threadIdx.x; j < nr * ld; j += blockDim.x) {
-    const int r = j / ld, k = j - r * ld;
-    db[j] = k < n ? __ldcs(sb + (long long)r * n + k) : 0.0;
+// Zero-padded source rows for the full-operator TMA path: rows of n doubles
+// -> rows of ld doubles.  Several arrays (the levels of a step) in one launch;
+// a warp copies whole rows (coalesced 256-B loads and stores, no division).
+struct PadJob {
+  double* dst;
+  const double* src;
+  long long rows;
+  long long blk0;  // first block of this job
+  int ld, n;
+};
+constexpr int kMaxPadJobs = 8;
+struct PadJobs {
+  PadJob j[kMaxPadJobs];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) k_pad_rows(const PadJobs jobs) {
+  int q = 0;
+  while (q + 1 < jobs.n && (long long)blockIdx.x >= jobs.j[q + 1].blk0) ++q;
+  const PadJob& J = jobs.j[q];
+  const long long r0 = ((long long)blockIdx.x - J.blk0) * kPadRowsPerBlock;
+  const int nr = int(J.rows - r0 < kPadRowsPerBlock ? J.rows - r0 : kPadRowsPerBlock);
+  const int lane = threadIdx.x & 31;
+  for (int r = threadIdx.x >> 5; r < nr; r += blockDim.x >> 5) {
+    const double* sr = J.src + (r0 + r) * J.n;
+    double* dr = J.dst + (r0 + r) * J.ld;
+    for (int k = lane; k < J.ld; k += 32) dr[k] = k < J.n ? __ldcs(sr + k) : 0.0;
+  }
+}
+
+static void launch_pads(const std::vector<PadJob>& in, cudaStream_t s, int threads = 256) {
+  for (size_t a = 0; a < in.size(); a += kMaxPadJobs) {
+    PadJobs jobs{};
+    long long blocks = 0;
+    for (size_t b = a; b < in.size() && b < a + kMaxPadJobs; ++b) {
+      PadJob J = in[b];
+      J.blk0 = blocks;
+      blocks += (J.rows + kPadRowsPerBlock - 1) / kPadRowsPerBlock;
+      jobs.j[jobs.n++] = J;
+    }
+    if (blocks == 0) continue;
+    if (blocks >= (1ll << 31)) throw Error(CFM_ERR_VALUE, "too many rows to pad");
+    k_pad_rows<<<unsigned(blocks), threads, 0, s>>>(jobs);
+    CUDA_CHECK(cudaGetLastError());
   }
 }
 
 // rows [r0, r1) of a (rows x n) source array (host or device) into the padded layout
 static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s,
-                      int threads = 256) {
+                      int threads = 256, std::vector<PadJob>* batch = nullptr) {
   if (r1 <= r0) return;
   if (is_device_ptr(src)) {
-    const long long rows = r1 - r0;
-    const long long blocks = (rows + kPadRowsPerBlock - 1) / kPadRowsPerBlock;
-    if (blocks >= (1ll << 31)) throw Error(CFM_ERR_VALUE, "too many rows to pad");
-    k_pad_rows<<<unsigned(blocks), threads, 0, s>>>(dst + size_t(r0) * ld, ld, src + size_t(r0) * h->n, h->n, rows);
-    CUDA_CHECK(cudaGetLastError());
+    const PadJob J{dst + size_t(r0) * ld, src + size_t(r0) * h->n, (long long)(r1 - r0), 0, ld, h->n};
+    if (batch)
+      batch->push_back(J);
+    else
+      launch_pads({J}, s, threads);
     return;
   }
   CUDA_CHECK(cudaMemcpy2DAsync(dst + size_t(r0) * ld, size_t(ld) * sizeof(double), src + size_t(r0) * h->n,
@@ -2102,6 +2137,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   }
   std::vector<size_t> xoff;
   std::vector<const double*> staged_x(lv.size(), nullptr);
+  std::vector<PadJob> pad_batch;  // the levels' source padding, one launch after the loop
   if (!lay.empty()) xoff = xpad_layout(h, lay, s_in);
   for (size_t i = 0; i < lv.size(); ++i) {
     auto& L = lv[i];
@@ -2126,7 +2162,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       if (piped[i])
         ftl[i] = pad_pipe ? 3 : 2;
       else
-        xpad_copy(h, xp, lay[lay_idx[i]].second, src, 0, L.lp->n_rows, s_in);
+        xpad_copy(h, xp, lay[lay_idx[i]].second, src, 0, L.lp->n_rows, s_in, 256, &pad_batch);
       L.x = xp;
     } else if (!is_device_ptr(L.x)) {
       double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
@@ -2143,6 +2179,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       off += L.bytes;
     }
   }
+  launch_pads(pad_batch, s_in);
   if (any_piped) {
     // the kernel may start once the non-pipelined levels and the zeroed flags are in
     CUDA_CHECK(cudaEventRecord(h->ev_in, s_in));
