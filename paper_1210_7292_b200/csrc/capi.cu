@@ -287,6 +287,8 @@ struct cfm_handler {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_late = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_prev = nullptr, ev_x = nullptr;
   cudaEvent_t ev_late0 = nullptr, ev_late1 = nullptr;
+  cudaStream_t s_mid = nullptr;  // middle launch group (e2e): its sources cross PCIe during the first launch
+  cudaEvent_t ev_mid = nullptr, ev_mid1 = nullptr;
   cudaStream_t s_pad = nullptr;  // pads pipelined full-operator slabs beside the running grid
   cudaEvent_t ev_slab[16] = {}, ev_pad_done = nullptr;
   cudaEvent_t ev_last = nullptr;  // end of the previous apply's work
@@ -372,6 +374,26 @@ static bool ft_pipe_enabled() {
     return e ? atoi(e) : 1;
   }();
   return v != 0;
+}
+
+// CFM_LATE_STREAM=0: later launch groups on the caller's stream, after the first
+static bool use_late_stream() {
+  static const bool v = [] {
+    const char* e = getenv("CFM_LATE_STREAM");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+
+// CFM_MID_GROUP=0: with host buffers next to a pipelined level, the largest
+// other target-tile level stays in the first launch (its upload then delays
+// the first launch; with the middle group it crosses PCIe during that launch)
+static bool mid_group_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("CFM_MID_GROUP");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
 }
 
 // CFM_EARLY_TGT_D2H=0: first-group target-tile levels download after the whole call
@@ -2135,6 +2157,18 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     ensure(h->pipe_flags, nflags * sizeof(unsigned));
     CUDA_CHECK(cudaMemsetAsync(h->pipe_flags.p, 0, nflags * sizeof(unsigned), s_in));
   }
+  // middle launch group (ftl 4): the largest other host-buffer target-tile
+  // full-operator level uploads after the first group's data, is padded on
+  // its own stream and launched behind the first group (filling its tail)
+  std::vector<char> mid(lv.size(), 0);
+  if (any_piped && mid_group_enabled() && use_late_stream()) {
+    size_t best = lv.size();
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (ftl[i] == 1 && !piped[i] && lv[i].lp->mode == 0 && !is_device_ptr(lv[i].x) && !is_device_ptr(lv[i].y) &&
+          lv[i].lp->n_rows >= 16384 && (best == lv.size() || lv[i].lp->n_rows > lv[best].lp->n_rows))
+        best = i;
+    if (best < lv.size()) mid[best] = 1;
+  }
   std::vector<size_t> xoff;
   std::vector<const double*> staged_x(lv.size(), nullptr);
   std::vector<PadJob> pad_batch;  // the levels' source padding, one launch after the loop
@@ -2155,12 +2189,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         double* d = reinterpret_cast<double*>(static_cast<char*>(h->x_stage.p) + off);
         host_x[i] = L.x;
         staged_x[i] = d;
-        if (!piped[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s_in));
+        if (!piped[i] && !mid[i]) CUDA_CHECK(cudaMemcpyAsync(d, L.x, L.bytes, cudaMemcpyHostToDevice, s_in));
         src = d;
         off += L.bytes;
       }
       if (piped[i])
         ftl[i] = pad_pipe ? 3 : 2;
+      else if (mid[i])
+        ftl[i] = 4;  // uploaded after the first group's data, padded before its own launch
       else
         xpad_copy(h, xp, lay[lay_idx[i]].second, src, 0, L.lp->n_rows, s_in, 256, &pad_batch);
       L.x = xp;
@@ -2185,6 +2221,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     CUDA_CHECK(cudaEventRecord(h->ev_in, s_in));
     CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_in, 0));
     CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_in, 0));
+    if (std::count(ftl.begin(), ftl.end(), 4)) {
+      for (size_t i = 0; i < lv.size(); ++i)
+        if (ftl[i] == 4)
+          CUDA_CHECK(cudaMemcpyAsync(const_cast<double*>(staged_x[i]), host_x[i], lv[i].bytes, cudaMemcpyHostToDevice,
+                                     s_in));
+      if (!h->ev_mid) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_mid, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventRecord(h->ev_mid, s_in));
+    }
     for (size_t i = 0; i < lv.size(); ++i) {
       if (!defer_loc[i]) continue;
       CUDA_CHECK(cudaMemcpyAsync(lv[i].y, lv[i].host_y, lv[i].bytes, cudaMemcpyHostToDevice, s_in));
@@ -2516,28 +2560,38 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
     // soon as its sources are in and its CTAs fill the SMs that the first
     // group's tail leaves idle (levels are independent in M2L); the caller's
     // stream joins it after the launches.
-    std::vector<std::vector<size_t>> groups(2);
+    // Groups: 0 = first launch, 1 = middle (ftl 4, e2e only), 2 = late (ftl 2).
+    std::vector<std::vector<size_t>> groups(3);
     for (size_t i = 0; i < lv.size(); ++i)
-      if (counts[i]) groups[ftl[i] == 2 ? 1 : 0].push_back(i);
+      if (counts[i]) groups[ftl[i] == 2 ? 2 : ftl[i] == 4 ? 1 : 0].push_back(i);
     for (size_t k : short_segs) groups[0].push_back(k);
     if (mp_plan) groups[0].push_back(merged_seg);
-    static const bool late_side = [] {
-      const char* e = getenv("CFM_LATE_STREAM");
-      return !e || atoi(e) != 0;
-    }();
-    const bool side = late_side && !groups[0].empty() && !groups[1].empty();
+    const bool side = use_late_stream() && !groups[0].empty() && (!groups[1].empty() || !groups[2].empty());
     if (side) {
       if (!h->s_late) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_late, cudaStreamNonBlocking));
       if (!h->ev_late0) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_late0, cudaEventDisableTiming));
       if (!h->ev_late1) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_late1, cudaEventDisableTiming));
       CUDA_CHECK(cudaEventRecord(h->ev_late0, s));  // everything this call (and earlier ones) queued so far
       CUDA_CHECK(cudaStreamWaitEvent(h->s_late, h->ev_late0, 0));
+      if (!groups[1].empty()) {
+        if (!h->s_mid) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_mid, cudaStreamNonBlocking));
+        if (!h->ev_mid1) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_mid1, cudaEventDisableTiming));
+        CUDA_CHECK(cudaStreamWaitEvent(h->s_mid, h->ev_late0, 0));
+      }
     }
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       const auto& grp = groups[gi];
       if (grp.empty()) continue;
       cudaStream_t sg = s;
       if (gi == 1) {
+        if (side) sg = h->s_mid;
+        CUDA_CHECK(cudaStreamWaitEvent(sg, h->ev_mid, 0));
+        std::vector<PadJob> pj;
+        for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
+                                       lv[i].lp->n_rows, sg, 256, &pj);
+        launch_pads(pj, sg);
+      }
+      if (gi == 2) {
         if (side) sg = h->s_late;
         CUDA_CHECK(cudaStreamWaitEvent(sg, h->ev_x, 0));
         for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
@@ -2566,7 +2620,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         CUDA_CHECK(cudaEventRecord(h->ev_out, s));
         CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_out, 0));
         for (size_t i = 0; i < lv.size(); ++i)
-          if (!piped[i] && lv[i].host_y) {
+          if (!piped[i] && lv[i].host_y && ftl[i] != 4) {
             CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
             copied_early[i] = 1;
           }
@@ -2576,18 +2630,32 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         // their locals download while the late group runs
         bool any = false;
         for (size_t i = 0; i < lv.size(); ++i)
-          any = any || (!piped[i] && lv[i].host_y && lv[i].lp->mode == 0 && !use_hyb[i]);
+          any = any || (!piped[i] && lv[i].host_y && lv[i].lp->mode == 0 && !use_hyb[i] && ftl[i] != 4);
         if (any) {
           CUDA_CHECK(cudaEventRecord(h->ev_out, s));
           CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_out, 0));
           for (size_t i = 0; i < lv.size(); ++i)
-            if (!piped[i] && lv[i].host_y && lv[i].lp->mode == 0 && !use_hyb[i]) {
+            if (!piped[i] && lv[i].host_y && lv[i].lp->mode == 0 && !use_hyb[i] && ftl[i] != 4) {
               CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
               copied_early[i] = 1;
             }
         }
       }
       if (gi == 1 && side) {
+        // the middle group's locals (target tiles, no pair reduction) go back
+        // while the late group runs
+        CUDA_CHECK(cudaEventRecord(h->ev_mid1, sg));
+        CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_mid1, 0));
+        if (early_tgt_d2h()) {
+          CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_mid1, 0));
+          for (size_t i : grp)
+            if (i < copied_early.size() && lv[i].host_y && lv[i].lp->mode == 0) {
+              CUDA_CHECK(cudaMemcpyAsync(lv[i].host_y, lv[i].y, lv[i].bytes, cudaMemcpyDeviceToHost, h->s_d2h));
+              copied_early[i] = 1;
+            }
+        }
+      }
+      if (gi == 2 && side) {
         CUDA_CHECK(cudaEventRecord(h->ev_late1, sg));
         CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_late1, 0));
       }
@@ -2939,6 +3007,9 @@ int cfm_handler_destroy(cfm_handler* h) {
     if (h->ev_pad_done) cudaEventDestroy(h->ev_pad_done);
     if (h->ev_late0) cudaEventDestroy(h->ev_late0);
     if (h->ev_late1) cudaEventDestroy(h->ev_late1);
+    if (h->s_mid) cudaStreamDestroy(h->s_mid);
+    if (h->ev_mid) cudaEventDestroy(h->ev_mid);
+    if (h->ev_mid1) cudaEventDestroy(h->ev_mid1);
     cudaStreamDestroy(h->stream);
     delete h;
   });

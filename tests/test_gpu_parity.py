@@ -541,9 +541,9 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, hybrid, monkeypat
     """Host buffers on a large level go through the slab copy pipeline
     (multipole/locals slabs streamed while the kernel runs, gated by device
     flags; l = 4 streams both, l = 5 -- full-operator mode -- streams the
-    locals, with the last slab split in halves/quarters/eighths, and the
-    first launch group's target-tile level 4 downloads while level 6 still
-    runs); the result must equal the device-resident path bitwise, including
+    locals, with the last slab split in halves/quarters/eighths, level 5 is
+    the middle launch group, and the target-tile levels 4 and 5 download while
+    level 6 still runs); the result must equal the device-resident path bitwise, including
     accumulation into non-zero host locals.  (Hybrid plans off: the
     device-resident reference then runs the same row-ordered tile plans as the
     pipelined call.  With hybrid plans on -- the bench's e2e setting -- the
@@ -553,7 +553,7 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, hybrid, monkeypat
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
     monkeypatch.setenv("CFM_HYBRID", hybrid)
-    lv = (3, 4, 6)
+    lv = (3, 4, 5, 6)  # l = 5: level 5 runs as the middle launch group (uploaded during the first launch)
     cells = {l: _full_level(l) for l in lv}
     full = O.full_far_field()
     h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
