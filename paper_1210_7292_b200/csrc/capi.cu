@@ -1550,7 +1550,8 @@ __global__ void __launch_bounds__(256) k_pad_rows(const PadJobs jobs) {
   }
 }
 
-static void launch_pads(const std::vector<PadJob>& in, cudaStream_t s, int threads = 256) {
+static int64_t launch_pads(const std::vector<PadJob>& in, cudaStream_t s, int threads = 256) {
+  int64_t n_launch = 0;
   for (size_t a = 0; a < in.size(); a += kMaxPadJobs) {
     PadJobs jobs{};
     long long blocks = 0;
@@ -1564,24 +1565,28 @@ static void launch_pads(const std::vector<PadJob>& in, cudaStream_t s, int threa
     if (blocks >= (1ll << 31)) throw Error(CFM_ERR_VALUE, "too many rows to pad");
     k_pad_rows<<<unsigned(blocks), threads, 0, s>>>(jobs);
     CUDA_CHECK(cudaGetLastError());
+    ++n_launch;
   }
+  return n_launch;
 }
 
 // rows [r0, r1) of a (rows x n) source array (host or device) into the padded layout
-static void xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s,
+// Returns the kernels launched (0 for a batched job or a host source).
+static int64_t xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s,
                       int threads = 256, std::vector<PadJob>* batch = nullptr) {
-  if (r1 <= r0) return;
+  if (r1 <= r0) return 0;
   if (is_device_ptr(src)) {
     const PadJob J{dst + size_t(r0) * ld, src + size_t(r0) * h->n, (long long)(r1 - r0), 0, ld, h->n};
-    if (batch)
+    if (batch) {
       batch->push_back(J);
-    else
-      launch_pads({J}, s, threads);
-    return;
+      return 0;
+    }
+    return launch_pads({J}, s, threads);
   }
   CUDA_CHECK(cudaMemcpy2DAsync(dst + size_t(r0) * ld, size_t(ld) * sizeof(double), src + size_t(r0) * h->n,
                                size_t(h->n) * sizeof(double), size_t(h->n) * sizeof(double), size_t(r1 - r0),
                                cudaMemcpyDefault, s));
+  return 0;
 }
 
 static void fill_full(TileParams& p, const cfm_handler* h, const Group& g, const double* xpad, int64_t x_rows) {
@@ -1621,7 +1626,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     if (full_mode(g, lp)) {
       const auto off = xpad_layout(h, {{lp.n_rows, g.full.ld}}, s);
       double* xp = h->xpad.as<double>() + off[0];
-      xpad_copy(h, xp, g.full.ld, d_x, 0, lp.n_rows, s);
+      launches += xpad_copy(h, xp, g.full.ld, d_x, 0, lp.n_rows, s);
       fill_full(p, h, g, xp, lp.n_rows);
       if (lp.mode == 1) p.entry_ncols = lp.entry_ncols.as<unsigned char>();
       p.n_entries = lp.hp.n_entries();
@@ -1664,7 +1669,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
     const int ldx = g.ts_v.ld;
     const auto xo = xpad_layout(h, {{lp.n_rows, ldx}}, s);
     double* xp = h->xpad.as<double>() + xo[0];
-    xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
+    launches += xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
     if (!lp.ts_y.p) {
       lp.ts_y.alloc(size_t(lp.ts_segs) * 20 * sizeof(double));
       CUDA_CHECK(cudaMemsetAsync(lp.ts_y.p, 0, lp.ts_y.bytes, s));  // segment pads stay zero
@@ -1746,7 +1751,7 @@ static int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* 
         const int ldx = g.lrf_right_h.ld;
         const auto xo = xpad_layout(h, {{lp.n_rows, ldx}}, s);
         double* xp = h->xpad.as<double>() + xo[0];
-        xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
+        launches += xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
         q.code_op = g.fullmap.d_op.as<int>();
         q.code_rperm = g.fullmap.d_rperm.as<int>();
         q.code_cperm = g.fullmap.d_cperm.as<int>();
@@ -2215,7 +2220,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
       off += L.bytes;
     }
   }
-  launch_pads(pad_batch, s_in);
+  const int64_t pad_launches = launch_pads(pad_batch, s_in);
   if (any_piped) {
     // the kernel may start once the non-pipelined levels and the zeroed flags are in
     CUDA_CHECK(cudaEventRecord(h->ev_in, s_in));
@@ -2306,7 +2311,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
   const auto t_host1 = std::chrono::steady_clock::now();
   std::vector<char> copied_early(lv.size(), 0);  // device->host copies already queued
-  int64_t launches = 0;
+  int64_t launches = pad_launches;
   bool all_dense = true;
   for (auto& L : lv) all_dense = all_dense && group_for_level(h, L.level).kind == kDense;
   if (all_dense) {
@@ -2589,13 +2594,14 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         std::vector<PadJob> pj;
         for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
                                        lv[i].lp->n_rows, sg, 256, &pj);
-        launch_pads(pj, sg);
+        launches += launch_pads(pj, sg);
       }
       if (gi == 2) {
         if (side) sg = h->s_late;
         CUDA_CHECK(cudaStreamWaitEvent(sg, h->ev_x, 0));
-        for (size_t i : grp) xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
-                                       lv[i].lp->n_rows, sg);
+        for (size_t i : grp)
+          launches += xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
+                                lv[i].lp->n_rows, sg);
       }
       if (same_shape && int(segs.size()) <= kMaxSegments) {
         std::vector<TileParams> sub;
