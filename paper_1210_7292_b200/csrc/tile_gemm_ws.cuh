@@ -538,7 +538,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
           // KC - 3, e.g. l = 5) runs as a rank-1 DFMA update instead of a DMMA
           // over 3 zero columns: DMMA and DFMA share the FP64 pipe
           // (tools/fp64_mix.cu), so this drops 3/4 of that step's pipe time
-          const bool ktail = p.ft_ktail && (qq + 1) % nch == 0;
+          // (FTM 1 only: in the FTM 3 stage-1 kernel the extra registers spill)
+          const bool ktail = FTM == 1 && p.ft_ktail && (qq + 1) % nch == 0;
 #pragma unroll
           for (int kk = 0; kk < KC; kk += 8) {
             double bt[NTL];
