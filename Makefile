@@ -6,7 +6,13 @@ PKG := paper_1210_7292_b200
 SRC := $(PKG)/csrc/capi.cu
 HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp) include/chebm2l.h
 
-all: $(PKG)/libchebm2l.so
+PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
+
+all: $(PKG)/libchebm2l.so $(PKG)/libcfm_batch.so
+
+# reference batch (Python objects) -> CSR, in C (loaded with ctypes.PyDLL)
+$(PKG)/libcfm_batch.so: $(PKG)/csrc/batch_csr.cpp include/chebm2l_batch.h
+	g++ -O3 -std=c++17 -shared -fPIC -pthread -I$(PYINC) -o $@ $<
 
 $(PKG)/libchebm2l.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -lcudart
@@ -18,6 +24,6 @@ sass: $(PKG)/libchebm2l.so
 	/usr/local/cuda/bin/cuobjdump -sass $< | grep -oE "DMMA[.0-9x]*|LDGSTS[.A-Z0-9]*" | sort | uniq -c
 
 clean:
-	rm -f $(PKG)/libchebm2l.so
+	rm -f $(PKG)/libchebm2l.so $(PKG)/libcfm_batch.so
 
 .PHONY: all ptxas sass clean

@@ -65,7 +65,7 @@ def bench_points(cfg):
 
     n, depth, order, geom, _, _ = CONFIGS[cfg]
     chunk = 10_000_000
-    base = 2 if geom == "cube" else 3
+    base = 2 if geom == "cube" else (5 if cfg == "cfg5" else 3)  # cfg3 / cfg5 = the golden fixtures' points
     parts = []
     for i in range(0, n, chunk):
         m = min(chunk, n - i)
@@ -171,6 +171,78 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def reference_batches(cells, device):
+    """The level batches exactly as the reference's FmmPlan._level_data builds
+    them (engine.py:113-119): [(target_row, [(source_row, (t0, t1, t2)), ...]),
+    ...] for every target with a non-empty far list, in row order.  The lists
+    come from the device classifier (bit-exact with octree.py:148-178); the t
+    tuples are shared per distinct vector (the reference allocates one per
+    pair; the values are identical)."""
+    import ctypes
+
+    from paper_1210_7292_b200 import _native
+
+    lib = _native.load()
+    tvec = [(c // 49 - 3, (c // 7) % 7 - 3, c % 7 - 3) for c in range(343)]
+    out = {}
+    for lvl, c in cells.items():
+        c = np.ascontiguousarray(c, dtype=np.int32)
+        n = len(c)
+        off = np.zeros(n + 1, np.int64)
+        tot = ctypes.c_int64()
+        _native.check(lib.cfm_classify_count(device, int(lvl), n, c.ctypes.data, off.ctypes.data, ctypes.byref(tot)))
+        src = np.empty(tot.value, np.int32)
+        t = np.empty((tot.value, 3), np.int8)
+        _native.check(lib.cfm_classify_fill(device, int(lvl), n, c.ctypes.data, off.ctypes.data, src.ctypes.data,
+                                            t.ctypes.data, None, None))
+        code = ((t[:, 0].astype(np.int32) + 3) * 49 + (t[:, 1] + 3) * 7 + (t[:, 2] + 3)).tolist()
+        pairs = list(zip(src.tolist(), map(tvec.__getitem__, code)))
+        del code
+        o = off.tolist()
+        out[lvl] = [(i, pairs[o[i]:o[i + 1]]) for i in range(n) if o[i + 1] > o[i]]
+        del pairs
+    return out
+
+
+def reference_api_e2e(h, cells, levels, size, dtype, steps, device):
+    """M2L of all levels through the reference's own call, as FmmPlan._m2l
+    issues it (engine.py:140-157): apply_level(level, batch, mpoles, locals)
+    with the Python batch and fresh np.zeros (pageable) level arrays
+    (engine.py:98-120).  Times the first call (plans built) and the steady
+    state (plans cached under the batch content)."""
+    import torch
+
+    t0 = time.perf_counter()
+    batches = reference_batches({l: cells[l] for l in levels}, device)
+    build_s = time.perf_counter() - t0
+    rng = np.random.default_rng(7)
+    mp = {}
+    for l in levels:
+        m = rng.uniform(-1, 1, (len(cells[l]), size))
+        mp[l] = m if dtype == np.float64 else m + 1j * rng.uniform(-1, 1, m.shape)
+    pairs = sum(len(f) for l in levels for _, f in batches[l])
+
+    def run():
+        loc = {l: np.zeros((len(cells[l]), size), dtype=dtype) for l in levels}
+        torch.cuda.synchronize()
+        tic = time.perf_counter()
+        for l in levels:
+            h.apply_level(l, batches[l], mp[l], loc[l])
+        return time.perf_counter() - tic, loc
+
+    first_s, _ = run()
+    times = [run()[0] for _ in range(max(1, steps))]
+    s = statistics.median(times)
+    bytes_step = sum(3 * len(cells[l]) * size * np.dtype(dtype).itemsize for l in levels)
+    return {"value": pairs / s, "unit": "pairs/s", "ms_per_step": s * 1e3, "first_call_ms": first_s * 1e3,
+            "pairs_per_step": pairs, "steps": len(times), "batch_build_s_untimed": build_s,
+            "h2d_bytes_per_step": bytes_step * 2 // 3, "d2h_bytes_per_step": bytes_step // 3,
+            "plan_cache_hit": bool(h.last_plan_cache_hit),
+            "path": "B200M2LHandler.apply_level(level, batch, mpoles, locals) per level with the reference's "
+                    "Python batch and np.zeros level arrays (pageable), as FmmPlan._m2l calls it; timed region = "
+                    "batch->CSR (C), plan lookup, H2D, kernels, D2H; first_call_ms also builds the plans"}
 
 
 def dist_env():

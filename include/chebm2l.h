@@ -231,6 +231,12 @@ int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights
 int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, const double* nodes, double width,
                            int n_t, const int8_t* transfers, double* out, void* stream);
 
+/* 1 if the last cfm_apply_level_csr reused a cached plan: plans of ad-hoc
+ * batches are cached under their exact CSR content (the reference's FmmPlan
+ * rebuilds identical batches on every run, engine.py:98-120), separately from
+ * the level plans of cfm_plan_level_* (which they never replace). */
+int cfm_last_plan_cache_hit(cfm_handler* h, int* hit);
+
 /* Device-side timing of the last apply (ms, CUDA events on the apply stream),
  * and the number of kernels it launched. */
 int cfm_last_apply_stats(cfm_handler* h, double* ms, int64_t* launches);

@@ -395,6 +395,7 @@ class OracleM2L:
 
     # ---- faithful apply (m2l.py:279-452)
     def apply_faithful(self, level, batch, mpoles, locals_out) -> int:
+        self.flush_log = []
         if not batch:
             return 0
         key = self.level_group[level]
@@ -450,6 +451,7 @@ class OracleM2L:
                     flops += 4 * n * L.shape[1] * c
                 for col, (tgt, tab) in enumerate(pend[ri]):
                     locals_out[tgt] += scale * F[tab, col]
+                self.flush_log.append((tuple(cone[ri]), c))  # block_stats["flushes"] (m2l.py:428)
                 cnt[ri] = 0
                 pend[ri] = []
 

@@ -61,7 +61,12 @@ EXPORTS = (
     "cfm_fmm_l2p",
     "cfm_fmm_p2p",
     "cfm_assemble_operators",
+    "cfm_last_plan_cache_hit",
 )
+
+# libcfm_batch.so (include/chebm2l_batch.h): the reference batch -> CSR in C.
+BATCH_LIB_NAME = "libcfm_batch.so"
+BATCH_EXPORTS = ("cfm_batch_count", "cfm_batch_fill", "cfm_flush_sequence")
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -104,6 +109,7 @@ _SIGS = {
     "cfm_fmm_l2p": ([_P, _P, _I, _P, _P], _I),
     "cfm_fmm_p2p": ([_P, _I, _D, _P, _I, _P, _I, _P], _I),
     "cfm_assemble_operators": ([_I, _I, _D, _I, _P, _D, _I, _P, _P, _P], _I),
+    "cfm_last_plan_cache_hit": ([_P, _P], _I),
 }
 
 _lib = None
@@ -135,6 +141,28 @@ def load(path: str | os.PathLike | None = None):
     if path is None:
         _lib = lib
     return lib
+
+
+_batch_lib = None
+
+
+def load_batch():
+    """Load libcfm_batch.so with ctypes.PyDLL (the GIL stays held during its
+    calls, which read the caller's Python objects)."""
+    global _batch_lib
+    if _batch_lib is None:
+        p = LIB_PATH.parent / BATCH_LIB_NAME
+        if not p.exists():
+            raise ImportError(f"{p} is missing: build the native extensions first (`make`)")
+        lib = ctypes.PyDLL(str(p))
+        lib.cfm_batch_count.argtypes = [ctypes.py_object, _P, _P, _P]
+        lib.cfm_batch_count.restype = _I
+        lib.cfm_batch_fill.argtypes = [ctypes.py_object, _P, _P, _P, _P, _I]
+        lib.cfm_batch_fill.restype = _I
+        lib.cfm_flush_sequence.argtypes = [_I64, _P, _P, _I, _I, _P, _P, _I64]
+        lib.cfm_flush_sequence.restype = _I64
+        _batch_lib = lib
+    return _batch_lib
 
 
 def check(rc: int, precompute_error=None, budget_error=None) -> None:

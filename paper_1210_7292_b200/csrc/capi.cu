@@ -21,6 +21,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -263,6 +265,15 @@ struct AuxStream {
   cudaStream_t s = nullptr;
   cudaEvent_t done = nullptr;
 };
+struct CsrPlanEntry {  // one cached plan of cfm_apply_level_csr and the exact batch it was built from
+  int level = 0, dc_flag = 0;
+  int64_t n_rows = 0;
+  std::vector<int64_t> tgt, off, src;
+  std::vector<int8_t> t;
+  LevelPlan plan;
+  size_t host_bytes() const { return (tgt.size() + off.size() + src.size()) * 8 + t.size(); }
+};
+
 struct LevelScratch {  // per-level scratch of concurrently applied levels
   DevBuf fbuf, xpad, ybuf;
   std::vector<int64_t> xpad_sig;
@@ -279,6 +290,8 @@ struct cfm_handler {
   std::map<int, Group> groups;
   std::map<int, std::pair<int, double>> levels;
   std::map<int, LevelPlan> plans;
+  std::list<CsrPlanEntry> csr_cache;  // plans of ad-hoc CSR batches (cfm_apply_level_csr), most recent first
+  size_t csr_cache_bytes = 0;
   DevBuf x_stage, y_stage, ybuf, wt, z, fbuf, fzbuf, counters, pipe_flags;
   DevBuf xpad;                     // zero-padded source rows of full-operator levels
   long long wt_ld_zeroed = -1;     // SA: leading dimension the W~ padding was zeroed for
@@ -300,6 +313,7 @@ struct cfm_handler {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
+  bool last_csr_hit = false;  // the last cfm_apply_level_csr reused a cached plan
 };
 
 namespace cfm {
@@ -1264,8 +1278,9 @@ static void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, 
   lp.hyb = std::move(hy);
 }
 
-static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
-                            const int64_t* src, const int16_t* codes, int data_complex, int64_t n_rows) {
+static LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt,
+                                  const int64_t* off, const int64_t* src, const int16_t* codes, int data_complex,
+                                  int64_t n_rows) {
   Group& g = group_for_level(h, level);
   const int dc = (data_complex && !h->op_complex) ? 2 : 1;
   if (h->op_complex && !data_complex)
@@ -1471,10 +1486,66 @@ static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const 
       throw Error(e.code == 2 ? CFM_ERR_PRECOMPUTE : CFM_ERR_VALUE, e.what());
     }
   }
-  static uint64_t plan_gen = 0;
+  static std::atomic<uint64_t> plan_gen{0};
   lp.gen = ++plan_gen;
+  return lp;
+}
+
+// The level's cached plan (plan_level_* / plan_level_csr; apply_planned and
+// apply_levels run it).  Ad-hoc batches of cfm_apply_level_csr never land here
+// (they use the CSR plan cache below), so a cached plan is only replaced by an
+// explicit re-plan of its level.
+static LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
+                            const int64_t* src, const int16_t* codes, int data_complex, int64_t n_rows) {
+  LevelPlan lp = build_level_plan(h, level, n_targets, tgt, off, src, codes, data_complex, n_rows);
   h->plans[level] = std::move(lp);
   return h->plans[level];
+}
+
+// Plans of the reference call path (apply_level with a batch, engine.py:140-157):
+// FmmPlan rebuilds the same batches on every run (engine.py:98-120), so a plan is
+// cached under its exact CSR content (targets, offsets, sources, transfer vectors,
+// row count, data kind) and reused when the same batch comes back.  Keys are
+// compared in full (memcmp), never by hash alone.
+static constexpr size_t kCsrCacheMaxEntries = 64;
+static constexpr size_t kCsrCacheMaxBytes = size_t(8) << 30;
+
+static LevelPlan& csr_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
+                           const int64_t* src, const int8_t* t, int data_complex, int64_t n_rows, bool* hit_out) {
+  const int64_t P = n_targets ? off[n_targets] : 0;
+  for (auto it = h->csr_cache.begin(); it != h->csr_cache.end(); ++it) {
+    CsrPlanEntry& e = *it;
+    if (e.level != level || e.dc_flag != data_complex || e.n_rows != n_rows || int64_t(e.tgt.size()) != n_targets ||
+        int64_t(e.src.size()) != P)
+      continue;
+    if (n_targets && std::memcmp(e.tgt.data(), tgt, size_t(n_targets) * 8)) continue;
+    if (std::memcmp(e.off.data(), off, size_t(n_targets + 1) * 8)) continue;
+    if (P && std::memcmp(e.src.data(), src, size_t(P) * 8)) continue;
+    if (P && std::memcmp(e.t.data(), t, size_t(P) * 3)) continue;
+    h->csr_cache.splice(h->csr_cache.begin(), h->csr_cache, it);  // most recently used first
+    if (hit_out) *hit_out = true;
+    return h->csr_cache.front().plan;
+  }
+  if (hit_out) *hit_out = false;
+  auto codes = codes_from_t(P, t);
+  CsrPlanEntry e;
+  e.plan = build_level_plan(h, level, n_targets, tgt, off, src, codes.data(), data_complex, n_rows);
+  e.level = level;
+  e.dc_flag = data_complex;
+  e.n_rows = n_rows;
+  e.tgt.assign(tgt, tgt + n_targets);
+  e.off.assign(off, off + n_targets + 1);
+  e.src.assign(src, src + P);
+  e.t.assign(t, t + 3 * P);
+  const size_t bytes = e.host_bytes();
+  h->csr_cache.push_front(std::move(e));
+  h->csr_cache_bytes += bytes;
+  while (h->csr_cache.size() > 1 &&
+         (h->csr_cache.size() > kCsrCacheMaxEntries || h->csr_cache_bytes > kCsrCacheMaxBytes)) {
+    h->csr_cache_bytes -= h->csr_cache.back().host_bytes();
+    h->csr_cache.pop_back();
+  }
+  return h->csr_cache.front().plan;
 }
 
 // ------------------------------------------------------------------ apply
@@ -2398,6 +2469,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
                   L.lp->hyb->main.n_tiles);
       else
         fill_plan(p, L.lp->tile_col, L.lp->tile_off, L.lp->entry_code, L.lp->entry_src, L.lp->hp.n_tiles);
+#ifdef CFM_EXPERIMENTS
       {
         // timing experiments only (results are wrong): CFM_EXP=norow|nocol|noperm drops permutations
         static const char* exp = getenv("CFM_EXP");
@@ -2415,6 +2487,7 @@ static void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, c
         if (exp && !strcmp(exp, "noB")) p.debug = 32;
         if (exp && !strcmp(exp, "noA")) p.debug = 64;
       }
+#endif
       const long long row_ld = (long long)h->n * (L.lp->dc == 2 || h->op_complex ? 2 : 1);
       p.x = L.x; p.x_ld = row_ld; p.x_dc = L.lp->dc;
       if (ftl[i]) {
@@ -2771,15 +2844,33 @@ struct DeviceLists {
   std::vector<int64_t> h_off;
 };
 
+// c_cone_index is per-device __constant__ memory: upload it once per device
+// (the caller has selected the device).
 static void init_cone_table() {
-  static bool done = false;
-  if (done) return;
+  static std::mutex mu;
+  static std::vector<bool> done;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (size_t(dev) < done.size() && done[dev]) return;
   int8_t tab[kNumCodes];
   std::fill(tab, tab + kNumCodes, int8_t(-1));
   auto cone = full_cone_codes();
   for (size_t i = 0; i < cone.size(); ++i) tab[cone[i]] = int8_t(i);
   CUDA_CHECK(cudaMemcpyToSymbol(c_cone_index, tab, sizeof(tab)));
-  done = true;
+  if (done.size() <= size_t(dev)) done.resize(dev + 1, false);
+  done[dev] = true;
+}
+
+// Reusable classifier scratch of the device-output entry points, per calling
+// thread AND per device (a buffer allocated on one device is never handed to
+// a kernel running on another).
+struct ClassifyScratch {
+  DevBuf grid, counts;
+};
+static ClassifyScratch& classify_scratch(int device) {
+  static thread_local std::map<int, ClassifyScratch> per_device;
+  return per_device[device];
 }
 
 static void classify_device(int level, int64_t n_cells, const int32_t* ijk, cudaStream_t s, DeviceLists& out,
@@ -3045,6 +3136,8 @@ int cfm_set_dense_group(cfm_handler* h, int key, int n_transfers, const int8_t* 
     if (use_full_ops(h)) build_full_ops(h, g, n_transfers, transfers, ops);
     h->groups[key] = std::move(g);
     h->plans.clear();
+    h->csr_cache.clear();
+    h->csr_cache_bytes = 0;
   });
 }
 
@@ -3068,6 +3161,8 @@ int cfm_set_lowrank_group(cfm_handler* h, int key, int n_transfers, const int8_t
     if (use_full_ops(h)) build_lowrank_full(h, g, n_transfers, transfers, n_ops, ranks, left, right);
     h->groups[key] = std::move(g);
     h->plans.clear();
+    h->csr_cache.clear();
+    h->csr_cache_bytes = 0;
   });
 }
 
@@ -3169,6 +3264,8 @@ int cfm_set_shared_group(cfm_handler* h, int key, int r_u, int r_b, const double
     g.sa_fac2.push();
     h->groups[key] = std::move(g);
     h->plans.clear();
+    h->csr_cache.clear();
+    h->csr_cache_bytes = 0;
   });
 }
 
@@ -3179,6 +3276,14 @@ int cfm_set_level(cfm_handler* h, int level, int key, double scale) {
     if (!h->groups.count(key)) throw Error(CFM_ERR_VALUE, "unknown group key");
     h->levels[level] = {key, scale};
     h->plans.erase(level);
+    for (auto it = h->csr_cache.begin(); it != h->csr_cache.end();) {
+      if (it->level == level) {
+        h->csr_cache_bytes -= it->host_bytes();
+        it = h->csr_cache.erase(it);
+      } else {
+        ++it;
+      }
+    }
   });
 }
 
@@ -3220,9 +3325,9 @@ int cfm_apply_level_csr(cfm_handler* h, int level, int64_t n_targets, const int6
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_CHECK(cudaSetDevice(h->device));
     if (n_targets < 0 || n_rows < 0) throw Error(CFM_ERR_VALUE, "negative size");
-    const int64_t P = n_targets ? off[n_targets] : 0;
-    auto codes = codes_from_t(P, t);
-    LevelPlan& lp = make_plan(h, level, n_targets, tgt, off, src, codes.data(), data_complex, n_rows);
+    bool hit = false;
+    LevelPlan& lp = csr_plan(h, level, n_targets, tgt, off, src, t, data_complex, n_rows, &hit);
+    h->last_csr_hit = hit;
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
     {
       cudaStream_t st = pick_stream(h, stream);
@@ -3397,7 +3502,9 @@ int cfm_classify_count_device(int device, int level, int64_t n_cells, const int3
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     init_cone_table();
     const int S = 1 << level;
-    static thread_local DevBuf grid, counts;
+    ClassifyScratch& scr = classify_scratch(device);
+    DevBuf& grid = scr.grid;
+    DevBuf& counts = scr.counts;
     grid.alloc(size_t(S) * S * S * sizeof(int));
     counts.alloc(std::max<size_t>(size_t(n_cells + 1) * sizeof(long long), 16));
     CUDA_CHECK(cudaMemsetAsync(grid.p, 0xff, size_t(S) * S * S * sizeof(int), s));
@@ -3436,7 +3543,7 @@ int cfm_classify_fill_device(int device, int level, int64_t n_cells, const int32
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     init_cone_table();
     const int S = 1 << level;
-    static thread_local DevBuf grid;
+    DevBuf& grid = classify_scratch(device).grid;
     grid.alloc(size_t(S) * S * S * sizeof(int));
     CUDA_CHECK(cudaMemsetAsync(grid.p, 0xff, size_t(S) * S * S * sizeof(int), s));
     const unsigned nb = unsigned((n_cells + 255) / 256);
@@ -3906,6 +4013,14 @@ int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, con
                                                                  dt.as<int8_t>(), out);
     CUDA_CHECK(cudaGetLastError());
     CUDA_CHECK(cudaStreamSynchronize(st));  // the staging buffers are freed on return
+  });
+}
+
+int cfm_last_plan_cache_hit(cfm_handler* h, int* hit) {
+  return guarded([&] {
+    if (!h || !hit) throw Error(CFM_ERR_VALUE, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    *hit = h->last_csr_hit ? 1 : 0;
   });
 }
 

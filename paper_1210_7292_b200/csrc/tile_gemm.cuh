@@ -25,6 +25,14 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// Timing-experiment bits of TileParams::debug (they give wrong results) exist
+// only in builds with -DCFM_EXPERIMENTS; release builds fold them to 0.
+#ifdef CFM_EXPERIMENTS
+#define CFM_DEBUG(p) ((p).debug)
+#else
+#define CFM_DEBUG(p) 0
+#endif
+
 namespace cfm {
 
 struct TileParams {
@@ -59,7 +67,8 @@ struct TileParams {
   double scale;
   int accumulate;
   int pair_out;  // 1: write each entry's result to y rows (e * BN + c) when the entry ends
-  int debug;     // timing experiments only (bit 0: consumers skip the full-barrier wait)
+  int debug;     // timing experiments only (bit 0: consumers skip the full-barrier wait);
+                 // read through CFM_DEBUG(), which is 0 unless built with -DCFM_EXPERIMENTS
   const double* zero_row;  // >= op_ld zeros (rows past an operator, bulk-copy path)
   // pair mode, small segments: the last CTA of the segment reduces the per-pair
   // rows into the targets itself (ordered, no extra launch)

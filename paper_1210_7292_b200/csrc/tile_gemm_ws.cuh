@@ -268,12 +268,12 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
         const int k0 = kc * KC;
         double* bs = Bs + s * BN * LDB;
-        if (p.debug & (4 | 32 | 64)) {
+        if (CFM_DEBUG(p) & (4 | 32 | 64)) {
           // timing experiments only (stale stage data): debug 4 no copies,
           // 32 no source gathers, 64 no operator tile
-          if (p.debug & 4) {
+          if (CFM_DEBUG(p) & 4) {
             mbar_arrive(full + s);
-          } else if (p.debug & 32) {
+          } else if (CFM_DEBUG(p) & 32) {
             mbar_arrive_expect_tx(full + s, unsigned(BM * LDA * 8));
             tma_load_2d(As + s * BM * LDA, &p.tmap_a, acol + k0, arow, full + s);
           } else {
@@ -365,12 +365,12 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
         const int s = q % STAGES;
         if (q >= STAGES) {
-          if (p.debug & 2)
+          if (CFM_DEBUG(p) & 2)
             mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
           else
             mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
         }
-        if (p.debug & 4) {  // timing experiment: no copies, stale stage data
+        if (CFM_DEBUG(p) & 4) {  // timing experiment: no copies, stale stage data
           mbar_arrive(full + s);
           if (BULK_A && pt == 0) mbar_arrive(full + s);  // the expect_tx arrival of the bulk path
           continue;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
           for (int u = 0; u < A_PER_T; ++u) {
             const int id = pt + u * NP;
             const int i = id / (KC / 2), kp = id % (KC / 2);
-            const bool ok = a_ok[u] && !(p.debug & 8);
+            const bool ok = a_ok[u] && !(CFM_DEBUG(p) & 8);
             cp_async16(as + i * LDA + 2 * kp, ok ? (const void*)(a_row[u] + k0) : (const void*)p.ops, ok);
           }
         }
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
 #pragma unroll
         for (int u = 0; u < B_PER_T; ++u) {
           const int c = pt / KC + u * (NP / KC);
-          const bool ok = kvalid && b_col[u] != nullptr && !(p.debug & 16);
+          const bool ok = kvalid && b_col[u] != nullptr && !(CFM_DEBUG(p) & 16);
           cp_async8(bs + c * LDB + kk, ok ? (const void*)(b_col[u] + (long long)p.x_dc * j) : (const void*)p.ops, ok);
         }
         mbar_cp_async_arrive(full + s);
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     const int mrows = d.rows - r0 - wm * WTM;
     for (int kc = 0; kc < d.nchunks; ++kc, ++q) {
       const int s = q % STAGES;
-      if (!(p.debug & 1)) mbar_wait(full + s, (q / STAGES) & 1);
+      if (!(CFM_DEBUG(p) & 1)) mbar_wait(full + s, (q / STAGES) & 1);
       const double* as = As + s * BM * LDA + (mrow(0) + g) * LDA + tg;
       const double* bs = Bs + s * BN * LDB + (ncol(0) + g) * LDB + tg;
       const int kmax = min(KC, d.klen - kc * KC);

@@ -101,7 +101,28 @@ class _Group:
 
 
 def _batch_to_csr(batch):
-    """Reference batch [(tgt, [(src, t), ...]), ...] -> CSR numpy arrays."""
+    """Reference batch [(tgt, [(src, t), ...]), ...] (engine.py:113-119) -> CSR
+    numpy arrays (targets, offsets, sources, int8 t[P, 3]).
+
+    Walked in C (libcfm_batch.so, several threads, ~10 ns per pair instead of
+    ~380 ns for the Python loop); objects outside the fast shapes (numpy
+    scalars, big ints, other sequence types) take the Python conversion."""
+    lib = _native.load_batch()
+    n = len(batch)
+    off = np.empty(n + 1, np.int64)
+    n_pairs = ctypes.c_int64()
+    if lib.cfm_batch_count(batch, None, ctypes.byref(n_pairs), off.ctypes.data) == 0:
+        P = n_pairs.value
+        tgt = np.empty(n, np.int64)
+        src = np.empty(P, np.int64)
+        t = np.empty((P, 3), np.int8)
+        if lib.cfm_batch_fill(batch, off.ctypes.data, tgt.ctypes.data, src.ctypes.data, t.ctypes.data, 0) == 0:
+            return tgt, off, src, t
+    return _batch_to_csr_py(batch)
+
+
+def _batch_to_csr_py(batch):
+    """Python conversion of any batch the C walker declines."""
     n = len(batch)
     tgt = np.empty(n, np.int64)
     counts = np.empty(n, np.int64)
@@ -175,6 +196,8 @@ class B200M2LHandler:
                                                    int(self._op_complex), ctypes.byref(h)))
         self._h = h
         self._planned: dict[int, dict] = {}
+        self._rep_code_tab: dict[object, np.ndarray] = {}
+        self.last_plan_cache_hit = False  # the last apply_level(_csr) reused a cached plan of the same batch
         self._acct: dict[int, tuple] = {}  # level -> (plan stats, group key, flops, block summary)
 
     @staticmethod
@@ -507,9 +530,42 @@ class B200M2LHandler:
                 data_complex, _native.ptr(x), int(n_rows), _native.ptr(y), self._stream_of(x), counts.ctypes.data))
             if wb is not None:
                 wb[...] = y
+            self.last_plan_cache_hit = self._plan_cache_hit()
             flops = self._count_flops(key, counts, n_targets_nonempty, n_sources)
-            self._record(level, key, counts, flops)
+            summary = self._flush_summary(key, t) if self.uses_blocking else None
+            self._record(level, key, counts, flops, summary=summary)
         return flops
+
+    def _plan_cache_hit(self) -> bool:
+        hit = ctypes.c_int()
+        self._check(self._lib.cfm_last_plan_cache_hit(self._h, ctypes.byref(hit)))
+        return bool(hit.value)
+
+    def _rep_of_code(self, key) -> np.ndarray:
+        """t-code -> representative index of a group (symmetry.assignment)."""
+        tab = self._rep_code_tab.get(key)
+        if tab is None:
+            tab = np.full(343, -1, np.int16)
+            for t, (rep_idx, _) in self._groups[key].symmetry.assignment.items():
+                tab[(t[0] + 3) * 49 + (t[1] + 3) * 7 + (t[2] + 3)] = rep_idx
+            self._rep_code_tab[key] = tab
+        return tab
+
+    def _flush_summary(self, key, t):
+        """block_stats of one blocked apply of a batch exactly as the reference
+        counts them (m2l.py:397-452): the flush sequence of its pairs in batch
+        order for buffers of ``block_size`` columns (computed in C)."""
+        cone = self._groups[key].symmetry.cone
+        P = len(t)
+        cap = P // max(self.block_size, 1) + len(cone) + 1
+        reps = np.empty(cap, np.int32)
+        cols = np.empty(cap, np.int32)
+        k = _native.load_batch().cfm_flush_sequence(P, t.ctypes.data, self._rep_of_code(key).ctypes.data, len(cone),
+                                                    self.block_size, reps.ctypes.data, cols.ctypes.data, cap)
+        if k < 0:
+            raise PrecomputeIncompleteError(f"variant {self.variant}: a transfer vector has no operator")
+        flushes = [(cone[r], c) for r, c in zip(reps[:k].tolist(), cols[:k].tolist())]
+        return P, int(k), flushes, {cone[r] for r in np.unique(reps[:k]).tolist()}
 
     # -------- device-built lists: classify on the GPU, plan once, apply many
     def plan_level_cells(self, level: int, cells_ijk, complex_data: bool | None = None) -> dict:
@@ -669,7 +725,7 @@ class B200M2LHandler:
         return int(total)
 
     def _record_summary(self, level, key, counts, planned: bool = True):
-        """Per-call block statistics of a counts vector: (columns, products, [(rep, columns)])."""
+        """Per-call block statistics of a counts vector: (columns, products, [(rep, columns)] flushes)."""
         if not self.uses_blocking:
             return None
         group = self._groups[key]
@@ -679,21 +735,31 @@ class B200M2LHandler:
             t = (c // 49 - 3, (c // 7) % 7 - 3, c % 7 - 3)
             rep = group.symmetry.lookup(t)[0]
             per_rep[rep] = per_rep.get(rep, 0) + int(counts[c])
-        products = self.plan_stats(level)["entries"] if planned else 0
-        return int(counts.sum()), products, [(rep, per_rep[rep]) for rep in sorted(per_rep)]
+        # products = the reference's flush count for these columns (each
+        # representative flushes every block_size columns plus once for the
+        # remainder, m2l.py:412-451), whatever the pair order; planned levels
+        # have no reference batch order, so their flush list holds the same
+        # multiset of (rep, columns) grouped by representative
+        bs = max(self.block_size, 1)
+        flushes = []
+        for rep in sorted(per_rep, key=lambda r: group.symmetry.cone.index(r)):
+            full, rem = divmod(per_rep[rep], bs)
+            flushes.extend([(rep, bs)] * full)
+            if rem:
+                flushes.append((rep, rem))
+        return int(counts.sum()), len(flushes), flushes, set(per_rep)
 
     def _record(self, level, key, counts, flops, planned: bool = True, summary=None) -> None:
         self.flops[level] = self.flops.get(level, 0) + flops
         if self.uses_blocking:
             if summary is None:
                 summary = self._record_summary(level, key, counts, planned)
-            pairs, products, flushes = summary
+            pairs, products, flushes, reps = summary
             st = self.block_stats.setdefault(level, {"columns": 0, "products": 0, "reps_used": set(), "flushes": []})
             st["columns"] += pairs
             st["products"] += products
-            for rep, cols in flushes:
-                st["reps_used"].add(rep)
-                st["flushes"].append((rep, cols))
+            st["reps_used"].update(reps)
+            st["flushes"].extend(flushes)
 
     # ------------------------------------------------------------------
     # accounting (m2l.py:458-536)

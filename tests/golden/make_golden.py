@@ -182,6 +182,9 @@ def run_case(name, points, weights, bbox, depth, kernel, order, eps, variants,
                 out[f"blk_columns_{v}_{lvl}"] = bs["columns"]
                 out[f"blk_products_{v}_{lvl}"] = bs["products"]
                 out[f"blk_reps_{v}_{lvl}"] = len(bs["reps_used"])
+                # the flush sequence itself: (representative transfer vector, columns) per flush
+                out[f"blk_flush_t_{v}_{lvl}"] = np.asarray([r for r, _ in bs["flushes"]], np.int8).reshape(-1, 3)
+                out[f"blk_flush_c_{v}_{lvl}"] = np.asarray([c for _, c in bs["flushes"]], np.int32)
         if potentials_for and v in potentials_for:
             # full reference pipeline (engine.py:201-222) with this handler
             plan_v = FmmPlan(tree, lists, grid, kernel, h, eps, 1)
@@ -212,9 +215,20 @@ def main() -> None:
             aca_case()
         if "fmm" in only:
             fmm_cases()
+        if "cfg3" in only:
+            cfg3_case()
+        if "cfg5" in only:
+            cfg5_case()
+        if "cfg1" in only:
+            cfg1_case()
         return
     symmetry_fixture()
 
+    cfg1_case()
+    _other_cases()
+
+
+def cfg1_case() -> None:
     # BASELINE config 1: N=10,000 uniform cube, height 4 -> reference depth 3,
     # l=4, Laplace, charges U[-1,1]; multipoles from the reference's P2M/M2M.
     pts = cube_points(10_000, seed=1)
@@ -228,6 +242,9 @@ def main() -> None:
 
     run_case("cfg1", pts, w, AffineMap((0.5, 0.5, 0.5), 0.5), 3, laplace_kernel(), 4, 1e-5,
              VARIANTS, extra=cfg1_extra)
+
+
+def _other_cases() -> None:
 
     # Helmholtz (complex128) on a radius-1 sphere, k = 8*pi, l = 4, eps = 1e-4:
     # config 5's non-directional pipeline at fixture scale, complex charges.
@@ -277,6 +294,36 @@ def fmm_cases() -> None:
     wc = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
     run_case("fmm_lapcplx", pts, wc, AffineMap((0.5, 0.5, 0.5), 0.5), 3, laplace_kernel(), 5, 1e-5,
              ("nablk",), potentials_for=("nablk",))
+
+
+def cfg3_case() -> None:
+    """BASELINE config 3 at its full shape: 8e6 points on the unit sphere
+    (bbox centre 0, half width 1), height 6 = reference depth 5 (levels 2-5,
+    296,768 far pairs; the sparse levels 4-5 run the GPU's merged pair-mode
+    plans), l = 9, Laplace, nablk vs sa at eps = 1e-8 (budget 4e9 since the SA
+    estimate is 2.69e9 > the 2e9 default, m2l.py:171-186).  Seeded multipoles
+    (M2L is linear) and 64 sampled output rows per level keep the fixture small;
+    flops / ranks / shared rank are over whole levels.  The points are exactly
+    bench.py's cfg3 points (sphere_points(8e6, seed=3))."""
+    pts = sphere_points(8_000_000, seed=3)
+    w = np.random.default_rng(4).uniform(-1.0, 1.0, len(pts))
+    run_case("cfg3", pts, w, AffineMap((0.0, 0.0, 0.0), 1.0), 5, laplace_kernel(), 9, 1e-8,
+             ("nablk", "sa"), budget=4_000_000_000, store_rows=64, seeded_mpoles=303)
+
+
+def cfg5_case() -> None:
+    """BASELINE config 5's pinnable (non-directional) part at its full shape:
+    2e6 points on the radius-1 sphere, height 6 = depth 5 (leaf width 1/16 =
+    lambda/4 at k = 8 pi), l = 5, Helmholtz e^{ikr}/(4 pi r) complex128,
+    iablk and iasym at eps = 1e-4 (per-level ranks up to 45 at level 2: the
+    realified 90-row factors exceed the fused kernel's 64 and take the
+    two-pass path).  Complex seeded multipoles (re, im ~ U[-1,1]), 64 sampled
+    rows per level.  Points = bench.py's cfg5 points (sphere_points(2e6, seed=5))."""
+    pts = sphere_points(2_000_000, seed=5)
+    rng = np.random.default_rng(6)
+    wc = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    run_case("cfg5", pts, wc, AffineMap((0.0, 0.0, 0.0), 1.0), 5, helmholtz_kernel(8 * np.pi), 5, 1e-4,
+             ("iablk", "iasym"), store_rows=64, seeded_mpoles=505)
 
 
 def aca_case() -> None:

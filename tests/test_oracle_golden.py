@@ -116,7 +116,7 @@ def _oracle_for(g, variant):
 def _mpoles(g, lvl, case):
     if f"mpoles_{lvl}" in g:
         return g[f"mpoles_{lvl}"]
-    seed = {"sphere9": 33, "sphere_lists": 44}[case]
+    seed = {"sphere9": 33, "sphere_lists": 44, "cfg3": 303, "cfg5": 505}[case]
     n = len(g[f"cells_{lvl}"])
     rng = np.random.default_rng(seed + lvl)
     size = int(g["order"]) ** 3
@@ -158,6 +158,51 @@ def test_oracle_apply_matches_reference(golden, case, variant):
             loc2 = loc2[g[f"rows_{lvl}"]]
         assert fl2 == fl
         assert O.rel_l2(loc2, ref) <= 1e-13
+        if f"blk_flush_c_{variant}_{lvl}" in g:  # the reference's flush sequence (m2l.py:412-451)
+            exp = [(tuple(int(c) for c in r), int(c)) for r, c in
+                   zip(g[f"blk_flush_t_{variant}_{lvl}"], g[f"blk_flush_c_{variant}_{lvl}"])]
+            assert orc.flush_log == exp
+            assert len(exp) == int(g[f"blk_products_{variant}_{lvl}"])
+
+
+def _row_subset(g, lvl):
+    """CSR of the fixture's sampled target rows only (the rows whose reference
+    locals are stored), so an oracle check at BASELINE shapes stays small."""
+    tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
+    want = set(int(r) for r in g[f"rows_{lvl}"])
+    keep = [i for i, r in enumerate(tgt) if int(r) in want]
+    s_off = [0]
+    s_src, s_t = [], []
+    for i in keep:
+        s_src.append(src[off[i]:off[i + 1]])
+        s_t.append(t[off[i]:off[i + 1]])
+        s_off.append(s_off[-1] + int(off[i + 1] - off[i]))
+    return (tgt[keep], np.asarray(s_off, np.int64), np.concatenate(s_src) if s_src else src[:0],
+            np.concatenate(s_t) if s_t else t[:0])
+
+
+@pytest.mark.parametrize("case,variant", [("cfg3", "nablk"), ("cfg5", "iablk"), ("cfg5", "iasym")])
+def test_oracle_baseline_shapes(golden, case, variant):
+    """BASELINE configs 3 (l=9 unit sphere, depth 5) and 5 (l=5 Helmholtz
+    k=8 pi complex128, depth 5) at full shape: the oracle on the fixture's
+    sampled targets equals the executed reference; ranks equal; pair counts
+    are the surveyed ones."""
+    g = golden(case)
+    orc, levels = _oracle_for(g, variant)
+    pairs = {lvl: int(g[f"off_{lvl}"][-1]) for lvl in levels}
+    assert pairs == ({2: 2504, 3: 12216, 4: 54000, 5: 228048} if case == "cfg3"
+                     else {2: 2504, 3: 12216, 4: 54000, 5: 226540})
+    for lvl in levels:
+        mp = _mpoles(g, lvl, case)
+        tgt, off, src, t = _row_subset(g, lvl)
+        loc = np.zeros(mp.shape, dtype=np.result_type(orc.dtype, mp.dtype))
+        orc.apply_fast(lvl, tgt, off, src, t, mp, loc)
+        err = O.rel_l2(loc[g[f"rows_{lvl}"]], g[f"locals_{variant}_{lvl}"])
+        assert err <= 1e-13, (case, variant, lvl, err)
+        assert orc.level_ranks(lvl) == list(g[f"ranks_{variant}_{lvl}"])
+    if variant == "nablk":
+        for lvl in levels:
+            assert int(g[f"flops_nablk_{lvl}"]) == 2 * int(g["order"]) ** 6 * pairs[lvl]
 
 
 @pytest.mark.skipif(os.environ.get("ORACLE_SLOW") != "1", reason="l=9 shared-basis precompute takes ~1 min")
