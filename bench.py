@@ -370,356 +370,356 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_b200(args):
+class Ctx:
+    """Per-process run context: rank layout, device, process group, L2 flush buffer."""
+
+    def __init__(self, args):
+        import torch
+
+        self.ws, self.rank, self.local = dist_env()
+        self.shared_gpu = os.environ.get("CFM_BENCH_SHARE_GPU") == "1"
+        self.dist = None
+        if self.ws > 1:
+            import torch.distributed as dist
+
+            # CFM_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo group (a
+            # functional multi-rank run on a 1-GPU box; not a scaling number)
+            dist.init_process_group("gloo" if self.shared_gpu else "nccl")
+            self.dist = dist
+        self.device_index = 0 if self.shared_gpu else self.local
+        torch.cuda.set_device(self.device_index)
+        self.dev = torch.device("cuda", self.device_index)
+        self.flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=self.dev)  # 256 MB > 126 MB L2
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def reduce(self, x, op="sum", dtype=None):
+        if self.dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=dtype or (torch.float64 if isinstance(x, float) else torch.int64), device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return t.item()
+
+
+def _kernel_of(cfg):
+    from paper_1210_7292_b200 import helmholtz_kernel, laplace_kernel
+
+    return helmholtz_kernel(HELMHOLTZ[cfg]) if cfg in HELMHOLTZ else laplace_kernel()
+
+
+def measure(ctx, cfg, variant=None, steps=10, warmup=3, e2e_steps=None, want_handler=False):
+    """One configuration: GPU tree -> precompute -> device lists + plans ->
+    `steps` timed M2L steps (L2 flushed before each, CUDA events on the
+    launching stream, max over ranks) -> the same step end to end from pinned
+    host buffers.  N > 1: shard-local arrays (owned rows + halo), the halo
+    exchanged every step (distributed.ShardedM2L)."""
     import torch
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, make_handler
 
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-
-    from paper_1210_7292_b200 import (
-        ChebyshevGrid,
-        full_far_field_vectors,
-        helmholtz_kernel,
-        laplace_kernel,
-        make_handler,
-    )
-
-    cfg = args.config
-    n, depth, order, geom, variant, eps = CONFIGS[cfg]
-    variant = args.variant or variant
+    n, depth, order, geom, v0, eps = CONFIGS[cfg]
+    variant = variant or v0
     size = order**3
-    cells, widths, tree_ms = gpu_level_cells(cfg, local)
+    cplx = cfg in HELMHOLTZ
+    dt = torch.complex128 if cplx else torch.float64
+    cells, widths, tree_ms = gpu_level_cells(cfg, ctx.device_index)
     levels = sorted(cells)
     full = full_far_field_vectors()
-    cplx = cfg in HELMHOLTZ
-    kernel = helmholtz_kernel(HELMHOLTZ[cfg]) if cplx else laplace_kernel()
-    dt = torch.complex128 if cplx else torch.float64
     budget = 4_000_000_000 if variant in ("sa", "sarcmp") else 2_000_000_000
-    h = make_handler(variant, kernel, ChebyshevGrid(order), eps, device=local, budget_bytes=budget)
-    t_pre = time.perf_counter()
-    h.precompute({l: full for l in levels}, widths)
-    t_pre = time.perf_counter() - t_pre
 
-    # N > 1: each rank owns a contiguous Morton range of every level's targets
-    # (paper_1210_7292_b200.distributed); the source-multipole halo is exchanged
-    # with one NCCL all_to_all per level inside every timed step, overlapped by
-    # the interior targets (all sources owned) held by a second handler: the
-    # boundary targets run once the exchange is in (distributed.overlapped_step).
-    stats, halos, owned = {}, {}, {}
-    h_int, int_levels, bnd_levels = None, [], list(levels)
-    if ws > 1:
-        from paper_1210_7292_b200.distributed import (PreparedHalo, build_halo, owner_of_rows, partition_rows,
-                                                      split_interior)
+    def new_handler():
+        hh = make_handler(variant, _kernel_of(cfg), ChebyshevGrid(order), eps, device=ctx.device_index,
+                          budget_bytes=budget)
+        hh.precompute({l: full for l in levels}, widths)
+        return hh
 
-        h_int = make_handler(variant, kernel, ChebyshevGrid(order), eps, device=local, budget_bytes=budget)
-        h_int.precompute({l: full for l in levels}, widths)
-        bnd_levels = []
-    for lvl in levels:
-        c = cells[lvl].astype(np.int32)
-        if ws == 1:
-            stats[lvl] = h.plan_level_cells(lvl, c)
-            owned[lvl] = None
-            continue
-        parts = partition_rows(c, ws)
-        owned[lvl] = parts[rank]
-        inner, bnd = split_interior(c, lvl, parts[rank], owner_of_rows(parts, len(c)))
-        st = {"pairs": 0, "slots": 0, "mode": ""}
-        srcs = [np.zeros(0, np.int64)]
-        for hh, rows, lst, tag in ((h_int, inner, int_levels, "interior"), (h, bnd, bnd_levels, "boundary")):
-            if len(rows) == 0:
-                continue
-            st_h, srcs_h = hh.plan_level_cells_subset(lvl, c, rows)
-            if st_h["pairs"]:
-                lst.append(lvl)
-                st["pairs"] += st_h["pairs"]
-                st["slots"] += st_h["slots"]
-                st["mode"] += f"{tag}:{st_h['mode']} "
-                srcs.append(srcs_h)
-        srcs = np.unique(np.concatenate(srcs))
-        gathered = [None] * ws
-        dist.all_gather_object(gathered, srcs)
-        halos[lvl] = PreparedHalo(build_halo(parts, srcs, gathered, rank), dev)
-        stats[lvl] = st
-    pairs_local = sum(st["pairs"] for st in stats.values())
-    pairs_total = pairs_local
-    if ws > 1:
-        t = torch.tensor([pairs_local], dtype=torch.int64, device=dev)
-        dist.all_reduce(t)
-        pairs_total = int(t.item())
-
-    gen = torch.Generator(device=dev).manual_seed(11)
-    mp = {l: torch.rand((len(cells[l]), size), dtype=dt, device=dev, generator=gen) * 2 - (1 + 1j if cplx else 1)
-          for l in levels}
-    if ws > 1:  # a rank starts with its own rows only; the halo arrives through the exchange
+    t0 = time.perf_counter()
+    h = new_handler()
+    pre_s = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh, stats = None, {}
+    if ctx.ws == 1:
         for l in levels:
-            keep = torch.zeros(len(cells[l]), dtype=torch.bool, device=dev)
-            keep[torch.as_tensor(owned[l], device=dev)] = True
-            mp[l][~keep] = 0
-    loc = {l: torch.zeros_like(mp[l]) for l in levels}
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+            stats[l] = h.plan_level_cells(l, cells[l].astype(np.int32))
+        pairs_local = sum(st["pairs"] for st in stats.values())
+    else:
+        from paper_1210_7292_b200.distributed import ShardedM2L
 
-    step_flops = [0]
+        sh = ShardedM2L(ctx.dist, h, new_handler(), {l: cells[l] for l in levels}, device=ctx.dev,
+                        complex_data=cplx)
+        pairs_local = sh.pairs
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    pairs_total = int(ctx.reduce(pairs_local))
 
-    def apply_sharded(x, y):
-        """One M2L step on this rank: returns the launches issued."""
-        if ws == 1:
-            step_flops[0] = h.apply_levels({l: (x[l], y[l]) for l in levels})
-            return h.last_apply_stats()[1]
-        from paper_1210_7292_b200.distributed import overlapped_step
-
-        fl, nl = [0], [0]
-
-        def run(hh, lvls):
-            def go():
-                if lvls:
-                    fl[0] += hh.apply_levels({l: (x[l], y[l]) for l in lvls})
-                    nl[0] += hh.last_apply_stats()[1]
-            return go
-
-        overlapped_step(dist, x, halos, run(h_int, int_levels), run(h, bnd_levels))
-        step_flops[0] = fl[0]
-        return nl[0]
+    # seeded U[-1,1] multipoles of the whole level (identical for every N); a
+    # rank keeps its owned rows, the halo arrives through the exchange
+    gen = torch.Generator(device=ctx.dev).manual_seed(11)
+    arrays = {}
+    for l in levels:
+        glob = torch.rand((len(cells[l]), size), dtype=dt, device=ctx.dev, generator=gen) * 2 - (1 + 1j if cplx else 1)
+        if sh is None:
+            arrays[l] = (glob, torch.zeros_like(glob))
+        else:
+            sl = sh.levels[l]
+            mp = torch.zeros((sl.n_local, size), dtype=dt, device=ctx.dev)
+            mp[: sl.n_owned] = glob[torch.as_tensor(sl.owned, device=ctx.dev)]
+            arrays[l] = (mp, torch.zeros_like(mp))
+        del glob
+    torch.cuda.empty_cache()
+    flops = [0]
 
     def step():
-        return apply_sharded(mp, loc)
+        if sh is None:
+            flops[0] = h.apply_levels(arrays)
+            return h.last_apply_stats()[1]
+        flops[0] = sh.step(arrays)
+        return sh.launches()
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ctx.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     launches = 0
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.fill_(float(i))
+    with ClockSampler(ctx.device_index) as clk:
+        for i in range(steps):
+            ctx.flush.fill_(float(i))
             torch.cuda.synchronize()
             ev[i][0].record()
             launches += step()
             ev[i][1].record()
             torch.cuda.synchronize()
-    torch.cuda.synchronize()
-    # per-level launches (diagnostic only, not part of the timed steps)
-    lvl_ms = {}
-    for l in levels:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        flush.fill_(0.0)
-        e0.record()
-        if ws == 1 or l in bnd_levels:
-            h.apply_planned(l, mp[l], loc[l])
-        if ws > 1 and l in int_levels:
-            h_int.apply_planned(l, mp[l], loc[l])
-        e1.record()
-        torch.cuda.synchronize()
-        lvl_ms[l] = e0.elapsed_time(e1)
     step_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    total_ms = sum(step_ms)
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = t.item()
-    value = pairs_total * args.steps / (total_ms * 1e-3)
+    total_ms = ctx.reduce(float(sum(step_ms)), "max")
+    med_ms = ctx.reduce(float(statistics.median(step_ms)), "max")
+    real_flops = int(ctx.reduce(int(flops[0]))) * (4 if cplx else 1)
 
-    # e2e: same step through the handler with pinned host buffers
-    h_mp = {l: torch.empty(mp[l].shape, dtype=dt, pin_memory=True) for l in levels}
-    h_loc = {l: torch.zeros(mp[l].shape, dtype=dt, pin_memory=True) for l in levels}
-    for l in levels:
-        h_mp[l].copy_(mp[l].cpu())
-    np_mp = {l: h_mp[l].numpy() for l in levels}
-    np_loc = {l: h_loc[l].numpy() for l in levels}
-    d_mp = {l: torch.empty_like(mp[l]) for l in levels}
-
-    def e2e_step():
-        if ws == 1:
-            h.apply_levels({l: (np_mp[l], np_loc[l]) for l in levels})
-            return
-        for l in levels:  # host -> device, overlapped halo exchange + apply, locals back to the host
-            d_mp[l].copy_(h_mp[l], non_blocking=True)
-        apply_sharded(d_mp, loc)
+    # end to end: the same step from pinned host buffers (H2D multipoles +
+    # locals, kernels, D2H locals in the timed region).  N = 1: through the
+    # handler's host-buffer pipeline; N > 1: each rank moves its owned rows.
+    e2e_steps = e2e_steps or steps
+    if sh is None:
+        h_mp = {l: torch.empty(arrays[l][0].shape, dtype=dt, pin_memory=True) for l in levels}
+        h_loc = {l: torch.zeros(arrays[l][0].shape, dtype=dt, pin_memory=True) for l in levels}
         for l in levels:
-            h_loc[l].copy_(loc[l], non_blocking=True)
-        torch.cuda.synchronize()
+            h_mp[l].copy_(arrays[l][0].cpu())
+        np_arr = {l: (h_mp[l].numpy(), h_loc[l].numpy()) for l in levels}
 
-    for _ in range(max(1, args.warmup // 2)):
-        e2e_step()
+        def e2e_step():
+            h.apply_levels(np_arr)
+
+        h2d = sum(2 * a[0].numel() * a[0].element_size() for a in arrays.values())
+        d2h = sum(a[0].numel() * a[0].element_size() for a in arrays.values())
+    else:
+        own = {l: sh.levels[l].n_owned for l in levels}
+        h_mp = {l: torch.empty((own[l], size), dtype=dt, pin_memory=True) for l in levels}
+        h_loc = {l: torch.zeros((own[l], size), dtype=dt, pin_memory=True) for l in levels}
+        for l in levels:
+            h_mp[l].copy_(arrays[l][0][: own[l]].cpu())
+
+        def e2e_step():
+            for l in levels:
+                arrays[l][0][: own[l]].copy_(h_mp[l], non_blocking=True)
+                arrays[l][1][: own[l]].copy_(h_loc[l], non_blocking=True)
+            sh.step(arrays)
+            for l in levels:
+                h_loc[l].copy_(arrays[l][1][: own[l]], non_blocking=True)
+            torch.cuda.synchronize()
+
+        h2d = int(ctx.reduce(sum(2 * own[l] * size * (16 if cplx else 8) for l in levels)))
+        d2h = int(ctx.reduce(sum(own[l] * size * (16 if cplx else 8) for l in levels)))
+    e2e_step()
     torch.cuda.synchronize()
-    e2e_steps = max(1, args.steps)
-    if ws > 1:
-        dist.barrier()
+    ctx.barrier()
     tic = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
-    e2e_s = (time.perf_counter() - tic) / e2e_steps
-    if ws > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = t.item()
-    bytes_lvl = {l: mp[l].numel() * mp[l].element_size() for l in levels}
-    if ws == 1:
-        h2d = sum(2 * b for b in bytes_lvl.values())  # multipoles + locals (accumulated in place)
-    else:
-        h2d = sum(bytes_lvl.values()) * ws  # every rank uploads its multipole arrays; locals stay resident
-    d2h = sum(bytes_lvl.values()) * ws
+    torch.cuda.synchronize()
+    e2e_s = ctx.reduce((time.perf_counter() - tic) / e2e_steps, "max")
 
-    # roofline of the dominant kernel: the single multi-level tile_gemm launch of a step
     peak, peak_src = fp64_peak()
-    deep = levels[-1]
-    step_ms_med = statistics.median(step_ms)
-    # algorithmic flops of one step = the reference's own accounting (m2l.py:333-426),
-    # converted to real flops (x4 for complex128 operators)
-    real_flops = step_flops[0] * (4 if cplx else 1)
-    if ws > 1:  # whole-job flops; the roofline is per GPU (average over ranks)
-        t = torch.tensor([real_flops], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        real_flops = t.item()
-    flops_pair = real_flops / pairs_total
-    achieved = real_flops / ws / (step_ms_med * 1e-3) / 1e12
+    achieved = real_flops / ctx.ws / (med_ms * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            t = json.loads(prof.read_text()).get(cfg, {}).get(variant)
-            traffic = t["dram_bytes"] if isinstance(t, dict) else t
+            tr = json.loads(prof.read_text()).get(cfg, {}).get(variant)
+            traffic = tr["dram_bytes"] if isinstance(tr, dict) else tr
         except Exception:
             traffic = None
+    rec = {
+        "config": cfg, "variant": variant, "workload": workload_name(cfg, variant),
+        "value": pairs_total * steps / (total_ms * 1e-3), "unit": "pairs/s", "ms_per_step": total_ms / steps,
+        "steps": steps, "warmup": warmup, "pairs_per_step": pairs_total,
+        "dtype": "c128" if cplx else "f64",
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": f"M2L step over levels {levels[0]}-{levels[-1]} "
+                               f"({pairs_total} pairs x {real_flops / max(pairs_total, 1):.0f} flop avg, "
+                               f"reference accounting{' x4 complex' if cplx else ''})",
+                     "peak_source": peak_src, "dominant_ms": med_ms},
+        "e2e": {"value": pairs_total / e2e_s, "unit": "pairs/s", "ms_per_step": e2e_s * 1e3,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "path": ("B200M2LHandler.apply_levels with pinned host numpy buffers (C ABI; H2D multipoles + "
+                         "locals, kernels, D2H locals in the timed region)") if sh is None else
+                        ("per rank: H2D of its owned multipole + local rows, halo exchange + apply "
+                         "(ShardedM2L.step), D2H of its owned locals")},
+        "gpu_launches": launches, "clocks": clk.summary(),
+        "precompute_s": pre_s, "plan_s": plan_s, "tree_build_ms": tree_ms,
+        "levels": {str(l): int(ctx.reduce(stats[l]["pairs"] if sh is None else sh.levels[l].pairs)) for l in levels},
+        "l2": "flushed between steps (256 MB write)", "multipoles": "seeded U[-1,1]",
+    }
+    if sh is None:
+        slots = sum(st["slots"] for st in stats.values())
+        rec["tile_fill"] = pairs_local / max(slots, 1)
+        rec["plan_modes"] = {str(l): stats[l].get("mode") for l in levels}
+    else:
+        rec["shard"] = {str(l): {"owned": sh.levels[l].n_owned, "halo": len(sh.levels[l].halo),
+                                 "interior_pairs": sh.levels[l].interior_pairs,
+                                 "boundary_pairs": sh.levels[l].boundary_pairs} for l in levels}
+        rec["local_array_bytes"] = int(sum(2 * a[0].numel() * a[0].element_size() for a in arrays.values()))
+    out = (rec, h, cells, levels) if want_handler else (rec,)
+    del arrays, sh
+    torch.cuda.empty_cache()
+    return out
 
-    # Classifier (row a) on its own: device far-list classification of the
-    # deepest level (HBM-bound integer work), timed with CUDA events.
-    classifier = None
-    if rank == 0:
-        import ctypes
 
-        from paper_1210_7292_b200 import _native
+def classifier_record(ctx, cells, level):
+    """Row a1 on its own: device far-list classification of one level
+    (HBM-bound integer work), device outputs, L2 flushed, CUDA events."""
+    import ctypes
 
-        lib = _native.load()
-        lvl_c = levels[-1]
-        deep_cells = torch.from_numpy(cells[lvl_c].astype(np.int32)).to(dev)
-        ncell = len(cells[lvl_c])
-        offs = torch.empty(ncell + 1, dtype=torch.int64, device=dev)
-        tot = ctypes.c_int64()
-        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        _native.check(lib.cfm_classify_count_device(local, lvl_c, ncell, deep_cells.data_ptr(), offs.data_ptr(),
-                                                    ctypes.byref(tot), stream))
-        src_d = torch.empty(tot.value, dtype=torch.int32, device=dev)
-        code_d = torch.empty(tot.value, dtype=torch.int16, device=dev)
-        ms_c = []
-        for i in range(4):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            flush.fill_(float(i))
-            e0.record()
-            _native.check(lib.cfm_classify_fill_device(local, lvl_c, ncell, deep_cells.data_ptr(), offs.data_ptr(),
-                                                       src_d.data_ptr(), code_d.data_ptr(), stream))
-            e1.record()
-            torch.cuda.synchronize()
-            ms_c.append(e0.elapsed_time(e1))
-        cl_ms = min(ms_c[1:])
-        # algorithmic bytes of the fill pass: occupancy grid memset + scatter, cells read,
-        # offsets read, per pair 4 B source row + 2 B t-code written
-        S3 = (1 << lvl_c) ** 3
-        cl_bytes = S3 * 4 + ncell * (4 + 12 + 12 + 8) + tot.value * 6
-        peak_hbm = 6551.4
-        try:
-            peak_hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
-        except Exception:
-            pass
-        classifier = {"level": lvl_c, "pairs": tot.value, "fill_ms": cl_ms, "pairs_per_s": tot.value / (cl_ms * 1e-3),
-                      "roofline": {"bound": "hbm", "achieved": cl_bytes / (cl_ms * 1e-3) / 1e9, "peak": peak_hbm,
-                                   "unit": "GB/s", "frac": cl_bytes / (cl_ms * 1e-3) / 1e9 / peak_hbm},
-                      "note": "cfm_classify_fill_device (grid build + 216-candidate enumeration + canonical codes), "
-                              "device outputs, L2 flushed"}
-        del deep_cells, src_d, code_d, offs
+    import torch
 
-    # BASELINE config 2 also names the per-pair SVD-compressed variant (iablk,
-    # eps=1e-5): measured in the same run on the same device-resident inputs.
-    secondary = None
-    if cfg == "cfg2" and variant == "nablk" and not args.no_secondary:
-        h2 = make_handler("iablk", kernel, ChebyshevGrid(order), eps, device=local)
-        h2.precompute({l: full for l in levels}, widths)
-        for l in levels:
-            if ws == 1:
-                h2.plan_level_cells(l, cells[l].astype(np.int32))
-            else:
-                h2.plan_level_cells_subset(l, cells[l].astype(np.int32), owned[l])
-        loc2 = {l: torch.zeros_like(mp[l]) for l in levels}
-        fl2 = 0
-        for _ in range(args.warmup):
-            fl2 = h2.apply_levels({l: (mp[l], loc2[l]) for l in levels})
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
+    from paper_1210_7292_b200 import _native
+
+    lib = _native.load()
+    dev = ctx.dev
+    deep_cells = torch.from_numpy(cells.astype(np.int32)).to(dev)
+    ncell = len(cells)
+    offs = torch.empty(ncell + 1, dtype=torch.int64, device=dev)
+    tot = ctypes.c_int64()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _native.check(lib.cfm_classify_count_device(ctx.device_index, level, ncell, deep_cells.data_ptr(),
+                                                offs.data_ptr(), ctypes.byref(tot), stream))
+    src_d = torch.empty(tot.value, dtype=torch.int32, device=dev)
+    code_d = torch.empty(tot.value, dtype=torch.int16, device=dev)
+    ms_c = []
+    for i in range(4):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.flush.fill_(float(i))
         e0.record()
-        for _ in range(args.steps):
-            if ws > 1:
-                for l in halos:
-                    halos[l].exchange(dist, mp[l])
-            h2.apply_levels({l: (mp[l], loc2[l]) for l in levels})
+        _native.check(lib.cfm_classify_fill_device(ctx.device_index, level, ncell, deep_cells.data_ptr(),
+                                                   offs.data_ptr(), src_d.data_ptr(), code_d.data_ptr(), stream))
         e1.record()
         torch.cuda.synchronize()
-        ms2 = e0.elapsed_time(e1) / args.steps
-        if ws > 1:
-            t = torch.tensor([ms2], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms2 = t.item()
-            t = torch.tensor([fl2], dtype=torch.int64, device=dev)
-            dist.all_reduce(t)
-            fl2 = int(t.item())
-        secondary = {"variant": "iablk", "eps": eps, "value": pairs_total / (ms2 * 1e-3), "unit": "pairs/s",
-                     "ms_per_step": ms2, "flops_per_step_reference_accounting": fl2,
-                     "achieved_tflops": fl2 / (ms2 * 1e-3) / 1e12,
-                     "note": "same inputs; L2 not flushed between these steps"}
-        del h2, loc2
+        ms_c.append(e0.elapsed_time(e1))
+    cl_ms = min(ms_c[1:])
+    # algorithmic bytes of the fill pass: occupancy grid memset + scatter, cells
+    # read, offsets read, per pair 4 B source row + 2 B t-code written
+    S3 = (1 << level) ** 3
+    cl_bytes = S3 * 4 + ncell * (4 + 12 + 12 + 8) + tot.value * 6
+    peak_hbm = 6551.4
+    try:
+        peak_hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        pass
+    return {"level": level, "pairs": tot.value, "fill_ms": cl_ms, "pairs_per_s": tot.value / (cl_ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": cl_bytes / (cl_ms * 1e-3) / 1e9, "peak": peak_hbm,
+                         "unit": "GB/s", "frac": cl_bytes / (cl_ms * 1e-3) / 1e9 / peak_hbm},
+            "note": "cfm_classify_fill_device (grid build + 216-candidate enumeration + canonical codes), "
+                    "device outputs, L2 flushed"}
+
+
+SUB_DEFAULT = {1: "cfg2_ia,cfg3,cfg3_sa,cfg5,cfg4", "multi": "cfg4"}
+
+
+def run_b200(args):
+    import torch
+
+    ctx = Ctx(args)
+    cfg = args.config
+    rec, h, cells, levels = measure(ctx, cfg, args.variant, args.steps, args.warmup, want_handler=True)
+    variant = rec["variant"]
+    size = CONFIGS[cfg][2] ** 3
+
+    extras = {}
+    if ctx.rank == 0:
+        extras["classifier"] = classifier_record(ctx, cells[levels[-1]], levels[-1])
+    # the reference's own call path (apply_level with the Python batch and
+    # pageable np.zeros level arrays, engine.py:140-157), single GPU
+    if ctx.ws == 1 and not args.no_reference_api:
+        extras["e2e_reference_api"] = reference_api_e2e(
+            h, cells, levels, size, np.complex128 if cfg in HELMHOLTZ else np.float64, 3, ctx.device_index)
+    del h
+    torch.cuda.empty_cache()
+
+    subs = {}
+    sub_list = args.subconfigs if args.subconfigs is not None else SUB_DEFAULT[1 if ctx.ws == 1 else "multi"]
+    for name in [s for s in sub_list.split(",") if s]:
+        sub_steps = min(args.steps, 3 if name == "cfg4" else 10)
+        r = measure(ctx, name, None, sub_steps, max(3, args.warmup if name != "cfg4" else 3), e2e_steps=
+                    min(sub_steps, 3))[0]
+        subs[name] = r
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        v, pairs, dt = cpu_port_sample(cfg, args.cpu_targets, 1)
+    if ctx.rank == 0 and ctx.ws == 1 and not args.no_cpu:
+        v, pairs, dt_s = cpu_port_sample(cfg, args.cpu_targets, 1)
+        deep = CONFIGS[cfg][1]
         cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port",
                "sample": f"{pairs} pairs ({args.cpu_targets} level-{deep} targets, full far lists), faithful port "
-                         f"of m2l.py _apply_blocked, 1 thread, {dt:.1f} s"}
+                         f"of m2l.py _apply_blocked, 1 thread, {dt_s:.1f} s"}
 
-    if rank == 0:
-        slots = sum(st["slots"] for st in stats.values())
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, variant), "pairs_per_step": pairs_total, "precompute_s": t_pre,
-                       "tree_build_ms": tree_ms,
-                       "levels": {str(l): stats[l]["pairs"] for l in levels},
-                       "tile_fill": pairs_local / max(slots, 1),
-                       "plan_modes": {str(l): stats[l].get("mode") for l in levels},
-                       "parallelism": f"{ws} GPU(s): targets sharded by Morton range, NCCL halo all_to_all per level"
-                                      if ws > 1 else "1 GPU",
-                       "l2": "flushed between steps (256 MB write)", "multipoles": "seeded U[-1,1]"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"tile_gemm_ws over levels {levels[0]}-{deep} "
-                                   f"({pairs_total} pairs x {flops_pair:.0f} flop avg, reference accounting"
-                                   f"{' x4 complex' if cplx else ''})",
-                         "peak_source": peak_src, "dominant_ms": step_ms_med,
-                         "step_tflops": real_flops / (total_ms / args.steps * 1e-3) / 1e12},
-            "e2e": {"value": pairs_total / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                    "path": "B200M2LHandler.apply_levels with pinned host numpy buffers (C ABI; H2D multipoles "
-                            "+ locals, kernels, D2H locals inside the timed region)"},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "level_ms_separate_launches": {str(l): lvl_ms[l] for l in levels},
+            "metric": METRIC, "value": rec["value"], "unit": "pairs/s", "n_gpus": ctx.ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": rec["dtype"], "data": "synthetic",
+            "config": {"workload": rec["workload"], "pairs_per_step": rec["pairs_per_step"],
+                       "precompute_s": rec["precompute_s"], "plan_s": rec["plan_s"],
+                       "tree_build_ms": rec["tree_build_ms"], "levels": rec["levels"],
+                       "tile_fill": rec.get("tile_fill"), "plan_modes": rec.get("plan_modes"),
+                       "parallelism": (f"{ctx.ws} ranks: targets sharded by Morton range, shard-local arrays, "
+                                       f"{'gloo (shared GPU)' if ctx.shared_gpu else 'NCCL'} halo all_to_all per "
+                                       f"level") if ctx.ws > 1 else "1 GPU",
+                       "l2": rec["l2"], "multipoles": rec["multipoles"]},
+            "roofline": rec["roofline"], "e2e": rec["e2e"], "gpu_launches": rec["gpu_launches"],
+            "clocks": rec["clocks"],
         }
+        if "shard" in rec:
+            line["config"]["shard"] = rec["shard"]
+            line["config"]["local_array_bytes_rank0"] = rec["local_array_bytes"]
         if cpu:
             line["cpu_baseline"] = cpu
-        if secondary:
-            line["secondary_variant"] = secondary
-        if classifier:
-            line["classifier"] = classifier
+        line.update(extras)
+        if subs:
+            line["configs"] = subs
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    if ctx.dist is not None:
+        ctx.dist.destroy_process_group()
+
+
+def respawn(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-launch this
+    script under torch.distributed.run with N ranks (127.0.0.1 rendezvous);
+    rank 0 prints the line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -733,8 +733,16 @@ def main():
     ap.add_argument("--cpu-targets", type=int, default=8192,
                     help="CPU-port sample size in deepest-level targets (per process for --impl reference)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the iablk measurement of config 2")
+    ap.add_argument("--no-reference-api", action="store_true", help="skip the apply_level(batch) e2e measurement")
+    ap.add_argument("--subconfigs", default=None,
+                    help="comma list of extra configs measured after the main line (default: cfg2_ia,cfg3,"
+                         "cfg3_sa,cfg5,cfg4 at N=1, cfg4 at N>1; '' for none)")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        sys.exit(respawn(args))
+    if ws and ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch N ranks for --gpus N")
     if args.impl == "reference":
         run_reference(args)
     else:

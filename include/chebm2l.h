@@ -188,6 +188,23 @@ int cfm_classify_fill(int device, int level, int64_t n_cells, const int32_t* ijk
                       const int64_t* offsets, int32_t* src_out, int8_t* t_out,
                       uint8_t* rep_out, uint8_t* perm_out);
 
+/* The far lists of a subset of a level's cells as targets (a multi-GPU
+ * rank's Morton range): sources are all n_cells occupied
+ * cells (host ijk), targets are target_rows[n_targets]; offsets_out has
+ * n_targets + 1 entries, src_out holds global source rows, t_out t[3P].
+ * Same lists and order as octree.py:148-178 for those targets. */
+int cfm_classify_targets_count(int device, int level, int64_t n_cells, const int32_t* ijk,
+                               int64_t n_targets, const int64_t* target_rows,
+                               int64_t* offsets_out, int64_t* total_out);
+int cfm_classify_targets_fill(int device, int level, int64_t n_cells, const int32_t* ijk,
+                              int64_t n_targets, const int64_t* target_rows,
+                              const int64_t* offsets, int32_t* src_out, int8_t* t_out);
+
+/* Multi-GPU halo packing: dst[k, :] = src[rows[k], :] for rows of
+ * row_doubles doubles (device pointers; rows int64 on the device). */
+int cfm_gather_rows(int device, const double* src, int64_t row_doubles, const int64_t* rows,
+                    int64_t n, double* dst, void* stream);
+
 /* Octree construction on the GPU (octree.py:93-127):
  * points n x 3 (host or device), bounding cube (center, half_width), depth
  * >= 2.  Per level: occupied cells in the reference's row order
@@ -231,11 +248,14 @@ int cfm_fmm_p2p(cfm_fmm* f, int kernel, double wavenumber, const double* weights
 int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, const double* nodes, double width,
                            int n_t, const int8_t* transfers, double* out, void* stream);
 
-/* 1 if the last cfm_apply_level_csr reused a cached plan: plans of ad-hoc
- * batches are cached under their exact CSR content (the reference's FmmPlan
- * rebuilds identical batches on every run, engine.py:98-120), separately from
- * the level plans of cfm_plan_level_* (which they never replace). */
-int cfm_last_plan_cache_hit(cfm_handler* h, int* hit);
+/* The plan of the last cfm_apply_level_csr: cache_hit = 1 if it was reused
+ * (plans of ad-hoc batches are cached under their exact CSR content, since
+ * the reference's FmmPlan rebuilds identical batches on every run,
+ * engine.py:98-120; they are kept apart from the level plans of
+ * cfm_plan_level_*, which they never replace); mode 0 target tiles / 1 pair
+ * entries; two_stage 1 for the two-stage low-rank plan.  NULL outputs are
+ * skipped. */
+int cfm_last_csr_plan_info(cfm_handler* h, int* cache_hit, int* mode, int* two_stage);
 
 /* Device-side timing of the last apply (ms, CUDA events on the apply stream),
  * and the number of kernels it launched. */

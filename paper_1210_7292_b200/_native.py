@@ -61,7 +61,10 @@ EXPORTS = (
     "cfm_fmm_l2p",
     "cfm_fmm_p2p",
     "cfm_assemble_operators",
-    "cfm_last_plan_cache_hit",
+    "cfm_last_csr_plan_info",
+    "cfm_classify_targets_count",
+    "cfm_classify_targets_fill",
+    "cfm_gather_rows",
 )
 
 # libcfm_batch.so (include/chebm2l_batch.h): the reference batch -> CSR in C.
@@ -109,7 +112,10 @@ _SIGS = {
     "cfm_fmm_l2p": ([_P, _P, _I, _P, _P], _I),
     "cfm_fmm_p2p": ([_P, _I, _D, _P, _I, _P, _I, _P], _I),
     "cfm_assemble_operators": ([_I, _I, _D, _I, _P, _D, _I, _P, _P, _P], _I),
-    "cfm_last_plan_cache_hit": ([_P, _P], _I),
+    "cfm_last_csr_plan_info": ([_P, _P, _P, _P], _I),
+    "cfm_classify_targets_count": ([_I, _I, _I64, _P, _I64, _P, _P, _P], _I),
+    "cfm_classify_targets_fill": ([_I, _I, _I64, _P, _I64, _P, _P, _P, _P], _I),
+    "cfm_gather_rows": ([_I, _P, _I64, _P, _I64, _P, _P], _I),
 }
 
 _lib = None

@@ -314,6 +314,7 @@ struct cfm_handler {
   double last_ms = 0.0;
   int64_t last_launches = 0;
   bool last_csr_hit = false;  // the last cfm_apply_level_csr reused a cached plan
+  int last_csr_mode = -1, last_csr_two_stage = 0;  // and that plan's mode / two-stage flag
 };
 
 namespace cfm {
@@ -2875,11 +2876,12 @@ static ClassifyScratch& classify_scratch(int device) {
 
 static void classify_device(int level, int64_t n_cells, const int32_t* ijk, cudaStream_t s, DeviceLists& out,
                             bool want_codes, int32_t* h_src = nullptr, int8_t* h_t = nullptr, uint8_t* h_rep = nullptr,
-                            uint8_t* h_perm = nullptr, const int64_t* given_off = nullptr) {
+                            uint8_t* h_perm = nullptr, const int64_t* given_off = nullptr,
+                            const int64_t* target_rows = nullptr, int64_t n_targets = -1) {
   if (level < 0 || level > 9) throw Error(CFM_ERR_VALUE, "classifier supports levels 0..9");
   init_cone_table();
   const int S = 1 << level;
-  DevBuf d_ijk, grid, counts;
+  DevBuf d_ijk, grid, counts, d_tgt;
   const int32_t* dijk = ijk;
   if (!is_device_ptr(ijk)) {
     d_ijk.alloc(std::max<size_t>(size_t(n_cells) * 3 * sizeof(int32_t), 16));
@@ -2895,9 +2897,24 @@ static void classify_device(int level, int64_t n_cells, const int32_t* ijk, cuda
   grid.alloc(size_t(S) * S * S * sizeof(int));
   CUDA_CHECK(cudaMemsetAsync(grid.p, 0xff, grid.bytes, s));
   const int tb = 256;
-  const unsigned nb = unsigned((n_cells + tb - 1) / tb);
-  if (n_cells) k_grid_scatter<<<nb, tb, 0, s>>>(dijk, n_cells, S, grid.as<int>());
+  if (n_cells) k_grid_scatter<<<unsigned((n_cells + tb - 1) / tb), tb, 0, s>>>(dijk, n_cells, S, grid.as<int>());
   CUDA_CHECK(cudaGetLastError());
+  // a subset of the level's cells as targets (a rank's Morton range): the
+  // grid holds every occupied cell (sources), the lists are built for the
+  // given target rows only
+  if (target_rows) {
+    if (is_device_ptr(ijk)) throw Error(CFM_ERR_VALUE, "target subsets need host cell arrays");
+    std::vector<int32_t> sub(size_t(std::max<int64_t>(n_targets, 0)) * 3);
+    for (int64_t k = 0; k < n_targets; ++k) {
+      const int64_t r = target_rows[k];
+      if (r < 0 || r >= n_cells) throw Error(CFM_ERR_VALUE, "target row out of range");
+      std::copy(ijk + 3 * r, ijk + 3 * r + 3, sub.begin() + 3 * k);
+    }
+    upload(d_tgt, sub);
+    dijk = d_tgt.as<int32_t>();
+    n_cells = n_targets;
+  }
+  const unsigned nb = unsigned((n_cells + tb - 1) / tb);
   out.h_off.assign(n_cells + 1, 0);
   if (given_off) {
     std::copy(given_off, given_off + n_cells + 1, out.h_off.begin());
@@ -3328,6 +3345,8 @@ int cfm_apply_level_csr(cfm_handler* h, int level, int64_t n_targets, const int6
     bool hit = false;
     LevelPlan& lp = csr_plan(h, level, n_targets, tgt, off, src, t, data_complex, n_rows, &hit);
     h->last_csr_hit = hit;
+    h->last_csr_mode = lp.mode;
+    h->last_csr_two_stage = lp.ts ? 1 : 0;
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
     {
       cudaStream_t st = pick_stream(h, stream);
@@ -3488,6 +3507,85 @@ int cfm_classify_fill(int device, int level, int64_t n_cells, const int32_t* ijk
       throw;
     }
     cudaStreamDestroy(s);
+  });
+}
+
+int cfm_classify_targets_count(int device, int level, int64_t n_cells, const int32_t* ijk, int64_t n_targets,
+                               const int64_t* target_rows, int64_t* offsets_out, int64_t* total_out) {
+  return guarded([&] {
+    if (n_targets < 0 || (n_targets && !target_rows)) throw Error(CFM_ERR_VALUE, "bad target rows");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DeviceLists dl;
+    try {
+      classify_device(level, n_cells, ijk, s, dl, false, nullptr, nullptr, nullptr, nullptr, nullptr, target_rows,
+                      n_targets);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaStreamDestroy(s);
+    if (offsets_out) std::copy(dl.h_off.begin(), dl.h_off.end(), offsets_out);
+    if (total_out) *total_out = dl.total;
+  });
+}
+
+int cfm_classify_targets_fill(int device, int level, int64_t n_cells, const int32_t* ijk, int64_t n_targets,
+                              const int64_t* target_rows, const int64_t* offsets, int32_t* src_out, int8_t* t_out) {
+  return guarded([&] {
+    if (!offsets || !src_out) throw Error(CFM_ERR_VALUE, "offsets and src_out are required");
+    if (n_targets < 0 || (n_targets && !target_rows)) throw Error(CFM_ERR_VALUE, "bad target rows");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DeviceLists dl;
+    try {
+      classify_device(level, n_cells, ijk, s, dl, false, src_out, t_out, nullptr, nullptr, offsets, target_rows,
+                      n_targets);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaStreamDestroy(s);
+  });
+}
+
+// Row gather for the multi-GPU halo (pack the rows a peer needs into one
+// contiguous send buffer): dst[k] = src[rows[k]], rows of `row_doubles`
+// doubles.  One warp per row, 16-B loads when the rows allow it.
+__global__ void k_gather_rows(const double* __restrict__ src, long long row_doubles,
+                              const long long* __restrict__ rows, long long n, double* __restrict__ dst) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  const bool vec = (row_doubles & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  for (long long k = warp; k < n; k += nw) {
+    const double* s = src + rows[k] * row_doubles;
+    double* d = dst + k * row_doubles;
+    if (vec) {
+      const double2* s2 = reinterpret_cast<const double2*>(s);
+      double2* d2 = reinterpret_cast<double2*>(d);
+      for (long long j = lane; j < row_doubles / 2; j += 32) d2[j] = __ldg(s2 + j);
+    } else {
+      for (long long j = lane; j < row_doubles; j += 32) d[j] = __ldg(s + j);
+    }
+  }
+}
+
+int cfm_gather_rows(int device, const double* src, int64_t row_doubles, const int64_t* rows, int64_t n, double* dst,
+                    void* stream) {
+  return guarded([&] {
+    if (n < 0 || row_doubles <= 0) throw Error(CFM_ERR_VALUE, "bad sizes");
+    if (n == 0) return;
+    if (!is_device_ptr(src) || !is_device_ptr(rows) || !is_device_ptr(dst))
+      throw Error(CFM_ERR_VALUE, "device pointers required");
+    CUDA_CHECK(cudaSetDevice(device));
+    const int threads = 256;
+    const long long blocks = std::min<long long>((n + 7) / 8, 148LL * 16);
+    k_gather_rows<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        src, row_doubles, reinterpret_cast<const long long*>(rows), n, dst);
+    CUDA_CHECK(cudaGetLastError());
   });
 }
 
@@ -4016,11 +4114,13 @@ int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, con
   });
 }
 
-int cfm_last_plan_cache_hit(cfm_handler* h, int* hit) {
+int cfm_last_csr_plan_info(cfm_handler* h, int* cache_hit, int* mode, int* two_stage) {
   return guarded([&] {
-    if (!h || !hit) throw Error(CFM_ERR_VALUE, "null argument");
+    if (!h) throw Error(CFM_ERR_VALUE, "null handler");
     std::lock_guard<std::mutex> lk(h->mu);
-    *hit = h->last_csr_hit ? 1 : 0;
+    if (cache_hit) *cache_hit = h->last_csr_hit ? 1 : 0;
+    if (mode) *mode = h->last_csr_mode;
+    if (two_stage) *two_stage = h->last_csr_two_stage;
   });
 }
 

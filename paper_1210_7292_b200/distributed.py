@@ -234,3 +234,215 @@ def overlapped_step(dist, mpoles: dict, halos: dict, apply_interior, apply_bound
     for p in pending:
         p.finish()
     apply_boundary()
+
+
+# ---------------------------------------------------------------------------
+# Shard-local sharded M2L (owned rows + compacted halo per rank)
+# ---------------------------------------------------------------------------
+
+
+def device_far_lists(cells_ijk, level: int, target_rows, device: int = 0):
+    """CSR far lists of ``target_rows`` of a level (sources = every occupied
+    cell, global row numbers) from the device classifier
+    (cfm_classify_targets_*; the lists of octree.py:148-178).  Returns
+    (offsets[n + 1], src[P] int64, t[P, 3] int8)."""
+    import ctypes
+
+    from . import _native
+
+    lib = _native.load()
+    c = np.ascontiguousarray(cells_ijk, dtype=np.int32).reshape(-1, 3)
+    rows = np.ascontiguousarray(target_rows, dtype=np.int64)
+    off = np.zeros(len(rows) + 1, np.int64)
+    tot = ctypes.c_int64()
+    _native.check(lib.cfm_classify_targets_count(int(device), int(level), len(c), c.ctypes.data, len(rows),
+                                                 rows.ctypes.data, off.ctypes.data, ctypes.byref(tot)))
+    src = np.empty(tot.value, np.int32)
+    t = np.empty((tot.value, 3), np.int8)
+    if tot.value:
+        _native.check(lib.cfm_classify_targets_fill(int(device), int(level), len(c), c.ctypes.data, len(rows),
+                                                    rows.ctypes.data, off.ctypes.data, src.ctypes.data,
+                                                    t.ctypes.data))
+    return off, src.astype(np.int64), t
+
+
+def native_pack(src, rows_dev, out):
+    """out[k] = src[rows[k]] on the device (cfm_gather_rows, the halo pack kernel)."""
+    import torch
+
+    from . import _native
+
+    row_doubles = src.shape[1] * (2 if src.is_complex() else 1)
+    _native.check(_native.load().cfm_gather_rows(src.device.index, src.data_ptr(), row_doubles, rows_dev.data_ptr(),
+                                                 len(rows_dev), out.data_ptr(),
+                                                 ctypes_stream(torch.cuda.current_stream(src.device))))
+    return out
+
+
+def ctypes_stream(stream):
+    import ctypes
+
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+@dataclass
+class ShardLevel:
+    """One level on one rank.  Local row space: [owned rows (ascending global
+    row), halo rows grouped by owning peer (peer ascending, rows ascending)],
+    so the all_to_all receive buffer IS the halo block of the local array."""
+
+    level: int
+    owned: np.ndarray        # global rows owned here (ascending)
+    halo: np.ndarray         # global rows received, in local order
+    send_local: np.ndarray   # local rows (< n_owned) packed for the peers, peer-major
+    send_counts: list
+    recv_counts: list
+    pairs: int
+    interior_pairs: int
+    boundary_pairs: int
+
+    @property
+    def n_owned(self) -> int:
+        return len(self.owned)
+
+    @property
+    def n_local(self) -> int:
+        return len(self.owned) + len(self.halo)
+
+
+class ShardedM2L:
+    """Targets of every level sharded by contiguous Morton range (SURVEY.md
+    §8e), shard-local level arrays (owned rows + the compacted halo), one
+    halo all_to_all per level per step, overlapped by the interior targets.
+
+    ``h_boundary`` / ``h_interior``: two precomputed handlers of the same
+    variant (each holds one plan per level).  ``lists_fn(cells, level, rows)``
+    gives CSR far lists of target rows in global rows (default: the device
+    classifier); ``pack_fn(src, rows_dev, out)`` packs send rows (default:
+    the cfm_gather_rows kernel).  Results equal the single-GPU apply bitwise:
+    every target sums its own pairs in the same order on its owner."""
+
+    def __init__(self, dist, h_boundary, h_interior, cells: dict, device=None, lists_fn=None, pack_fn=None,
+                 complex_data: bool | None = None, group=None):
+        import torch
+
+        self.dist, self.group = dist, group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.h_bnd, self.h_int = h_boundary, h_interior
+        self.device = torch.device(device) if device is not None else torch.device("cpu")
+        dev_index = self.device.index if self.device.type == "cuda" else 0
+        self.lists_fn = lists_fn or (lambda c, lvl, rows: device_far_lists(c, lvl, rows, dev_index))
+        self.pack_fn = pack_fn or native_pack
+        self.staged = dist.get_backend(group) == "gloo" and self.device.type == "cuda"
+        self.levels: dict[int, ShardLevel] = {}
+        self.int_levels, self.bnd_levels = [], []
+        self._send_idx = {}
+        for lvl in sorted(cells):
+            self._setup_level(lvl, np.asarray(cells[lvl]), complex_data)
+
+    def _setup_level(self, lvl, cells, complex_data):
+        import torch
+
+        parts = partition_rows(cells, self.world)
+        owned = parts[self.rank]
+        off, src, t = self.lists_fn(cells, lvl, owned)
+        need = np.unique(src)
+        owner = owner_of_rows(parts, len(cells))
+        halo_need = need[owner[need] != self.rank]
+        gathered = [None] * self.world
+        self.dist.all_gather_object(gathered, halo_need, group=self.group)
+        recv = [np.sort(halo_need[owner[halo_need] == q]) if q != self.rank else np.zeros(0, np.int64)
+                for q in range(self.world)]
+        halo = np.concatenate(recv) if recv else np.zeros(0, np.int64)
+        send = []
+        for q in range(self.world):
+            if q == self.rank:
+                send.append(np.zeros(0, np.int64))
+                continue
+            nq = np.asarray(gathered[q], dtype=np.int64)
+            send.append(np.sort(nq[owner[nq] == self.rank]))
+        g2l = np.full(len(cells), -1, np.int64)
+        g2l[owned] = np.arange(len(owned))
+        g2l[halo] = len(owned) + np.arange(len(halo))
+        send_local = g2l[np.concatenate(send)] if send else np.zeros(0, np.int64)
+        src_l = g2l[src]
+        counts = np.diff(off)
+        tgt_l = np.arange(len(owned), dtype=np.int64)
+        # interior targets: every source owned here (none in the halo block)
+        halo_pairs = np.add.reduceat((src_l >= len(owned)).astype(np.int64), off[:-1]) if len(src_l) else \
+            np.zeros(len(owned), np.int64)
+        halo_pairs = np.where(counts > 0, halo_pairs, 0)
+        inner = halo_pairs == 0
+        n_local = len(owned) + len(halo)
+        sl = ShardLevel(lvl, owned, halo, send_local, [len(s) for s in send], [len(r) for r in recv],
+                        int(off[-1]), 0, 0)
+        for hh, mask, lst, attr in ((self.h_int, inner, self.int_levels, "interior_pairs"),
+                                    (self.h_bnd, ~inner, self.bnd_levels, "boundary_pairs")):
+            sel = np.nonzero(mask & (counts > 0))[0]
+            if len(sel) == 0:
+                continue
+            c = counts[sel]
+            o = np.zeros(len(sel) + 1, np.int64)
+            np.cumsum(c, out=o[1:])
+            take = np.repeat(off[sel], c) + (np.arange(int(o[-1])) - np.repeat(o[:-1], c))
+            hh.plan_level_csr(lvl, tgt_l[sel], o, src_l[take], t[take], n_local, complex_data)
+            setattr(sl, attr, int(o[-1]))
+            lst.append(lvl)
+        self.levels[lvl] = sl
+        self._send_idx[lvl] = torch.as_tensor(send_local, dtype=torch.int64, device=self.device)
+
+    # -------------------------------------------------------------- arrays
+    def allocate(self, size: int, dtype):
+        """Zeroed shard-local (mpoles, locals) per level: n_local rows each."""
+        import torch
+
+        return {lvl: (torch.zeros((sl.n_local, size), dtype=dtype, device=self.device),
+                      torch.zeros((sl.n_local, size), dtype=dtype, device=self.device))
+                for lvl, sl in self.levels.items()}
+
+    @property
+    def pairs(self) -> int:
+        return sum(sl.pairs for sl in self.levels.values())
+
+    # -------------------------------------------------------------- step
+    def _start(self, lvl, mp):
+        import torch
+
+        sl = self.levels[lvl]
+        send = torch.empty((len(sl.send_local),) + tuple(mp.shape[1:]), dtype=mp.dtype, device=mp.device)
+        if len(sl.send_local):
+            self.pack_fn(mp, self._send_idx[lvl], send)
+        recv = mp[sl.n_owned:]
+        real = (lambda x: torch.view_as_real(x)) if mp.is_complex() else (lambda x: x)
+        if self.staged:  # gloo cannot move CUDA tensors: stage the packed rows through the host
+            h_send = send.cpu()
+            h_recv = torch.empty(recv.shape, dtype=recv.dtype)
+            self.dist.all_to_all_single(real(h_recv), real(h_send), sl.recv_counts, sl.send_counts,
+                                        group=self.group)
+            recv.copy_(h_recv)
+            return None, send
+        work = self.dist.all_to_all_single(real(recv), real(send), sl.recv_counts, sl.send_counts,
+                                           group=self.group, async_op=True)
+        return work, send
+
+    def step(self, arrays: dict) -> int:
+        """One M2L step of this rank: exchange every level's halo (async),
+        interior targets meanwhile, then the boundary targets.  ``arrays``:
+        level -> (mpoles_local, locals_local).  Returns the counted flops."""
+        pending = [self._start(lvl, arrays[lvl][0]) for lvl in sorted(self.levels)]
+        flops = 0
+        if self.int_levels:
+            flops += self.h_int.apply_levels({l: arrays[l] for l in self.int_levels})
+        for work, _ in pending:
+            if work is not None:
+                work.wait()
+        if self.bnd_levels:
+            flops += self.h_bnd.apply_levels({l: arrays[l] for l in self.bnd_levels})
+        return flops
+
+    def launches(self) -> int:
+        n = 0
+        for hh, lv in ((self.h_int, self.int_levels), (self.h_bnd, self.bnd_levels)):
+            if lv and hasattr(hh, "last_apply_stats"):
+                n += hh.last_apply_stats()[1]
+        return n + sum(1 for sl in self.levels.values() if len(sl.send_local))

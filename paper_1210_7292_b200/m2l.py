@@ -537,9 +537,16 @@ class B200M2LHandler:
         return flops
 
     def _plan_cache_hit(self) -> bool:
-        hit = ctypes.c_int()
-        self._check(self._lib.cfm_last_plan_cache_hit(self._h, ctypes.byref(hit)))
-        return bool(hit.value)
+        return self.last_csr_plan_info()["cache_hit"]
+
+    def last_csr_plan_info(self) -> dict:
+        """Plan of the last apply_level / apply_level_csr call (batch plans are
+        cached apart from the level plans of plan_level_*)."""
+        hit, mode, ts = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self._check(self._lib.cfm_last_csr_plan_info(self._h, ctypes.byref(hit), ctypes.byref(mode),
+                                                     ctypes.byref(ts)))
+        return {"cache_hit": bool(hit.value), "mode": {0: "target", 1: "pair"}.get(mode.value),
+                "two_stage": bool(ts.value)}
 
     def _rep_of_code(self, key) -> np.ndarray:
         """t-code -> representative index of a group (symmetry.assignment)."""
@@ -608,6 +615,32 @@ class B200M2LHandler:
         stats["complex"] = bool(complex_data)
         self._planned[level] = stats
         return stats, srcs[: nsrc.value].copy()
+
+    def plan_level_csr(self, level: int, tgt, offsets, src, t, n_rows: int, complex_data: bool | None = None) -> dict:
+        """Cache the apply plan of a level from CSR lists (targets, offsets,
+        sources, int8 t[P, 3]) over level arrays of ``n_rows`` rows; rows may
+        be any local numbering (a multi-GPU rank's owned + halo rows).  Then
+        :meth:`apply_planned` / :meth:`apply_levels` run it."""
+        self._level_key(level)
+        tgt = np.ascontiguousarray(tgt, dtype=np.int64)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        t = np.ascontiguousarray(t, dtype=np.int8).reshape(-1, 3)
+        if off.shape != (len(tgt) + 1,) or (len(tgt) and (off[0] != 0 or off[-1] != len(src) or len(t) != len(src))):
+            raise ValueError("inconsistent CSR batch")
+        if complex_data is None:
+            complex_data = self._op_complex
+        counts = np.zeros(343, np.int64)
+        with self._lock:
+            self._check(self._lib.cfm_plan_level_csr(self._h, int(level), len(tgt), tgt.ctypes.data, off.ctypes.data,
+                                                     src.ctypes.data, t.ctypes.data, int(bool(complex_data)),
+                                                     int(n_rows), counts.ctypes.data))
+        stats = self.plan_stats(level)
+        stats["counts"] = counts
+        stats["n_rows"] = int(n_rows)
+        stats["complex"] = bool(complex_data)
+        self._planned[level] = stats
+        return stats
 
     def plan_stats(self, level: int) -> dict:
         vals = [ctypes.c_int64() for _ in range(6)]

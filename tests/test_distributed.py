@@ -221,3 +221,98 @@ def test_overlapped_step_equals_single_process(world, case, golden):
     ref = np.zeros_like(glob)
     orc.apply_fast(level, tgt, off, src, t, glob, ref)
     assert O.rel_l2(res, ref) <= 1e-14
+
+
+class _OracleHandler:
+    """CPU stand-in for B200M2LHandler's plan/apply interface (test only): the
+    shard-local index maps and the halo exchange are what is under test."""
+
+    def __init__(self, order, level):
+        self.order = order
+        self.orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+            {level: O.full_far_field()}, {level: 1.0 / (1 << level)})
+        self.plans = {}
+
+    def plan_level_csr(self, lvl, tgt, off, src, t, n_rows, complex_data=None):
+        self.plans[lvl] = (np.asarray(tgt), np.asarray(off), np.asarray(src), np.asarray(t), n_rows)
+
+    def apply_levels(self, arrays):
+        fl = 0
+        for lvl, (mp, loc) in arrays.items():
+            tgt, off, src, t, n_rows = self.plans[lvl]
+            assert mp.shape[0] == n_rows
+            fl += self.orc.apply_fast(lvl, tgt, off, src, t, mp.numpy().copy(), loc.numpy())
+        return fl
+
+
+def _sharded_worker(rank, world, port, cells, level, order, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_7292_b200.distributed import ShardedM2L
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        glob = np.random.default_rng(5).uniform(-1, 1, (len(cells), order**3))
+
+        def lists(c, lvl, rows):  # offsets over every given row (empty lists included)
+            tgt, off, src, t = O.far_lists(c, lvl, targets=rows)
+            counts = np.zeros(len(rows), np.int64)
+            counts[np.searchsorted(rows, tgt)] = np.diff(off)
+            full = np.zeros(len(rows) + 1, np.int64)
+            np.cumsum(counts, out=full[1:])
+            return full, src, t
+
+        sh = ShardedM2L(dist, _OracleHandler(order, level), _OracleHandler(order, level), {level: cells},
+                        lists_fn=lists, pack_fn=lambda s, r, o: o.copy_(s.index_select(0, r)))
+        sl = sh.levels[level]
+        arrays = sh.allocate(order**3, torch.float64)
+        mp, loc = arrays[level]
+        mp[: sl.n_owned] = torch.from_numpy(glob[sl.owned])  # a rank starts with its own rows only
+        fl = sh.step(arrays)
+        assert np.array_equal(mp[sl.n_owned:].numpy(), glob[sl.halo])  # halo block = its owners' rows
+        assert sl.interior_pairs + sl.boundary_pairs == sl.pairs
+        parts_out = [None] * world
+        dist.all_gather_object(parts_out, (sl.owned, loc[: sl.n_owned].numpy(), fl, sl.n_local, len(sl.halo)))
+        if rank == 0:
+            out.put(parts_out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,case", [(2, "cube"), (3, "sphere")])
+def test_shard_local_step_equals_single_process(world, case, golden):
+    """ShardedM2L (shard-local arrays: owned rows + compacted halo, halo
+    received straight into the local array's halo block): gathered owned
+    locals equal the single-process apply; per-rank arrays hold owned + halo
+    rows only."""
+    import multiprocessing as mp
+
+    level, order = 4, 3
+    if case == "cube":
+        side = 1 << level
+        cells = np.stack(np.meshgrid(*(np.arange(side),) * 3, indexing="ij"), -1).reshape(-1, 3)
+    else:
+        cells = golden("sphere_lists")["cells_4"].astype(np.int64)
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, cells, level, order, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    glob = np.random.default_rng(5).uniform(-1, 1, (len(cells), order**3))
+    tgt, off, src, t = O.far_lists(cells, level)
+    orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+        {level: O.full_far_field()}, {level: 1.0 / (1 << level)})
+    ref = np.zeros_like(glob)
+    ref_fl = orc.apply_fast(level, tgt, off, src, t, glob, ref)
+    res = np.zeros_like(glob)
+    for rows, vals, _, n_local, n_halo in parts:
+        res[rows] = vals
+        assert n_local == len(rows) + n_halo < len(cells)
+    assert O.rel_l2(res, ref) <= 1e-14
+    assert sum(p[2] for p in parts) == ref_fl

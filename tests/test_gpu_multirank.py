@@ -1,0 +1,162 @@
+"""Multi-rank sharded M2L with the real CUDA handlers.
+
+Two ranks on ONE GPU (this box has one): each rank runs the product path --
+device classifier lists of its Morton range, shard-local level arrays (owned
+rows + compacted halo), the cfm_gather_rows pack kernel and the tile kernels
+-- while the halo moves over a gloo group staged through the host (NCCL
+cannot run two ranks on one device).  No kernel of one rank waits on the
+other's: the exchange is a host collective between the launches.  The
+gathered owned locals must equal the single-rank apply bitwise (every target
+sums its own pairs in the same order on its owner).  A log goes to
+gpurun_out/multirank_<case>.json.
+"""
+
+import json
+import os
+import socket
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case(name):
+    """(cells per level, widths, order, variant, eps, kernel spec)."""
+    if name == "cube_l5":
+        depth, order = 4, 5
+        cells = {}
+        for l in range(2, depth + 1):
+            s = 1 << l
+            cells[l] = np.stack(np.meshgrid(*(np.arange(s),) * 3, indexing="ij"), -1).reshape(-1, 3)
+        return cells, {l: 1.0 / (1 << l) for l in cells}, order, "nablk", 1e-5, ("laplace", None)
+    g = np.load(ROOT / "tests" / "golden" / "cfg5.npz")
+    levels = [int(l) for l in g["levels"]]
+    cells = {l: g[f"cells_{l}"].astype(np.int64) for l in levels}
+    return cells, dict(zip(levels, map(float, g["widths"]))), int(g["order"]), "iablk", float(g["eps"]), \
+        ("helmholtz", float(g["wavenumber"]))
+
+
+def _handler(kspec, order, variant, eps, levels, widths):
+    from paper_1210_7292_b200 import (ChebyshevGrid, full_far_field_vectors, helmholtz_kernel, laplace_kernel,
+                                      make_handler)
+
+    k = laplace_kernel() if kspec[0] == "laplace" else helmholtz_kernel(kspec[1])
+    h = make_handler(variant, k, ChebyshevGrid(order), eps, device=0)
+    h.precompute({l: full_far_field_vectors() for l in levels}, widths)
+    return h
+
+
+def _global_mpoles(cells, order, cplx):
+    rng = np.random.default_rng(21)
+    out = {}
+    for l, c in cells.items():
+        m = rng.uniform(-1, 1, (len(c), order**3))
+        out[l] = m + 1j * rng.uniform(-1, 1, m.shape) if cplx else m
+    return out
+
+
+def _rank_main(rank, world, port, name, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_7292_b200.distributed import ShardedM2L
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        cells, widths, order, variant, eps, kspec = _case(name)
+        levels = sorted(cells)
+        cplx = kspec[0] != "laplace"
+        sh = ShardedM2L(dist, _handler(kspec, order, variant, eps, levels, widths),
+                        _handler(kspec, order, variant, eps, levels, widths), cells, device="cuda:0",
+                        complex_data=cplx)
+        assert sh.staged  # gloo group, CUDA arrays: the halo is staged through the host
+        glob = _global_mpoles(cells, order, cplx)
+        dt = torch.complex128 if cplx else torch.float64
+        arrays = sh.allocate(order**3, dt)
+        for l in levels:
+            sl = sh.levels[l]
+            arrays[l][0][: sl.n_owned] = torch.from_numpy(glob[l][sl.owned]).cuda()
+        flops = sh.step(arrays)
+        torch.cuda.synchronize()
+        res, info = {}, {}
+        for l in levels:
+            sl = sh.levels[l]
+            assert torch.equal(arrays[l][0][sl.n_owned:].cpu(), torch.from_numpy(glob[l][sl.halo]))
+            res[l] = (sl.owned, arrays[l][1][: sl.n_owned].cpu().numpy())
+            info[l] = {"owned": sl.n_owned, "halo": len(sl.halo), "pairs": sl.pairs,
+                       "interior_pairs": sl.interior_pairs, "boundary_pairs": sl.boundary_pairs,
+                       "sent_rows": int(sum(sl.send_counts))}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (res, info, flops, sh.launches()))
+        if rank == 0:
+            q.put(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["cube_l5", "cfg5_helmholtz"])
+def test_two_ranks_one_gpu_equal_single_rank(name):
+    import torch
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    cells, widths, order, variant, eps, kspec = _case(name)
+    levels = sorted(cells)
+    cplx = kspec[0] != "laplace"
+    # single-rank reference on the same device: device lists, one launch
+    h = _handler(kspec, order, variant, eps, levels, widths)
+    glob = _global_mpoles(cells, order, cplx)
+    dt = torch.complex128 if cplx else torch.float64
+    arrays = {}
+    for l in levels:
+        h.plan_level_cells(l, cells[l].astype(np.int32))
+        mp_ = torch.from_numpy(glob[l]).to("cuda:0", dt)
+        arrays[l] = (mp_, torch.zeros_like(mp_))
+    ref_flops = h.apply_levels(arrays)
+    torch.cuda.synchronize()
+    ref = {l: arrays[l][1].cpu().numpy() for l in levels}
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    log = {"case": name, "world": world, "device": "cuda:0 shared", "backend": "gloo (host-staged halo)",
+           "ranks": []}
+    for l in levels:
+        got = np.zeros_like(ref[l])
+        seen = np.zeros(len(ref[l]), bool)
+        for res, _, _, _ in gathered:
+            rows, vals = res[l]
+            assert not seen[rows].any()
+            seen[rows] = True
+            got[rows] = vals
+        assert seen.all()
+        assert np.array_equal(got, ref[l]), (name, l, float(np.abs(got - ref[l]).max()))
+    assert sum(g[2] for g in gathered) == ref_flops
+    for r, (_, info, fl, nl) in enumerate(gathered):
+        log["ranks"].append({"rank": r, "flops": fl, "launches": nl, "levels": {str(k): v for k, v in info.items()}})
+    log["bitwise_equal_to_single_rank"] = True
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    (out / f"multirank_{name}.json").write_text(json.dumps(log, indent=1))

@@ -492,7 +492,7 @@ def test_pair_mode_matches_reference(torch_cuda, golden, case, variant, monkeypa
         tgt, off, src, t = (g[f"{k}_{lvl}"] for k in ("tgt", "off", "src", "t"))
         loc = np.zeros(mp.shape, dtype=np.result_type(h.kernel.dtype, mp.dtype))
         fl = h.apply_level_csr(lvl, tgt, off, src, t, mp, loc)
-        assert h.plan_stats(lvl)["mode"] == "pair"
+        assert h.last_csr_plan_info()["mode"] == "pair"
         err = O.rel_l2(loc, g[f"locals_{variant}_{lvl}"])
         assert err <= TOL[variant], (case, variant, lvl, err)
         assert fl == int(g[f"flops_{variant}_{lvl}"])
