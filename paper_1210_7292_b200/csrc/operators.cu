@@ -1,0 +1,273 @@
+// Operator cache: permutation tables, full-operator / low-rank / two-stage stacks (m2l.py:136-273 on the device).
+#include "internal.hpp"
+
+namespace cfm {
+
+// ------------------------------------------------------------------ handler ops
+void build_tables(cfm_handler* h) {
+  const int nf = h->n * h->f;
+  std::vector<int16_t> row(size_t(kNumPerms) * nf), inv(size_t(kNumPerms) * nf);
+  for (int pid = 0; pid < kNumPerms; ++pid) {
+    auto tab = permutation_table(pid, h->order);
+    auto itab = inverse_table(tab);
+    for (int i = 0; i < h->n; ++i)
+      for (int q = 0; q < h->f; ++q) {
+        row[size_t(pid) * nf + i * h->f + q] = int16_t(tab[i] * h->f + q);
+        inv[size_t(pid) * nf + i * h->f + q] = int16_t(itab[i] * h->f + q);
+      }
+  }
+  upload(h->rowtab, row);
+  upload(h->invtab, inv);
+}
+
+// Map every transfer of the group to (op index, perm) following the variant:
+// symmetric variants go through canonicalize (symmetry.py:63-75, lookup :142-144),
+// plain ones index the operator of t itself.
+void map_transfers(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, int n_ops,
+                          const int8_t* op_t, bool rows_permuted, bool cols_permuted, CodeMap& m) {
+  std::array<int, kNumCodes> op_of_code;
+  op_of_code.fill(-1);
+  for (int i = 0; i < n_ops; ++i) {
+    const int t0 = op_t[3 * i], t1 = op_t[3 * i + 1], t2 = op_t[3 * i + 2];
+    if (t0 < -3 || t0 > 3 || t1 < -3 || t1 > 3 || t2 < -3 || t2 > 3)
+      throw Error(CFM_ERR_VALUE, "operator transfer vector outside [-3,3]^3");
+    op_of_code[tcode(t0, t1, t2)] = i;
+  }
+  for (int k = 0; k < n_transfers; ++k) {
+    const int t0 = transfers[3 * k], t1 = transfers[3 * k + 1], t2 = transfers[3 * k + 2];
+    if (t0 < -3 || t0 > 3 || t1 < -3 || t1 > 3 || t2 < -3 || t2 > 3)
+      throw Error(CFM_ERR_VALUE, "transfer vector outside [-3,3]^3");
+    const int c = tcode(t0, t1, t2);
+    g.valid[c] = 1;
+    if (h->sym) {
+      int ts[3], pid;
+      canonicalize(t0, t1, t2, ts, pid);
+      const int o = op_of_code[tcode(ts[0], ts[1], ts[2])];
+      if (o < 0) throw Error(CFM_ERR_PRECOMPUTE, "no representative operator for a transfer vector");
+      m.op[c] = o;
+      m.rperm[c] = rows_permuted ? pid : -1;
+      m.cperm[c] = cols_permuted ? pid : -1;
+    } else {
+      const int o = op_of_code[c];
+      if (o < 0) throw Error(CFM_ERR_PRECOMPUTE, "no operator for a transfer vector");
+      m.op[c] = o;
+    }
+  }
+}
+
+
+// Full-operator stack for the TMA tile kernel: K_t[i][j] = Op[tab_r[i]][tab_c[j]]
+// for every transfer of the group (the same products the permuted apply forms,
+// acc[i] += sum_k Op[rowtab[i]][k] x[invtab[k]] with j = invtab[k]), rows padded
+// to a multiple of 8, columns to the KC multiple; plus the 2-D tensor map.
+void build_full_ops(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, const double* ops) {
+  const int n = h->n;
+  const int rows = round_up(n, 8);
+  OpStack& fs = g.full;
+  make_stack(fs, n_transfers, rows, n);
+  g.full_rows = rows;
+  std::vector<double> blockv(fs.stride);
+  std::vector<int> ident(n);
+  std::iota(ident.begin(), ident.end(), 0);
+  for (int k = 0; k < n_transfers; ++k) {
+    const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
+    const int o = g.main.op[c], rp = g.main.rperm[c], cp = g.main.cperm[c];
+    const std::vector<int> tr = rp >= 0 ? permutation_table(rp, h->order) : ident;
+    const std::vector<int> tc = cp >= 0 ? permutation_table(cp, h->order) : ident;
+    std::fill(blockv.begin(), blockv.end(), 0.0);
+    const double* src = ops + size_t(o) * n * n;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) blockv[size_t(i) * fs.ld + j] = src[size_t(tr[i]) * n + tc[j]];
+    put_stack(fs, k, blockv);
+    g.fullmap.op[c] = k;
+  }
+  g.fullmap.push();
+  const cuuint64_t dims[2] = {cuuint64_t(fs.ld), cuuint64_t(n_transfers) * rows};
+  const cuuint64_t strides[1] = {cuuint64_t(fs.ld) * sizeof(double)};
+  const cuuint32_t box[2] = {cuuint32_t(kKC + 4), 128u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = resolve_encode_tiled()(&g.full_tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, fs.d.p, dims, strides,
+                                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for the operator stack");
+  g.has_full = true;
+}
+
+void make_stack(OpStack& s, int n_ops, int rows, int cols) {
+  s.n_ops = n_ops;
+  s.rows = rows;
+  s.cols = cols;
+  s.ld = round_up(std::max(cols, 1), kKC);
+  s.stride = (long long)rows * s.ld;
+  s.d.alloc(std::max<size_t>(size_t(n_ops) * s.stride * sizeof(double), 16));
+  CUDA_CHECK(cudaMemset(s.d.p, 0, s.d.bytes));
+}
+
+void put_stack(OpStack& s, int i, const std::vector<double>& hostblock) {
+  CUDA_CHECK(cudaMemcpy(s.d.as<double>() + (size_t)i * s.stride, hostblock.data(),
+                        hostblock.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+void set_per_op(OpStack& s, const std::vector<int>& rows, const std::vector<int>& klen) {
+  if (!rows.empty()) {
+    upload(s.d_rows, rows);
+    s.has_rows = true;
+  }
+  if (!klen.empty()) {
+    upload(s.d_klen, klen);
+    s.has_klen = true;
+  }
+}
+
+// Low-rank factor stacks: pass 1 op = right^H (r f x n f), pass 2 op = left (n f x r f).
+void build_lowrank_stacks(cfm_handler* h, OpStack& left, OpStack& right_h, int n_ops, const int* ranks,
+                                 const double* L, const double* R, int rows_left, int rows_right) {
+  // rows_left: rows of left (n or r_u); rows_right: rows of right (n or r_b)
+  const int f = h->f;
+  const bool cplx = h->op_complex;
+  int rmax = 0;
+  for (int i = 0; i < n_ops; ++i) rmax = std::max(rmax, ranks[i]);
+  make_stack(left, n_ops, rows_left * f, std::max(rmax * f, 1));
+  make_stack(right_h, n_ops, std::max(rmax * f, 1), rows_right * f);
+  std::vector<int> rrows(n_ops), rk(n_ops);
+  size_t offL = 0, offR = 0;
+  const int sc = cplx ? 2 : 1;
+  for (int i = 0; i < n_ops; ++i) {
+    const int r = ranks[i];
+    rrows[i] = r * f;
+    rk[i] = r * f;
+    std::vector<double> bl((size_t)left.stride, 0.0), br((size_t)right_h.stride, 0.0);
+    if (r > 0) {
+      realify_into(L + offL, rows_left, r, cplx, bl.data(), left.ld);
+      realify_into(R + offR, r, rows_right, cplx, br.data(), right_h.ld, /*conj_t=*/true);
+    }
+    put_stack(left, i, bl);
+    put_stack(right_h, i, br);
+    offL += (size_t)rows_left * r * sc;
+    offR += (size_t)rows_right * r * sc;
+    left.host_bytes += (size_t)rows_left * r * sc * 8;
+    right_h.host_bytes += (size_t)rows_right * r * sc * 8;
+  }
+  set_per_op(left, {}, rk);       // pass 2: inner length = rank
+  set_per_op(right_h, rrows, {});  // pass 1: rows = rank
+}
+
+bool use_two_stage() {  // read at every precompute (tests switch it)
+  const char* e = getenv("CFM_LR_TWOSTAGE");
+  return !e || atoi(e) != 0;
+}
+
+// Two-stage low-rank operators (see Group::has_ts): per class the V_t^H rows
+// of its transfers in 16-row segments, and the tensor maps of both stages.
+void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers,
+                            const std::vector<int>& rk, const std::vector<double>& all_v) {
+  g.has_ts = false;
+  if (!use_two_stage()) return;
+  const int n = h->n;
+  int rmax = 0;
+  for (int r : rk) rmax = std::max(rmax, r);
+  if (rmax == 0 || rmax > 32 || g.lrf_left.ld != 32) return;
+  g.ts_ntr = n_transfers;
+  g.ts_rank = rk;
+  g.ts_slot.assign(size_t(8) * n_transfers * 2, -1);
+  int max_slots = 0;
+  for (int cls = 0; cls < 8; ++cls) {
+    int ns = 0;
+    for (int k = 0; k < n_transfers; ++k) {
+      bool in = rk[k] > 0;
+      for (int a = 0; a < 3 && in; ++a) {
+        const int t = transfers[3 * k + a], bit = (cls >> a) & 1;
+        in = t >= (bit ? -2 : -3) && t <= (bit ? 3 : 2);
+      }
+      if (!in) continue;
+      for (int j = 0; j * 16 < rk[k]; ++j) g.ts_slot[(size_t(cls) * n_transfers + k) * 2 + j] = ns++;
+    }
+    max_slots = std::max(max_slots, ns);
+  }
+  const int nb = (max_slots * 16 + 127) / 128;
+  g.ts_nb = nb;
+  make_stack(g.ts_v, 8 * nb, 128, n);
+  const int vld = g.lrf_right_h.ld;
+  const size_t vstride = size_t(g.lrf_right_h.stride);
+  std::vector<double> blk(size_t(g.ts_v.stride));
+  for (int cls = 0; cls < 8; ++cls)
+    for (int b = 0; b < nb; ++b) {
+      std::fill(blk.begin(), blk.end(), 0.0);
+      for (int k = 0; k < n_transfers; ++k)
+        for (int j = 0; j < 2; ++j) {
+          const int sl = g.ts_slot[(size_t(cls) * n_transfers + k) * 2 + j];
+          if (sl < 0 || sl / 8 != b) continue;
+          for (int a = 0; a < 16 && 16 * j + a < rk[k]; ++a)
+            std::copy_n(all_v.begin() + size_t(k) * vstride + size_t(16 * j + a) * vld, n,
+                        blk.begin() + size_t((sl % 8) * 16 + a) * g.ts_v.ld);
+        }
+      put_stack(g.ts_v, cls * nb + b, blk);
+    }
+  auto encode = [](CUtensorMap* m, const OpStack& st, long long rows, unsigned box0) {
+    const cuuint64_t dims[2] = {cuuint64_t(st.ld), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(st.ld) * sizeof(double)};
+    const cuuint32_t box[2] = {box0, 128u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = resolve_encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, st.d.p, dims, strides, box, estr,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for a two-stage stack");
+  };
+  encode(&g.ts_vmap, g.ts_v, (long long)8 * nb * 128, kKC + 4);
+  encode(&g.ts_umap, g.lrf_left, (long long)n_transfers * n, 16 + 4);
+  // stage 2 skips the k-steps of a 16-wide rank segment past the rank: their
+  // U_t columns and Y rows are exact zeros, so the sums are unchanged
+  std::vector<int> ks(size_t(2) * n_transfers, 0);
+  for (int k = 0; k < n_transfers; ++k)
+    for (int j = 0; j < 2; ++j) {
+      const int w = std::min(16, std::max(0, rk[k] - 16 * j));
+      ks[size_t(2) * k + j] = (w + 3) / 4;
+    }
+  upload(g.ts_ksteps, ks);
+  g.has_ts = true;
+}
+
+// Per-transfer low-rank factors for real operators: U_t[i][a] = left_o[tab_r[i]][a],
+// V_t^H[a][j] = right_o[tab_c[j]][a] (the products the permuted apply forms:
+// Y[a] = sum_k right^H[a][k] x[inv[k]] = sum_j right^H[a][tab[j]] x[j]).
+void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, int n_ops,
+                               const int* ranks, const double* L, const double* R) {
+  const int n = h->n;
+  int rmax = 0;
+  for (int i = 0; i < n_ops; ++i) rmax = std::max(rmax, ranks[i]);
+  std::vector<size_t> off(n_ops + 1, 0);
+  for (int i = 0; i < n_ops; ++i) off[i + 1] = off[i] + size_t(n) * ranks[i];
+  make_stack(g.lrf_left, n_transfers, n, std::max(rmax, 1));
+  make_stack(g.lrf_right_h, n_transfers, std::max(rmax, 1), n);
+  std::vector<int> ident(n), rk(n_transfers);
+  std::iota(ident.begin(), ident.end(), 0);
+  std::vector<double> bl(g.lrf_left.stride), br(g.lrf_right_h.stride);
+  std::vector<double> all_v(size_t(n_transfers) * g.lrf_right_h.stride);
+  for (int k = 0; k < n_transfers; ++k) {
+    const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
+    const int o = g.main.op[c];
+    const std::vector<int> tr = g.main.rperm[c] >= 0 ? permutation_table(g.main.rperm[c], h->order) : ident;
+    const std::vector<int> tc = g.pass1.cperm[c] >= 0 ? permutation_table(g.pass1.cperm[c], h->order) : ident;
+    const int r = ranks[o];
+    rk[k] = r;
+    std::fill(bl.begin(), bl.end(), 0.0);
+    std::fill(br.begin(), br.end(), 0.0);
+    const double* Lo = L + off[o];
+    const double* Ro = R + off[o];
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < r; ++a) bl[size_t(i) * g.lrf_left.ld + a] = Lo[size_t(tr[i]) * r + a];
+    for (int a = 0; a < r; ++a)
+      for (int j = 0; j < n; ++j) br[size_t(a) * g.lrf_right_h.ld + j] = Ro[size_t(tc[j]) * r + a];
+    put_stack(g.lrf_left, k, bl);
+    put_stack(g.lrf_right_h, k, br);
+    std::copy(br.begin(), br.end(), all_v.begin() + size_t(k) * br.size());
+    g.fullmap.op[c] = k;
+  }
+  g.fullmap.push();
+  set_per_op(g.lrf_left, {}, rk);
+  set_per_op(g.lrf_right_h, rk, {});
+  g.has_lrfull = true;
+  build_two_stage(h, g, n_transfers, transfers, rk, all_v);
+}
+
+}  // namespace cfm
