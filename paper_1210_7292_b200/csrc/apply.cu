@@ -182,8 +182,10 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     double* xp = h->xpad.as<double>() + xo[0];
     launches += xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
     if (!lp.ts_y.p) {
-      lp.ts_y.alloc(size_t(lp.ts_segs) * 20 * sizeof(double));
-      CUDA_CHECK(cudaMemsetAsync(lp.ts_y.p, 0, lp.ts_y.bytes, s));  // segment pads stay zero
+      // rows of sources no pair reads are never written by stage 1 nor read by
+      // stage 2; zeroed once so every Y value a gather can touch is finite
+      lp.ts_y.alloc(size_t(lp.n_rows) * g.ts_ldy * sizeof(double));
+      CUDA_CHECK(cudaMemsetAsync(lp.ts_y.p, 0, lp.ts_y.bytes, s));
     }
     TileParams a{};
     fill_ops(a, g.ts_v, g.main);
@@ -197,7 +199,8 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     a.ft_rows = 128;
     a.tmap_a = g.ts_vmap;
     a.x = xp; a.x_ld = ldx; a.x_dc = 1; a.x_rows = lp.n_rows;
-    a.y = lp.ts_y.as<double>(); a.y_ld = 8 * 20; a.y_dc = 1; a.y_seg = 20; a.y_map = lp.ts_map.as<int>();
+    a.y = lp.ts_y.as<double>(); a.y_ld = g.ts_ldy; a.y_dc = 1; a.y_rowblk = g.ts_nb;
+    a.y_colmap = g.ts_colmap.as<int>();
     a.scale = 1.0; a.accumulate = 0; a.pair_out = 1;
     a.zero_row = h->zeros.as<double>();
     a.n_entries = lp.ts1.n_entries();
@@ -215,7 +218,8 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     b.ft_opshift = 1;
     b.ft_colseg = 16;
     b.tmap_a = g.ts_umap;
-    b.x = lp.ts_y.as<double>(); b.x_ld = 20; b.x_dc = 1; b.x_rows = lp.ts_segs; b.b_block = 1;
+    b.x = lp.ts_y.as<double>(); b.x_ld = g.ts_ldy; b.x_dc = 1; b.x_rows = lp.n_rows; b.b_block = 0;
+    b.op_col = g.ts_opcol.as<int>();
     b.y = d_y; b.y_ld = row_ld; b.y_dc = 1;
     b.scale = scale; b.accumulate = 1; b.pair_out = 0;
     b.zero_row = h->zeros.as<double>();
@@ -224,11 +228,7 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
       const char* e = getenv("CFM_SEG_KSKIP");  // 0: run all 4 k-steps of every segment (A/B)
       b.seg_ksteps = (!e || atoi(e) != 0) ? g.ts_ksteps.as<int>() : nullptr;
     }
-    static const bool seg_pair = [] {
-      const char* e = getenv("CFM_SEG_PAIR");
-      return !e || atoi(e) != 0;
-    }();
-    launches += seg_pair ? launch_seg_pair(b, lp.ts2.n_tiles, s) : launch_ft16(b, lp.ts2.n_tiles, s);
+    launches += launch_seg_pair(b, lp.ts2.n_tiles, s);
     return launches;
   }
 

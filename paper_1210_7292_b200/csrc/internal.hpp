@@ -169,7 +169,10 @@ struct Group {
   bool has_ts = false;
   int ts_nb = 0;                 // 128-row blocks per class stack
   std::vector<int> ts_rank;      // per transfer index
-  std::vector<int> ts_slot;      // [8][n_transfers][2] segment slot in the class stack, -1 if absent
+  std::vector<int> ts_rho0;      // [8][n_transfers] first row of the transfer's rank rows in the class stack, -1 if absent
+  int ts_ldy = 0;                // Y row length: every transfer's rank rows (ceil4) at a fixed column
+  DevBuf ts_colmap;              // [8 * ts_nb * 128] class-stack row -> Y column (-1: padding row)
+  DevBuf ts_opcol;               // [2 * n_transfers] stage-2 operator 2k + j -> first Y column of its segment
   int ts_ntr = 0;
   OpStack ts_v;                  // 8 * ts_nb blocks of 128 rows x n
   CUtensorMap ts_vmap, ts_umap;  // box 36 x 128 over ts_v; box 20 x 128 over lrf_left
@@ -206,8 +209,7 @@ struct LevelPlan {
   bool ts = false;
   HostPlan ts1, ts2;
   DevBuf ts1_col, ts1_off, ts1_code, ts1_src, ts2_col, ts2_off, ts2_code, ts2_src;
-  int64_t ts_segs = 0;  // stage-2 B rows (entries x 64): the stage-1 output in stage-2 order, 20 doubles each (4 zero)
-  DevBuf ts_y, ts_map;  // ts_map: stage-1 segment -> its row in ts_y (-1: no pair needs it)
+  DevBuf ts_y;          // stage-1 output Y[source row][class-stack row] (n_rows x ts_ldy)
   // hybrid (dense full-operator target tiles): the tiles that are less than
   // half full -- the partial last tile of each boundary class of targets --
   // go to a pair-mode sub-plan; device-resident applies run the remaining

@@ -150,7 +150,7 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
         mp.seg[i].ft_pipe = ft_pipe_enabled() && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
         mp.seg[i].ft_ktail = mp.seg[i].ft_pipe && rem == KC - 3 && !mp.seg[i].op_rows && ktail_enabled();
       }
-      auto kf = q.y_map ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
+      auto kf = (q.y_map || q.y_rowblk) ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
                 : skip    ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
                           : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
       CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));

@@ -157,10 +157,16 @@ bool use_two_stage() {  // read at every precompute (tests switch it)
   return !e || atoi(e) != 0;
 }
 
-// Two-stage low-rank operators (see Group::has_ts): per class the V_t^H rows
-// of its transfers in 16-row segments, and the tensor maps of both stages.
+// Two-stage low-rank operators (see Group::has_ts): per source class the V_t^H
+// rows of its transfers packed back to back (transfer k's r_k rows start at
+// ts_rho0[cls][k], rounded up to 4 rows = one stage-2 k-step), so stage 1
+// computes sum_k ceil4(r_k) rows per source instead of 16-row segments
+// (l = 5, eps = 1e-5: 20 row blocks of 128 instead of 26).  Stage 1 writes a
+// source's rows to Y[source][ycol[k] + a] (ts_colmap), one column range per
+// transfer for all classes: stage 2 gathers an entry's B at column
+// ycol[k] + 16 j (ts_opcol; 32-B aligned) whatever its sources' classes.
 void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers,
-                            const std::vector<int>& rk, const std::vector<double>& all_v) {
+                     const std::vector<int>& rk, const std::vector<double>& all_v) {
   g.has_ts = false;
   if (!use_two_stage()) return;
   const int n = h->n;
@@ -169,10 +175,10 @@ void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* tr
   if (rmax == 0 || rmax > 32 || g.lrf_left.ld != 32) return;
   g.ts_ntr = n_transfers;
   g.ts_rank = rk;
-  g.ts_slot.assign(size_t(8) * n_transfers * 2, -1);
-  int max_slots = 0;
+  g.ts_rho0.assign(size_t(8) * n_transfers, -1);
+  int max_rows = 0;
   for (int cls = 0; cls < 8; ++cls) {
-    int ns = 0;
+    int rows = 0;
     for (int k = 0; k < n_transfers; ++k) {
       bool in = rk[k] > 0;
       for (int a = 0; a < 3 && in; ++a) {
@@ -180,12 +186,35 @@ void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* tr
         in = t >= (bit ? -2 : -3) && t <= (bit ? 3 : 2);
       }
       if (!in) continue;
-      for (int j = 0; j * 16 < rk[k]; ++j) g.ts_slot[(size_t(cls) * n_transfers + k) * 2 + j] = ns++;
+      g.ts_rho0[size_t(cls) * n_transfers + k] = rows;
+      rows += (rk[k] + 3) / 4 * 4;  // 32-B aligned starts: stage 2's gather column coordinates
     }
-    max_slots = std::max(max_slots, ns);
+    max_rows = std::max(max_rows, rows);
   }
-  const int nb = (max_slots * 16 + 127) / 128;
+  const int nb = (max_rows + 127) / 128;
   g.ts_nb = nb;
+  // Y columns: transfer k's ceil4(r_k) rows at the same column for every
+  // class (a stage-2 entry's sources may sit in different classes)
+  std::vector<int> ycol(n_transfers, -1);
+  int ldy = 0;
+  for (int k = 0; k < n_transfers; ++k)
+    if (rk[k] > 0) {
+      ycol[k] = ldy;
+      ldy += (rk[k] + 3) / 4 * 4;
+    }
+  g.ts_ldy = ldy;
+  std::vector<int> colmap(size_t(8) * nb * 128, -1);
+  for (int cls = 0; cls < 8; ++cls)
+    for (int k = 0; k < n_transfers; ++k) {
+      const int r0 = g.ts_rho0[size_t(cls) * n_transfers + k];
+      if (r0 < 0) continue;
+      for (int a = 0; a < (rk[k] + 3) / 4 * 4; ++a) colmap[size_t(cls) * nb * 128 + r0 + a] = ycol[k] + a;
+    }
+  upload(g.ts_colmap, colmap);
+  std::vector<int> opcol(size_t(2) * n_transfers, 0);
+  for (int k = 0; k < n_transfers; ++k)
+    for (int j = 0; j < 2; ++j) opcol[size_t(2) * k + j] = std::max(ycol[k], 0) + 16 * j;
+  upload(g.ts_opcol, opcol);
   make_stack(g.ts_v, 8 * nb, 128, n);
   const int vld = g.lrf_right_h.ld;
   const size_t vstride = size_t(g.lrf_right_h.stride);
@@ -193,14 +222,16 @@ void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* tr
   for (int cls = 0; cls < 8; ++cls)
     for (int b = 0; b < nb; ++b) {
       std::fill(blk.begin(), blk.end(), 0.0);
-      for (int k = 0; k < n_transfers; ++k)
-        for (int j = 0; j < 2; ++j) {
-          const int sl = g.ts_slot[(size_t(cls) * n_transfers + k) * 2 + j];
-          if (sl < 0 || sl / 8 != b) continue;
-          for (int a = 0; a < 16 && 16 * j + a < rk[k]; ++a)
-            std::copy_n(all_v.begin() + size_t(k) * vstride + size_t(16 * j + a) * vld, n,
-                        blk.begin() + size_t((sl % 8) * 16 + a) * g.ts_v.ld);
+      for (int k = 0; k < n_transfers; ++k) {
+        const int r0 = g.ts_rho0[size_t(cls) * n_transfers + k];
+        if (r0 < 0) continue;
+        for (int a = 0; a < rk[k]; ++a) {
+          const int row = r0 + a;
+          if (row / 128 != b) continue;
+          std::copy_n(all_v.begin() + size_t(k) * vstride + size_t(a) * vld, n,
+                      blk.begin() + size_t(row % 128) * g.ts_v.ld);
         }
+      }
       put_stack(g.ts_v, cls * nb + b, blk);
     }
   auto encode = [](CUtensorMap* m, const OpStack& st, long long rows, unsigned box0) {
@@ -215,8 +246,9 @@ void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* tr
   };
   encode(&g.ts_vmap, g.ts_v, (long long)8 * nb * 128, kKC + 4);
   encode(&g.ts_umap, g.lrf_left, (long long)n_transfers * n, 16 + 4);
-  // stage 2 skips the k-steps of a 16-wide rank segment past the rank: their
-  // U_t columns and Y rows are exact zeros, so the sums are unchanged
+  // stage 2 skips the k-steps of a 16-wide rank segment past the rank (in a
+  // partial last k-step the U_t columns and Y rows past the rank are exact
+  // zeros), so sums are unchanged
   std::vector<int> ks(size_t(2) * n_transfers, 0);
   for (int k = 0; k < n_transfers; ++k)
     for (int j = 0; j < 2; ++j) {

@@ -28,19 +28,20 @@ Group& group_for_level(cfm_handler* h, int level) {
 
 // Two-stage low-rank plans from a level's target-tile plan (Group::has_ts).
 // Stage 1: source tiles (64 sources of one class) x ts_nb entries (one per
-// 128-row block of the class stack), pair-mode output rows v = e * 64 + c
-// written as 8 segments of 16 at a 20-double pitch.  Stage 2: the target tiles
-// with every entry (t, 64 sources) split into its rank segments j, operator id
-// 2 k + j (k = transfer index), source ids = stage-1 segment rows.  Taken only
-// when stage 1 computes at most ~1.7x the segments the pairs need and the
-// stage-1 output fits CFM_LR_TWOSTAGE_GB (default 24 GB).
+// 128-row block of the class stack); each entry's 128 x 64 result is written
+// to the sources' Y rows (Y: n_rows x ts_ldy, columns by ts_colmap).
+// Stage 2: the target tiles with every entry (t, 64 sources) split into its
+// 16-wide rank segments j (operator id 2 k + j, k = transfer index); the B
+// tile of an entry is gathered from the 64 sources' Y rows at column
+// ts_opcol[2 k + j].  Taken only when stage 1 computes at most ~1.7x the rank rows the
+// pairs need and Y fits CFM_LR_TWOSTAGE_GB (default 24 GB).
 void build_two_stage_plan(const Group& g, LevelPlan& lp) {
   const HostPlan& hp = lp.hp;
   const int64_t n_rows = lp.n_rows;
   const int ntr = g.ts_ntr, nb = g.ts_nb;
   std::vector<int8_t> mn(size_t(n_rows) * 3, 127), mx(size_t(n_rows) * 3, -128);
   std::vector<char> used(n_rows, 0);
-  int64_t need_segs = 0;
+  int64_t need_rows = 0;
   const int64_t E = hp.n_entries();
   for (int64_t e = 0; e < E; ++e) {
     const int c = hp.entry_code[e];
@@ -48,12 +49,11 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp) {
     if (k < 0 || k >= ntr || g.ts_rank[k] <= 0) return;
     int t[3];
     tcode_decode(c, t[0], t[1], t[2]);
-    const int nseg = (g.ts_rank[k] + 15) / 16;
     for (int col = 0; col < kBN; ++col) {
       const int v = hp.entry_src[size_t(e) * kBN + col];
       if (v < 0) continue;
       used[v] = 1;
-      need_segs += nseg;
+      need_rows += g.ts_rank[k];
       for (int a = 0; a < 3; ++a) {
         mn[size_t(v) * 3 + a] = std::min<int8_t>(mn[size_t(v) * 3 + a], int8_t(t[a]));
         mx[size_t(v) * 3 + a] = std::max<int8_t>(mx[size_t(v) * 3 + a], int8_t(t[a]));
@@ -75,18 +75,12 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp) {
   }
   // stage 1 plan
   HostPlan p1;
-  std::vector<int> tile1(n_rows, -1), col1(n_rows, -1);
   for (int b = 0; b < 8; ++b)
     for (size_t i = 0; i < by_cls[b].size(); i += kBN) {
-      const int64_t t = p1.n_tiles++;
+      p1.n_tiles++;
       p1.tile_off.push_back(int(p1.entry_code.size()));
       std::vector<int> cols(kBN, -1);
-      for (int c = 0; c < kBN && i + c < by_cls[b].size(); ++c) {
-        const int64_t v = by_cls[b][i + c];
-        cols[c] = int(v);
-        tile1[v] = int(t);
-        col1[v] = c;
-      }
+      for (int c = 0; c < kBN && i + c < by_cls[b].size(); ++c) cols[c] = int(by_cls[b][i + c]);
       p1.tile_col.insert(p1.tile_col.end(), cols.begin(), cols.end());
       for (int blk = 0; blk < nb; ++blk) {
         p1.entry_code.push_back(b * nb + blk);
@@ -94,15 +88,14 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp) {
       }
     }
   p1.tile_off.push_back(int(p1.entry_code.size()));
-  const int64_t segs1 = p1.n_entries() * kBN * 8;
   static const double budget_gb = [] {
     const char* e = getenv("CFM_LR_TWOSTAGE_GB");
     return e ? atof(e) : 24.0;
   }();
-  if (segs1 >= (int64_t(1) << 31) || double(need_segs) * 1.2 * 20 * 8 > budget_gb * 1e9) return;
-  if (double(p1.n_tiles) * kBN * nb * 8 > 1.7 * double(need_segs)) return;  // sparse level: fused kernel
-  // stage 2 plan; its B rows (entry e2, column c) = the stage-1 segment of that pair
-  std::vector<int> ymap(size_t(segs1), -1);
+  if (double(n_rows) * g.ts_ldy * 8 > budget_gb * 1e9) return;
+  if (double(p1.n_tiles) * kBN * nb * 128 > 1.7 * double(need_rows)) return;  // sparse level: fused kernel
+  // stage 2 plan: the target tiles, every entry split into its rank segments
+  // (operator 2 k + j); B = the sources' Y rows from column ts_opcol[2 k + j]
   HostPlan p2;
   p2.n_tiles = hp.n_tiles;
   p2.tile_col = hp.tile_col;
@@ -110,36 +103,22 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp) {
   for (int64_t t = 0; t < hp.n_tiles; ++t) {
     p2.tile_off.push_back(int(p2.entry_code.size()));
     for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e) {
-      const int c = hp.entry_code[e];
-      const int k = g.fullmap.op[c];
+      const int k = g.fullmap.op[hp.entry_code[e]];
       for (int j = 0; j * 16 < g.ts_rank[k]; ++j) {
         p2.entry_code.push_back(2 * k + j);
-        for (int col = 0; col < kBN; ++col) {
-          const int v = hp.entry_src[size_t(e) * kBN + col];
-          int id = -1;
-          if (v >= 0) {
-            const int sl = g.ts_slot[(size_t(cls[v]) * ntr + k) * 2 + j];
-            if (sl < 0) return;
-            id = int(((int64_t(tile1[v]) * nb + sl / 8) * kBN + col1[v]) * 8 + sl % 8);
-            const int64_t row2 = int64_t(p2.entry_code.size() - 1) * kBN + col;
-            if (row2 >= (int64_t(1) << 31)) return;
-            ymap[size_t(id)] = int(row2);
-          }
-          p2.entry_src.push_back(id);
-        }
+        p2.entry_src.insert(p2.entry_src.end(), hp.entry_src.begin() + size_t(e) * kBN,
+                            hp.entry_src.begin() + size_t(e + 1) * kBN);
       }
     }
   }
   p2.tile_off.push_back(int(p2.entry_code.size()));
+  if (p2.n_entries() >= (int64_t(1) << 31) / kBN) return;
   lp.ts1 = std::move(p1);
   lp.ts2 = std::move(p2);
   push_plan(lp.ts1, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src);
   push_plan(lp.ts2, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src);
-  upload(lp.ts_map, ymap);
-  lp.ts_segs = lp.ts2.n_entries() * kBN;
   lp.ts = true;
 }
-
 
 // Hybrid plans (CFM_HYBRID=0 disables): measured at config 2 the step kernel
 // drops 50.56 -> 50.28 ms; with all reductions of a step in one launch the

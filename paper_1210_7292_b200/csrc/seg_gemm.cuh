@@ -5,12 +5,14 @@
 // rank-r intermediate Y produced by stage 1 in this kernel's reading order.
 //
 // Every entry is a 16-wide K slice: A = U_t[:, 16 j : 16 j + 16] (one 2-D TMA
-// box of 20 x 128 from the per-transfer factor stack), B = 64 rows of Y (one
-// 2-D box of 20 x 64, rows 16..19 zero).  Two entries share one pipeline stage
+// box of 20 x 128 from the per-transfer factor stack), B = the 64 sources'
+// rank rows of Y (stage 1's packed output, one row per source): 16 TMA
+// tile::gather4 copies of 4 rows x 20 columns from the entry's column
+// (op_col); the rows past the rank are zero in U_t and in Y.  Two entries share one pipeline stage
 // (two A and two B sub-tiles at a 20-double pitch), so the consumer warps run
 // 8 k-steps (128 DMMA per warp) between barrier operations instead of 4.
-// Warp specialisation as in tile_gemm_ws_kernel: one producer lane issues all
-// copies, 8 consumer warps run mma.sync.m8n8k4.f64 with the next stage's first
+// Warp specialisation as in tile_gemm_ws_kernel: one producer warp issues the
+// copies (a gather per lane), 8 consumer warps run mma.sync.m8n8k4.f64 with the next stage's first
 // fragments loaded before the current stage's last k-step; accumulators stay
 // in registers and every target column is written once, in order, no atomics.
 #pragma once
@@ -54,21 +56,38 @@ __global__ void __launch_bounds__(12 * 32, 1) seg_pair_gemm_kernel(const __grid_
   __syncthreads();
 
   if (tid >= NC) {
-    // ---- producer: one lane issues 2 A boxes + 2 B boxes per stage; the odd
-    // last entry pairs with an all-zero B sub-tile (rows out of bounds)
-    if (tid != NC) return;
+    // ---- producer warp: per stage two entries, each A = one 2-D box (lane 0 /
+    // lane 16) and B = 16 tile::gather4 copies of 4 source rows x 20 columns
+    // at the entry's column, one per lane (lane l: entry l / 16, rows 4 (l % 16)
+    // .. +3).  Each lane's source rows and the entry's column/operator of the
+    // next stage are loaded before waiting for its slot, so the index loads'
+    // latency hides under the wait.  The odd last entry (no partner) reads
+    // row -1 everywhere (zeros, skipped by the consumers' k-step mask).
+    if (warp != NC / 32) return;
+    const int hl = lane >> 4, jl = lane & 15;
+    auto fetch = [&](int q, int4& rows, int& col, int& op) {
+      const int e = e_begin + 2 * q + hl;
+      const bool live = q < n_pairs && e < e_end;
+      rows = live ? __ldg(reinterpret_cast<const int4*>(p.entry_src + (long long)e * BN) + jl) : make_int4(-1, -1, -1, -1);
+      op = __ldg(p.entry_code + (live ? e : e_begin));
+      col = live ? __ldg(p.op_col + op) : 0;
+    };
+    int4 rows_n;
+    int col_n, op_n;
+    fetch(0, rows_n, col_n, op_n);
     for (int q = 0; q < n_pairs; ++q) {
       const int s = q % STAGES;
-      if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
-      mbar_arrive_expect_tx(full + s, STAGE_TX);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = e_begin + 2 * q + h;
-        const bool live = e < e_end;
-        const int op = __ldg(p.entry_code + (live ? e : e_begin));
-        tma_load_2d(As + (s * 2 + h) * SUB_A, &p.tmap_a, (op & 1) * p.ft_colseg, (op >> 1) * p.ft_rows, full + s);
-        tma_load_2d(Bs + (s * 2 + h) * SUB_B, &p.tmap_b, 0, live ? e * BN : -2 * BN, full + s);
+      const int4 rows = rows_n;
+      const int col = col_n, op = op_n;
+      if (q + 1 < n_pairs) fetch(q + 1, rows_n, col_n, op_n);
+      if (lane == 0) {
+        if (q >= STAGES) mbar_wait_backoff(empty + s, ((q / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(full + s, STAGE_TX);
       }
+      __syncwarp();
+      if (jl == 0)
+        tma_load_2d(As + (s * 2 + hl) * SUB_A, &p.tmap_a, (op & 1) * p.ft_colseg, (op >> 1) * p.ft_rows, full + s);
+      tma_gather4(Bs + (s * 2 + hl) * SUB_B + 4 * jl * LD, &p.tmap_b, col, rows, full + s);
     }
     return;
   }

@@ -109,7 +109,12 @@ struct TileParams {
   int ft_colseg;
   int y_seg;        // pair-mode output rows written as 16-row segments at this pitch (0: contiguous rows)
   const int* y_map; // with y_seg: segment (v * 8 + row / 16) -> destination segment index (-1: not needed)
+  int y_rowblk;     // pair-mode stage-1 output (0: off): row i of entry code c lands at
+                    // y[source * y_ld + y_colmap[c * 128 + i]] (skipped where -1)
+  const int* y_colmap;
   int b_block;      // B of entry e = rows [e * BN, e * BN + BN) of tmap_b (one 2-D box; no gathers)
+  const int* op_col;  // seg_pair_gemm_kernel: B of entry e gathered from its sources' rows of
+                      // tmap_b at column op_col[entry_code[e]]
   const int* seg_ksteps;  // seg_pair_gemm_kernel: live k-steps (0..4) per entry code (null: all 4)
   int l2_hints;     // TMA copies with L2 policies: operators evict_last, sources evict_first
   CUtensorMap tmap_a;

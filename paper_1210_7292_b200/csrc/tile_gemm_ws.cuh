@@ -489,7 +489,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     // measured 4% faster that way, a scheduling side effect; the KC = 32 FTM 1
     // step kernel compiles without it, 0.4% faster)
     constexpr bool kSegCapable = FTM == 3 || KC == 16;
-    const bool seg_out = kSegCapable && p.pair_out && p.y_seg && p.code_is_op;
+    const bool seg_out = kSegCapable && p.pair_out && (p.y_seg || p.y_rowblk) && p.code_is_op;
     if ((seg_out || !p.pair_out) && p.ft_pipe) {
       // Full-operator target tiles whose every chunk is KC/4 whole k-steps
       // (host-checked): one flat chunk stream, software-pipelined across chunk
@@ -599,6 +599,26 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
                         g < 4 ? make_double2(a0, a1) : make_double2(b0, b1);
                   acc[2 * sg][nj][h] = acc[2 * sg + 1][nj][h] = 0.0;
                 }
+          } else if (seg_out && p.y_rowblk && (qq + 1) % nch == 0) {
+            // packed two-stage stage 1: the entry's 128 rows of every source's
+            // Y row, at the columns of ts_colmap (a transfer's rows are
+            // contiguous: the 8 lanes of a tg write runs of up to 64 B)
+            const int* cm = p.y_colmap + (long long)__ldg(p.entry_code + e_begin + qq / nch) * BM + r0 + g;
+            int ycol[MT];
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi) ycol[mi] = __ldg(cm + mrow(mi));
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int v = s_col[ncol(nj) + 2 * tg + h];
+                double* dst = p.y + (long long)v * p.y_ld;
+#pragma unroll
+                for (int mi = 0; mi < MT; ++mi) {
+                  if (v >= 0 && ycol[mi] >= 0) dst[ycol[mi]] = acc[mi][nj][h];
+                  acc[mi][nj][h] = 0.0;
+                }
+              }
           } else if (seg_out && (qq + 1) % nch == 0) {
             const long long ve = (long long)(e_begin + qq / nch) * BN;
 #pragma unroll

@@ -6,11 +6,11 @@ rows + compacted halo), the cfm_gather_rows pack kernel and the tile kernels
 -- while the halo moves over a gloo group staged through the host (NCCL
 cannot run two ranks on one device).  No kernel of one rank waits on the
 other's: the exchange is a host collective between the launches.  The
-gathered owned locals equal the single-rank apply: bitwise with plain
-target-tile plans (CFM_HYBRID=0: every target sums its own pairs in the same
-order on its owner), within round-off (1e-14 relative) with the default
-hybrid plans, where a rank's partial tiles can become pair entries (summed in
-another order) that are full tiles on one rank.  A log goes to
+gathered owned locals equal the single-rank apply: bitwise with target-tile
+plans forced (CFM_PLAN_MODE=target: every target sums its own pairs in its
+tile's entry order, which depends on its transfer multiset only), within
+round-off (1e-14 relative) with the default plans, where a rank's boundary
+subset can plan as pair entries or hybrid tiles (summed in another order).  A log goes to
 gpurun_out/multirank_<case>_<plans>.json.
 """
 
@@ -119,7 +119,7 @@ def test_two_ranks_one_gpu_equal_single_rank(name, plans, monkeypatch):
     from oracle import oracle as O
 
     if plans == "plain":
-        monkeypatch.setenv("CFM_HYBRID", "0")  # inherited by the spawned ranks
+        monkeypatch.setenv("CFM_PLAN_MODE", "target")  # inherited by the spawned ranks
 
     if not torch.cuda.is_available():
         pytest.fail("CUDA device required for -m gpu tests")
