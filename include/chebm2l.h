@@ -36,7 +36,8 @@
  *
  * Memory: mpoles/locals pointers may be host or device memory (detected with
  * cudaPointerGetAttributes).  Host buffers are staged through the handler's
- * device scratch; device buffers are used in place.  `stream` is a
+ * device scratch (only the rows a batch reads / writes; pageable memory through
+ * pinned slots on several host threads); device buffers are used in place.  `stream` is a
  * cudaStream_t (NULL = the CUDA default stream, so work is ordered with the
  * caller's default-stream work).  Calls on one handler are
  * serialized by an internal mutex (the reference may call apply_level from
@@ -253,9 +254,10 @@ int cfm_assemble_operators(int device, int kernel, double wavenumber, int n, con
  * the reference's FmmPlan rebuilds identical batches on every run,
  * engine.py:98-120; they are kept apart from the level plans of
  * cfm_plan_level_*, which they never replace); mode 0 target tiles / 1 pair
- * entries; two_stage 1 for the two-stage low-rank plan.  NULL outputs are
+ * entries; two_stage 1 for the two-stage low-rank plan; plan_id unique per
+ * built plan (a cache hit returns the cached plan's id).  NULL outputs are
  * skipped. */
-int cfm_last_csr_plan_info(cfm_handler* h, int* cache_hit, int* mode, int* two_stage);
+int cfm_last_csr_plan_info(cfm_handler* h, int* cache_hit, int* mode, int* two_stage, uint64_t* plan_id);
 
 /* Device-side timing of the last apply (ms, CUDA events on the apply stream),
  * and the number of kernels it launched. */

@@ -112,7 +112,7 @@ _SIGS = {
     "cfm_fmm_l2p": ([_P, _P, _I, _P, _P], _I),
     "cfm_fmm_p2p": ([_P, _I, _D, _P, _I, _P, _I, _P], _I),
     "cfm_assemble_operators": ([_I, _I, _D, _I, _P, _D, _I, _P, _P, _P], _I),
-    "cfm_last_csr_plan_info": ([_P, _P, _P, _P], _I),
+    "cfm_last_csr_plan_info": ([_P, _P, _P, _P, _P], _I),
     "cfm_classify_targets_count": ([_I, _I, _I64, _P, _I64, _P, _P, _P], _I),
     "cfm_classify_targets_fill": ([_I, _I, _I64, _P, _I64, _P, _P, _P, _P], _I),
     "cfm_gather_rows": ([_I, _P, _I64, _P, _I64, _P, _P], _I),

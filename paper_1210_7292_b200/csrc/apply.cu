@@ -430,27 +430,50 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
 }
 
 void apply_with_buffers(cfm_handler* h, int level, LevelPlan& lp, const double* mpoles, double* locals,
-                               cudaStream_t s) {
+                        cudaStream_t s) {
   const int dc = lp.dc;
-  const size_t row_d = size_t(h->n) * (dc == 2 || h->op_complex ? 2 : 1);
-  const size_t bytes = size_t(lp.n_rows) * row_d * sizeof(double);
+  const size_t row_b = size_t(h->n) * (dc == 2 || h->op_complex ? 2 : 1) * sizeof(double);
+  const size_t bytes = size_t(lp.n_rows) * row_b;
   const bool dev_x = is_device_ptr(mpoles), dev_y = is_device_ptr(locals);
   const double* d_x = mpoles;
   double* d_y = locals;
+  // host buffers: only the rows the plan reads (sources) and writes (targets)
+  // cross PCIe; pageable memory goes through the multi-threaded pinned stager
+  auto h2d = [&](void* dst, const void* src, size_t len) {
+    if (!len) return;
+    if (is_pinned_host(src)) {
+      CUDA_CHECK(cudaMemcpyAsync(dst, src, len, cudaMemcpyHostToDevice, s));
+    } else {
+      if (!h->stager) h->stager = std::make_unique<PinnedStager>();
+      h->stager->h2d(dst, src, len, s, h->device);
+    }
+  };
   if (!dev_x) {
     ensure(h->x_stage, bytes);
-    CUDA_CHECK(cudaMemcpyAsync(h->x_stage.p, mpoles, bytes, cudaMemcpyHostToDevice, s));
+    h2d(h->x_stage.as<char>() + lp.src_lo * row_b, reinterpret_cast<const char*>(mpoles) + lp.src_lo * row_b,
+        size_t(lp.src_hi - lp.src_lo) * row_b);
     d_x = h->x_stage.as<double>();
   }
   if (!dev_y) {
     ensure(h->y_stage, bytes);
-    CUDA_CHECK(cudaMemcpyAsync(h->y_stage.p, locals, bytes, cudaMemcpyHostToDevice, s));
+    h2d(h->y_stage.as<char>() + lp.tgt_lo * row_b, reinterpret_cast<const char*>(locals) + lp.tgt_lo * row_b,
+        size_t(lp.tgt_hi - lp.tgt_lo) * row_b);
     d_y = h->y_stage.as<double>();
   }
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
   h->last_launches = run_plan(h, level, lp, d_x, d_y, s);
   CUDA_CHECK(cudaEventRecord(h->ev1, s));
-  if (!dev_y) CUDA_CHECK(cudaMemcpyAsync(locals, d_y, bytes, cudaMemcpyDeviceToHost, s));
+  if (!dev_y && lp.tgt_hi > lp.tgt_lo) {
+    char* dst = reinterpret_cast<char*>(locals) + lp.tgt_lo * row_b;
+    const char* src = reinterpret_cast<const char*>(d_y) + lp.tgt_lo * row_b;
+    const size_t len = size_t(lp.tgt_hi - lp.tgt_lo) * row_b;
+    if (is_pinned_host(locals)) {
+      CUDA_CHECK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDeviceToHost, s));
+    } else {
+      if (!h->stager) h->stager = std::make_unique<PinnedStager>();
+      h->stager->d2h(dst, src, len, s, h->device);
+    }
+  }
   CUDA_CHECK(cudaStreamSynchronize(s));
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));

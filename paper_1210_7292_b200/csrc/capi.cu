@@ -307,6 +307,7 @@ int cfm_apply_level_csr(cfm_handler* h, int level, int64_t n_targets, const int6
     h->last_csr_hit = hit;
     h->last_csr_mode = lp.mode;
     h->last_csr_two_stage = lp.ts ? 1 : 0;
+    h->last_csr_gen = lp.gen;
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
     {
       cudaStream_t st = pick_stream(h, stream);
@@ -433,13 +434,14 @@ int cfm_plan_two_stage(cfm_handler* h, int level, int* two_stage) {
   });
 }
 
-int cfm_last_csr_plan_info(cfm_handler* h, int* cache_hit, int* mode, int* two_stage) {
+int cfm_last_csr_plan_info(cfm_handler* h, int* cache_hit, int* mode, int* two_stage, uint64_t* plan_id) {
   return guarded([&] {
     if (!h) throw Error(CFM_ERR_VALUE, "null handler");
     std::lock_guard<std::mutex> lk(h->mu);
     if (cache_hit) *cache_hit = h->last_csr_hit ? 1 : 0;
     if (mode) *mode = h->last_csr_mode;
     if (two_stage) *two_stage = h->last_csr_two_stage;
+    if (plan_id) *plan_id = h->last_csr_gen;
   });
 }
 

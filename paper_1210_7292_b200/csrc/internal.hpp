@@ -204,6 +204,8 @@ struct LevelPlan {
   DevBuf s_tile_col, s_tile_off, s_entry_code, s_entry_src;
   DevBuf t_tile_col, t_tile_off, t_entry_code, t_entry_src;
   int64_t n_rows = 0;
+  // rows a host-buffer apply must move: sources [src_lo, src_hi), targets [tgt_lo, tgt_hi)
+  int64_t src_lo = 0, src_hi = 0, tgt_lo = 0, tgt_hi = 0;
   uint64_t gen = 0;  // unique per built plan (merged plans remember what they were built from)
   // two-stage low-rank plans (Group::has_ts): stage 1 over source tiles, stage 2 over target tiles
   bool ts = false;
@@ -263,7 +265,10 @@ struct LevelScratch {  // per-level scratch of concurrently applied levels
   std::vector<int64_t> xpad_sig;
 };
 
+namespace cfm { struct PinnedStager; }
+
 struct cfm_handler {
+  std::unique_ptr<cfm::PinnedStager> stager;  // pageable host buffers (host_stage.hpp)
   int device = 0, variant = 0, order = 0, op_complex = 0;
   int n = 0, f = 1;
   bool sym = false, lowrank = false, shared = false;
@@ -299,6 +304,7 @@ struct cfm_handler {
   int64_t last_launches = 0;
   bool last_csr_hit = false;  // the last cfm_apply_level_csr reused a cached plan
   int last_csr_mode = -1, last_csr_two_stage = 0;  // and that plan's mode / two-stage flag
+  uint64_t last_csr_gen = 0;                        // and its id (unique per built plan)
 };
 
 
@@ -458,3 +464,5 @@ inline void mark_stream(cfm_handler* h, cudaStream_t st) {
 }
 
 }  // namespace cfm
+
+#include "host_stage.hpp"

@@ -1,6 +1,8 @@
 // Apply plans of a level: target tiles, pair entries, hybrid, two-stage low rank, the CSR plan cache.
 #include "internal.hpp"
 
+#include <thread>
+
 namespace cfm {
 
 // ------------------------------------------------------------------ planning
@@ -268,6 +270,14 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
   }
   lp.dc = dc;
   lp.n_rows = n_rows;
+  {  // row spans a host-buffer apply moves (engine.py's thread chunks are contiguous target ranges)
+    int64_t slo = n_rows, shi = 0, tlo = n_rows, thi = 0;
+    const int64_t P = n_targets ? off[n_targets] : 0;
+    for (int64_t i = 0; i < n_targets; ++i)
+      if (off[i + 1] > off[i]) tlo = std::min(tlo, tgt[i]), thi = std::max(thi, tgt[i] + 1);
+    for (int64_t q = 0; q < P; ++q) slo = std::min(slo, src[q]), shi = std::max(shi, src[q] + 1);
+    lp.src_lo = std::min(slo, shi), lp.src_hi = shi, lp.tgt_lo = std::min(tlo, thi), lp.tgt_hi = thi;
+  }
   push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
   const int64_t E = lp.hp.n_entries();
   if (lp.mode == 1) {
@@ -455,6 +465,24 @@ LevelPlan& make_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t
 static constexpr size_t kCsrCacheMaxEntries = 64;
 static constexpr size_t kCsrCacheMaxBytes = size_t(8) << 30;
 
+// memcmp on several threads (a config-2 batch key is ~0.6 GB)
+static bool equal_mt(const void* a, const void* b, size_t bytes) {
+  if (bytes < (size_t(16) << 20)) return std::memcmp(a, b, bytes) == 0;
+  const int T = int(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+  std::vector<std::thread> th;
+  std::atomic<bool> eq{true};
+  const size_t part = (bytes + T - 1) / T;
+  for (int w = 0; w < T; ++w)
+    th.emplace_back([&, w] {
+      const size_t o = size_t(w) * part;
+      if (o < bytes && std::memcmp(static_cast<const char*>(a) + o, static_cast<const char*>(b) + o,
+                                   std::min(part, bytes - o)))
+        eq = false;
+    });
+  for (auto& x : th) x.join();
+  return eq;
+}
+
 LevelPlan& csr_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt, const int64_t* off,
                            const int64_t* src, const int8_t* t, int data_complex, int64_t n_rows, bool* hit_out) {
   const int64_t P = n_targets ? off[n_targets] : 0;
@@ -465,8 +493,8 @@ LevelPlan& csr_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t*
       continue;
     if (n_targets && std::memcmp(e.tgt.data(), tgt, size_t(n_targets) * 8)) continue;
     if (std::memcmp(e.off.data(), off, size_t(n_targets + 1) * 8)) continue;
-    if (P && std::memcmp(e.src.data(), src, size_t(P) * 8)) continue;
-    if (P && std::memcmp(e.t.data(), t, size_t(P) * 3)) continue;
+    if (!equal_mt(e.src.data(), src, size_t(P) * 8)) continue;
+    if (!equal_mt(e.t.data(), t, size_t(P) * 3)) continue;
     h->csr_cache.splice(h->csr_cache.begin(), h->csr_cache, it);  // most recently used first
     if (hit_out) *hit_out = true;
     return h->csr_cache.front().plan;

@@ -197,6 +197,7 @@ class B200M2LHandler:
         self._h = h
         self._planned: dict[int, dict] = {}
         self._rep_code_tab: dict[object, np.ndarray] = {}
+        self._flush_cache: dict[tuple, tuple] = {}  # (native plan id, block_size) -> block statistics of one apply
         self.last_plan_cache_hit = False  # the last apply_level(_csr) reused a cached plan of the same batch
         self._acct: dict[int, tuple] = {}  # level -> (plan stats, group key, flops, block summary)
 
@@ -530,23 +531,31 @@ class B200M2LHandler:
                 data_complex, _native.ptr(x), int(n_rows), _native.ptr(y), self._stream_of(x), counts.ctypes.data))
             if wb is not None:
                 wb[...] = y
-            self.last_plan_cache_hit = self._plan_cache_hit()
+            info = self.last_csr_plan_info()
+            self.last_plan_cache_hit = info["cache_hit"]
             flops = self._count_flops(key, counts, n_targets_nonempty, n_sources)
-            summary = self._flush_summary(key, t) if self.uses_blocking else None
+            summary = None
+            if self.uses_blocking:
+                # the flush sequence is a function of the batch, like the plan:
+                # computed once per plan and reused while the plan is cached
+                ck = (info["plan_id"], self.block_size)
+                summary = self._flush_cache.get(ck)
+                if summary is None:
+                    summary = self._flush_summary(key, t)
+                    if len(self._flush_cache) >= 64:
+                        self._flush_cache.pop(next(iter(self._flush_cache)))
+                    self._flush_cache[ck] = summary
             self._record(level, key, counts, flops, summary=summary)
         return flops
-
-    def _plan_cache_hit(self) -> bool:
-        return self.last_csr_plan_info()["cache_hit"]
 
     def last_csr_plan_info(self) -> dict:
         """Plan of the last apply_level / apply_level_csr call (batch plans are
         cached apart from the level plans of plan_level_*)."""
-        hit, mode, ts = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        hit, mode, ts, pid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_uint64()
         self._check(self._lib.cfm_last_csr_plan_info(self._h, ctypes.byref(hit), ctypes.byref(mode),
-                                                     ctypes.byref(ts)))
+                                                     ctypes.byref(ts), ctypes.byref(pid)))
         return {"cache_hit": bool(hit.value), "mode": {0: "target", 1: "pair"}.get(mode.value),
-                "two_stage": bool(ts.value)}
+                "two_stage": bool(ts.value), "plan_id": int(pid.value)}
 
     def _rep_of_code(self, key) -> np.ndarray:
         """t-code -> representative index of a group (symmetry.assignment)."""

@@ -215,13 +215,15 @@ def test_threaded_chunks_like_fmmplan(torch_cuda, golden):
     batch = O.csr_to_batch(tgt, off, src, t)
     one = np.zeros_like(mp)
     h.apply_level(lvl, batch, mp, one)
-    chunks = [[batch[i] for i in c] for c in np.array_split(np.arange(len(batch)), 4)]
-    for rep in range(2):
-        loc = np.zeros_like(mp)
-        ths = [threading.Thread(target=h.apply_level, args=(lvl, c, mp, loc)) for c in chunks]
-        for th in ths:
-            th.start()
-        for th in ths:
-            th.join()
-        assert O.rel_l2(loc, one) <= 1e-14
+    contiguous = [[batch[i] for i in c] for c in np.array_split(np.arange(len(batch)), 4)]
+    interleaved = [batch[i::4] for i in range(4)]  # overlapping row spans: stresses the span copies
+    for chunks in (contiguous, interleaved):
+        for rep in range(2):
+            loc = np.zeros_like(mp)
+            ths = [threading.Thread(target=h.apply_level, args=(lvl, c, mp, loc)) for c in chunks]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            assert O.rel_l2(loc, one) <= 1e-14
     assert O.rel_l2(one[g[f"rows_{lvl}"]], g[f"locals_iablk_{lvl}"]) <= 1e-10

@@ -27,6 +27,16 @@ for l in levels:
     t0 = time.perf_counter()
     _batch_to_csr(batches[l])
     out[f"csr_ms_L{l}"] = (time.perf_counter() - t0) * 1e3
+# one steady-state call per level, broken down (plans cached by the first call)
+mp = {l: np.random.default_rng(l).uniform(-1, 1, (len(cells[l]), order**3)) for l in levels}
+loc = {l: np.zeros_like(mp[l]) for l in levels}
+for l in levels:
+    h.apply_level(l, batches[l], mp[l], loc[l])
+for l in levels:
+    t0 = time.perf_counter()
+    h.apply_level(l, batches[l], mp[l], loc[l])
+    out[f"call_ms_L{l}"] = (time.perf_counter() - t0) * 1e3
+    out[f"kernel_ms_L{l}"] = h.last_apply_stats()[0]
 del batches
 out["e2e"] = bench.reference_api_e2e(h, cells, levels, order**3, np.float64, 3, 0)
 print(json.dumps(out, indent=1))
