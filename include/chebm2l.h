@@ -201,6 +201,16 @@ int cfm_classify_targets_fill(int device, int level, int64_t n_cells, const int3
                               int64_t n_targets, const int64_t* target_rows,
                               const int64_t* offsets, int32_t* src_out, int8_t* t_out);
 
+/* Partially pivoted ACA (lowrank.py:65-160) of n_ops operators [n_ops][n][n]
+ * (device, row-major, complex interleaved when data_complex), one CTA per
+ * operator, the reference's pivoting and stopping rule at accuracy eps.
+ * u_out / v_out (device, [n_ops][kmax][n]): cross q of operator o in row q
+ * (A ~ sum_q u_q v_q^T before conjugation, lowrank.py:152-153).
+ * rank_out / flag_out (host, n_ops): crosses, 1 converged / 0 stagnated /
+ * 2 more than kmax crosses needed.  m2l.py:206-214, 241-255. */
+int cfm_aca_batch(int device, int n, int data_complex, int n_ops, const double* ops, double eps,
+                  int kmax, double* u_out, double* v_out, int* rank_out, int* flag_out, void* stream);
+
 /* Multi-GPU halo packing: dst[k, :] = src[rows[k], :] for rows of
  * row_doubles doubles (device pointers; rows int64 on the device). */
 int cfm_gather_rows(int device, const double* src, int64_t row_doubles, const int64_t* rows,

@@ -65,6 +65,7 @@ EXPORTS = (
     "cfm_classify_targets_count",
     "cfm_classify_targets_fill",
     "cfm_gather_rows",
+    "cfm_aca_batch",
 )
 
 # libcfm_batch.so (include/chebm2l_batch.h): the reference batch -> CSR in C.
@@ -116,6 +117,7 @@ _SIGS = {
     "cfm_classify_targets_count": ([_I, _I, _I64, _P, _I64, _P, _P, _P], _I),
     "cfm_classify_targets_fill": ([_I, _I, _I64, _P, _I64, _P, _P, _P, _P], _I),
     "cfm_gather_rows": ([_I, _P, _I64, _P, _I64, _P, _P], _I),
+    "cfm_aca_batch": ([_I, _I, _I, _I, _P, _D, _I, _P, _P, _P, _P, _P], _I),
 }
 
 _lib = None

@@ -44,7 +44,7 @@ from .numerics import (
     node_evaluator,
     truncated_svd,
 )
-from .precompute import assemble_stack, device_kernel_kind, shared_basis, truncated_svds
+from .precompute import aca_plus_svds_device, assemble_stack, device_kernel_kind, shared_basis, truncated_svds
 from .symmetry import SymmetryMap
 
 __all__ = [
@@ -325,6 +325,9 @@ class B200M2LHandler:
             vectors = group.symmetry.cone if self.uses_symmetry else group.transfers
             if self.compression == "svd" and self.precompute_on == "device":
                 facs = truncated_svds(self._operators(list(vectors), group.width), self.epsilon)
+                self.factorization_calls += len(facs)
+            elif self.compression == "aca" and self.precompute_on == "device":
+                facs = aca_plus_svds_device(self._operators(list(vectors), group.width), self.epsilon)
                 self.factorization_calls += len(facs)
             else:
                 facs = [self._factorize(t, group.width) for t in vectors]

@@ -227,3 +227,36 @@ def test_threaded_chunks_like_fmmplan(torch_cuda, golden):
                 th.join()
             assert O.rel_l2(loc, one) <= 1e-14
     assert O.rel_l2(one[g[f"rows_{lvl}"]], g[f"locals_iablk_{lvl}"]) <= 1e-10
+
+
+def test_device_aca_matches_host_aca(torch_cuda):
+    """compression="aca" on the device (csrc/aca.cu, one CTA per operator)
+    against the host restatement of lowrank.py:65-184 on the same matrices:
+    equal ranks, equal via_fallback (stagnation -> dense truncated SVD), equal
+    products to round-off.  Operators: l = 5 Laplace at eps 1e-5 and 1e-9, an
+    l = 4 Helmholtz set (complex), a matrix whose probed rows are all zero
+    (stagnation), an exact rank-2 matrix and a random full-rank one."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, assemble_for_transfer, full_far_field_vectors, helmholtz_kernel
+    from paper_1210_7292_b200 import laplace_kernel
+    from paper_1210_7292_b200.numerics import aca_plus_svd
+    from paper_1210_7292_b200.precompute import aca_plus_svds_device
+
+    ts = full_far_field_vectors()[::13]
+    rng = np.random.default_rng(3)
+    lap = np.stack([assemble_for_transfer(laplace_kernel(), t, 0.25, ChebyshevGrid(5)) for t in ts])
+    n = lap.shape[1]
+    stag = np.zeros((n, n))
+    stag[-1] = rng.uniform(-1, 1, n)
+    rank2 = np.outer(rng.uniform(size=n), rng.uniform(size=n)) + np.outer(rng.uniform(size=n), rng.uniform(size=n))
+    full = rng.standard_normal((n, n))
+    helm = np.stack([assemble_for_transfer(helmholtz_kernel(8 * np.pi), t, 0.5, ChebyshevGrid(4)) for t in ts])
+    cases = [(np.concatenate([lap, stag[None], rank2[None], full[None]]), 1e-5), (lap, 1e-9), (helm, 1e-4)]
+    for ops, eps in cases:
+        dev = aca_plus_svds_device(torch.from_numpy(ops).cuda(), eps)
+        for a, f in zip(ops, dev):
+            ref = aca_plus_svd(lambda r, c: a[np.asarray(r), np.asarray(c)], a.shape[0], a.shape[1], eps)
+            assert f.rank == ref.rank and f.via_fallback == ref.via_fallback, (eps, f.rank, ref.rank)
+            p, q = f.reconstruct(), ref.reconstruct()
+            assert np.linalg.norm(p - q) <= 1e-12 * max(np.linalg.norm(q), 1e-300)
+    assert aca_plus_svds_device(torch.from_numpy(cases[0][0]).cuda(), 1e-5)[len(lap)].via_fallback

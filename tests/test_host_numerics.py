@@ -75,3 +75,34 @@ def test_lowrank_ranks_match_reference(golden):
              for t in transfers}
     assert [ranks[t] for t in transfers] == list(g["ranks_ia_2"]) or \
         [ranks[t] for t in transfers if t in set(map(tuple, g["t_2"].tolist()))] == list(g["ranks_ia_2"])
+
+
+def _ops(kernel, order, width, ts):
+    return np.stack([assemble_for_transfer(kernel, t, width, ChebyshevGrid(order)) for t in ts])
+
+
+def test_randomized_truncated_svd_matches_lapack():
+    """The device path's randomized truncated SVD (precompute.truncated_svds_device,
+    run here on CPU tensors) gives the reference's ranks (lowrank.py:53-62:
+    #{s_i > eps s_1}) and factors whose product matches the LAPACK truncation;
+    a full-rank operator (sketch tail above the threshold) falls back to LAPACK."""
+    import torch
+
+    from paper_1210_7292_b200.precompute import truncated_svds_device
+
+    cases = [(laplace_kernel(), 9, 1e-8, 2.0 / 4, [(3, 0, 0), (2, 2, 1), (3, 3, 3), (-2, 3, -1)]),
+             (laplace_kernel(), 5, 1e-5, 1.0 / 4, [(2, 0, 0), (3, 2, 1)]),
+             (helmholtz_kernel(8 * np.pi), 7, 1e-4, 2.0 / 4, [(2, 1, 0), (3, 3, 2)])]
+    for kernel, order, eps, width, ts in cases:
+        ops = _ops(kernel, order, width, ts)
+        dev = truncated_svds_device(torch.from_numpy(ops), eps)
+        for a, f in zip(ops, dev):
+            ref = truncated_svd(a, eps)
+            assert f.rank == ref.rank, (order, f.rank, ref.rank)
+            prod = f.left @ f.right.conj().T
+            ref_prod = ref.left @ ref.right.conj().T
+            assert np.linalg.norm(prod - ref_prod) <= 1e-12 * np.linalg.norm(ref_prod)
+    full = np.random.default_rng(0).standard_normal((2, 200, 200))
+    got = truncated_svds_device(torch.from_numpy(full), 1e-6)
+    for a, f in zip(full, got):
+        assert f.rank == truncated_svd(a, 1e-6).rank == 200
