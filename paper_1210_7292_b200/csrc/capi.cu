@@ -15,6 +15,8 @@
 // only by floating-point reassociation.
 #include "internal.hpp"
 
+#include <thread>
+
 namespace cfm {
 thread_local std::string g_last_error;
 }  // namespace cfm
@@ -324,19 +326,38 @@ int cfm_plan_level_cells(cfm_handler* h, int level, int64_t n_cells, const int32
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_CHECK(cudaSetDevice(h->device));
     cudaStream_t s = pick_stream(h, stream);
+    const double t0 = trace_on() ? wall_ms() : 0.0;
     DeviceLists dl;
     classify_device(level, n_cells, ijk, s, dl, /*want_codes=*/true);
+    const double t1 = trace_on() ? wall_ms() : 0.0;
     std::vector<int32_t> hsrc(dl.total);
     std::vector<int16_t> hcode(dl.total);
-    if (dl.total) {
-      CUDA_CHECK(cudaMemcpyAsync(hsrc.data(), dl.src.p, size_t(dl.total) * 4, cudaMemcpyDeviceToHost, s));
-      CUDA_CHECK(cudaMemcpyAsync(hcode.data(), dl.code.p, size_t(dl.total) * 2, cudaMemcpyDeviceToHost, s));
-      CUDA_CHECK(cudaStreamSynchronize(s));
+    if (dl.total) {  // lists to the host through the multi-threaded pinned stager
+      if (!h->stager) h->stager = std::make_unique<PinnedStager>();
+      h->stager->d2h(hsrc.data(), dl.src.p, size_t(dl.total) * 4, s, h->device);
+      h->stager->d2h(hcode.data(), dl.code.p, size_t(dl.total) * 2, s, h->device);
     }
-    std::vector<int64_t> tgt(n_cells), src64(hsrc.begin(), hsrc.end());
+    const double t2 = trace_on() ? wall_ms() : 0.0;
+    std::vector<int64_t> tgt(n_cells), src64(dl.total);
     std::iota(tgt.begin(), tgt.end(), 0);
+    {  // widen the source rows on several threads
+      const int64_t P = dl.total;
+      const unsigned nth = unsigned(std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                                      std::max<int64_t>(1, P / (int64_t(1) << 20))));
+      std::vector<std::thread> th;
+      auto wid = [&](unsigned w) {
+        for (int64_t q = P * w / nth; q < P * (w + 1) / nth; ++q) src64[q] = hsrc[q];
+      };
+      for (unsigned w = 1; w < nth; ++w) th.emplace_back(wid, w);
+      wid(0);
+      for (auto& x : th) x.join();
+    }
+    const double t3 = trace_on() ? wall_ms() : 0.0;
     LevelPlan& lp = make_plan(h, level, n_cells, tgt.data(), dl.h_off.data(), src64.data(), hcode.data(),
                               data_complex, n_cells);
+    if (trace_on())
+      fprintf(stderr, "[cfm plan L%d] classify %.1f ms, lists D2H %.1f ms, widen %.1f ms, make_plan %.1f ms\n", level,
+              t1 - t0, t2 - t1, t3 - t2, wall_ms() - t3);
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
   });
 }

@@ -348,6 +348,15 @@ struct ClassifyScratch {
   DevBuf grid, counts;
 };
 
+// CFM_TRACE=1: host-side stage timings of plans and applies on stderr
+inline bool trace_on() {
+  static const bool on = getenv("CFM_TRACE") && atoi(getenv("CFM_TRACE"));
+  return on;
+}
+inline double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 // ---- functions defined in launch.cu / operators.cu / plan.cu / apply.cu / classify.cu
 int tile_kernel_kind(int nk = 0);
 bool use_bulk_a(int kc);

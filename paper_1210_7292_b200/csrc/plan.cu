@@ -155,14 +155,26 @@ void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, const i
   const HostPlan& hp = lp.hp;
   std::vector<char> leftover_tile(hp.n_tiles, 0);
   std::vector<char> leftover_row(lp.n_rows, 0);
+  {  // tiles less than half full (parallel scan of the entries)
+    const unsigned nth = unsigned(std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                                    std::max<int64_t>(1, hp.n_tiles / 256)));
+    auto scan = [&](unsigned w) {
+      for (int64_t t = int64_t(w) * hp.n_tiles / nth; t < int64_t(w + 1) * hp.n_tiles / nth; ++t) {
+        int64_t valid = 0;
+        const int64_t slots = int64_t(hp.tile_off[t + 1] - hp.tile_off[t]) * kBN;
+        for (size_t i = size_t(hp.tile_off[t]) * kBN; i < size_t(hp.tile_off[t + 1]) * kBN; ++i)
+          valid += hp.entry_src[i] >= 0;
+        leftover_tile[t] = slots != 0 && 2 * valid < slots;
+      }
+    };
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nth; ++w) th.emplace_back(scan, w);
+    scan(0);
+    for (auto& x : th) x.join();
+  }
   int64_t n_left = 0;
   for (int64_t t = 0; t < hp.n_tiles; ++t) {
-    int64_t valid = 0;
-    const int64_t slots = int64_t(hp.tile_off[t + 1] - hp.tile_off[t]) * kBN;
-    for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e)
-      for (int c = 0; c < kBN; ++c) valid += hp.entry_src[size_t(e) * kBN + c] >= 0;
-    if (slots == 0 || 2 * valid >= slots) continue;
-    leftover_tile[t] = 1;
+    if (!leftover_tile[t]) continue;
     ++n_left;
     for (int c = 0; c < kBN; ++c) {
       const int v = hp.tile_col[size_t(t) * kBN + c];
@@ -185,17 +197,35 @@ void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, const i
   });
   const int max_e = kept.empty() ? 0 : hp.tile_off[kept[0] + 1] - hp.tile_off[kept[0]];
   for (int64_t t : kept) hy->n_long += (hp.tile_off[t + 1] - hp.tile_off[t]) * 10 >= max_e * 9;
-  for (int64_t t : kept) {
-    mn.tile_col.insert(mn.tile_col.end(), hp.tile_col.begin() + t * kBN, hp.tile_col.begin() + (t + 1) * kBN);
-    mn.tile_off.push_back(int(mn.entry_code.size()));
-    for (int e = hp.tile_off[t]; e < hp.tile_off[t + 1]; ++e) {
-      mn.entry_code.push_back(hp.entry_code[e]);
-      mn.entry_src.insert(mn.entry_src.end(), hp.entry_src.begin() + size_t(e) * kBN,
-                          hp.entry_src.begin() + size_t(e + 1) * kBN);
+  {  // copy the kept tiles (offsets first, then the entries in parallel)
+    mn.n_tiles = int64_t(kept.size());
+    mn.tile_off.resize(kept.size() + 1);
+    mn.tile_col.resize(kept.size() * kBN);
+    int64_t ne = 0;
+    for (size_t i = 0; i < kept.size(); ++i) {
+      mn.tile_off[i] = int(ne);
+      ne += hp.tile_off[kept[i] + 1] - hp.tile_off[kept[i]];
     }
-    ++mn.n_tiles;
+    mn.tile_off[kept.size()] = int(ne);
+    mn.entry_code.resize(ne);
+    mn.entry_src.resize(size_t(ne) * kBN);
+    const unsigned nth = unsigned(std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                                    std::max<int64_t>(1, int64_t(kept.size()) / 256)));
+    auto copy = [&](unsigned w) {
+      for (size_t i = kept.size() * w / nth; i < kept.size() * (w + 1) / nth; ++i) {
+        const int64_t t = kept[i];
+        std::copy(hp.tile_col.begin() + t * kBN, hp.tile_col.begin() + (t + 1) * kBN, mn.tile_col.begin() + i * kBN);
+        std::copy(hp.entry_code.begin() + hp.tile_off[t], hp.entry_code.begin() + hp.tile_off[t + 1],
+                  mn.entry_code.begin() + mn.tile_off[i]);
+        std::copy(hp.entry_src.begin() + size_t(hp.tile_off[t]) * kBN, hp.entry_src.begin() + size_t(hp.tile_off[t + 1]) * kBN,
+                  mn.entry_src.begin() + size_t(mn.tile_off[i]) * kBN);
+      }
+    };
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nth; ++w) th.emplace_back(copy, w);
+    copy(0);
+    for (auto& x : th) x.join();
   }
-  mn.tile_off.push_back(int(mn.entry_code.size()));
   // leftover targets' far lists (CSR order kept) -> pair entries
   std::vector<int64_t> t2, o2{0}, s2;
   std::vector<int16_t> c2;
@@ -238,7 +268,10 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
     for (int c = 0; c < kNumCodes; ++c) key[c] = g.valid[c] ? c : -1;
   LevelPlan lp;
   try {
+    const double tp0 = trace_on() ? wall_ms() : 0.0;
     lp.hp = build_plan_csr(n_targets, tgt, off, src, codes, dc, key, n_rows);
+    if (trace_on()) fprintf(stderr, "[cfm plan L%d] build_plan_csr %.1f ms (%lld pairs)\n", level, wall_ms() - tp0,
+                            (long long)(n_targets ? off[n_targets] : 0));
     const double slots = double(lp.hp.n_entries()) * kBN;
     lp.target_fill = slots > 0 ? double(lp.hp.n_pairs) * dc / slots : 1.0;
     const char* m = getenv("CFM_PLAN_MODE");
@@ -268,6 +301,7 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
   } catch (const PlanError& e) {
     throw Error(e.code == 2 ? CFM_ERR_PRECOMPUTE : CFM_ERR_VALUE, e.what());
   }
+  const double tu0 = trace_on() ? wall_ms() : 0.0;
   lp.dc = dc;
   lp.n_rows = n_rows;
   {  // row spans a host-buffer apply moves (engine.py's thread chunks are contiguous target ranges)
@@ -441,6 +475,7 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
       throw Error(e.code == 2 ? CFM_ERR_PRECOMPUTE : CFM_ERR_VALUE, e.what());
     }
   }
+  if (trace_on()) fprintf(stderr, "[cfm plan L%d] uploads + hybrid / two-stage plans %.1f ms\n", level, wall_ms() - tu0);
   static std::atomic<uint64_t> plan_gen{0};
   lp.gen = ++plan_gen;
   return lp;

@@ -94,26 +94,48 @@ inline HostPlan build_plan_csr(int64_t n_targets, const int64_t* tgt, const int6
   grp_start.push_back(int64_t(grp_items.size()));
   const int64_t nu = int64_t(uniq_first.size());
 
-  // 2. code-multiset hash per unique target (order independent)
+  unsigned nth = n_threads > 0 ? unsigned(n_threads) : std::max(1u, std::thread::hardware_concurrency());
+  // 2. code-multiset hash per unique target (order independent), validity
+  //    checks; parallel over unique targets (the first error in target order wins)
   std::vector<uint64_t> hash(nu, 0);
-  for (int64_t u = 0; u < nu; ++u) {
-    uint64_t h = 0;
-    for (int64_t gi = grp_start[u]; gi < grp_start[u + 1]; ++gi) {
-      const int64_t b = grp_items[gi];
-      for (int64_t q = off[b]; q < off[b + 1]; ++q) {
-        const int c = codes[q];
-        if (c < 0 || c >= kNumCodes) throw PlanError(1, "transfer vector outside [-3,3]^3");
-        if (opkey[c] < 0) {
-          int t0, t1, t2;
-          tcode_decode(c, t0, t1, t2);
-          throw PlanError(2, "no operator for transfer vector (" + std::to_string(t0) + ", " +
-                                 std::to_string(t1) + ", " + std::to_string(t2) + ")");
+  {
+    const unsigned nh = unsigned(std::min<int64_t>(nth, std::max<int64_t>(1, nu / 4096)));
+    std::vector<int64_t> bad_u(nh, nu);
+    std::vector<int> bad_kind(nh, 0), bad_code(nh, 0);
+    auto hwork = [&](unsigned w) {
+      for (int64_t u = int64_t(w) * nu / nh; u < int64_t(w + 1) * nu / nh; ++u) {
+        uint64_t h = 0;
+        for (int64_t gi = grp_start[u]; gi < grp_start[u + 1]; ++gi) {
+          const int64_t b = grp_items[gi];
+          for (int64_t q = off[b]; q < off[b + 1]; ++q) {
+            const int c = codes[q];
+            int kind = 0;
+            if (c < 0 || c >= kNumCodes) kind = 1;
+            else if (opkey[c] < 0) kind = 2;
+            else if (src[q] < 0 || src[q] >= n_rows) kind = 3;
+            if (kind) {
+              bad_u[w] = u, bad_kind[w] = kind, bad_code[w] = c;
+              return;
+            }
+            h += splitmix64(uint64_t(c) + 1);
+          }
         }
-        if (src[q] < 0 || src[q] >= n_rows) throw PlanError(1, "source row out of range");
-        h += splitmix64(uint64_t(c) + 1);
+        hash[u] = h;
       }
+    };
+    std::vector<std::thread> hp;
+    for (unsigned w = 1; w < nh; ++w) hp.emplace_back(hwork, w);
+    hwork(0);
+    for (auto& th : hp) th.join();
+    for (unsigned w = 0; w < nh; ++w) {
+      if (bad_u[w] == nu) continue;
+      if (bad_kind[w] == 1) throw PlanError(1, "transfer vector outside [-3,3]^3");
+      if (bad_kind[w] == 3) throw PlanError(1, "source row out of range");
+      int t0, t1, t2;
+      tcode_decode(bad_code[w], t0, t1, t2);
+      throw PlanError(2, "no operator for transfer vector (" + std::to_string(t0) + ", " + std::to_string(t1) +
+                             ", " + std::to_string(t2) + ")");
     }
-    hash[u] = h;
   }
   // 3. order: by hash, then by first appearance in the batch
   std::vector<int64_t> uord(nu);
@@ -134,7 +156,6 @@ inline HostPlan build_plan_csr(int64_t n_targets, const int64_t* tgt, const int6
   // 5. entries per tile (parallel over tiles)
   std::vector<std::vector<int>> t_code(n_tiles), t_src(n_tiles);
   std::vector<std::array<int64_t, kNumCodes>> part_count;
-  unsigned nth = n_threads > 0 ? unsigned(n_threads) : std::max(1u, std::thread::hardware_concurrency());
   nth = unsigned(std::min<int64_t>(nth, std::max<int64_t>(1, n_tiles / 64)));
   part_count.resize(nth);
   auto work = [&](unsigned w) {
@@ -203,10 +224,19 @@ inline HostPlan build_plan_csr(int64_t n_targets, const int64_t* tgt, const int6
   plan.tile_off[n_tiles] = int(e);
   plan.entry_code.resize(e);
   plan.entry_src.resize(size_t(e) * kBN);
-  for (int64_t tile = 0; tile < n_tiles; ++tile) {
-    std::copy(t_code[tile].begin(), t_code[tile].end(), plan.entry_code.begin() + plan.tile_off[tile]);
-    std::copy(t_src[tile].begin(), t_src[tile].end(),
-              plan.entry_src.begin() + size_t(plan.tile_off[tile]) * kBN);
+  {  // parallel over tile ranges (the copy of a level-7 plan is ~1.5 GB)
+    auto cwork = [&](unsigned w) {
+      for (int64_t tile = int64_t(w) * n_tiles / nth; tile < int64_t(w + 1) * n_tiles / nth; ++tile) {
+        std::copy(t_code[tile].begin(), t_code[tile].end(), plan.entry_code.begin() + plan.tile_off[tile]);
+        std::copy(t_src[tile].begin(), t_src[tile].end(),
+                  plan.entry_src.begin() + size_t(plan.tile_off[tile]) * kBN);
+        std::vector<int>().swap(t_src[tile]);
+      }
+    };
+    std::vector<std::thread> cp;
+    for (unsigned w = 1; w < nth; ++w) cp.emplace_back(cwork, w);
+    cwork(0);
+    for (auto& th : cp) th.join();
   }
   return plan;
 }
