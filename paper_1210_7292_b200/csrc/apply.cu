@@ -201,6 +201,9 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     a.x = xp; a.x_ld = ldx; a.x_dc = 1; a.x_rows = lp.n_rows;
     a.y = lp.ts_y.as<double>(); a.y_ld = g.ts_ldy; a.y_dc = 1; a.y_rowblk = g.ts_nb;
     a.y_colmap = g.ts_colmap.as<int>();
+#ifdef CFM_EXPERIMENTS
+    if (getenv("CFM_EXP") && !strcmp(getenv("CFM_EXP"), "nostore1")) a.debug = 128;  // timing only: no Y stores
+#endif
     a.scale = 1.0; a.accumulate = 0; a.pair_out = 1;
     a.zero_row = h->zeros.as<double>();
     a.n_entries = lp.ts1.n_entries();

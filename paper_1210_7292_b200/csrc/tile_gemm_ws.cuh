@@ -615,7 +615,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
                 double* dst = p.y + (long long)v * p.y_ld;
 #pragma unroll
                 for (int mi = 0; mi < MT; ++mi) {
-                  if (v >= 0 && ycol[mi] >= 0) dst[ycol[mi]] = acc[mi][nj][h];
+                  if (v >= 0 && ycol[mi] >= 0 && !(CFM_DEBUG(p) & 128)) dst[ycol[mi]] = acc[mi][nj][h];
                   acc[mi][nj][h] = 0.0;
                 }
               }
