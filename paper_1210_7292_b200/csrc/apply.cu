@@ -1207,14 +1207,19 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
     }
     if (!reduced_early) reduce_pairs(s);
   } else {
+    // low-rank and shared-basis levels: independent per-level launch chains
     bool all_lr = lv.size() > 1 && use_concurrent_levels();
-    for (auto& L : lv) all_lr = all_lr && group_for_level(h, L.level).kind == kLowRank;
+    for (auto& L : lv) {
+      const int kind = group_for_level(h, L.level).kind;
+      all_lr = all_lr && (kind == kLowRank || kind == kShared);
+    }
     if (!all_lr) {
       for (auto& L : lv) launches += run_plan(h, L.level, *L.lp, L.x, L.y, s);
     } else {
-      // low-rank levels are independent and each is a separate launch chain:
-      // run them side by side on forked streams, each with its own scratch
-      // (per-pair rows, padded sources), so small latency-bound levels overlap
+      // low-rank / shared-basis levels are independent and each is a separate
+      // launch chain: run them side by side on forked streams, each with its
+      // own scratch (per-pair rows, padded sources, SA W~ / Z), so small
+      // latency-bound levels overlap
       const size_t nl = lv.size();
       if (h->aux.size() < nl) {
         h->aux.resize(nl);
@@ -1230,23 +1235,24 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
         }
         CUDA_CHECK(cudaStreamWaitEvent(a.s, h->ev_fork, 0));
         LevelScratch& sc = h->lvl_scratch[k];
-        std::swap(h->fbuf, sc.fbuf);
-        std::swap(h->xpad, sc.xpad);
-        std::swap(h->xpad_sig, sc.xpad_sig);
-        std::swap(h->ybuf, sc.ybuf);
-        try {
-          launches += run_plan(h, lv[k].level, *lv[k].lp, lv[k].x, lv[k].y, a.s);
-        } catch (...) {
+        auto swap_scratch = [&] {
           std::swap(h->fbuf, sc.fbuf);
           std::swap(h->xpad, sc.xpad);
           std::swap(h->xpad_sig, sc.xpad_sig);
           std::swap(h->ybuf, sc.ybuf);
+          std::swap(h->wt, sc.wt);
+          std::swap(h->z, sc.z);
+          std::swap(h->fzbuf, sc.fzbuf);
+          std::swap(h->wt_ld_zeroed, sc.wt_ld_zeroed);
+        };
+        swap_scratch();
+        try {
+          launches += run_plan(h, lv[k].level, *lv[k].lp, lv[k].x, lv[k].y, a.s);
+        } catch (...) {
+          swap_scratch();
           throw;
         }
-        std::swap(h->fbuf, sc.fbuf);
-        std::swap(h->xpad, sc.xpad);
-        std::swap(h->xpad_sig, sc.xpad_sig);
-        std::swap(h->ybuf, sc.ybuf);
+        swap_scratch();
         CUDA_CHECK(cudaEventRecord(a.done, a.s));
         CUDA_CHECK(cudaStreamWaitEvent(s, a.done, 0));
       }

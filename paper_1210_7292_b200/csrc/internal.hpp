@@ -261,8 +261,9 @@ struct CsrPlanEntry {  // one cached plan of cfm_apply_level_csr and the exact b
 };
 
 struct LevelScratch {  // per-level scratch of concurrently applied levels
-  DevBuf fbuf, xpad, ybuf;
+  DevBuf fbuf, xpad, ybuf, wt, z, fzbuf;
   std::vector<int64_t> xpad_sig;
+  long long wt_ld_zeroed = -1;
 };
 
 namespace cfm { struct PinnedStager; }
