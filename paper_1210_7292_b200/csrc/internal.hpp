@@ -378,7 +378,6 @@ int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int6
 int64_t launch_range(const TileParams& p, int64_t first, int64_t count, cudaStream_t s);
 int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s);
 int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s);
-int64_t launch_ft16(TileParams q, int64_t n_tiles, cudaStream_t s);
 void fill_ops(TileParams& p, const OpStack& s, const CodeMap& m);
 void fill_plan(TileParams& p, const DevBuf& col, const DevBuf& toff, const DevBuf& code, const DevBuf& src,
                       int64_t n_tiles);

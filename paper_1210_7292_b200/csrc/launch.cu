@@ -150,7 +150,7 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
         mp.seg[i].ft_pipe = ft_pipe_enabled() && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
         mp.seg[i].ft_ktail = mp.seg[i].ft_pipe && rem == KC - 3 && !mp.seg[i].op_rows && ktail_enabled();
       }
-      auto kf = (q.y_map || q.y_rowblk) ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
+      auto kf = q.y_rowblk ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
                 : skip    ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
                           : tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 1>;
       CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ft));
@@ -382,30 +382,6 @@ int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s) {
   const int smem = seg_pair_smem_bytes();
   CUDA_CHECK(cudaFuncSetAttribute(seg_pair_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   seg_pair_gemm_kernel<<<unsigned(n_tiles), 12 * 32, smem, s>>>(q);
-  CUDA_CHECK(cudaGetLastError());
-  return 1;
-}
-
-// Full-operator kernel with 16-wide K chunks (two-stage low-rank stage 2: one
-// chunk per rank segment), one segment, pipelined consumer loop.
-int64_t launch_ft16(TileParams q, int64_t n_tiles, cudaStream_t s) {
-  constexpr int KC = 16, STAGES = 6;
-  if (n_tiles <= 0) return 0;
-  if (n_tiles >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
-  MultiTileParams mp{};
-  mp.n_seg = 1;
-  mp.nrb = 1;
-  mp.start[0] = 0;
-  mp.start[1] = int(n_tiles);
-  q.tile_base = 0;
-  encode_source_map(q, KC);
-  q.ft_pipe = ft_pipe_enabled() && q.nk % KC == 0;
-  q.l2_hints = getenv("CFM_L2_HINTS") ? atoi(getenv("CFM_L2_HINTS")) : 0;
-  mp.seg[0] = q;
-  auto kf = tile_gemm_ws_kernel<128, kBN, 4, 2, KC, STAGES, false, false, 1>;
-  const int smem = ws_ring_bytes<128, kBN, KC, STAGES>() + tile_table_bytes(q.nr, q.nk, false) + kMaxTileEntries;
-  CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kf<<<unsigned(n_tiles), (4 * 2 + 4) * 32, smem, s>>>(mp);
   CUDA_CHECK(cudaGetLastError());
   return 1;
 }

@@ -107,8 +107,6 @@ struct TileParams {
   int code_is_op;   // entry codes are operator ids (no code tables, identity permutations)
   int ft_opshift;   // operator id o -> A block row (o >> ft_opshift) * ft_rows, column (o & mask) * ft_colseg
   int ft_colseg;
-  int y_seg;        // pair-mode output rows written as 16-row segments at this pitch (0: contiguous rows)
-  const int* y_map; // with y_seg: segment (v * 8 + row / 16) -> destination segment index (-1: not needed)
   int y_rowblk;     // pair-mode stage-1 output (0: off): row i of entry code c lands at
                     // y[source * y_ld + y_colmap[c * 128 + i]] (skipped where -1)
   const int* y_colmap;

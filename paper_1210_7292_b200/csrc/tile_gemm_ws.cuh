@@ -481,7 +481,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     }
   };
   if constexpr (FTM == 1 || FTM == 3) {
-    // FTM 3: pair-mode stage-1 tiles of the two-stage low-rank path (y_seg,
+    // FTM 3: pair-mode stage-1 tiles of the two-stage low-rank path (y_rowblk,
     // operator-id codes: every entry has the same chunk count and the tile's
     // columns) run the flat loop too, writing each entry's rows when its last
     // chunk is done
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
     // measured 4% faster that way, a scheduling side effect; the KC = 32 FTM 1
     // step kernel compiles without it, 0.4% faster)
     constexpr bool kSegCapable = FTM == 3 || KC == 16;
-    const bool seg_out = kSegCapable && p.pair_out && (p.y_seg || p.y_rowblk) && p.code_is_op;
+    const bool seg_out = kSegCapable && p.pair_out && p.y_rowblk && p.code_is_op;
     if ((seg_out || !p.pair_out) && p.ft_pipe) {
       // Full-operator target tiles whose every chunk is KC/4 whole k-steps
       // (host-checked): one flat chunk stream, software-pipelined across chunk
@@ -519,21 +519,8 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
         };
         mbar_wait(full, 0);
         load(a0, b0, 0, 0);
-        // seg_out with a destination map: each thread's 2 segments x 8 columns,
-        // looked up at the start of an entry's last chunk (latency under its MMAs)
-        int dmap[2][NTL][2];
         for (int qq = 0; qq < total; ++qq) {
           const int s = qq % STAGES;
-          if (seg_out && p.y_map && (qq + 1) % nch == 0) {
-            const long long ve = (long long)(e_begin + qq / nch) * BN;
-#pragma unroll
-            for (int sg = 0; sg < 2; ++sg)
-#pragma unroll
-              for (int nj = 0; nj < NTL; ++nj)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-                  dmap[sg][nj][h] = __ldg(p.y_map + (ve + ncol(nj) + 2 * tg + h) * 8 + ((r0 + mrow(2 * sg)) >> 4));
-          }
           // an entry's last k-step with one real column (p.ft_ktail: nk % KC ==
           // KC - 3, e.g. l = 5) runs as a rank-1 DFMA update instead of a DMMA
           // over 3 zero columns: DMMA and DFMA share the FP64 pipe
@@ -578,28 +565,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + s);
-          if (seg_out && p.y_map && (qq + 1) % nch == 0) {
-            // each (column, 16-row segment) is held by the 8 lanes of one tg
-            // (rows g and g + 8): shuffle so lane g holds rows 2g, 2g + 1 and
-            // store 16 B per lane -- one warp store writes 4 whole 128-B segments
-            static_assert(MT % 2 == 0, "segments are pairs of m-tiles");
-#pragma unroll
-            for (int sg = 0; sg < MT / 2; ++sg)
-#pragma unroll
-              for (int nj = 0; nj < NTL; ++nj)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const double vlo = acc[2 * sg][nj][h], vhi = acc[2 * sg + 1][nj][h];
-                  const int s0 = ((2 * g) & 7) * 4 + tg, s1 = ((2 * g + 1) & 7) * 4 + tg;
-                  const double a0 = __shfl_sync(0xffffffffu, vlo, s0), b0 = __shfl_sync(0xffffffffu, vhi, s0);
-                  const double a1 = __shfl_sync(0xffffffffu, vlo, s1), b1 = __shfl_sync(0xffffffffu, vhi, s1);
-                  const int d = dmap[sg][nj][h];
-                  if (d >= 0)
-                    *reinterpret_cast<double2*>(p.y + (long long)d * p.y_seg + 2 * g) =
-                        g < 4 ? make_double2(a0, a1) : make_double2(b0, b1);
-                  acc[2 * sg][nj][h] = acc[2 * sg + 1][nj][h] = 0.0;
-                }
-          } else if (seg_out && p.y_rowblk && (qq + 1) % nch == 0) {
+          if (seg_out && (qq + 1) % nch == 0) {
             // packed two-stage stage 1: the entry's 128 rows of every source's
             // Y row, at the columns of ts_colmap (a transfer's rows are
             // contiguous: the 8 lanes of a tg write runs of up to 64 B)
@@ -619,21 +585,6 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
                   acc[mi][nj][h] = 0.0;
                 }
               }
-          } else if (seg_out && (qq + 1) % nch == 0) {
-            const long long ve = (long long)(e_begin + qq / nch) * BN;
-#pragma unroll
-            for (int mi = 0; mi < MT; ++mi) {
-              const int row = r0 + mrow(mi) + g;
-              const long long ro = (long long)(row >> 4) * p.y_seg + (row & 15);
-#pragma unroll
-              for (int nj = 0; nj < NTL; ++nj)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const int c = ncol(nj) + 2 * tg + h;
-                  if (row < p.nr && s_col[c] >= 0) p.y[(ve + c) * p.y_ld + ro] = acc[mi][nj][h];
-                  acc[mi][nj][h] = 0.0;
-                }
-            }
           }
         }
       }
@@ -731,7 +682,7 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
             const int c = ncol(nj) + 2 * tg + h;
             if (row < p.nr && __ldg(p.entry_src + (long long)e * BN + c) >= 0) {
               const long long v = (long long)e * BN + c;
-              const long long ro = p.y_seg ? (long long)(row >> 4) * p.y_seg + (row & 15) : (long long)p.y_dc * row;
+              const long long ro = (long long)p.y_dc * row;
               double* dst = p.y + (v / p.y_dc) * p.y_ld + (v % p.y_dc) + ro;
               const double val = p.scale * acc[mi][nj][h];
               if (p.accumulate)
