@@ -330,6 +330,20 @@ int cfm_plan_level_cells(cfm_handler* h, int level, int64_t n_cells, const int32
     DeviceLists dl;
     classify_device(level, n_cells, ijk, s, dl, /*want_codes=*/true);
     const double t1 = trace_on() ? wall_ms() : 0.0;
+    {  // dense full-operator levels: the whole plan on the device (plan_device.cu)
+      Group& g = group_for_level(h, level);
+      if (use_device_plan() && g.kind == kDense && g.has_full && !data_complex && !h->op_complex) {
+        LevelPlan lp;
+        if (device_plan_dense(h, level, g, n_cells, reinterpret_cast<const int64_t*>(dl.off.p), dl.h_off,
+                              dl.src.as<int32_t>(), dl.code.as<int16_t>(), n_cells, s, lp)) {
+          lp.gen = next_plan_gen();
+          h->plans[level] = std::move(lp);
+          const LevelPlan& pl = h->plans[level];
+          if (pair_count_out) std::copy(pl.hp.code_count.begin(), pl.hp.code_count.end(), pair_count_out);
+          return;
+        }
+      }
+    }
     std::vector<int32_t> hsrc(dl.total);
     std::vector<int16_t> hcode(dl.total);
     if (dl.total) {  // lists to the host through the multi-threaded pinned stager

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <atomic>
 #include <list>
 #include <map>
@@ -357,6 +358,14 @@ inline bool trace_on() {
 inline double wall_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+
+uint64_t next_plan_gen();
+void set_slab_plan(cfm_handler* h, int level, LevelPlan& lp,
+                   const std::function<void(int64_t, int64_t&, int64_t&, int64_t&)>& tile_rows);
+bool use_device_plan();
+bool device_plan_dense(cfm_handler* h, int level, const Group& g, int64_t n, const int64_t* d_off,
+                       const std::vector<int64_t>& h_off, const int32_t* d_src, const int16_t* d_code,
+                       int64_t n_rows, cudaStream_t s, LevelPlan& lp);
 
 // ---- functions defined in launch.cu / operators.cu / plan.cu / apply.cu / classify.cu
 int tile_kernel_kind(int nk = 0);

@@ -1,6 +1,7 @@
 // Apply plans of a level: target tiles, pair entries, hybrid, two-stage low rank, the CSR plan cache.
 #include "internal.hpp"
 
+#include <functional>
 #include <thread>
 
 namespace cfm {
@@ -255,6 +256,79 @@ void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, const i
   lp.hyb = std::move(hy);
 }
 
+uint64_t next_plan_gen() {
+  static std::atomic<uint64_t> plan_gen{0};
+  return ++plan_gen;
+}
+
+// Host<->device copy pipeline of a target-tile level: row slabs, and per tile
+// the multipole / locals slabs it needs (tile_rows(t, min target row, max
+// target row, max source row)); every CTA (tile x row block) writing a slab is
+// counted so the download of a finished slab can start while the kernel runs.
+void set_slab_plan(cfm_handler* h, int level, LevelPlan& lp,
+                   const std::function<void(int64_t, int64_t&, int64_t&, int64_t&)>& tile_rows) {
+  const int64_t n_rows = lp.n_rows;
+  const int64_t nt = lp.hp.n_tiles;
+  // slabs of ~32K rows (at most 16); CFM_SLAB_ROWS / CFM_MAX_SLABS for experiments
+  static const int64_t slab_rows = [] {
+    const char* e = getenv("CFM_SLAB_ROWS");
+    return e ? std::max<int64_t>(1024, atoll(e)) : int64_t(32768);
+  }();
+  static const int64_t max_slabs = [] {
+    const char* e = getenv("CFM_MAX_SLABS");
+    return e ? std::max<int64_t>(2, atoll(e)) : int64_t(16);
+  }();
+  static const int64_t min_rows = [] {  // levels with fewer rows are not host-pipelined
+    const char* e = getenv("CFM_PIPE_MIN_ROWS");
+    return e ? atoll(e) : int64_t(0);
+  }();
+  int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
+  if (min_rows > 0) S = n_rows >= min_rows ? std::max(S, 2) : 1;
+  // the last slab's download cannot start before the kernel's last wave
+  // ends: split it into halves, quarters, eighths (CFM_SLAB_TAIL=0: uniform)
+  static const int slab_tail = [] {
+    const char* e = getenv("CFM_SLAB_TAIL");
+    return e ? std::max(0, atoi(e)) : 3;
+  }();
+  lp.slab_row0.clear();
+  for (int k = 0; k < S; ++k) lp.slab_row0.push_back(n_rows * k / S);
+  if (S >= 2) {
+    const int64_t a = n_rows * (S - 1) / S, len = n_rows - a;
+    int64_t r = a;
+    for (int d = 1; d <= slab_tail && S + d <= 16 && (len >> d) >= 1024; ++d) {
+      r += len >> d;
+      lp.slab_row0.push_back(r);
+    }
+  }
+  lp.slab_row0.push_back(n_rows);
+  const int S_all = int(lp.slab_row0.size()) - 1;
+  lp.n_slabs = S_all;
+  auto slab_of = [&](int64_t row) {
+    const auto it = std::upper_bound(lp.slab_row0.begin(), lp.slab_row0.end(), row);
+    return int(std::min<int64_t>(S_all - 1, std::max<int64_t>(0, (it - lp.slab_row0.begin()) - 1)));
+  };
+  std::vector<int> need_mp(nt, 0), need_loc(nt, 0), lo(nt, 0), hi(nt, -1);
+  lp.slab_expected.assign(S_all, 0);
+  const int nrb = (group_for_level(h, level).dense.rows + 127) / 128;
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t tmin, tmax, smax;
+    tile_rows(t, tmin, tmax, smax);  // slab_of is monotonic: the extreme rows give the extreme slabs
+    int l = S_all, hh = -1, m = 0;
+    if (tmax >= 0) l = slab_of(tmin), hh = slab_of(tmax);
+    if (smax >= 0) m = slab_of(smax) + 1;
+    if (hh < 0) { l = 0; hh = -1; }
+    need_mp[t] = m;
+    need_loc[t] = hh + 1;
+    lo[t] = l;
+    hi[t] = hh;
+    for (int k = l; k <= hh; ++k) lp.slab_expected[k] += unsigned(nrb);
+  }
+  upload(lp.p_need_mp, need_mp);
+  upload(lp.p_need_loc, need_loc);
+  upload(lp.p_lo, lo);
+  upload(lp.p_hi, hi);
+}
+
 LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const int64_t* tgt,
                                   const int64_t* off, const int64_t* src, const int16_t* codes, int data_complex,
                                   int64_t n_rows) {
@@ -400,72 +474,18 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
     np_.tile_off[nt] = int(np_.entry_code.size());
     lp.hp = std::move(np_);
     push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
-    // slabs of ~32K rows (at most 16); CFM_SLAB_ROWS / CFM_MAX_SLABS for experiments
-    static const int64_t slab_rows = [] {
-      const char* e = getenv("CFM_SLAB_ROWS");
-      return e ? std::max<int64_t>(1024, atoll(e)) : int64_t(32768);
-    }();
-    static const int64_t max_slabs = [] {
-      const char* e = getenv("CFM_MAX_SLABS");
-      return e ? std::max<int64_t>(2, atoll(e)) : int64_t(16);
-    }();
-    static const int64_t min_rows = [] {  // levels with fewer rows are not host-pipelined
-      const char* e = getenv("CFM_PIPE_MIN_ROWS");
-      return e ? atoll(e) : int64_t(0);
-    }();
-    int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
-    if (min_rows > 0) S = n_rows >= min_rows ? std::max(S, 2) : 1;
-    // the last slab's download cannot start before the kernel's last wave
-    // ends: split it into halves, quarters, eighths (CFM_SLAB_TAIL=0: uniform)
-    static const int slab_tail = [] {
-      const char* e = getenv("CFM_SLAB_TAIL");
-      return e ? std::max(0, atoi(e)) : 3;
-    }();
-    lp.slab_row0.clear();
-    for (int k = 0; k < S; ++k) lp.slab_row0.push_back(n_rows * k / S);
-    if (S >= 2) {
-      const int64_t a = n_rows * (S - 1) / S, len = n_rows - a;
-      int64_t r = a;
-      for (int d = 1; d <= slab_tail && S + d <= 16 && (len >> d) >= 1024; ++d) {
-        r += len >> d;
-        lp.slab_row0.push_back(r);
-      }
-    }
-    lp.slab_row0.push_back(n_rows);
-    const int S_all = int(lp.slab_row0.size()) - 1;
-    lp.n_slabs = S_all;
-    auto slab_of = [&](int64_t row) {
-      const auto it = std::upper_bound(lp.slab_row0.begin(), lp.slab_row0.end(), row);
-      return int(std::min<int64_t>(S_all - 1, std::max<int64_t>(0, (it - lp.slab_row0.begin()) - 1)));
-    };
-    std::vector<int> need_mp(nt, 0), need_loc(nt, 0), lo(nt, 0), hi(nt, -1);
-    lp.slab_expected.assign(S_all, 0);
-    const int nrb = (group_for_level(h, level).dense.rows + 127) / 128;
-    for (int64_t t = 0; t < nt; ++t) {
-      int l = S_all, hh = -1, m = 0;
+    set_slab_plan(h, level, lp, [&](int64_t t, int64_t& tmin, int64_t& tmax, int64_t& smax) {
+      tmin = INT64_MAX, tmax = -1, smax = -1;
       for (int c = 0; c < kBN; ++c) {
         const int v = lp.hp.tile_col[size_t(t) * kBN + c];
-        if (v < 0) continue;
-        const int k = slab_of(v / dc);
-        l = std::min(l, k);
-        hh = std::max(hh, k);
+        if (v >= 0) tmin = std::min<int64_t>(tmin, v / dc), tmax = std::max<int64_t>(tmax, v / dc);
       }
       for (int e = lp.hp.tile_off[t]; e < lp.hp.tile_off[t + 1]; ++e)
         for (int c = 0; c < kBN; ++c) {
           const int v = lp.hp.entry_src[size_t(e) * kBN + c];
-          if (v >= 0) m = std::max(m, slab_of(v / dc) + 1);
+          if (v >= 0) smax = std::max<int64_t>(smax, v / dc);
         }
-      if (hh < 0) { l = 0; hh = -1; }
-      need_mp[t] = m;
-      need_loc[t] = hh + 1;
-      lo[t] = l;
-      hi[t] = hh;
-      for (int k = l; k <= hh; ++k) lp.slab_expected[k] += unsigned(nrb);
-    }
-    upload(lp.p_need_mp, need_mp);
-    upload(lp.p_need_loc, need_loc);
-    upload(lp.p_lo, lo);
-    upload(lp.p_hi, hi);
+    });
   }
   if (g.kind == kLowRank && g.has_ts && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) build_two_stage_plan(g, lp);
   if (use_hybrid() && full_mode(g, lp) && lp.mode == 0 && lp.hp.n_tiles > 0) {
@@ -476,8 +496,7 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
     }
   }
   if (trace_on()) fprintf(stderr, "[cfm plan L%d] uploads + hybrid / two-stage plans %.1f ms\n", level, wall_ms() - tu0);
-  static std::atomic<uint64_t> plan_gen{0};
-  lp.gen = ++plan_gen;
+  lp.gen = next_plan_gen();
   return lp;
 }
 

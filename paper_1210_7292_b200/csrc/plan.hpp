@@ -38,7 +38,8 @@ struct HostPlan {
   std::vector<int> entry_src;   // E * bn, virtual source ids or -1
   int64_t n_pairs = 0;
   std::array<int64_t, kNumCodes> code_count{};
-  int64_t n_entries() const { return int64_t(entry_code.size()); }
+  int64_t n_entries_dev = -1;  // >= 0: the arrays were built on the device only (plan_device.cu)
+  int64_t n_entries() const { return n_entries_dev >= 0 ? n_entries_dev : int64_t(entry_code.size()); }
 };
 
 inline uint64_t splitmix64(uint64_t x) {

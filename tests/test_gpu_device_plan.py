@@ -1,0 +1,71 @@
+"""The device planner (csrc/plan_device.cu) against the host plan builder
+(plan.hpp build_plan_csr + plan.cu's row-order dispatch / slabs / hybrid split,
+CFM_DEVICE_PLAN=0): identical plan statistics and bitwise identical locals,
+device-resident (hybrid plans) and from host buffers (row-ordered plans with
+the slab pipeline), on full and partially occupied levels."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _cube(level):
+    s = 1 << level
+    return np.stack(np.meshgrid(*(np.arange(s),) * 3, indexing="ij"), -1).reshape(-1, 3).astype(np.int32)
+
+
+def _sparse(level, keep, seed):
+    c = _cube(level)
+    rng = np.random.default_rng(seed)
+    return c[rng.uniform(size=len(c)) < keep]
+
+
+@pytest.mark.parametrize("case", ["cube5_l5", "cube4_l7", "sparse6_l5", "shell5_l5"])
+def test_device_plan_matches_host_plan(case, monkeypatch):
+    import torch
+
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    if case == "cube5_l5":
+        level, order, cells = 5, 5, _cube(5)
+    elif case == "cube4_l7":
+        level, order, cells = 4, 7, _cube(4)
+    elif case == "sparse6_l5":
+        level, order, cells = 6, 5, _sparse(6, 0.6, 3)
+    else:  # a spherical shell: boundary-heavy, many partial tiles
+        level, order = 5, 5
+        c = _cube(level).astype(np.float64) + 0.5 - 16
+        r = np.linalg.norm(c, axis=1)
+        cells = _cube(level)[(r > 9) & (r < 14)]
+    n = order**3
+    rng = np.random.default_rng(1)
+    mp_h = rng.uniform(-1, 1, (len(cells), n))
+    out = {}
+    for dev_plan in ("1", "0"):
+        monkeypatch.setenv("CFM_DEVICE_PLAN", dev_plan)
+        h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+        h.precompute({level: full_far_field_vectors()}, {level: 1.0 / (1 << level)})
+        st = h.plan_level_cells(level, cells)
+        mp = torch.from_numpy(mp_h).cuda()
+        loc = torch.zeros_like(mp)
+        fl = h.apply_levels({level: (mp, loc)})
+        torch.cuda.synchronize()
+        pin_mp = torch.from_numpy(mp_h).pin_memory()
+        pin_loc = torch.zeros(mp_h.shape, dtype=torch.float64).pin_memory()
+        h.apply_levels({level: (pin_mp.numpy(), pin_loc.numpy())})
+        out[dev_plan] = (dict((k, v) for k, v in st.items() if k != "counts"), st["counts"].copy(), fl,
+                         loc.cpu().numpy(), pin_loc.numpy().copy())
+    (st1, c1, f1, d1, p1), (st0, c0, f0, d0, p0) = out["1"], out["0"]
+    assert st1 == st0
+    assert np.array_equal(c1, c0) and f1 == f0
+    assert np.array_equal(d1, d0), float(np.abs(d1 - d0).max())
+    assert np.array_equal(p1, p0), float(np.abs(p1 - p0).max())
+    tgt, off, src, t = O.far_lists(cells, level)
+    orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+        {level: O.full_far_field()}, {level: 1.0 / (1 << level)})
+    ref = np.zeros_like(mp_h)
+    orc.apply_fast(level, tgt, off, src, t, mp_h, ref)
+    assert O.rel_l2(d1, ref) <= 1e-12
