@@ -221,6 +221,8 @@ def main() -> None:
             cfg5_case()
         if "cfg1" in only:
             cfg1_case()
+        if "fmmtrace" in only:
+            fmmtrace_case()
         return
     symmetry_fixture()
 
@@ -324,6 +326,69 @@ def cfg5_case() -> None:
     wc = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
     run_case("cfg5", pts, wc, AffineMap((0.0, 0.0, 0.0), 1.0), 5, helmholtz_kernel(8 * np.pi), 5, 1e-4,
              ("iablk", "iasym"), store_rows=64, seeded_mpoles=505)
+
+
+def fmmtrace_case() -> None:
+    """The reference's own caller, recorded: FmmPlan.run with threads=3 (the
+    engine.py:145-155 thread pool) on a reference handler wrapped by a
+    recorder that stores every apply_level call FmmPlan makes (level, chunk
+    batch) plus the level arrays after the M2L phase.  The GPU test replays
+    exactly that call sequence through the B200 handler."""
+    import threading
+
+    from chebfmm.engine import build_plan
+
+    pts = cube_points(5_000, seed=51)
+    w = np.random.default_rng(52).uniform(-1.0, 1.0, len(pts))
+    bbox = AffineMap((0.5, 0.5, 0.5), 0.5)
+    depth, order, eps, threads = 3, 5, 1e-5, 3
+    tree = build_tree(pts, bbox, depth)
+    lists = build_interaction_lists(tree)
+    levels = lists.far_levels()
+    lt = {lvl: unique_transfer_vectors(lists, lvl) for lvl in levels}
+    lw = {lvl: tree.cell_width(lvl) for lvl in levels}
+    out = dict(order=order, eps=eps, depth=depth, levels=np.asarray(levels), threads=threads,
+               widths=np.asarray([lw[l] for l in levels]), kernel=np.asarray("laplace"))
+    for variant in ("nablk", "iablk"):
+        inner = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps)
+        inner.precompute(lt, lw)
+
+        class Recorder:
+            def __init__(self):
+                self.calls, self.lock = [], threading.Lock()
+
+            def __getattr__(self, name):
+                return getattr(inner, name)
+
+            def apply_level(self, level, batch, mpoles, locals_out):
+                with self.lock:
+                    self.calls.append((level, batch[0][0] if batch else -1, _csr(batch)))
+                return inner.apply_level(level, batch, mpoles, locals_out)
+
+        rec = Recorder()
+        plan = build_plan(pts, bbox, depth, laplace_kernel(), order, eps, variant=variant, threads=threads,
+                          handler=rec)
+        snap = {}
+        orig = plan._m2l
+
+        def m2l(lv, orig=orig, snap=snap):
+            orig(lv)
+            for lvl, d in lv.items():
+                snap[lvl] = (d.mpoles.copy(), d.locals_.copy())
+
+        plan._m2l = m2l
+        out[f"potentials_{variant}"] = plan.run(w)
+        calls = sorted(rec.calls, key=lambda c: (c[0], c[1]))  # chunk order within a level
+        for i, (lvl, _, (tgt, off, src, tv)) in enumerate(calls):
+            out[f"call_{variant}_{i}_level"] = lvl
+            out[f"call_{variant}_{i}_tgt"], out[f"call_{variant}_{i}_off"] = tgt, off
+            out[f"call_{variant}_{i}_src"], out[f"call_{variant}_{i}_t"] = src, tv
+        out[f"n_calls_{variant}"] = len(calls)
+        for lvl in levels:
+            out[f"mpoles_{variant}_{lvl}"], out[f"locals_{variant}_{lvl}"] = snap[lvl]
+            out[f"flops_{variant}_{lvl}"] = inner.flops.get(lvl, 0)
+    np.savez_compressed(OUT / "fmmtrace.npz", **out)
+    print("fmmtrace.npz", {k: out[k] for k in out if k.startswith("n_calls")})
 
 
 def aca_case() -> None:

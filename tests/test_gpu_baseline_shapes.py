@@ -260,3 +260,37 @@ def test_device_aca_matches_host_aca(torch_cuda):
             p, q = f.reconstruct(), ref.reconstruct()
             assert np.linalg.norm(p - q) <= 1e-12 * max(np.linalg.norm(q), 1e-300)
     assert aca_plus_svds_device(torch.from_numpy(cases[0][0]).cuda(), 1e-5)[len(lap)].via_fallback
+
+
+@pytest.mark.parametrize("variant", ["nablk", "iablk"])
+def test_replay_reference_fmmplan_calls(torch_cuda, golden, variant):
+    """The reference's own caller: the fixture recorded every apply_level call
+    `chebfmm.FmmPlan.run` made with threads=3 (engine.py:140-157: per level the
+    batch split by `_split` and applied from a thread pool on shared arrays)
+    and the level arrays after its M2L phase.  Replaying that exact call
+    sequence -- same chunks, same concurrency, fresh np.zeros locals shared by
+    a level's chunks -- through the B200 handler gives the reference's
+    locals and flops."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    g = golden("fmmtrace")
+    levels = [int(l) for l in g["levels"]]
+    lw = dict(zip(levels, (float(w) for w in g["widths"])))
+    calls = [(int(g[f"call_{variant}_{i}_level"]), O.csr_to_batch(*(g[f"call_{variant}_{i}_{k}"]
+                                                                   for k in ("tgt", "off", "src", "t"))))
+             for i in range(int(g[f"n_calls_{variant}"]))]
+    lt = {l: sorted({t for lv, b in calls if lv == l for _, far in b for _, t in far}) for l in levels}
+    h = make_handler(variant, laplace_kernel(), ChebyshevGrid(int(g["order"])), float(g["eps"]))
+    h.precompute(lt, lw)
+    for lvl in levels:
+        mp = g[f"mpoles_{variant}_{lvl}"]
+        loc = np.zeros_like(mp)
+        chunks = [b for lv, b in calls if lv == lvl]
+        with ThreadPoolExecutor(max_workers=int(g["threads"])) as pool:
+            for f in [pool.submit(h.apply_level, lvl, c, mp, loc) for c in chunks]:
+                f.result()
+        err = O.rel_l2(loc, g[f"locals_{variant}_{lvl}"])
+        assert err <= (1e-12 if variant == "nablk" else 1e-10), (variant, lvl, err)
+        assert h.flops[lvl] == int(g[f"flops_{variant}_{lvl}"])

@@ -217,3 +217,23 @@ def test_oracle_sphere9(golden):
             fl = orc.apply_fast(lvl, tgt, off, src, t, mp, loc)
             assert O.rel_l2(loc[g[f"rows_{lvl}"]], g[f"locals_{variant}_{lvl}"]) <= 1e-13
             assert fl == int(g[f"flops_{variant}_{lvl}"])
+
+
+@pytest.mark.parametrize("variant", ["nablk", "iablk"])
+def test_oracle_replays_reference_fmmplan_calls(golden, variant):
+    """The recorded FmmPlan call sequence (tests/golden/fmmtrace.npz) replayed
+    through the oracle reproduces the reference's post-M2L locals: pins the
+    fixture the GPU replay test uses."""
+    g = golden("fmmtrace")
+    levels = [int(l) for l in g["levels"]]
+    lw = dict(zip(levels, (float(w) for w in g["widths"])))
+    calls = [(int(g[f"call_{variant}_{i}_level"]), [g[f"call_{variant}_{i}_{k}"] for k in ("tgt", "off", "src", "t")])
+             for i in range(int(g[f"n_calls_{variant}"]))]
+    lt = {l: sorted({tuple(int(c) for c in t) for lv, csr in calls if lv == l for t in csr[3]}) for l in levels}
+    orc = O.OracleM2L(variant, O.laplace_profile, np.float64, int(g["order"]), float(g["eps"]), -1.0).precompute(lt, lw)
+    for lvl in levels:
+        mp = g[f"mpoles_{variant}_{lvl}"]
+        loc = np.zeros_like(mp)
+        fl = sum(orc.apply_faithful(lvl, O.csr_to_batch(*csr), mp, loc) for lv, csr in calls if lv == lvl)
+        assert O.rel_l2(loc, g[f"locals_{variant}_{lvl}"]) <= 1e-14
+        assert fl == int(g[f"flops_{variant}_{lvl}"])
