@@ -275,6 +275,37 @@ int cfm_plan_level_csr(cfm_handler* h, int level, int64_t n_targets, const int64
     if (n_targets < 0 || n_rows < 0) throw Error(CFM_ERR_VALUE, "negative size");
     const int64_t P = n_targets ? off[n_targets] : 0;
     auto codes = codes_from_t(P, t);
+    {  // dense full-operator levels with ascending target rows (a rank's shard-local
+       // lists): rows without a list get an empty one and the device planner runs
+      Group& g = group_for_level(h, level);
+      bool ok = use_device_plan() && g.kind == kDense && g.has_full && !data_complex && !h->op_complex &&
+                n_rows < (int64_t(1) << 31);
+      for (int64_t i = 0; ok && i < n_targets; ++i)
+        ok = tgt[i] >= 0 && tgt[i] < n_rows && (i == 0 || tgt[i] > tgt[i - 1]) && off[i + 1] >= off[i];
+      for (int64_t q = 0; ok && q < P; ++q) ok = src[q] >= 0 && src[q] < n_rows;
+      if (ok) {
+        std::vector<int64_t> h_off(n_rows + 1, 0);
+        for (int64_t i = 0; i < n_targets; ++i) h_off[tgt[i] + 1] = off[i + 1] - off[i];
+        for (int64_t r = 0; r < n_rows; ++r) h_off[r + 1] += h_off[r];
+        // pairs are already in row order (targets ascending, lists in CSR order)
+        std::vector<int32_t> src32(P);
+        for (int64_t q = 0; q < P; ++q) src32[q] = int32_t(src[q]);
+        cudaStream_t s = h->stream;
+        DevBuf d_off, d_src, d_code;
+        upload(d_off, h_off);
+        upload(d_src, src32);
+        upload(d_code, codes);
+        LevelPlan lp;
+        if (device_plan_dense(h, level, g, n_rows, d_off.as<int64_t>(), h_off, d_src.as<int32_t>(),
+                              d_code.as<int16_t>(), n_rows, s, lp)) {
+          lp.gen = next_plan_gen();
+          h->plans[level] = std::move(lp);
+          const LevelPlan& pl = h->plans[level];
+          if (pair_count_out) std::copy(pl.hp.code_count.begin(), pl.hp.code_count.end(), pair_count_out);
+          return;
+        }
+      }
+    }
     LevelPlan& lp = make_plan(h, level, n_targets, tgt, off, src, codes.data(), data_complex, n_rows);
     if (pair_count_out) std::copy(lp.hp.code_count.begin(), lp.hp.code_count.end(), pair_count_out);
   });

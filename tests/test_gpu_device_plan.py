@@ -69,3 +69,32 @@ def test_device_plan_matches_host_plan(case, monkeypatch):
     ref = np.zeros_like(mp_h)
     orc.apply_fast(level, tgt, off, src, t, mp_h, ref)
     assert O.rel_l2(d1, ref) <= 1e-12
+
+
+def test_device_plan_for_csr_subsets_matches_host(monkeypatch):
+    """plan_level_csr with a rank-like subset of ascending target rows (the
+    shard-local lists ShardedM2L plans) takes the device planner too: bitwise
+    equal to the host builder."""
+    import torch
+
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    level, order = 5, 5
+    cells = _cube(level)
+    rows = np.nonzero(cells[:, 0] < 12)[0]  # a Morton-free slab of targets, ascending
+    tgt, off, src, t = O.far_lists(cells, level, targets=rows)
+    n = order**3
+    mp_h = np.random.default_rng(2).uniform(-1, 1, (len(cells), n))
+    out = {}
+    for dev_plan in ("1", "0"):
+        monkeypatch.setenv("CFM_DEVICE_PLAN", dev_plan)
+        h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+        h.precompute({level: full_far_field_vectors()}, {level: 1.0 / (1 << level)})
+        st = h.plan_level_csr(level, tgt, off, src, t, len(cells))
+        mp = torch.from_numpy(mp_h).cuda()
+        loc = torch.zeros_like(mp)
+        fl = h.apply_levels({level: (mp, loc)})
+        torch.cuda.synchronize()
+        out[dev_plan] = ({k: v for k, v in st.items() if k != "counts"}, fl, loc.cpu().numpy())
+    assert out["1"][0] == out["0"][0] and out["1"][1] == out["0"][1]
+    assert np.array_equal(out["1"][2], out["0"][2])
