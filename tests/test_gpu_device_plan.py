@@ -98,3 +98,39 @@ def test_device_plan_for_csr_subsets_matches_host(monkeypatch):
         out[dev_plan] = ({k: v for k, v in st.items() if k != "counts"}, fl, loc.cpu().numpy())
     assert out["1"][0] == out["0"][0] and out["1"][1] == out["0"][1]
     assert np.array_equal(out["1"][2], out["0"][2])
+
+
+def test_device_planner_edge_levels():
+    """Levels the device planner must hand back or handle: no pairs at all, a
+    sparse level that plans as pair entries (host builder), a dense level whose
+    every tile is full (no hybrid leftovers); results vs the oracle."""
+    import torch
+
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    order, n = 5, 125
+    cases = {
+        "single_cell": (3, np.array([[1, 2, 3]], np.int32)),
+        "two_far_cells": (4, np.array([[0, 0, 0], [8, 8, 8]], np.int32)),
+        "sparse_pairs": (5, _sparse(5, 0.05, 7)),
+        "full_cube_l4": (4, _cube(4)),
+    }
+    for name, (level, cells) in cases.items():
+        h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+        h.precompute({level: full_far_field_vectors()}, {level: 1.0 / (1 << level)})
+        st = h.plan_level_cells(level, cells)
+        mp_h = np.random.default_rng(4).uniform(-1, 1, (len(cells), n))
+        mp = torch.from_numpy(mp_h).cuda()
+        loc = torch.zeros_like(mp)
+        fl = h.apply_levels({level: (mp, loc)})
+        torch.cuda.synchronize()
+        tgt, off, src, t = O.far_lists(cells, level)
+        ref = np.zeros_like(mp_h)
+        if len(src):
+            orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-5, -1.0).precompute(
+                {level: O.full_far_field()}, {level: 1.0 / (1 << level)})
+            orc.apply_fast(level, tgt, off, src, t, mp_h, ref)
+        assert st["pairs"] == len(src), name
+        assert fl == 2 * n * n * len(src), name
+        got = loc.cpu().numpy()
+        assert (np.abs(got).max() == 0.0) if not len(src) else O.rel_l2(got, ref) <= 1e-12, name
