@@ -17,7 +17,11 @@
  *   apply_level                    :279-305    cfm_apply_level_csr / cfm_apply_planned
  *   (_apply_plain/_sym/_shared/_blocked :320-452 are selected by the variant)
  *   octree.build_interaction_lists far part (octree.py:148-178) + symmetry
- *   canonicalize (symmetry.py:63-75)           cfm_classify_count / cfm_classify_fill
+ *   canonicalize (symmetry.py:63-75)           cfm_classify_count / cfm_classify_fill,
+ *                                              cfm_classify_targets_* (a rank's targets)
+ *   aca (lowrank.py:65-160) per operator       cfm_aca_batch (compression="aca")
+ *   FmmPlan._m2l batches (engine.py:140-157)   cfm_last_csr_plan_info (plan cache of batches)
+ *   (multi-GPU halo, no reference counterpart) cfm_gather_rows
  *
  * Conventions (all bit-for-bit those of the reference):
  *   - flat node index m = a1 + a2*l + a3*l^2 (first component fastest), interp.py:134-161;
