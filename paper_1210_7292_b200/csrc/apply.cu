@@ -231,7 +231,19 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
       const char* e = getenv("CFM_SEG_KSKIP");  // 0: run all 4 k-steps of every segment (A/B)
       b.seg_ksteps = (!e || atoi(e) != 0) ? g.ts_ksteps.as<int>() : nullptr;
     }
-    launches += launch_seg_pair(b, lp.ts2.n_tiles, s);
+    if (h->ts_before_stage2) CUDA_CHECK(cudaStreamWaitEvent(s, h->ts_before_stage2, 0));
+    const int64_t nt2 = lp.ts2.n_tiles;
+    if (h->ts_chunks > 1 && h->ts_after_chunk && int64_t(lp.ts_tile_tmin.size()) == nt2 && nt2 >= 2 * h->ts_chunks) {
+      // stage 2 in tile chunks (row-ordered tiles): after a chunk, every row
+      // below the next chunk's smallest target row is final
+      for (int c = 0; c < h->ts_chunks; ++c) {
+        const int64_t t0 = nt2 * c / h->ts_chunks, t1 = nt2 * (c + 1) / h->ts_chunks;
+        launches += launch_seg_pair(b, t1 - t0, s, t0);
+        h->ts_after_chunk(t1 < nt2 ? lp.ts_tile_tmin[t1] : lp.n_rows);
+      }
+    } else {
+      launches += launch_seg_pair(b, nt2, s);
+    }
     return launches;
   }
 
@@ -483,6 +495,11 @@ void apply_with_buffers(cfm_handler* h, int level, LevelPlan& lp, const double* 
   h->last_ms = ms;
 }
 
+static bool use_lr_pipeline() {
+  const char* e = getenv("CFM_LR_PIPELINE");
+  return !e || atoi(e) != 0;
+}
+
 bool use_merged_pairs() {
   static int v = [] {
     const char* e = getenv("CFM_MERGE_PAIRS");
@@ -620,6 +637,104 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
     if (!is_device_ptr(locals[i])) stage_bytes += bytes;
   }
   std::sort(lv.begin(), lv.end(), [](const Lv& a, const Lv& b) { return a.level < b.level; });
+  // ---- low-rank levels from host buffers: multipoles of every level go H2D
+  // first, then the locals, on a copy stream; the compute stream starts a
+  // level as soon as its multipoles are in, waits for its locals only before
+  // the accumulating stage (stage 2 of the two-stage path), and finished rows
+  // go back on a second copy stream -- for two-stage levels chunk by chunk of
+  // row-ordered stage-2 tiles -- while later work runs (CFM_LR_PIPELINE=0: off)
+  bool lr_host = !lv.empty() && use_copy_pipeline() && use_lr_pipeline();
+  for (auto& L : lv)
+    lr_host = lr_host && group_for_level(h, L.level).kind == kLowRank && !is_device_ptr(L.x) && !is_device_ptr(L.y);
+  if (lr_host) {
+    if (!h->s_h2d) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    if (!h->s_d2h) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    if (!h->ev_prev) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_prev, cudaEventDisableTiming));
+    size_t evi = 0;
+    auto next_ev = [&]() {
+      if (evi == h->ev_pool.size()) {
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_pool.push_back(e);
+      }
+      return h->ev_pool[evi++];
+    };
+    auto fence = [&](cudaStream_t from, cudaStream_t to) {  // `to` waits for the work queued on `from`
+      cudaEvent_t e = next_ev();
+      CUDA_CHECK(cudaEventRecord(e, from));
+      CUDA_CHECK(cudaStreamWaitEvent(to, e, 0));
+    };
+    const size_t n = lv.size();
+    size_t tot = 0;
+    for (auto& L : lv) tot += 2 * L.bytes;
+    ensure(h->x_stage, tot);
+    // the copy streams reuse the staging that earlier work on s may still read
+    CUDA_CHECK(cudaEventRecord(h->ev_prev, s));
+    CUDA_CHECK(cudaStreamWaitEvent(h->s_h2d, h->ev_prev, 0));
+    CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_prev, 0));
+    std::vector<char*> dx(n), dy(n);
+    std::vector<cudaEvent_t> ex(n), ey(n);
+    size_t o = 0;
+    for (size_t i = 0; i < n; ++i) {
+      dx[i] = static_cast<char*>(h->x_stage.p) + o;
+      dy[i] = dx[i] + lv[i].bytes;
+      o += 2 * lv[i].bytes;
+    }
+    for (size_t i = 0; i < n; ++i) {
+      CUDA_CHECK(cudaMemcpyAsync(dx[i], lv[i].x, lv[i].bytes, cudaMemcpyHostToDevice, h->s_h2d));
+      ex[i] = next_ev();
+      CUDA_CHECK(cudaEventRecord(ex[i], h->s_h2d));
+    }
+    for (size_t i = 0; i < n; ++i) {
+      CUDA_CHECK(cudaMemcpyAsync(dy[i], lv[i].y, lv[i].bytes, cudaMemcpyHostToDevice, h->s_h2d));
+      ey[i] = next_ev();
+      CUDA_CHECK(cudaEventRecord(ey[i], h->s_h2d));
+    }
+    CUDA_CHECK(cudaEventRecord(h->ev0, s));
+    int64_t launches = 0;
+    auto reset_hooks = [&] {
+      h->ts_before_stage2 = nullptr;
+      h->ts_chunks = 1;
+      h->ts_after_chunk = nullptr;
+    };
+    for (size_t i = 0; i < n; ++i) {
+      LevelPlan& P = *lv[i].lp;
+      const size_t row_b = lv[i].bytes / size_t(std::max<int64_t>(P.n_rows, 1));
+      CUDA_CHECK(cudaStreamWaitEvent(s, ex[i], 0));
+      int64_t done = 0;
+      auto download = [&](int64_t upto) {  // rows [done, upto) of level i are final
+        if (upto <= done) return;
+        fence(s, h->s_d2h);
+        CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(lv[i].y) + done * row_b, dy[i] + done * row_b,
+                                   size_t(upto - done) * row_b, cudaMemcpyDeviceToHost, h->s_d2h));
+        done = upto;
+      };
+      if (P.ts) {
+        h->ts_before_stage2 = ey[i];
+        h->ts_chunks = P.n_rows >= 65536 ? 8 : 1;
+        h->ts_after_chunk = download;
+      } else {
+        CUDA_CHECK(cudaStreamWaitEvent(s, ey[i], 0));
+      }
+      try {
+        launches += run_plan(h, lv[i].level, P, reinterpret_cast<const double*>(dx[i]),
+                             reinterpret_cast<double*>(dy[i]), s);
+      } catch (...) {
+        reset_hooks();
+        throw;
+      }
+      reset_hooks();
+      download(P.n_rows);
+    }
+    CUDA_CHECK(cudaEventRecord(h->ev1, s));
+    fence(h->s_d2h, s);  // the caller's stream joins the downloads
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms;
+    h->last_launches = launches;
+    return;
+  }
   if (stage_bytes) ensure(h->x_stage, stage_bytes);
   // ---- copy pipeline: large target-mode levels given as host buffers stream
   // their rows in slabs on a copy stream while the kernel runs (flags in device

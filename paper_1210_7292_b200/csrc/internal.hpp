@@ -212,6 +212,7 @@ struct LevelPlan {
   bool ts = false;
   HostPlan ts1, ts2;
   DevBuf ts1_col, ts1_off, ts1_code, ts1_src, ts2_col, ts2_off, ts2_code, ts2_src;
+  std::vector<int64_t> ts_tile_tmin;  // per stage-2 tile: smallest target row (tiles are in row order)
   DevBuf ts_y;          // stage-1 output Y[source row][class-stack row] (n_rows x ts_ldy)
   // hybrid (dense full-operator target tiles): the tiles that are less than
   // half full -- the partial last tile of each boundary class of targets --
@@ -304,6 +305,13 @@ struct cfm_handler {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
+  // host-buffer low-rank pipeline (apply.cu): while set, a two-stage level waits
+  // `ts_before_stage2` before stage 2 and runs stage 2 in `ts_chunks` tile
+  // chunks, calling ts_after_chunk(rows below this are final) after each
+  cudaEvent_t ts_before_stage2 = nullptr;
+  int ts_chunks = 1;
+  std::function<void(int64_t)> ts_after_chunk;
+  std::vector<cudaEvent_t> ev_pool;  // events of the host-buffer low-rank pipeline
   bool last_csr_hit = false;  // the last cfm_apply_level_csr reused a cached plan
   int last_csr_mode = -1, last_csr_two_stage = 0;  // and that plan's mode / two-stage flag
   uint64_t last_csr_gen = 0;                        // and its id (unique per built plan)
@@ -386,7 +394,7 @@ bool launch_lowrank_fused(const LowRankParams& lp_, int rmax, int64_t first, int
 int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int64_t>& counts, cudaStream_t s);
 int64_t launch_range(const TileParams& p, int64_t first, int64_t count, cudaStream_t s);
 int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s);
-int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s);
+int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s, int64_t tile_base = 0);
 void fill_ops(TileParams& p, const OpStack& s, const CodeMap& m);
 void fill_plan(TileParams& p, const DevBuf& col, const DevBuf& toff, const DevBuf& code, const DevBuf& src,
                       int64_t n_tiles);

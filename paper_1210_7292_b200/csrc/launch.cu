@@ -374,10 +374,10 @@ int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s) {
 // Two-stage low-rank stage 2 on seg_pair_gemm_kernel (two 16-wide rank
 // segments per pipeline stage); CFM_SEG_PAIR=0 runs the KC = 16 full-operator
 // kernel instead.
-int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s) {
+int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s, int64_t tile_base) {
   if (n_tiles <= 0) return 0;
-  if (n_tiles >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
-  q.tile_base = 0;
+  if (n_tiles + tile_base >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
+  q.tile_base = int(tile_base);
   encode_source_map(q, 16);
   const int smem = seg_pair_smem_bytes();
   CUDA_CHECK(cudaFuncSetAttribute(seg_pair_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -116,6 +116,14 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp) {
   }
   p2.tile_off.push_back(int(p2.entry_code.size()));
   if (p2.n_entries() >= (int64_t(1) << 31) / kBN) return;
+  lp.ts_tile_tmin.assign(p2.n_tiles, lp.n_rows);
+  for (int64_t t = 0; t < p2.n_tiles; ++t)
+    for (int c = 0; c < kBN; ++c) {
+      const int v = p2.tile_col[size_t(t) * kBN + c];
+      if (v >= 0) lp.ts_tile_tmin[t] = std::min<int64_t>(lp.ts_tile_tmin[t], v);
+    }
+  for (int64_t t = p2.n_tiles - 1; t > 0; --t)  // monotone: "rows below tmin[t] are final after tiles < t"
+    lp.ts_tile_tmin[t - 1] = std::min(lp.ts_tile_tmin[t - 1], lp.ts_tile_tmin[t]);
   lp.ts1 = std::move(p1);
   lp.ts2 = std::move(p2);
   push_plan(lp.ts1, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src);

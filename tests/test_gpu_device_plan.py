@@ -134,3 +134,38 @@ def test_device_planner_edge_levels():
         assert fl == 2 * n * n * len(src), name
         got = loc.cpu().numpy()
         assert (np.abs(got).max() == 0.0) if not len(src) else O.rel_l2(got, ref) <= 1e-12, name
+
+
+def test_lowrank_host_pipeline_bitwise(monkeypatch):
+    """iablk from pinned host buffers over levels 4-6 of a full cube (level 6
+    two-stage with stage 2 in row-ordered chunks whose rows download while
+    later chunks run): bitwise the device-resident apply, and the same with
+    the pipeline off (CFM_LR_PIPELINE=0)."""
+    import torch
+
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    order, n, levels = 5, 125, (4, 5, 6)
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), 1e-5)
+    h.precompute({l: full_far_field_vectors() for l in levels}, {l: 1.0 / (1 << l) for l in levels})
+    rng = np.random.default_rng(9)
+    mp_h = {l: rng.uniform(-1, 1, ((1 << l) ** 3, n)) for l in levels}
+    for l in levels:
+        h.plan_level_cells(l, _cube(l))
+    assert h.plan_stats(6)["two_stage"]
+    dev = {l: (torch.from_numpy(mp_h[l]).cuda(), torch.zeros(mp_h[l].shape, dtype=torch.float64, device="cuda"))
+           for l in levels}
+    fl_d = h.apply_levels(dev)
+    torch.cuda.synchronize()
+    out = {}
+    for pipe in ("1", "0"):
+        monkeypatch.setenv("CFM_LR_PIPELINE", pipe)
+        arrs = {l: (torch.from_numpy(mp_h[l]).pin_memory().numpy(),
+                    torch.zeros(mp_h[l].shape, dtype=torch.float64).pin_memory().numpy()) for l in levels}
+        fl = h.apply_levels(arrs)
+        assert fl == fl_d
+        out[pipe] = {l: arrs[l][1].copy() for l in levels}
+    for l in levels:
+        d = dev[l][1].cpu().numpy()
+        assert np.array_equal(out["1"][l], d), (l, float(np.abs(out["1"][l] - d).max()))
+        assert np.array_equal(out["0"][l], d)
