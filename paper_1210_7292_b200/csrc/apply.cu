@@ -174,6 +174,83 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     return launches;
   }
 
+  if (g.kind == kLowRank && lp.ts == 2) {
+    // target-major two-stage low rank: stage 1 Y_T[target][rho_T + a] = (V_k^H x_source)[a]
+    // (class V stacks on the full-operator kernel, scattered by the pair table),
+    // stage 2 locals[targets] += scale * U_c Y_T[targets]^T, a dense GEMM per
+    // target class on the step kernel
+    const int ldx = g.tsT_v.ld;
+    const int nb = g.tsT_nb;
+    const auto xo = xpad_layout(h, {{lp.n_rows, ldx}}, s);
+    double* xp = h->xpad.as<double>() + xo[0];
+    launches += xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
+    if (!lp.ts_y.p) {
+      // columns of pairs a target does not have are never written by stage 1;
+      // zeroed once, they contribute exact zeros to stage 2 in every step
+      lp.ts_y.alloc(size_t(lp.n_rows) * nb * 128 * sizeof(double));
+      CUDA_CHECK(cudaMemsetAsync(lp.ts_y.p, 0, lp.ts_y.bytes, s));
+    }
+    TileParams a{};
+    fill_ops(a, g.tsT_v, g.main);
+    fill_plan(a, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src, lp.ts1.n_tiles);
+    a.op_rows = nullptr;
+    a.op_klen = nullptr;
+    a.nr = 128;
+    a.nk = h->n;
+    a.code_is_op = 1;
+    a.ft = 1;
+    a.ft_rows = 128;
+    a.tmap_a = g.tsT_vmap;
+    a.x = xp; a.x_ld = ldx; a.x_dc = 1; a.x_rows = lp.n_rows;
+    a.y = lp.ts_y.as<double>(); a.y_ld = (long long)nb * 128; a.y_dc = 1; a.y_rowblk = nb;
+    a.y_colmap = g.tsT_rowinfo.as<int>();
+    a.y_nbr = lp.tsT_nbr.as<int>();
+    a.y_nslots = g.tsT_nslots;
+    a.scale = 1.0; a.accumulate = 0; a.pair_out = 1;
+    a.zero_row = h->zeros.as<double>();
+    a.n_entries = lp.ts1.n_entries();
+    const bool persist = use_ts_persistent();
+    launches += persist ? launch_ts_gemm(1, a, lp.ts1.n_tiles, 0, h->device, s) : launch_tiles(a, lp.ts1.n_tiles, s);
+    TileParams b{};
+    fill_ops(b, g.tsT_u, g.main);
+    fill_plan(b, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src, lp.ts2.n_tiles);
+    b.op_rows = nullptr;
+    b.op_klen = nullptr;
+    b.nr = h->n;
+    b.nk = 128;
+    b.code_is_op = 1;
+    b.ft = 1;
+    b.ft_rows = g.tsT_u.rows;
+    b.tmap_a = g.tsT_umap;
+    b.x = lp.ts_y.as<double>(); b.x_ld = 128; b.x_dc = 1; b.x_rows = lp.n_rows * nb;
+    b.y = d_y; b.y_ld = row_ld; b.y_dc = 1;
+    b.scale = scale; b.accumulate = 1; b.pair_out = 0;
+    b.zero_row = h->zeros.as<double>();
+    b.n_entries = lp.ts2.n_entries();
+    if (h->ts_before_stage2) CUDA_CHECK(cudaStreamWaitEvent(s, h->ts_before_stage2, 0));
+    const int64_t nt2 = lp.ts2.n_tiles;
+    if (h->ts_chunks > 1 && h->ts_after_chunk && int64_t(lp.ts_tile_tmin.size()) == nt2 && nt2 >= 2 * h->ts_chunks) {
+      // chunk boundaries on whole waves (one CTA per SM): a chunk of 3.5 waves
+      // would run as long as one of 4
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+      auto cut = [&](int c) {
+        if (c >= h->ts_chunks) return nt2;
+        const int64_t t = nt2 * c / h->ts_chunks;
+        return std::min<int64_t>(nt2, (t + sms / 2) / sms * sms);
+      };
+      for (int c = 0; c < h->ts_chunks; ++c) {
+        const int64_t t0 = cut(c), t1 = cut(c + 1);
+        if (t1 <= t0) continue;
+        launches += persist ? launch_ts_gemm(2, b, t1 - t0, t0, h->device, s) : launch_range(b, t0, t1 - t0, s);
+        h->ts_after_chunk(t1 < nt2 ? lp.ts_tile_tmin[t1] : lp.n_rows);
+      }
+    } else {
+      launches += persist ? launch_ts_gemm(2, b, nt2, 0, h->device, s) : launch_tiles(b, nt2, s);
+    }
+    return launches;
+  }
+
   if (g.kind == kLowRank && lp.ts) {
     // two-stage low-rank: stage 1 Y = V^H x per (source, class segment), stage 2
     // locals += scale * sum U_t Y per target tile (both on the full-operator kernel)
@@ -1342,7 +1419,13 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
       }
       if (!h->ev_fork) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
       CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
-      for (size_t k = 0; k < nl; ++k) {
+      // largest level first: its long kernels start at once and the host-side
+      // launch work of the small levels (and their short kernels) hides under them
+      std::vector<size_t> order(nl);
+      std::iota(order.begin(), order.end(), size_t(0));
+      std::stable_sort(order.begin(), order.end(),
+                       [&](size_t a, size_t b) { return lv[a].lp->n_rows > lv[b].lp->n_rows; });
+      for (size_t k : order) {
         AuxStream& a = h->aux[k];
         if (!a.s) {
           CUDA_CHECK(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));

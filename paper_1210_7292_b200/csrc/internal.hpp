@@ -178,6 +178,21 @@ struct Group {
   OpStack ts_v;                  // 8 * ts_nb blocks of 128 rows x n
   CUtensorMap ts_vmap, ts_umap;  // box 36 x 128 over ts_v; box 20 x 128 over lrf_left
   DevBuf ts_ksteps;              // per stage-2 entry code 2k + j: k-steps holding rank columns (ceil(w / 4))
+  // target-major two-stage mode (round 2, default): Y is laid out by TARGET --
+  // Y_T[target][rho_T[class(target)][k] + a] = (V_k^H x_source)[a] for the pair
+  // (target, source, k) -- with every class's transfers packed back to back at
+  // their exact ranks, so stage 2 is one dense GEMM per target class,
+  // locals[:, targets] += U_c (n x R_c) Y_T[targets]^T, with K = R_c running
+  // over whole 128-column blocks (no per-entry rank padding, contiguous B rows)
+  bool has_tsT = false;
+  int tsT_nb = 0;                // 128-wide blocks per class (rows of the V stack = columns of the U stack)
+  int tsT_nslots = 0;            // transfers per class (189 for octree lists)
+  std::vector<int> tsT_rho;      // [8][n_transfers] first packed row of transfer k in class c, -1 if absent
+  std::vector<int> tsT_slot;     // [8][n_transfers] index of transfer k among class c's transfers, -1 if absent
+  std::vector<int> tsT_nblk;     // [8] blocks holding rank rows of class c
+  DevBuf tsT_rowinfo;            // [8 * tsT_nb * 128] V-stack row -> (slot << 8 | a), -1: padding row
+  OpStack tsT_v, tsT_u;          // 8 * tsT_nb blocks: V rows (128 x n), U columns (round8(n) x 128)
+  CUtensorMap tsT_vmap, tsT_umap;
 };
 
 struct HybridPlan;
@@ -209,11 +224,13 @@ struct LevelPlan {
   int64_t src_lo = 0, src_hi = 0, tgt_lo = 0, tgt_hi = 0;
   uint64_t gen = 0;  // unique per built plan (merged plans remember what they were built from)
   // two-stage low-rank plans (Group::has_ts): stage 1 over source tiles, stage 2 over target tiles
-  bool ts = false;
+  int ts = 0;  // 0: none, 1: source-major Y + rank-segment stage 2, 2: target-major Y + dense stage 2
   HostPlan ts1, ts2;
   DevBuf ts1_col, ts1_off, ts1_code, ts1_src, ts2_col, ts2_off, ts2_code, ts2_src;
   std::vector<int64_t> ts_tile_tmin;  // per stage-2 tile: smallest target row (tiles are in row order)
   DevBuf ts_y;          // stage-1 output Y[source row][class-stack row] (n_rows x ts_ldy)
+  DevBuf tsT_nbr;       // target-major mode (ts == 2): [n_rows][tsT_nslots] element offset into Y_T of the
+                        // (source, class slot)'s rank run, -1 where the source has no such pair
   // hybrid (dense full-operator target tiles): the tiles that are less than
   // half full -- the partial last tile of each boundary class of targets --
   // go to a pair-mode sub-plan; device-resident applies run the remaining
@@ -395,6 +412,8 @@ int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int6
 int64_t launch_range(const TileParams& p, int64_t first, int64_t count, cudaStream_t s);
 int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s);
 int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s, int64_t tile_base = 0);
+bool use_ts_persistent();
+int64_t launch_ts_gemm(int stage, TileParams q, int64_t n_tiles, int64_t tile_base, int device, cudaStream_t s);
 void fill_ops(TileParams& p, const OpStack& s, const CodeMap& m);
 void fill_plan(TileParams& p, const DevBuf& col, const DevBuf& toff, const DevBuf& code, const DevBuf& src,
                       int64_t n_tiles);
@@ -410,7 +429,8 @@ void set_per_op(OpStack& s, const std::vector<int>& rows, const std::vector<int>
 void build_lowrank_stacks(cfm_handler* h, OpStack& left, OpStack& right_h, int n_ops, const int* ranks,
                                  const double* L, const double* R, int rows_left, int rows_right);
 void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers,
-                            const std::vector<int>& rk, const std::vector<double>& all_v);
+                            const std::vector<int>& rk, const std::vector<double>& all_v,
+                            const std::vector<double>& all_u);
 void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, int n_ops,
                                const int* ranks, const double* L, const double* R);
 std::vector<int16_t> codes_from_t(int64_t P, const int8_t* t);
@@ -419,6 +439,7 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp);
 inline bool full_mode(const Group& g, const LevelPlan& lp) { return g.kind == kDense && g.has_full && lp.dc == 1; }
 bool use_hybrid();
 bool use_two_stage();
+int two_stage_mode();
 PFN_encodeTiled resolve_encode_tiled();
 void push_pair_plan(LevelPlan& lp);
 void build_hybrid_plan(cfm_handler* h, LevelPlan& lp, int64_t n_targets, const int64_t* tgt,

@@ -1,6 +1,7 @@
 // Kernel selection and launch helpers of the tile kernels (tile_gemm_ws, seg_pair_gemm, lowrank_ws).
 #include "internal.hpp"
 #include "seg_gemm.cuh"
+#include "ts_gemm.cuh"
 
 namespace cfm {
 
@@ -149,6 +150,13 @@ static void launch_ws_multi(const MultiTileParams& mp_in, dim3 grid_tiles, cudaS
         const int rem = mp.seg[i].nk % KC;
         mp.seg[i].ft_pipe = ft_pipe_enabled() && (rem == 0 || rem > KC - 4) && !mp.seg[i].op_klen;
         mp.seg[i].ft_ktail = mp.seg[i].ft_pipe && rem == KC - 3 && !mp.seg[i].op_rows && ktail_enabled();
+        {
+          // CFM_FT_SKEW=a,b: skew (chunks) of the stage-1 (FTM 3) and the other flat-loop launches
+          const char* e = getenv("CFM_FT_SKEW");
+          int s3 = 2, s1 = 0;
+          if (e) sscanf(e, "%d,%d", &s3, &s1);
+          mp.seg[i].ft_skew = q.y_rowblk ? s3 : s1;
+        }
       }
       auto kf = q.y_rowblk ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 3>
                 : skip    ? tile_gemm_ws_kernel<BM, BN, WM, WN, KC, 4, SKIP, false, 2>
@@ -382,6 +390,55 @@ int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s, int64_t t
   const int smem = seg_pair_smem_bytes();
   CUDA_CHECK(cudaFuncSetAttribute(seg_pair_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   seg_pair_gemm_kernel<<<unsigned(n_tiles), 12 * 32, smem, s>>>(q);
+  CUDA_CHECK(cudaGetLastError());
+  return 1;
+}
+
+// Target-major two-stage path: tiles [tile_base, tile_base + n_tiles) of a
+// stage-1 (stage = 1) or stage-2 (stage = 2) plan on the persistent kernel
+// (ts_gemm.cuh), one CTA per SM.  `q` is the stage's TileParams as the
+// one-CTA-per-tile kernel takes it (CFM_TS_PERSIST=0 runs that one instead).
+bool use_ts_persistent() {
+  const char* e = getenv("CFM_TS_PERSIST");
+  return !e || atoi(e) != 0;
+}
+
+int64_t launch_ts_gemm(int stage, TileParams q, int64_t n_tiles, int64_t tile_base, int device, cudaStream_t s) {
+  if (n_tiles <= 0) return 0;
+  encode_source_map(q, kTsKC);
+  TsGemmParams t{};
+  t.nrb = (q.nr + 127) / 128;
+  if (n_tiles * t.nrb >= (int64_t(1) << 31)) throw Error(CFM_ERR_VALUE, "too many tiles for one launch");
+  t.n_work = int(n_tiles * t.nrb);
+  t.tile_base = int(tile_base);
+  t.tile_col = q.tile_col;
+  t.tile_off = q.tile_off;
+  t.entry_code = q.entry_code;
+  t.entry_src = q.entry_src;
+  t.nk = q.nk;
+  t.nr = q.nr;
+  t.a_rows = q.ft_rows;
+  const int nch = (q.nk + kTsKC - 1) / kTsKC;
+  {
+    const char* e = getenv("CFM_TS_SKEW");
+    t.skew = std::min(e ? atoi(e) : 2, nch - 1);
+  }
+  t.y = q.y;
+  t.rowinfo = q.y_colmap;
+  t.nbr = q.y_nbr;
+  t.nslots = q.y_nslots;
+  t.loc = q.y;
+  t.loc_ld = q.y_ld;
+  t.scale = q.scale;
+  t.tmap_a = q.tmap_a;
+  t.tmap_b = q.tmap_b;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int grid = std::min(t.n_work, sms);
+  const int smem = ts_gemm_smem_bytes();
+  auto kern = stage == 1 ? ts_gemm_kernel<1> : ts_gemm_kernel<2>;
+  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kTsThreads, smem, s>>>(t);
   CUDA_CHECK(cudaGetLastError());
   return 1;
 }

@@ -152,9 +152,113 @@ void build_lowrank_stacks(cfm_handler* h, OpStack& left, OpStack& right_h, int n
   set_per_op(right_h, rrows, {});  // pass 1: rows = rank
 }
 
-bool use_two_stage() {  // read at every precompute (tests switch it)
+// CFM_LR_TWOSTAGE: 0 off (fused kernel), 1 source-major Y with rank-segment
+// stage 2 (round 1), 2 target-major Y with a dense stage 2 (default).  Read at
+// every precompute and plan build (tests switch it).
+int two_stage_mode() {
   const char* e = getenv("CFM_LR_TWOSTAGE");
-  return !e || atoi(e) != 0;
+  return e ? atoi(e) : 2;
+}
+bool use_two_stage() { return two_stage_mode() != 0; }
+
+// Target-major two-stage stacks (Group::has_tsT).  Per class c (the 8 range
+// patterns of octree far lists; a target's transfers fall in one of them just
+// like a source's) its transfers k, ascending, own the packed rows
+// [rho_T[c][k], rho_T[c][k] + r_k): the V stack of class c holds V_k^H there
+// (stage 1, sources of class c), the U stack holds U_k's columns there (stage
+// 2, targets of class c).
+static void build_two_stage_target_major(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers,
+                                         const std::vector<int>& rk, const std::vector<double>& all_v,
+                                         const std::vector<double>& all_u) {
+  g.has_tsT = false;
+  const int n = h->n;
+  g.tsT_rho.assign(size_t(8) * n_transfers, -1);
+  g.tsT_slot.assign(size_t(8) * n_transfers, -1);
+  g.tsT_nblk.assign(8, 0);
+  int max_rows = 0, max_slots = 0;
+  for (int cls = 0; cls < 8; ++cls) {
+    int rows = 0, slots = 0;
+    std::vector<int> members;
+    for (int k = 0; k < n_transfers; ++k) {
+      bool in = rk[k] > 0;
+      for (int a = 0; a < 3 && in; ++a) {
+        const int t = transfers[3 * k + a], bit = (cls >> a) & 1;
+        in = t >= (bit ? -2 : -3) && t <= (bit ? 3 : 2);
+      }
+      if (in) members.push_back(k);
+    }
+    // slot order: transfers of equal component parities together, the last
+    // component fastest.  Consecutive slots then mostly differ by 2 in the last
+    // component, so for one target the two pairs' sources are same-class
+    // neighbours along the fastest cell axis -- the same stage-1 tile --
+    // and the 32-B sector their rank runs share in the target's Y_T row is
+    // completed by one CTA instead of being evicted half written.
+    auto key = [&](int k) {
+      const int t0 = transfers[3 * k], t1 = transfers[3 * k + 1], t2 = transfers[3 * k + 2];
+      const int par = ((t0 & 1) << 2) | ((t1 & 1) << 1) | (t2 & 1);
+      return (((par * 8 + (t0 + 3)) * 8 + (t1 + 3)) * 8) + (t2 + 3);
+    };
+    std::sort(members.begin(), members.end(), [&](int a, int b) { return key(a) < key(b); });
+    for (int k : members) {
+      g.tsT_rho[size_t(cls) * n_transfers + k] = rows;
+      g.tsT_slot[size_t(cls) * n_transfers + k] = slots++;
+      rows += rk[k];
+    }
+    g.tsT_nblk[cls] = (rows + 127) / 128;
+    max_rows = std::max(max_rows, rows);
+    max_slots = std::max(max_slots, slots);
+  }
+  if (max_rows == 0 || max_slots >= (1 << 23)) return;
+  const int nb = (max_rows + 127) / 128;
+  g.tsT_nb = nb;
+  g.tsT_nslots = max_slots;
+  std::vector<int> rowinfo(size_t(8) * nb * 128, -1);
+  for (int cls = 0; cls < 8; ++cls)
+    for (int k = 0; k < n_transfers; ++k) {
+      const int r0 = g.tsT_rho[size_t(cls) * n_transfers + k];
+      if (r0 < 0) continue;
+      const int slot = g.tsT_slot[size_t(cls) * n_transfers + k];
+      for (int a = 0; a < rk[k]; ++a) rowinfo[size_t(cls) * nb * 128 + r0 + a] = (slot << 8) | a;
+    }
+  upload(g.tsT_rowinfo, rowinfo);
+  const int urows = round_up(n, 8);
+  make_stack(g.tsT_v, 8 * nb, 128, n);
+  make_stack(g.tsT_u, 8 * nb, urows, 128);
+  const int vld = g.lrf_right_h.ld, uld = g.lrf_left.ld;
+  const size_t vstride = size_t(g.lrf_right_h.stride), ustride = size_t(g.lrf_left.stride);
+  std::vector<double> vb(size_t(g.tsT_v.stride)), ub(size_t(g.tsT_u.stride));
+  for (int cls = 0; cls < 8; ++cls)
+    for (int b = 0; b < nb; ++b) {
+      std::fill(vb.begin(), vb.end(), 0.0);
+      std::fill(ub.begin(), ub.end(), 0.0);
+      for (int k = 0; k < n_transfers; ++k) {
+        const int r0 = g.tsT_rho[size_t(cls) * n_transfers + k];
+        if (r0 < 0) continue;
+        for (int a = 0; a < rk[k]; ++a) {
+          const int row = r0 + a;
+          if (row / 128 != b) continue;
+          std::copy_n(all_v.begin() + size_t(k) * vstride + size_t(a) * vld, n,
+                      vb.begin() + size_t(row % 128) * g.tsT_v.ld);
+          for (int i = 0; i < n; ++i)
+            ub[size_t(i) * g.tsT_u.ld + row % 128] = all_u[size_t(k) * ustride + size_t(i) * uld + a];
+        }
+      }
+      put_stack(g.tsT_v, cls * nb + b, vb);
+      put_stack(g.tsT_u, cls * nb + b, ub);
+    }
+  auto encode = [](CUtensorMap* m, const OpStack& st, long long rows) {
+    const cuuint64_t dims[2] = {cuuint64_t(st.ld), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(st.ld) * sizeof(double)};
+    const cuuint32_t box[2] = {cuuint32_t(kKC + 4), 128u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = resolve_encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, st.d.p, dims, strides, box, estr,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuTensorMapEncodeTiled failed for a target-major two-stage stack");
+  };
+  encode(&g.tsT_vmap, g.tsT_v, (long long)8 * nb * 128);
+  encode(&g.tsT_umap, g.tsT_u, (long long)8 * nb * urows);
+  g.has_tsT = true;
 }
 
 // Two-stage low-rank operators (see Group::has_ts): per source class the V_t^H
@@ -166,13 +270,16 @@ bool use_two_stage() {  // read at every precompute (tests switch it)
 // transfer for all classes: stage 2 gathers an entry's B at column
 // ycol[k] + 16 j (ts_opcol; 32-B aligned) whatever its sources' classes.
 void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers,
-                     const std::vector<int>& rk, const std::vector<double>& all_v) {
+                     const std::vector<int>& rk, const std::vector<double>& all_v, const std::vector<double>& all_u) {
   g.has_ts = false;
+  g.has_tsT = false;
   if (!use_two_stage()) return;
   const int n = h->n;
   int rmax = 0;
   for (int r : rk) rmax = std::max(rmax, r);
-  if (rmax == 0 || rmax > 32 || g.lrf_left.ld != 32) return;
+  if (rmax == 0 || rmax > 255 || n > 1024) return;
+  if (two_stage_mode() >= 2) build_two_stage_target_major(h, g, n_transfers, transfers, rk, all_v, all_u);
+  if (rmax > 32 || g.lrf_left.ld != 32) return;
   g.ts_ntr = n_transfers;
   g.ts_rank = rk;
   g.ts_rho0.assign(size_t(8) * n_transfers, -1);
@@ -275,6 +382,7 @@ void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t*
   std::iota(ident.begin(), ident.end(), 0);
   std::vector<double> bl(g.lrf_left.stride), br(g.lrf_right_h.stride);
   std::vector<double> all_v(size_t(n_transfers) * g.lrf_right_h.stride);
+  std::vector<double> all_u(size_t(n_transfers) * g.lrf_left.stride);
   for (int k = 0; k < n_transfers; ++k) {
     const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
     const int o = g.main.op[c];
@@ -293,13 +401,14 @@ void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t*
     put_stack(g.lrf_left, k, bl);
     put_stack(g.lrf_right_h, k, br);
     std::copy(br.begin(), br.end(), all_v.begin() + size_t(k) * br.size());
+    std::copy(bl.begin(), bl.end(), all_u.begin() + size_t(k) * bl.size());
     g.fullmap.op[c] = k;
   }
   g.fullmap.push();
   set_per_op(g.lrf_left, {}, rk);
   set_per_op(g.lrf_right_h, rk, {});
   g.has_lrfull = true;
-  build_two_stage(h, g, n_transfers, transfers, rk, all_v);
+  build_two_stage(h, g, n_transfers, transfers, rk, all_v, all_u);
 }
 
 }  // namespace cfm

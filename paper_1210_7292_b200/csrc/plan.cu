@@ -128,7 +128,155 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp) {
   lp.ts2 = std::move(p2);
   push_plan(lp.ts1, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src);
   push_plan(lp.ts2, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src);
-  lp.ts = true;
+  lp.ts = 1;
+}
+
+// Target-major two-stage plans (Group::has_tsT; LevelPlan::ts == 2) straight
+// from the level's CSR lists.  Sources and targets are classed by the range
+// pattern of their transfers (a cell whose transfers fit both ranges of an
+// axis takes bit 0).  Stage 1: tiles of 64 sources of one class x tsT_nb
+// entries (128-row blocks of the class's V stack); the epilogue writes the row
+// (slot, a) of source s to Y_T at nbr[s][slot] + a, where nbr holds the element
+// offset target * ldY + rho_T[class(target)][k] of the pair's rank run (-1: the
+// source has no pair with that transfer, nothing is written and the
+// corresponding Y_T columns keep the zeros of the one-time memset).  Stage 2:
+// tiles of 64 targets of one class (ascending rows; tiles ordered by their
+// smallest row), one entry per 128-column block of the class's U stack whose
+// B rows are the targets' Y_T rows of that block -- a plain dense GEMM on the
+// full-operator step kernel.
+static bool build_two_stage_plan_T(const Group& g, LevelPlan& lp, int64_t n_targets, const int64_t* tgt,
+                                   const int64_t* off, const int64_t* src, const int16_t* codes) {
+  const int64_t n_rows = lp.n_rows;
+  const int ntr = g.ts_ntr, nb = g.tsT_nb, nslots = g.tsT_nslots;
+  const int64_t ldy = int64_t(nb) * 128;
+  if (n_rows <= 0 || double(n_rows) * double(ldy) >= 2147483647.0) return false;  // int32 offsets
+  static const double budget_gb = [] {
+    const char* e = getenv("CFM_LR_TWOSTAGE_GB");
+    return e ? atof(e) : 24.0;
+  }();
+  if (double(n_rows) * double(ldy) * 8 > budget_gb * 1e9) return false;
+  // decoded transfer components of every code
+  std::array<int8_t, 3 * kNumCodes> tc{};
+  for (int c = 0; c < kNumCodes; ++c) {
+    int t0, t1, t2;
+    tcode_decode(c, t0, t1, t2);
+    tc[3 * c] = int8_t(t0), tc[3 * c + 1] = int8_t(t1), tc[3 * c + 2] = int8_t(t2);
+  }
+  std::vector<int8_t> smn(size_t(n_rows) * 3, 127), smx(size_t(n_rows) * 3, -128);
+  std::vector<int8_t> tcls(n_targets, -1);
+  int64_t need_rows = 0;
+  for (int64_t i = 0; i < n_targets; ++i) {
+    if (tgt[i] < 0 || tgt[i] >= n_rows) return false;
+    int8_t mn[3] = {127, 127, 127}, mx[3] = {-128, -128, -128};
+    for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+      const int c = codes[q];
+      const int k = g.fullmap.op[c];
+      if (k < 0 || k >= ntr || g.ts_rank[k] <= 0) return false;
+      need_rows += g.ts_rank[k];
+      const int64_t v = src[q];
+      if (v < 0 || v >= n_rows) return false;
+      for (int a = 0; a < 3; ++a) {
+        const int8_t t = tc[3 * c + a];
+        mn[a] = std::min(mn[a], t), mx[a] = std::max(mx[a], t);
+        smn[size_t(v) * 3 + a] = std::min(smn[size_t(v) * 3 + a], t);
+        smx[size_t(v) * 3 + a] = std::max(smx[size_t(v) * 3 + a], t);
+      }
+    }
+    if (off[i + 1] == off[i]) continue;
+    int b = 0;
+    for (int a = 0; a < 3; ++a) {
+      if (mx[a] <= 2 && mn[a] >= -3) continue;
+      if (mn[a] >= -2 && mx[a] <= 3) b |= 1 << a;
+      else return false;  // not an octree far list
+    }
+    tcls[i] = int8_t(b);
+  }
+  std::vector<int8_t> scls(n_rows, -1);
+  std::vector<std::vector<int>> src_by(8);
+  for (int64_t v = 0; v < n_rows; ++v) {
+    if (smx[size_t(v) * 3] == -128) continue;
+    int b = 0;
+    for (int a = 0; a < 3; ++a) {
+      if (smx[size_t(v) * 3 + a] <= 2 && smn[size_t(v) * 3 + a] >= -3) continue;
+      if (smn[size_t(v) * 3 + a] >= -2 && smx[size_t(v) * 3 + a] <= 3) b |= 1 << a;
+      else return false;
+    }
+    scls[v] = int8_t(b);
+    src_by[b].push_back(int(v));
+  }
+  int64_t tiles1 = 0;
+  for (int b = 0; b < 8; ++b) tiles1 += (int64_t(src_by[b].size()) + kBN - 1) / kBN;
+  if (double(tiles1) * kBN * nb * 128 > 1.7 * double(need_rows)) return false;  // sparse level: fused kernel
+  // per (source, class slot): where the pair's rank run lands in Y_T
+  std::vector<int> nbr(size_t(n_rows) * nslots, -1);
+  std::vector<char> tseen(n_rows, 0);
+  for (int64_t i = 0; i < n_targets; ++i) {
+    if (off[i + 1] == off[i]) continue;
+    if (tseen[tgt[i]]) return false;  // a target listed twice: its Y_T row would be shared
+    tseen[tgt[i]] = 1;
+    const int ct = tcls[i];
+    for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+      const int k = g.fullmap.op[codes[q]];
+      const int64_t v = src[q];
+      const int slot = g.tsT_slot[size_t(scls[v]) * ntr + k];
+      const int rho = g.tsT_rho[size_t(ct) * ntr + k];
+      if (slot < 0 || rho < 0) return false;
+      int& w = nbr[size_t(v) * nslots + slot];
+      if (w >= 0) return false;  // the same (source, transfer) twice: not an octree list
+      w = int(tgt[i] * ldy + rho);
+    }
+  }
+  // stage 1 plan
+  HostPlan p1;
+  for (int b = 0; b < 8; ++b)
+    for (size_t i = 0; i < src_by[b].size(); i += kBN) {
+      p1.n_tiles++;
+      p1.tile_off.push_back(int(p1.entry_code.size()));
+      std::vector<int> cols(kBN, -1);
+      for (int c = 0; c < kBN && i + c < src_by[b].size(); ++c) cols[c] = src_by[b][i + c];
+      p1.tile_col.insert(p1.tile_col.end(), cols.begin(), cols.end());
+      for (int blk = 0; blk < g.tsT_nblk[b]; ++blk) {
+        p1.entry_code.push_back(b * nb + blk);
+        p1.entry_src.insert(p1.entry_src.end(), cols.begin(), cols.end());
+      }
+    }
+  p1.tile_off.push_back(int(p1.entry_code.size()));
+  // stage 2 plan: tiles of one class, ordered by their smallest target row
+  std::vector<std::vector<int>> tgt_by(8);
+  for (int64_t i = 0; i < n_targets; ++i)
+    if (tcls[i] >= 0) tgt_by[tcls[i]].push_back(int(tgt[i]));
+  struct T2 { int cls; int first; int count; int minrow; };
+  std::vector<T2> t2;
+  for (int b = 0; b < 8; ++b) {
+    std::sort(tgt_by[b].begin(), tgt_by[b].end());
+    for (size_t i = 0; i < tgt_by[b].size(); i += kBN)
+      t2.push_back({b, int(i), int(std::min<size_t>(kBN, tgt_by[b].size() - i)), tgt_by[b][i]});
+  }
+  std::stable_sort(t2.begin(), t2.end(), [](const T2& a, const T2& b) { return a.minrow < b.minrow; });
+  HostPlan p2;
+  p2.n_tiles = int64_t(t2.size());
+  lp.ts_tile_tmin.assign(t2.size(), n_rows);
+  for (size_t t = 0; t < t2.size(); ++t) {
+    p2.tile_off.push_back(int(p2.entry_code.size()));
+    std::vector<int> cols(kBN, -1);
+    for (int c = 0; c < t2[t].count; ++c) cols[c] = tgt_by[t2[t].cls][t2[t].first + c];
+    p2.tile_col.insert(p2.tile_col.end(), cols.begin(), cols.end());
+    lp.ts_tile_tmin[t] = t2[t].minrow;
+    for (int blk = 0; blk < g.tsT_nblk[t2[t].cls]; ++blk) {
+      p2.entry_code.push_back(t2[t].cls * nb + blk);
+      for (int c = 0; c < kBN; ++c) p2.entry_src.push_back(cols[c] >= 0 ? cols[c] * nb + blk : -1);
+    }
+  }
+  p2.tile_off.push_back(int(p2.entry_code.size()));
+  for (int64_t t = p2.n_tiles - 1; t > 0; --t)
+    lp.ts_tile_tmin[t - 1] = std::min(lp.ts_tile_tmin[t - 1], lp.ts_tile_tmin[t]);
+  lp.ts1 = std::move(p1);
+  lp.ts2 = std::move(p2);
+  push_plan(lp.ts1, lp.ts1_col, lp.ts1_off, lp.ts1_code, lp.ts1_src);
+  push_plan(lp.ts2, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src);
+  upload(lp.tsT_nbr, nbr);
+  lp.ts = 2;
+  return true;
 }
 
 // Hybrid plans (CFM_HYBRID=0 disables): measured at config 2 the step kernel
@@ -495,7 +643,11 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
         }
     });
   }
-  if (g.kind == kLowRank && g.has_ts && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) build_two_stage_plan(g, lp);
+  if (g.kind == kLowRank && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) {
+    bool done = false;
+    if (g.has_tsT && two_stage_mode() >= 2) done = build_two_stage_plan_T(g, lp, n_targets, tgt, off, src, codes);
+    if (!done && g.has_ts) build_two_stage_plan(g, lp);
+  }
   if (use_hybrid() && full_mode(g, lp) && lp.mode == 0 && lp.hp.n_tiles > 0) {
     try {
       build_hybrid_plan(h, lp, n_targets, tgt, off, src, codes, key);

@@ -102,6 +102,7 @@ struct TileParams {
   long long n_entries;               // host-side hint: entries of the plan (kernel choice)
   long long x_rows;                  // full-operator mode: rows of the padded source array x
   int ft_pipe;                       // full-operator target tiles: flat pipelined consumer loop
+  int ft_skew;                       // flat loop: chunks the odd-wn consumer warps start behind the even ones (0: off)
   int ft_ktail;                      // flat loop: an entry's last k-step has one real column (DFMA rank-1)
   // two-stage low-rank mode (full-operator kernels):
   int code_is_op;   // entry codes are operator ids (no code tables, identity permutations)
@@ -110,6 +111,8 @@ struct TileParams {
   int y_rowblk;     // pair-mode stage-1 output (0: off): row i of entry code c lands at
                     // y[source * y_ld + y_colmap[c * 128 + i]] (skipped where -1)
   const int* y_colmap;
+  const int* y_nbr;   // target-major stage 1 (null: off): y_colmap[c * 128 + i] = (slot << 8 | a), and row i of a
+  int y_nslots;       // source lands at y[y_nbr[source * y_nslots + slot] + a] (skipped where either is -1)
   int b_block;      // B of entry e = rows [e * BN, e * BN + BN) of tmap_b (one 2-D box; no gathers)
   const int* op_col;  // seg_pair_gemm_kernel: B of entry e gathered from its sources' rows of
                       // tmap_b at column op_col[entry_code[e]]

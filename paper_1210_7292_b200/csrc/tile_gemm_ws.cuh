@@ -198,10 +198,12 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
   const int e_begin = p.tile_off[tile], e_end = p.tile_off[tile + 1];
 
   for (int c = tid; c < BN; c += NC + NP) s_col[c] = p.tile_col[(long long)tile * BN + c];
-  for (int c = tid; c < 343; c += NC + NP) {
-    s_op[c] = p.code_op[c];
-    s_rp[c] = p.code_rperm[c];
-    s_cp[c] = p.code_cperm[c];
+  if (!p.code_is_op) {
+    for (int c = tid; c < 343; c += NC + NP) {
+      s_op[c] = p.code_op[c];
+      s_rp[c] = p.code_rperm[c];
+      s_cp[c] = p.code_cperm[c];
+    }
   }
   const int n_cached = min(e_end - e_begin, kMaxTileEntries);
   for (int i = tid; i < n_cached; i += NC + NP) s_ecode[i] = p.entry_code[e_begin + i];
@@ -517,10 +519,17 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
 #pragma unroll
             for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
         };
+        // skewed consumer halves (ft_skew chunks): the warps with odd wn start
+        // when the even ones have finished ft_skew chunks, so the two consumer
+        // warps of an SM sub-partition reach their per-entry / per-tile
+        // epilogues at different times and one keeps the DMMA pipe busy
+        const bool skewed = WN == 2 && p.ft_skew > 0 && total > p.ft_skew && p.ft_skew < STAGES;
+        if (skewed && wn == 1) asm volatile("bar.sync 2, %0;\n" ::"n"(NC) : "memory");
         mbar_wait(full, 0);
         load(a0, b0, 0, 0);
         for (int qq = 0; qq < total; ++qq) {
           const int s = qq % STAGES;
+          if (skewed && wn == 0 && qq == p.ft_skew) asm volatile("bar.arrive 2, %0;\n" ::"n"(NC) : "memory");
           // an entry's last k-step with one real column (p.ft_ktail: nk % KC ==
           // KC - 3, e.g. l = 5) runs as a rank-1 DFMA update instead of a DMMA
           // over 3 zero columns: DMMA and DFMA share the FP64 pipe
@@ -569,10 +578,31 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
             // packed two-stage stage 1: the entry's 128 rows of every source's
             // Y row, at the columns of ts_colmap (a transfer's rows are
             // contiguous: the 8 lanes of a tg write runs of up to 64 B)
-            const int* cm = p.y_colmap + (long long)__ldg(p.entry_code + e_begin + qq / nch) * BM + r0 + g;
+            const int* cm = p.y_colmap + (long long)code_of(e_begin + qq / nch) * BM + r0 + g;
             int ycol[MT];
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi) ycol[mi] = __ldg(cm + mrow(mi));
+            if (p.y_nbr) {
+              // target-major Y: row (slot, a) of source v goes to the Y_T row of the
+              // pair's target, at y_nbr[v][slot] + a (the 8 lanes of a tg mostly
+              // share a slot: one broadcast load, a run of up to 64 B stored)
+#pragma unroll
+              for (int nj = 0; nj < NTL; ++nj)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int v = s_col[ncol(nj) + 2 * tg + h];
+                  const int* nb = p.y_nbr + (long long)v * p.y_nslots;
+                  int w[MT];
+#pragma unroll
+                  for (int mi = 0; mi < MT; ++mi) w[mi] = (v >= 0 && ycol[mi] >= 0) ? __ldg(nb + (ycol[mi] >> 8)) : -1;
+#pragma unroll
+                  for (int mi = 0; mi < MT; ++mi) {
+                    if (w[mi] >= 0) p.y[(long long)w[mi] + (ycol[mi] & 255)] = acc[mi][nj][h];
+                    acc[mi][nj][h] = 0.0;
+                  }
+                }
+              continue;
+            }
 #pragma unroll
             for (int nj = 0; nj < NTL; ++nj)
 #pragma unroll

@@ -27,6 +27,7 @@ CPU fallback.
 
 from __future__ import annotations
 
+import collections.abc
 import ctypes
 import threading
 import time
@@ -141,6 +142,57 @@ def _batch_to_csr_py(batch):
     if t.size and (t.min() < -128 or t.max() > 127):
         t = np.clip(t, -128, 127)  # far outside [-3,3]: reported as missing operator by the native side
     return tgt, off, src, np.ascontiguousarray(t.astype(np.int8))
+
+
+class _FlushLog(collections.abc.Sequence):
+    """``block_stats[level]["flushes"]``: the reference's list of one ``(rep,
+    columns)`` tuple per GEMM flush (m2l.py:406, :429), grown by every apply.
+    A planned level flushes the same ~pairs / block_size tuples at every step
+    (181 k at BASELINE config 2's level 6), so ``extend`` keeps a reference to
+    the per-plan list instead of copying it (1.3 ms of the timed step and
+    unbounded growth otherwise); reading materialises the concatenation.
+    Compares equal to the plain list the reference builds."""
+
+    __slots__ = ("_chunks", "_flat")
+
+    def __init__(self, items=()):
+        self._chunks = [list(items)] if items else []
+        self._flat = None
+
+    def extend(self, items):
+        self._chunks.append(items if isinstance(items, list) else list(items))
+        self._flat = None
+
+    def append(self, item):
+        self.extend([item])
+
+    def _list(self):
+        if self._flat is None:
+            self._flat = [x for c in self._chunks for x in c]
+            self._chunks = [self._flat]
+        return self._flat
+
+    def __len__(self):
+        return sum(len(c) for c in self._chunks)
+
+    def __iter__(self):
+        return iter(self._list())
+
+    def __getitem__(self, i):
+        return self._list()[i]
+
+    def __eq__(self, other):
+        if isinstance(other, _FlushLog):
+            other = other._list()
+        return self._list() == other
+
+    def __ne__(self, other):
+        return not self == other
+
+    __hash__ = None
+
+    def __repr__(self):
+        return repr(self._list())
 
 
 class B200M2LHandler:
@@ -800,7 +852,8 @@ class B200M2LHandler:
             if summary is None:
                 summary = self._record_summary(level, key, counts, planned)
             pairs, products, flushes, reps = summary
-            st = self.block_stats.setdefault(level, {"columns": 0, "products": 0, "reps_used": set(), "flushes": []})
+            st = self.block_stats.setdefault(
+                level, {"columns": 0, "products": 0, "reps_used": set(), "flushes": _FlushLog()})
             st["columns"] += pairs
             st["products"] += products
             st["reps_used"].update(reps)

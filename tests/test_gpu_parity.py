@@ -291,9 +291,11 @@ def test_rank1_ktail_matches_padded_dmma(torch_cuda, monkeypatch):
 @pytest.mark.parametrize("variant", ["iablk", "iasym", "ia"])
 def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeypatch):
     """Dense low-rank levels run as two stages (Y = V_t^H x per source and class
-    transfer, then U_t Y per target tile).  Full level 5 at l = 5 (32,768 cells):
-    the two-stage path is taken, matches the oracle (<= 1e-10) and the fused
-    single-kernel path (CFM_LR_TWOSTAGE=0) to rounding, with equal flops."""
+    transfer, then U_t Y per target).  Full level 5 at l = 5 (32,768 cells):
+    both two-stage layouts (2: target-major Y + dense stage 2, the default;
+    1: source-major Y + rank-segment stage 2) are taken, match the oracle
+    (<= 1e-10) and the fused single-kernel path (CFM_LR_TWOSTAGE=0) to
+    rounding, with equal flops."""
     torch = torch_cuda
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
@@ -305,12 +307,12 @@ def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeyp
     rng = np.random.default_rng(7)
     mp = torch.from_numpy(rng.uniform(-1, 1, (len(cells), order**3))).cuda()
     out, flops = {}, {}
-    for ts in ("1", "0"):
+    for ts in ("2", "1", "0"):
         monkeypatch.setenv("CFM_LR_TWOSTAGE", ts)
         h = make_handler(variant, laplace_kernel(), ChebyshevGrid(order), eps)
         h.precompute({level: transfers}, lw)
         h.plan_level_cells(level, cells)
-        assert h.plan_stats(level)["two_stage"] == (ts == "1")
+        assert h.plan_stats(level)["two_stage"] == (ts != "0")
         loc = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
         flops[ts] = h.apply_planned(level, mp, loc)
         loc2 = torch.zeros_like(loc)
@@ -320,9 +322,47 @@ def test_two_stage_lowrank_matches_fused_and_oracle(torch_cuda, variant, monkeyp
     orc = O.OracleM2L(variant, O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
     ref = np.zeros(mp.shape)
     fr = orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
-    assert flops["1"] == flops["0"] == fr
-    assert O.rel_l2(out["1"], ref) <= 1e-10
-    assert O.rel_l2(out["1"], out["0"]) <= 1e-13
+    assert flops["2"] == flops["1"] == flops["0"] == fr
+    for ts in ("2", "1"):
+        assert O.rel_l2(out[ts], ref) <= 1e-10
+        assert O.rel_l2(out[ts], out["0"]) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", ["sparse", "slab"])
+def test_two_stage_target_major_missing_pairs(torch_cuda, shape, monkeypatch):
+    """Target-major two-stage path on levels whose targets miss part of their
+    class's transfers (a cube with 10% of the cells removed; a 32 x 32 x 12 slab):
+    the Y_T columns of absent pairs stay zero, locals match the oracle
+    (<= 1e-10) also when the apply is repeated on non-zero locals, and rows of
+    empty targets are untouched."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_LR_TWOSTAGE", "2")
+    monkeypatch.setenv("CFM_PLAN_MODE", "target")
+    order, level, eps = 5, 5, 1e-5
+    cells = _full_level(level)
+    rng = np.random.default_rng(23)
+    if shape == "sparse":
+        cells = cells[rng.random(len(cells)) >= 0.1]
+    else:
+        cells = cells[cells[:, 2] < 12]
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: transfers}, lw)
+    h.plan_level_cells(level, cells)
+    assert h.plan_stats(level)["two_stage"]
+    mp = torch.from_numpy(rng.uniform(-1, 1, (len(cells), order**3))).cuda()
+    loc = torch.full(mp.shape, 0.5, dtype=torch.float64, device="cuda")
+    h.apply_planned(level, mp, loc)
+    h.apply_planned(level, 2.0 * mp, loc)
+    orc = O.OracleM2L("iablk", O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    ref = np.full(mp.shape, 0.5)
+    orc.apply_fast(level, tgt, off, src, t, 3.0 * mp.cpu().numpy(), ref)
+    assert O.rel_l2(loc.cpu().numpy() - 0.5, ref - 0.5) <= 1e-10
 
 
 @pytest.mark.gpu
@@ -338,6 +378,7 @@ def test_two_stage_kstep_skip_bitwise(torch_cuda, monkeypatch):
     tgt, off, src, t = O.far_lists(cells, level)
     transfers = sorted({tuple(int(c) for c in v) for v in t})
     lw = {level: 1.0 / (1 << level)}
+    monkeypatch.setenv("CFM_LR_TWOSTAGE", "1")
     h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), eps)
     h.precompute({level: transfers}, lw)
     h.plan_level_cells(level, cells)

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--signed", action="store_true", help="multipoles U[-1,1] (as bench.py) instead of U[0,1]")
     ap.add_argument("--host", action="store_true", help="pinned host numpy buffers (the e2e path)")
     ap.add_argument("--flush", action="store_true", help="write 256 MB (> L2) and synchronize before each step")
+    ap.add_argument("--levels", default=None, help="comma list: apply only these levels (all are planned)")
     a = ap.parse_args()
     import torch
 
@@ -48,6 +49,8 @@ def main():
         mp = {l: hm[l].numpy() for l in levels}
         loc = {l: hl[l].numpy() for l in levels}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda") if a.flush else None
+    if a.levels:
+        levels = [int(x) for x in a.levels.split(",")]
     for i in range(a.reps):
         if flush is not None:
             flush.fill_(float(i))
