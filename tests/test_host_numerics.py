@@ -106,3 +106,24 @@ def test_randomized_truncated_svd_matches_lapack():
     got = truncated_svds_device(torch.from_numpy(full), 1e-6)
     for a, f in zip(full, got):
         assert f.rank == truncated_svd(a, 1e-6).rank == 200
+
+
+def test_flush_log_behaves_like_the_reference_list():
+    """block_stats[level]["flushes"] (m2l.py:406, :429 of the reference) is a
+    list of (rep, columns) tuples; the handler's lazy log keeps references to the
+    per-plan lists and must read, compare and grow like that list."""
+    from paper_1210_7292_b200.m2l import _FlushLog
+
+    per_plan = [((1, 0, 0), 256), ((1, 1, 0), 17)]
+    log, ref = _FlushLog(), []
+    for _ in range(3):
+        log.extend(per_plan)
+        ref.extend(per_plan)
+    log.append(((3, 2, 1), 5))
+    ref.append(((3, 2, 1), 5))
+    assert log == ref and ref == log and len(log) == len(ref) == 7
+    assert list(log) == ref and log[0] == ref[0] and log[-1] == ref[-1] and log[2:4] == ref[2:4]
+    assert per_plan == [((1, 0, 0), 256), ((1, 1, 0), 17)]  # the shared per-plan list is never mutated
+    log.extend(per_plan)
+    assert len(log) == 9 and log != ref
+    assert _FlushLog() == [] and not _FlushLog()
