@@ -414,6 +414,7 @@ int64_t launch_ts_gemm(int stage, TileParams q, int64_t n_tiles, int64_t tile_ba
   t.tile_col = q.tile_col;
   t.tile_off = q.tile_off;
   t.entry_code = q.entry_code;
+  t.code_op = q.code_is_op ? nullptr : q.code_op;
   t.entry_src = q.entry_src;
   t.nk = q.nk;
   t.nr = q.nr;

@@ -278,10 +278,10 @@ void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* tr
   int rmax = 0;
   for (int r : rk) rmax = std::max(rmax, r);
   if (rmax == 0 || rmax > 255 || n > 1024) return;
-  if (two_stage_mode() >= 2) build_two_stage_target_major(h, g, n_transfers, transfers, rk, all_v, all_u);
-  if (rmax > 32 || g.lrf_left.ld != 32) return;
   g.ts_ntr = n_transfers;
   g.ts_rank = rk;
+  if (two_stage_mode() >= 2) build_two_stage_target_major(h, g, n_transfers, transfers, rk, all_v, all_u);
+  if (rmax > 32 || g.lrf_left.ld != 32) return;
   g.ts_rho0.assign(size_t(8) * n_transfers, -1);
   int max_rows = 0;
   for (int cls = 0; cls < 8; ++cls) {

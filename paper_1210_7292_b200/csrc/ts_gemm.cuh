@@ -35,7 +35,8 @@ struct TsGemmParams {
   int tile_base;          // first tile of this launch in the plan
   const int* tile_col;    // [tiles * 64] stage 1: source rows, stage 2: target rows (-1: empty column)
   const int* tile_off;    // [tiles + 1] entry range per tile (every tile has >= 1 entry)
-  const int* entry_code;  // [E] operator block id
+  const int* entry_code;  // [E] operator block id (code_op null) or transfer code
+  const int* code_op;     // optional transfer code -> operator block id
   const int* entry_src;   // [E * 64] rows of tmap_b (-1: empty)
   int nk;                 // inner length of an entry
   int nr;                 // result rows (stage 1: 128 per entry; stage 2: n)
@@ -94,7 +95,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) ts_gemm_kernel(const __grid_con
         const int4* srow = reinterpret_cast<const int4*>(p.entry_src + (long long)e * BN);
 #pragma unroll
         for (int j = 0; j < BN / 4; ++j) rows[j] = __ldg(srow + j);
-        const int arow = __ldg(p.entry_code + e) * p.a_rows + r0;
+        int op = __ldg(p.entry_code + e);
+        if (p.code_op) op = __ldg(p.code_op + op);
+        const int arow = op * p.a_rows + r0;
         for (int kc = 0; kc < nch; ++kc, ++q) {
           const int s = q % ST;
           if (q >= ST) mbar_wait_backoff(empty + s, ((q / ST) & 1) ^ 1);

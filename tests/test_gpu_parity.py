@@ -1076,3 +1076,34 @@ def test_device_classifier_bit_exact(torch_cuda, case):
         ref_code[a:b] = (tt[:, 0] + 3) * 49 + (tt[:, 1] + 3) * 7 + (tt[:, 2] + 3)
     assert np.array_equal(src.astype(np.int64), ref_src)
     assert np.array_equal(code.astype(np.int64), ref_code)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order,eps", [(6, 1e-5), (7, 1e-7), (4, 1e-4)])
+def test_two_stage_target_major_other_orders(torch_cuda, order, eps, monkeypatch):
+    """Target-major two-stage path at other expansion sizes: l = 6 (216 rows: two
+    128-row result blocks per stage-2 tile, 7 K-chunks in stage 1), l = 7 with
+    ranks above 32 (343 rows, three row blocks), and l = 4 (n = 64: below the
+    full-operator TMA sizes, so the level must fall back to the fused kernel).
+    Full level 4 (4,096 cells), iablk, vs the oracle (<= 1e-10)."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_LR_TWOSTAGE", "2")
+    level = 4
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: transfers}, lw)
+    h.plan_level_cells(level, cells)
+    assert h.plan_stats(level)["two_stage"] == (order >= 5)
+    mp = torch.from_numpy(np.random.default_rng(29).uniform(-1, 1, (len(cells), order**3))).cuda()
+    loc = torch.full(mp.shape, -0.75, dtype=torch.float64, device="cuda")
+    flops = h.apply_planned(level, mp, loc)
+    orc = O.OracleM2L("iablk", O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    ref = np.full(mp.shape, -0.75)
+    fr = orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert flops == fr
+    assert O.rel_l2(loc.cpu().numpy() + 0.75, ref + 0.75) <= 1e-10
