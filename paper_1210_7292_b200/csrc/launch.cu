@@ -2,6 +2,7 @@
 #include "internal.hpp"
 #include "seg_gemm.cuh"
 #include "ts_gemm.cuh"
+#include "step_gemm.cuh"
 
 namespace cfm {
 
@@ -320,9 +321,132 @@ bool launch_lowrank_fused(const LowRankParams& lp_, int rmax, int64_t first, int
   return false;
 }
 
+// ---- persistent step kernel (step_gemm.cuh)
+// CFM_STEP_PERSIST=0: one CTA per tile on tile_gemm_ws_kernel instead
+bool use_step_persistent() {
+  const char* e = getenv("CFM_STEP_PERSIST");
+  return !e || atoi(e) != 0;
+}
+
+// A zeroed work counter for one launch: per device a small pool of counters,
+// handed out round-robin and zeroed on the launch's stream right before it
+// (256 launches would have to be in flight at once for two to share one).
+static unsigned* step_queue_slot(cudaStream_t s) {
+  constexpr int kSlots = 256;
+  static std::mutex mu;
+  static std::map<int, std::pair<unsigned*, int>> pools;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  unsigned* slot = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& pl = pools[dev];
+    if (!pl.first) CUDA_CHECK(cudaMalloc(&pl.first, kSlots * sizeof(unsigned)));
+    slot = pl.first + pl.second;
+    pl.second = (pl.second + 1) % kSlots;
+  }
+  CUDA_CHECK(cudaMemsetAsync(slot, 0, sizeof(unsigned), s));
+  return slot;
+}
+
+// Can these tile lists run on the persistent kernel?  Full-operator staging
+// with KC = 32, whole operators (no per-operator row / inner counts), real
+// data, every list target tiles, pair entries or a Y_T scatter; dense lists
+// only when the last 128-row block wastes less than a warp's rows (l = 5: the
+// row-skipping kernel serves l = 7, 9).
+static bool step_persistent_ok(const std::vector<TileParams>& segs, const std::vector<int64_t>& counts) {
+  if (!use_step_persistent() || segs.empty()) return false;
+  int live = 0;
+  int64_t tiles = 0;
+  const int* code_op = nullptr;
+  const TileParams& q0 = segs[0];
+  for (size_t i = 0; i < segs.size(); ++i) {
+    if (counts[i] == 0) continue;
+    const TileParams& q = segs[i];
+    ++live;
+    tiles += counts[i];
+    if (!q.ft || q.op_rows || q.op_klen || q.x_dc != 1 || q.y_dc != 1 || q.red_counter || q.b_block) return false;
+    if (q.nk > 512 || q.nr != q0.nr || q.nk != q0.nk || q.ft_rows != q0.ft_rows || q.ft_opshift) return false;
+    if (!q.code_is_op) {
+      if (code_op && code_op != q.code_op) return false;
+      code_op = q.code_op;
+    }
+    if (q.pair_out && q.y_rowblk && !q.y_nbr) return false;  // round-1 two-stage layout
+    if (!q.y_rowblk && (q.nr + 127) / 128 * 128 - q.nr >= 32) return false;
+    if (q.pair_out && (q.pipe_mp || q.pipe_loc || q.pipe_done)) return false;
+    if (!q.pair_out && !q.accumulate) return false;
+  }
+  return live > 0 && live <= kStepMaxSegs && tiles * ((q0.nr + 127) / 128) < (int64_t(1) << 31);
+}
+
+static int64_t launch_step_persistent(const std::vector<TileParams>& segs, const std::vector<int64_t>& counts,
+                                      cudaStream_t s) {
+  static StepParams zero{};
+  StepParams sp = zero;
+  const TileParams* first = nullptr;
+  int64_t work = 0;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    if (counts[i] == 0) continue;
+    TileParams q = segs[i];
+    if (!first) first = &segs[i];
+    encode_source_map(q, kStepKC);
+    StepSeg& g = sp.seg[sp.n_seg++];
+    const int nrb = (q.nr + 127) / 128;
+    g.start = int(work);
+    g.tile_base = q.tile_base;
+    g.mode = !q.pair_out ? 0 : (q.y_rowblk ? 2 : 1);
+    g.tile_col = q.tile_col;
+    g.tile_off = q.tile_off;
+    g.entry_code = q.entry_code;
+    g.entry_src = q.entry_src;
+    g.y = q.y;
+    g.y_ld = q.y_ld;
+    g.scale = q.scale;
+    g.rowinfo = q.y_colmap;
+    g.nbr = q.y_nbr;
+    g.nslots = q.y_nslots;
+    g.code_is_op = q.code_is_op;
+    g.pipe_mp = q.pipe_mp;
+    g.pipe_loc = q.pipe_loc;
+    g.pipe_done = q.pipe_done;
+    g.pipe_need_mp = q.pipe_need_mp;
+    g.pipe_need_loc = q.pipe_need_loc;
+    g.pipe_lo = q.pipe_lo;
+    g.pipe_hi = q.pipe_hi;
+    g.tmap_a = q.tmap_a;
+    g.tmap_b = q.tmap_b;
+    if (!q.code_is_op) sp.code_op = q.code_op;
+    work += counts[i] * nrb;
+  }
+  sp.n_work = int(work);
+  sp.nrb = (first->nr + 127) / 128;
+  sp.nk = first->nk;
+  sp.nr = first->nr;
+  sp.a_rows = first->ft_rows;
+  const int nch = (sp.nk + kStepKC - 1) / kStepKC;
+  {
+    const char* e = getenv("CFM_TS_SKEW");
+    sp.skew = std::min(e ? atoi(e) : 2, nch - 1);
+  }
+  sp.queue = step_queue_slot(s);
+  int dev = 0, sms = 148;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = int(std::min<int64_t>(work, sms));
+  const int smem = step_gemm_smem_bytes();
+  bool scatter = false;
+  for (int i = 0; i < sp.n_seg; ++i) scatter = scatter || sp.seg[i].mode == 2;
+  auto kern = scatter ? step_gemm_kernel<true> : step_gemm_kernel<false>;
+  CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kStepThreads, smem, s>>>(sp);
+  CUDA_CHECK(cudaGetLastError());
+  return 1;
+}
+
 // One launch over several tile lists sharing operator shapes (all levels of a
 // homogeneous dense group).  Segments are launched in the given order.
 int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int64_t>& counts, cudaStream_t s) {
+  if (step_persistent_ok(segs, counts)) return launch_step_persistent(segs, counts, s);
   MultiTileParams mp{};
   int64_t total = 0;
   mp.n_seg = 0;
@@ -405,6 +529,15 @@ bool use_ts_persistent() {
 
 int64_t launch_ts_gemm(int stage, TileParams q, int64_t n_tiles, int64_t tile_base, int device, cudaStream_t s) {
   if (n_tiles <= 0) return 0;
+  {
+    // CFM_TS_KERNEL=step: the dynamic-queue step kernel (step_gemm.cuh) instead of the
+    // round-robin kernel of ts_gemm.cuh (measured 1.2% slower on these uniform tiles)
+    const char* e = getenv("CFM_TS_KERNEL");
+    if (e && !strcmp(e, "step")) {
+      q.tile_base = int(tile_base);
+      return launch_step_persistent({q}, {n_tiles}, s);
+    }
+  }
   encode_source_map(q, kTsKC);
   TsGemmParams t{};
   t.nrb = (q.nr + 127) / 128;
