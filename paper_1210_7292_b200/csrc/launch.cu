@@ -372,7 +372,12 @@ static bool step_persistent_ok(const std::vector<TileParams>& segs, const std::v
       code_op = q.code_op;
     }
     if (q.pair_out && q.y_rowblk && !q.y_nbr) return false;  // round-1 two-stage layout
-    if (!q.y_rowblk && (q.nr + 127) / 128 * 128 - q.nr >= 32) return false;
+    // dead m-tiles in the last row block / empty k-steps in an entry's last chunk (l = 6, 7):
+    // the row- and k-step-skipping kernel stays ahead there (measured on the config-2 tree:
+    // l = 7 363.3 vs 367.5 ms, l = 6 147.2 vs 147.7 ms with skipping variants of this kernel;
+    // its tiles are 2,000+ chunks long, so the per-CTA overhead this kernel removes is < 0.2%)
+    if (!q.y_rowblk && (q.nr % 128 != 0 && 128 - q.nr % 128 >= 8)) return false;
+    if (!q.y_rowblk && q.nk % 32 != 0 && q.nk % 32 <= 24) return false;
     if (q.pair_out && (q.pipe_mp || q.pipe_loc || q.pipe_done)) return false;
     if (!q.pair_out && !q.accumulate) return false;
   }

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--signed", action="store_true", help="multipoles U[-1,1] (as bench.py) instead of U[0,1]")
     ap.add_argument("--host", action="store_true", help="pinned host numpy buffers (the e2e path)")
     ap.add_argument("--flush", action="store_true", help="write 256 MB (> L2) and synchronize before each step")
+    ap.add_argument("--order", type=int, default=None, help="expansion order override (same tree)")
     ap.add_argument("--levels", default=None, help="comma list: apply only these levels (all are planned)")
     a = ap.parse_args()
     import torch
@@ -26,6 +27,7 @@ def main():
 
     n, depth, order, geom, variant, eps = bench.CONFIGS[a.config]
     variant = a.variant or variant
+    order = a.order or order
     if a.gpu_tree:
         cells, widths, _ = bench.gpu_level_cells(a.config, 0)
     else:
