@@ -183,7 +183,8 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     const int nb = g.tsT_nb;
     const auto xo = xpad_layout(h, {{lp.n_rows, ldx}}, s);
     double* xp = h->xpad.as<double>() + xo[0];
-    launches += xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
+    const cfm_handler::TsPipe* pipe = h->ts_pipe;
+    if (!pipe) launches += xpad_copy(h, xp, ldx, d_x, 0, lp.n_rows, s);
     if (!lp.ts_y.p) {
       // columns of pairs a target does not have are never written by stage 1;
       // zeroed once, they contribute exact zeros to stage 2 in every step
@@ -210,7 +211,18 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     a.zero_row = h->zeros.as<double>();
     a.n_entries = lp.ts1.n_entries();
     const bool persist = use_ts_persistent();
-    launches += persist ? launch_ts_gemm(1, a, lp.ts1.n_tiles, 0, h->device, s) : launch_tiles(a, lp.ts1.n_tiles, s);
+    if (pipe) {
+      // host-buffer pipeline: stage 1 in chunks of row-ordered tiles, each padded and
+      // launched as soon as its multipole rows are resident
+      for (size_t c = 0; c + 1 < pipe->cut1.size(); ++c) {
+        CUDA_CHECK(cudaStreamWaitEvent(s, pipe->x_ready[c], 0));
+        launches += xpad_copy(h, xp, ldx, d_x, pipe->x_rows[c], pipe->x_rows[c + 1], s);
+        const int64_t t0 = pipe->cut1[c], t1 = pipe->cut1[c + 1];
+        launches += persist ? launch_ts_gemm(1, a, t1 - t0, t0, h->device, s) : launch_range(a, t0, t1 - t0, s);
+      }
+    } else {
+      launches += persist ? launch_ts_gemm(1, a, lp.ts1.n_tiles, 0, h->device, s) : launch_tiles(a, lp.ts1.n_tiles, s);
+    }
     TileParams b{};
     fill_ops(b, g.tsT_u, g.main);
     fill_plan(b, lp.ts2_col, lp.ts2_off, lp.ts2_code, lp.ts2_src, lp.ts2.n_tiles);
@@ -227,26 +239,31 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     b.scale = scale; b.accumulate = 1; b.pair_out = 0;
     b.zero_row = h->zeros.as<double>();
     b.n_entries = lp.ts2.n_entries();
-    if (h->ts_before_stage2) CUDA_CHECK(cudaStreamWaitEvent(s, h->ts_before_stage2, 0));
     const int64_t nt2 = lp.ts2.n_tiles;
+    auto run2 = [&](int64_t t0, int64_t t1) {
+      launches += persist ? launch_ts_gemm(2, b, t1 - t0, t0, h->device, s) : launch_range(b, t0, t1 - t0, s);
+    };
+    if (pipe) {
+      // stage 2 in chunks of row-ordered tiles: chunk c starts when its targets'
+      // locals are resident; after it, every row below the next chunk's smallest
+      // target row is final and goes back
+      for (size_t c = 0; c + 1 < pipe->cut2.size(); ++c) {
+        CUDA_CHECK(cudaStreamWaitEvent(s, pipe->y_ready[c], 0));
+        const int64_t t1 = pipe->cut2[c + 1];
+        run2(pipe->cut2[c], t1);
+        if (h->ts_after_chunk) h->ts_after_chunk(t1 < nt2 ? lp.ts_tile_tmin[t1] : lp.n_rows);
+      }
+      return launches;
+    }
+    if (h->ts_before_stage2) CUDA_CHECK(cudaStreamWaitEvent(s, h->ts_before_stage2, 0));
     if (h->ts_chunks > 1 && h->ts_after_chunk && int64_t(lp.ts_tile_tmin.size()) == nt2 && nt2 >= 2 * h->ts_chunks) {
-      // chunk boundaries on whole waves (one CTA per SM): a chunk of 3.5 waves
-      // would run as long as one of 4
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-      auto cut = [&](int c) {
-        if (c >= h->ts_chunks) return nt2;
-        const int64_t t = nt2 * c / h->ts_chunks;
-        return std::min<int64_t>(nt2, (t + sms / 2) / sms * sms);
-      };
-      for (int c = 0; c < h->ts_chunks; ++c) {
-        const int64_t t0 = cut(c), t1 = cut(c + 1);
-        if (t1 <= t0) continue;
-        launches += persist ? launch_ts_gemm(2, b, t1 - t0, t0, h->device, s) : launch_range(b, t0, t1 - t0, s);
-        h->ts_after_chunk(t1 < nt2 ? lp.ts_tile_tmin[t1] : lp.n_rows);
+      const std::vector<int64_t> cut = ts_chunk_cuts(nt2, h->ts_chunks, h->device);
+      for (size_t c = 0; c + 1 < cut.size(); ++c) {
+        run2(cut[c], cut[c + 1]);
+        h->ts_after_chunk(cut[c + 1] < nt2 ? lp.ts_tile_tmin[cut[c + 1]] : lp.n_rows);
       }
     } else {
-      launches += persist ? launch_ts_gemm(2, b, nt2, 0, h->device, s) : launch_tiles(b, nt2, s);
+      run2(0, nt2);
     }
     return launches;
   }
@@ -757,19 +774,64 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
       dy[i] = dx[i] + lv[i].bytes;
       o += 2 * lv[i].bytes;
     }
+    // large target-major two-stage levels stream their rows (CFM_TS_SLABS=0: whole arrays):
+    // multipoles in the row slabs the stage-1 chunks need, locals in the slabs of the
+    // stage-2 chunks, one event per slab
+    static const bool ts_slabs = [] {
+      const char* e = getenv("CFM_TS_SLABS");
+      return !e || atoi(e) != 0;
+    }();
+    std::vector<cfm_handler::TsPipe> pipes(n);
+    std::vector<char> has_pipe(n, 0);
+    std::vector<std::vector<int64_t>> y_rows(n);
     for (size_t i = 0; i < n; ++i) {
-      CUDA_CHECK(cudaMemcpyAsync(dx[i], lv[i].x, lv[i].bytes, cudaMemcpyHostToDevice, h->s_h2d));
-      ex[i] = next_ev();
-      CUDA_CHECK(cudaEventRecord(ex[i], h->s_h2d));
+      const LevelPlan& P = *lv[i].lp;
+      if (!ts_slabs || P.ts != 2 || P.n_rows < 65536 || P.ts1_need.empty() || P.ts2_need.empty()) continue;
+      cfm_handler::TsPipe& tp = pipes[i];
+      tp.cut1 = ts_chunk_cuts(int64_t(P.ts1_need.size()), 8, h->device);
+      tp.cut2 = ts_chunk_cuts(int64_t(P.ts2_need.size()), 8, h->device);
+      tp.x_rows.assign(1, 0);
+      for (size_t c = 1; c < tp.cut1.size(); ++c)
+        tp.x_rows.push_back(c + 1 == tp.cut1.size() ? P.n_rows : std::min(P.n_rows, P.ts1_need[tp.cut1[c] - 1] + 1));
+      y_rows[i].assign(1, 0);
+      for (size_t c = 1; c < tp.cut2.size(); ++c)
+        y_rows[i].push_back(c + 1 == tp.cut2.size() ? P.n_rows : std::min(P.n_rows, P.ts2_need[tp.cut2[c] - 1] + 1));
+      has_pipe[i] = 1;
     }
-    for (size_t i = 0; i < n; ++i) {
-      CUDA_CHECK(cudaMemcpyAsync(dy[i], lv[i].y, lv[i].bytes, cudaMemcpyHostToDevice, h->s_h2d));
-      ey[i] = next_ev();
-      CUDA_CHECK(cudaEventRecord(ey[i], h->s_h2d));
-    }
+    auto upload = [&](size_t i, bool locals) {
+      const LevelPlan& P = *lv[i].lp;
+      const size_t row_b = lv[i].bytes / size_t(std::max<int64_t>(P.n_rows, 1));
+      char* dst = locals ? dy[i] : dx[i];
+      const char* src = reinterpret_cast<const char*>(locals ? lv[i].y : lv[i].x);
+      if (!has_pipe[i]) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, lv[i].bytes, cudaMemcpyHostToDevice, h->s_h2d));
+        (locals ? ey[i] : ex[i]) = next_ev();
+        CUDA_CHECK(cudaEventRecord(locals ? ey[i] : ex[i], h->s_h2d));
+        return;
+      }
+      const std::vector<int64_t>& rows = locals ? y_rows[i] : pipes[i].x_rows;
+      std::vector<cudaEvent_t>& evs = locals ? pipes[i].y_ready : pipes[i].x_ready;
+      for (size_t c = 0; c + 1 < rows.size(); ++c) {
+        if (rows[c + 1] > rows[c])
+          CUDA_CHECK(cudaMemcpyAsync(dst + size_t(rows[c]) * row_b, src + size_t(rows[c]) * row_b,
+                                     size_t(rows[c + 1] - rows[c]) * row_b, cudaMemcpyHostToDevice, h->s_h2d));
+        evs.push_back(next_ev());
+        CUDA_CHECK(cudaEventRecord(evs.back(), h->s_h2d));
+      }
+      (locals ? ey[i] : ex[i]) = evs.back();
+    };
+    // small levels first (multipoles, then locals): they compute while the streamed
+    // levels' multipole slabs cross PCIe; then those slabs, then their locals slabs
+    for (int locals = 0; locals < 2; ++locals)
+      for (size_t i = 0; i < n; ++i)
+        if (!has_pipe[i]) upload(i, locals != 0);
+    for (int locals = 0; locals < 2; ++locals)
+      for (size_t i = 0; i < n; ++i)
+        if (has_pipe[i]) upload(i, locals != 0);
     CUDA_CHECK(cudaEventRecord(h->ev0, s));
     int64_t launches = 0;
     auto reset_hooks = [&] {
+      h->ts_pipe = nullptr;
       h->ts_before_stage2 = nullptr;
       h->ts_chunks = 1;
       h->ts_after_chunk = nullptr;
@@ -777,7 +839,7 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
     for (size_t i = 0; i < n; ++i) {
       LevelPlan& P = *lv[i].lp;
       const size_t row_b = lv[i].bytes / size_t(std::max<int64_t>(P.n_rows, 1));
-      CUDA_CHECK(cudaStreamWaitEvent(s, ex[i], 0));
+      if (!has_pipe[i]) CUDA_CHECK(cudaStreamWaitEvent(s, ex[i], 0));
       int64_t done = 0;
       auto download = [&](int64_t upto) {  // rows [done, upto) of level i are final
         if (upto <= done) return;
@@ -786,7 +848,10 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
                                    size_t(upto - done) * row_b, cudaMemcpyDeviceToHost, h->s_d2h));
         done = upto;
       };
-      if (P.ts) {
+      if (has_pipe[i]) {
+        h->ts_pipe = &pipes[i];
+        h->ts_after_chunk = download;
+      } else if (P.ts) {
         h->ts_before_stage2 = ey[i];
         h->ts_chunks = P.n_rows >= 65536 ? 8 : 1;
         h->ts_after_chunk = download;

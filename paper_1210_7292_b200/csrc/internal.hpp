@@ -228,6 +228,9 @@ struct LevelPlan {
   HostPlan ts1, ts2;
   DevBuf ts1_col, ts1_off, ts1_code, ts1_src, ts2_col, ts2_off, ts2_code, ts2_src;
   std::vector<int64_t> ts_tile_tmin;  // per stage-2 tile: smallest target row (tiles are in row order)
+  // target-major plans, host-buffer pipeline: rows that must be resident before a tile runs --
+  // per stage-1 tile the largest source row of tiles 0..t, per stage-2 tile the largest target row of tiles 0..t
+  std::vector<int64_t> ts1_need, ts2_need;
   DevBuf ts_y;          // stage-1 output Y[source row][class-stack row] (n_rows x ts_ldy)
   DevBuf tsT_nbr;       // target-major mode (ts == 2): [n_rows][tsT_nslots] element offset into Y_T of the
                         // (source, class slot)'s rank run, -1 where the source has no such pair
@@ -325,6 +328,15 @@ struct cfm_handler {
   // host-buffer low-rank pipeline (apply.cu): while set, a two-stage level waits
   // `ts_before_stage2` before stage 2 and runs stage 2 in `ts_chunks` tile
   // chunks, calling ts_after_chunk(rows below this are final) after each
+  // ... and a large target-major level streams its rows: stage-1 chunk c starts when
+  // multipole rows < x_rows[c + 1] are resident (x_ready[c]; padded chunk by chunk),
+  // stage-2 chunk c when the locals of its targets are (y_ready[c])
+  struct TsPipe {
+    std::vector<int64_t> cut1, cut2;  // tile boundaries of the stage-1 / stage-2 chunks
+    std::vector<int64_t> x_rows;      // cut1.size() row boundaries
+    std::vector<cudaEvent_t> x_ready, y_ready;
+  };
+  const TsPipe* ts_pipe = nullptr;
   cudaEvent_t ts_before_stage2 = nullptr;
   int ts_chunks = 1;
   std::function<void(int64_t)> ts_after_chunk;
@@ -413,6 +425,7 @@ int64_t launch_range(const TileParams& p, int64_t first, int64_t count, cudaStre
 int64_t launch_tiles(const TileParams& p, int64_t n_tiles, cudaStream_t s);
 int64_t launch_seg_pair(TileParams q, int64_t n_tiles, cudaStream_t s, int64_t tile_base = 0);
 bool use_ts_persistent();
+std::vector<int64_t> ts_chunk_cuts(int64_t n_tiles, int chunks, int device);
 int64_t launch_ts_gemm(int stage, TileParams q, int64_t n_tiles, int64_t tile_base, int device, cudaStream_t s);
 void fill_ops(TileParams& p, const OpStack& s, const CodeMap& m);
 void fill_plan(TileParams& p, const DevBuf& col, const DevBuf& toff, const DevBuf& code, const DevBuf& src,

@@ -532,6 +532,20 @@ bool use_ts_persistent() {
   return !e || atoi(e) != 0;
 }
 
+// Tile boundaries of `chunks` launches over n_tiles uniform tiles, on whole waves
+// (one CTA per SM: a chunk of 3.5 waves would run as long as one of 4).
+std::vector<int64_t> ts_chunk_cuts(int64_t n_tiles, int chunks, int device) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  std::vector<int64_t> cut{0};
+  for (int c = 1; c < chunks; ++c) {
+    const int64_t t = std::min<int64_t>(n_tiles, (n_tiles * c / chunks + sms / 2) / sms * sms);
+    if (t > cut.back() && t < n_tiles) cut.push_back(t);
+  }
+  cut.push_back(n_tiles);
+  return cut;
+}
+
 int64_t launch_ts_gemm(int stage, TileParams q, int64_t n_tiles, int64_t tile_base, int device, cudaStream_t s) {
   if (n_tiles <= 0) return 0;
   {

@@ -226,20 +226,28 @@ static bool build_two_stage_plan_T(const Group& g, LevelPlan& lp, int64_t n_targ
       w = int(tgt[i] * ldy + rho);
     }
   }
-  // stage 1 plan
-  HostPlan p1;
+  // stage 1 plan: tiles of 64 same-class sources (ascending rows), ordered by their
+  // first row, so a host-buffer apply can start on the first multipole slabs
+  struct T1 { int cls; int first; int count; int minrow; };
+  std::vector<T1> t1;
   for (int b = 0; b < 8; ++b)
-    for (size_t i = 0; i < src_by[b].size(); i += kBN) {
-      p1.n_tiles++;
-      p1.tile_off.push_back(int(p1.entry_code.size()));
-      std::vector<int> cols(kBN, -1);
-      for (int c = 0; c < kBN && i + c < src_by[b].size(); ++c) cols[c] = src_by[b][i + c];
-      p1.tile_col.insert(p1.tile_col.end(), cols.begin(), cols.end());
-      for (int blk = 0; blk < g.tsT_nblk[b]; ++blk) {
-        p1.entry_code.push_back(b * nb + blk);
-        p1.entry_src.insert(p1.entry_src.end(), cols.begin(), cols.end());
-      }
+    for (size_t i = 0; i < src_by[b].size(); i += kBN)
+      t1.push_back({b, int(i), int(std::min<size_t>(kBN, src_by[b].size() - i)), src_by[b][i]});
+  std::stable_sort(t1.begin(), t1.end(), [](const T1& a, const T1& b) { return a.minrow < b.minrow; });
+  HostPlan p1;
+  lp.ts1_need.assign(t1.size(), 0);
+  for (size_t t = 0; t < t1.size(); ++t) {
+    p1.n_tiles++;
+    p1.tile_off.push_back(int(p1.entry_code.size()));
+    std::vector<int> cols(kBN, -1);
+    for (int c = 0; c < t1[t].count; ++c) cols[c] = src_by[t1[t].cls][t1[t].first + c];
+    p1.tile_col.insert(p1.tile_col.end(), cols.begin(), cols.end());
+    lp.ts1_need[t] = std::max<int64_t>(t ? lp.ts1_need[t - 1] : 0, cols[t1[t].count - 1]);
+    for (int blk = 0; blk < g.tsT_nblk[t1[t].cls]; ++blk) {
+      p1.entry_code.push_back(t1[t].cls * nb + blk);
+      p1.entry_src.insert(p1.entry_src.end(), cols.begin(), cols.end());
     }
+  }
   p1.tile_off.push_back(int(p1.entry_code.size()));
   // stage 2 plan: tiles of one class, ordered by their smallest target row
   std::vector<std::vector<int>> tgt_by(8);
@@ -256,12 +264,14 @@ static bool build_two_stage_plan_T(const Group& g, LevelPlan& lp, int64_t n_targ
   HostPlan p2;
   p2.n_tiles = int64_t(t2.size());
   lp.ts_tile_tmin.assign(t2.size(), n_rows);
+  lp.ts2_need.assign(t2.size(), 0);
   for (size_t t = 0; t < t2.size(); ++t) {
     p2.tile_off.push_back(int(p2.entry_code.size()));
     std::vector<int> cols(kBN, -1);
     for (int c = 0; c < t2[t].count; ++c) cols[c] = tgt_by[t2[t].cls][t2[t].first + c];
     p2.tile_col.insert(p2.tile_col.end(), cols.begin(), cols.end());
     lp.ts_tile_tmin[t] = t2[t].minrow;
+    lp.ts2_need[t] = std::max<int64_t>(t ? lp.ts2_need[t - 1] : 0, cols[t2[t].count - 1]);
     for (int blk = 0; blk < g.tsT_nblk[t2[t].cls]; ++blk) {
       p2.entry_code.push_back(t2[t].cls * nb + blk);
       for (int c = 0; c < kBN; ++c) p2.entry_src.push_back(cols[c] >= 0 ? cols[c] * nb + blk : -1);
