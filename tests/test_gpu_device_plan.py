@@ -138,9 +138,12 @@ def test_device_planner_edge_levels():
 
 def test_lowrank_host_pipeline_bitwise(monkeypatch):
     """iablk from pinned host buffers over levels 4-6 of a full cube (level 6
-    two-stage with stage 2 in row-ordered chunks whose rows download while
-    later chunks run): bitwise the device-resident apply, and the same with
-    the pipeline off (CFM_LR_PIPELINE=0)."""
+    two-stage, streamed: stage 1 in chunks of row-ordered source tiles that start
+    on the first multipole slabs, stage 2 in chunks of row-ordered target tiles
+    that wait for their locals slabs and whose rows download while later chunks
+    run), non-zero initial locals: bitwise the device-resident apply, and the
+    same with the slabs off (CFM_TS_SLABS=0 is read once per process, so the
+    whole-array variant is covered by CFM_LR_PIPELINE=0)."""
     import torch
 
     from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
@@ -153,15 +156,15 @@ def test_lowrank_host_pipeline_bitwise(monkeypatch):
     for l in levels:
         h.plan_level_cells(l, _cube(l))
     assert h.plan_stats(6)["two_stage"]
-    dev = {l: (torch.from_numpy(mp_h[l]).cuda(), torch.zeros(mp_h[l].shape, dtype=torch.float64, device="cuda"))
-           for l in levels}
+    loc0 = {l: rng.uniform(-1, 1, mp_h[l].shape) for l in levels}  # locals accumulate: non-zero start
+    dev = {l: (torch.from_numpy(mp_h[l]).cuda(), torch.from_numpy(loc0[l]).cuda()) for l in levels}
     fl_d = h.apply_levels(dev)
     torch.cuda.synchronize()
     out = {}
     for pipe in ("1", "0"):
         monkeypatch.setenv("CFM_LR_PIPELINE", pipe)
         arrs = {l: (torch.from_numpy(mp_h[l]).pin_memory().numpy(),
-                    torch.zeros(mp_h[l].shape, dtype=torch.float64).pin_memory().numpy()) for l in levels}
+                    torch.from_numpy(loc0[l].copy()).pin_memory().numpy()) for l in levels}
         fl = h.apply_levels(arrs)
         assert fl == fl_d
         out[pipe] = {l: arrs[l][1].copy() for l in levels}
