@@ -37,13 +37,14 @@ def _free_port():
 
 def _case(name):
     """(cells per level, widths, order, variant, eps, kernel spec)."""
-    if name == "cube_l5":
+    if name in ("cube_l5", "cube_l5_iablk"):
         depth, order = 4, 5
         cells = {}
         for l in range(2, depth + 1):
             s = 1 << l
             cells[l] = np.stack(np.meshgrid(*(np.arange(s),) * 3, indexing="ij"), -1).reshape(-1, 3)
-        return cells, {l: 1.0 / (1 << l) for l in cells}, order, "nablk", 1e-5, ("laplace", None)
+        variant = "nablk" if name == "cube_l5" else "iablk"
+        return cells, {l: 1.0 / (1 << l) for l in cells}, order, variant, 1e-5, ("laplace", None)
     g = np.load(ROOT / "tests" / "golden" / "cfg5.npz")
     levels = [int(l) for l in g["levels"]]
     cells = {l: g[f"cells_{l}"].astype(np.int64) for l in levels}
@@ -111,7 +112,7 @@ def _rank_main(rank, world, port, name, q):
 
 
 @pytest.mark.parametrize("plans", ["plain", "hybrid"])
-@pytest.mark.parametrize("name", ["cube_l5", "cfg5_helmholtz"])
+@pytest.mark.parametrize("name", ["cube_l5", "cfg5_helmholtz", "cube_l5_iablk"])
 def test_two_ranks_one_gpu_equal_single_rank(name, plans, monkeypatch):
     import torch
     import torch.multiprocessing as mp
@@ -161,7 +162,11 @@ def test_two_ranks_one_gpu_equal_single_rank(name, plans, monkeypatch):
             seen[rows] = True
             got[rows] = vals
         assert seen.all()
-        if plans == "plain":
+        if name == "cube_l5_iablk":
+            # one rank runs level 4 on the target-major two-stage path, a rank's interior /
+            # boundary subsets may take the fused kernel: equal to round-off, not bitwise
+            assert O.rel_l2(got, ref[l]) <= 1e-13, (name, l, O.rel_l2(got, ref[l]))
+        elif plans == "plain":
             assert np.array_equal(got, ref[l]), (name, l, float(np.abs(got - ref[l]).max()))
         else:
             assert O.rel_l2(got, ref[l]) <= 1e-14, (name, l, O.rel_l2(got, ref[l]))
@@ -169,7 +174,8 @@ def test_two_ranks_one_gpu_equal_single_rank(name, plans, monkeypatch):
     for r, (_, info, fl, nl) in enumerate(gathered):
         log["ranks"].append({"rank": r, "flops": fl, "launches": nl, "levels": {str(k): v for k, v in info.items()}})
     log["plans"] = plans
-    log["equal_to_single_rank"] = "bitwise" if plans == "plain" else "<= 1e-14 relative L2"
+    log["equal_to_single_rank"] = ("<= 1e-13 relative L2" if name == "cube_l5_iablk" else
+                                   "bitwise" if plans == "plain" else "<= 1e-14 relative L2")
     out = ROOT / "gpurun_out"
     out.mkdir(exist_ok=True)
     (out / f"multirank_{name}_{plans}.json").write_text(json.dumps(log, indent=1))
