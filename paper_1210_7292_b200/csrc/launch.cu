@@ -366,7 +366,7 @@ static bool step_persistent_ok(const std::vector<TileParams>& segs, const std::v
     ++live;
     tiles += counts[i];
     if (!q.ft || q.op_rows || q.op_klen || q.x_dc != 1 || q.y_dc != 1 || q.red_counter || q.b_block) return false;
-    if (q.nk > 512 || q.nr != q0.nr || q.nk != q0.nk || q.ft_rows != q0.ft_rows || q.ft_opshift) return false;
+    if (q.nk > 1024 || q.nr != q0.nr || q.nk != q0.nk || q.ft_rows != q0.ft_rows || q.ft_opshift) return false;
     if (!q.code_is_op) {
       if (code_op && code_op != q.code_op) return false;
       code_op = q.code_op;
@@ -376,8 +376,8 @@ static bool step_persistent_ok(const std::vector<TileParams>& segs, const std::v
     // the row- and k-step-skipping kernel stays ahead there (measured on the config-2 tree:
     // l = 7 363.3 vs 367.5 ms, l = 6 147.2 vs 147.7 ms with skipping variants of this kernel;
     // its tiles are 2,000+ chunks long, so the per-CTA overhead this kernel removes is < 0.2%)
-    if (!q.y_rowblk && (q.nr % 128 != 0 && 128 - q.nr % 128 >= 8)) return false;
     if (!q.y_rowblk && q.nk % 32 != 0 && q.nk % 32 <= 24) return false;
+    // (dead m-tiles alone -- l = 9: 729 = 22 x 32 + 25 columns, 89-row last block -- run on the MPART variant)
     if (q.pair_out && (q.pipe_mp || q.pipe_loc || q.pipe_done)) return false;
     if (!q.pair_out && !q.accumulate) return false;
   }
@@ -441,7 +441,9 @@ static int64_t launch_step_persistent(const std::vector<TileParams>& segs, const
   const int smem = step_gemm_smem_bytes();
   bool scatter = false;
   for (int i = 0; i < sp.n_seg; ++i) scatter = scatter || sp.seg[i].mode == 2;
-  auto kern = scatter ? step_gemm_kernel<true> : step_gemm_kernel<false>;
+  // MPART: the last row block has dead m-tiles (l = 9: 89 of 128 rows), skipped per warp
+  const bool mpart = !scatter && sp.nr % 128 != 0 && 128 - sp.nr % 128 >= 8;
+  auto kern = scatter ? step_gemm_kernel<true, false> : mpart ? step_gemm_kernel<false, true> : step_gemm_kernel<false, false>;
   CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, kStepThreads, smem, s>>>(sp);
   CUDA_CHECK(cudaGetLastError());

@@ -92,8 +92,10 @@ constexpr int step_gemm_smem_bytes() {
   return kStepStages * (128 + 64) * (kStepKC + 4) * 8 + 2 * kStepStages * 8 + kStepRing * 4;
 }
 
-// SCATTER: compile output mode 2 (two-stage launches)
-template <bool SCATTER>
+// SCATTER: compile output mode 2 (two-stage launches); MPART: the last row block has dead m-tiles
+// (128 - nr % 128 >= 8: l = 9), skipped per warp on a separate path, so the full row blocks keep the
+// flat unrolled stream of the l = 5 launches.
+template <bool SCATTER, bool MPART>
 __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid_constant__ StepParams p) {
   constexpr int BM = 128, BN = 64, KC = kStepKC, ST = kStepStages, LD = KC + 4;
   constexpr int WM = 4, NC = 8 * 32;
@@ -171,9 +173,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
   }
 
   // ============================ consumer warps ============================
+  // Interleaved warp tiles: warp (wm, wn) owns the m-tiles (mi * 4 + wm) * 8, so in a
+  // partial last row block (l = 7: 87 of 128 rows) every SM sub-partition keeps
+  // about the same number of live m-tiles; the dead ones are skipped.
   const int g = lane >> 2, tg = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
-  const int aoff = (wm * 32 + g) * LD + tg, boff = (wn * 32 + g) * LD + tg;
+  const int aoff = (wm * 8 + g) * LD + tg, boff = (wn * 32 + g) * LD + tg;
+  constexpr int MSTEP = WM * 8;  // rows between a warp's m-tiles
   double acc[MT][NTL][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
     const double* as = As + s * BM * LD + aoff;
     const double* bs = Bs + s * BN * LD + boff;
 #pragma unroll
-    for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * 8 * LD + kk];
+    for (int mi = 0; mi < MT; ++mi) a[mi] = as[mi * MSTEP * LD + kk];
 #pragma unroll
     for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LD + kk];
   };
@@ -218,6 +224,74 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
       if (lane == 0) mbar_arrive(empty + s);
       ++q;
     }
+    int ml = MT;  // live m-tiles of this warp in this row block
+    if (MPART) {
+      ml = 0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+        if (r0 + (mi * WM + wm) * 8 < p.nr) ml = mi + 1;
+    }
+    if (MPART && ml < MT && total > 0) {
+      // a partial row block: the same chunk stream over this warp's ML live m-tiles
+      auto run_partial = [&](auto mlc) {
+        constexpr int ML = decltype(mlc)::value;
+        auto loadp = [&](double* a, double* b, int s, int kk) {
+          const double* as = As + s * BM * LD + aoff;
+          const double* bs = Bs + s * BN * LD + boff;
+#pragma unroll
+          for (int mi = 0; mi < ML; ++mi) a[mi] = as[mi * MSTEP * LD + kk];
+#pragma unroll
+          for (int nj = 0; nj < NTL; ++nj) b[nj] = bs[nj * 8 * LD + kk];
+        };
+        auto mmap = [&](const double* a, const double* b) {
+#pragma unroll
+          for (int mi = 0; mi < ML; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        };
+        for (int c = 0; c < total; ++c, ++q) {
+          const int s = q % ST;
+          if (skewed && wn == 0 && !arrived && q >= p.skew) {
+            asm volatile("bar.arrive 2, %0;\n" ::"n"(NC) : "memory");
+            arrived = true;
+          }
+          const bool last_of_entry = (c + 1) % nch == 0;
+#pragma unroll
+          for (int kk = 0; kk < KC; kk += 8) {
+            loadp(a1, b1, s, kk + 4);
+            mmap(a0, b0);
+            if (kk + 8 < KC) {
+              loadp(a0, b0, s, kk + 8);
+            } else {
+              const int s1 = (q + 1) % ST;
+              mbar_wait(full + s1, ((q + 1) / ST) & 1);
+              load(a0, b0, s1, 0);  // (maybe another item's chunk: all m-tiles)
+            }
+            mmap(a1, b1);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+          if (mode == 1 && last_of_entry) {
+            const int e = e0 + c / nch;
+#pragma unroll
+            for (int nj = 0; nj < NTL; ++nj)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const long long v = (long long)e * BN + wn * 32 + nj * 8 + 2 * tg + h;
+                const bool live = __ldg(sg.entry_src + v) >= 0;
+                double* dst = sg.y + v * sg.y_ld + r0 + wm * 8 + g;
+#pragma unroll
+                for (int mi = 0; mi < MT; ++mi) {
+                  if (live && r0 + (mi * WM + wm) * 8 + g < p.nr) dst[mi * MSTEP] = sg.scale * acc[mi][nj][h];
+                  acc[mi][nj][h] = 0.0;
+                }
+              }
+          }
+        }
+      };
+      if (ml == 3) run_partial(std::integral_constant<int, 3>{});
+      else run_partial(std::integral_constant<int, 2>{});  // (rows past the operator are never stored)
+    } else
     for (int c = 0; c < total; ++c, ++q) {
       const int s = q % ST;
       if (skewed && wn == 0 && !arrived && q >= p.skew) {
@@ -225,6 +299,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
         arrived = true;
       }
       const bool last_of_entry = (c + 1) % nch == 0;
+      // the next chunk always exists (this tile's, the next item's first, or the
+      // end marker's empty stage): it is waited for and its first fragments
+      // loaded before this chunk's last k-step
 #pragma unroll
       for (int kk = 0; kk < KC; kk += 8) {
         load(a1, b1, s, kk + 4);
@@ -232,9 +309,6 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
         if (kk + 8 < KC) {
           load(a0, b0, s, kk + 8);
         } else {
-          // the next chunk always exists (this tile's, the next item's first, or
-          // the end marker's empty stage): wait for it and load its first
-          // fragments before this chunk's last k-step
           const int s1 = (q + 1) % ST;
           mbar_wait(full + s1, ((q + 1) / ST) & 1);
           load(a0, b0, s1, 0);
@@ -254,10 +328,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
             for (int h = 0; h < 2; ++h) {
               const long long v = (long long)e * BN + wn * 32 + nj * 8 + 2 * tg + h;
               const bool live = __ldg(sg.entry_src + v) >= 0;
-              double* dst = sg.y + v * sg.y_ld + r0 + wm * 32 + g;
+              double* dst = sg.y + v * sg.y_ld + r0 + wm * 8 + g;
 #pragma unroll
               for (int mi = 0; mi < MT; ++mi) {
-                if (live && r0 + wm * 32 + mi * 8 + g < p.nr) dst[mi * 8] = sg.scale * acc[mi][nj][h];
+                if (live && r0 + (mi * WM + wm) * 8 + g < p.nr) dst[mi * MSTEP] = sg.scale * acc[mi][nj][h];
                 acc[mi][nj][h] = 0.0;
               }
             }
@@ -265,10 +339,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
           // Y_T scatter: each (slot, a) row of every source goes to the Y_T row
           // of the pair's target (the 8 lanes of a tg mostly share a slot: one
           // broadcast load, a run of up to 64 B stored)
-          const int* ri = sg.rowinfo + (long long)__ldg(sg.entry_code + e) * BM + wm * 32 + g;
+          const int* ri = sg.rowinfo + (long long)__ldg(sg.entry_code + e) * BM + wm * 8 + g;
           int info[MT];
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi) info[mi] = __ldg(ri + mi * 8);
+          for (int mi = 0; mi < MT; ++mi) info[mi] = __ldg(ri + mi * MSTEP);
 #pragma unroll
           for (int nj = 0; nj < NTL; ++nj)
 #pragma unroll
@@ -296,13 +370,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int v = __ldg(sg.tile_col + (long long)tile * BN + wn * 32 + nj * 8 + 2 * tg + h);
-          double* dst = sg.y + (long long)v * sg.y_ld + r0 + wm * 32 + g;
+          double* dst = sg.y + (long long)v * sg.y_ld + r0 + wm * 8 + g;
           double old[MT];
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi) old[mi] = (v >= 0 && r0 + wm * 32 + mi * 8 + g < p.nr) ? dst[mi * 8] : 0.0;
+          for (int mi = 0; mi < MT; ++mi) old[mi] = (v >= 0 && r0 + (mi * WM + wm) * 8 + g < p.nr) ? dst[mi * MSTEP] : 0.0;
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi) {
-            if (v >= 0 && r0 + wm * 32 + mi * 8 + g < p.nr) dst[mi * 8] = old[mi] + sg.scale * acc[mi][nj][h];
+            if (v >= 0 && r0 + (mi * WM + wm) * 8 + g < p.nr) dst[mi * MSTEP] = old[mi] + sg.scale * acc[mi][nj][h];
             acc[mi][nj][h] = 0.0;
           }
         }
