@@ -490,6 +490,12 @@ int64_t launch_multi(const std::vector<TileParams>& segs, const std::vector<int6
 
 // Launch tiles [first, first + count) of the plan in p.
 int64_t launch_range(const TileParams& p, int64_t first, int64_t count, cudaStream_t s) {
+  if (count > 0 && first + count < (int64_t(1) << 31)) {
+    // single tile lists of per-level applies: the persistent kernel where it is eligible
+    TileParams q = p;
+    q.tile_base = int(first);
+    if (step_persistent_ok({q}, {count})) return launch_step_persistent({q}, {count}, s);
+  }
   int64_t launches = 0;
   const int64_t max_grid = 1 << 30;
   for (int64_t base = first; base < first + count; base += max_grid) {

@@ -260,11 +260,13 @@ def test_full_level_against_oracle(torch_cuda, order, level, variant):
 def test_rank1_ktail_matches_padded_dmma(torch_cuda, monkeypatch):
     """l = 5 (125 = 3 x 32 + 29 inner columns): the last k-step of every entry
     runs as a rank-1 DFMA update (default) instead of a DMMA over three zero
-    columns (CFM_KTAIL=0).  Full level 5: both agree to rounding and match the
-    oracle at the full-rank tolerance."""
+    columns (CFM_KTAIL=0) on the one-CTA-per-tile kernel (CFM_STEP_PERSIST=0; the
+    persistent step kernel has no k-tail).  Full level 5: both agree to rounding
+    and match the oracle at the full-rank tolerance."""
     torch = torch_cuda
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
+    monkeypatch.setenv("CFM_STEP_PERSIST", "0")
     order, level = 5, 5
     cells = _full_level(level)
     tgt, off, src, t = O.far_lists(cells, level)
@@ -1107,3 +1109,50 @@ def test_two_stage_target_major_other_orders(torch_cuda, order, eps, monkeypatch
     fr = orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
     assert flops == fr
     assert O.rel_l2(loc.cpu().numpy() + 0.75, ref + 0.75) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order,shape", [(5, "cube"), (9, "shell")])
+def test_persistent_step_kernel_matches_tile_kernel(torch_cuda, order, shape, monkeypatch):
+    """The persistent step kernel (default) against the one-CTA-per-tile kernel
+    (CFM_STEP_PERSIST=0), multi-level apply_levels and per-level apply_planned:
+    l = 5 on full levels 3-4 (target tiles + hybrid pair entries), l = 9 on a
+    spherical shell (pair entries, 89-row last block: the dead-m-tile path).
+    Both run the same chunks in the same order per accumulator; only the
+    rank-1 k-tail of the l = 5 tile kernel differs (round-off)."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    levels = (3, 4)
+    cells = {}
+    for l in levels:
+        c = _full_level(l)
+        if shape == "shell":
+            r = np.linalg.norm((c + 0.5) / (1 << l) * 2 - 1, axis=1)
+            c = c[(r > 0.6) & (r < 0.95)]
+        cells[l] = c
+    rng = np.random.default_rng(31)
+    mp = {l: torch.from_numpy(rng.uniform(-1, 1, (len(cells[l]), order**3))).cuda() for l in levels}
+    out, single = {}, {}
+    for persist in ("1", "0"):
+        monkeypatch.setenv("CFM_STEP_PERSIST", persist)
+        h = make_handler("nablk", laplace_kernel(), ChebyshevGrid(order), 1e-8)
+        h.precompute({l: full_far_field_vectors() for l in levels}, {l: 1.0 / (1 << l) for l in levels})
+        for l in levels:
+            h.plan_level_cells(l, cells[l])
+        loc = {l: torch.full_like(mp[l], 0.125) for l in levels}
+        h.apply_levels({l: (mp[l], loc[l]) for l in levels})
+        one = torch.full_like(mp[4], 0.125)
+        h.apply_planned(4, mp[4], one)
+        out[persist] = {l: loc[l].cpu().numpy() for l in levels}
+        single[persist] = one.cpu().numpy()
+    for l in levels:
+        assert O.rel_l2(out["1"][l], out["0"][l]) <= 1e-14, (l, O.rel_l2(out["1"][l], out["0"][l]))
+        tgt, off, src, t = O.far_lists(cells[l], l)
+        orc = O.OracleM2L("nablk", O.laplace_profile, np.float64, order, 1e-8, -1.0).precompute(
+            {l: sorted({tuple(int(c) for c in v) for v in t})}, {l: 1.0 / (1 << l)})
+        ref = np.full(mp[l].shape, 0.125)
+        orc.apply_fast(l, tgt, off, src, t, mp[l].cpu().numpy(), ref)
+        assert O.rel_l2(out["1"][l] - 0.125, ref - 0.125) <= 1e-12
+    assert O.rel_l2(single["1"], single["0"]) <= 1e-14
+    assert O.rel_l2(single["1"], out["1"][4]) <= 1e-14
