@@ -479,7 +479,9 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
   int z_pair = 0, z_acc = 1;
   if (lp.mode == 1) {
     ensure(h->fzbuf, size_t(lp.red.n_frows) * z_ld * sizeof(double));
-    CUDA_CHECK(cudaMemsetAsync(h->fzbuf.p, 0, size_t(lp.red.n_frows) * z_ld * sizeof(double), s));
+    // (no zeroing: every live pair row is stored once, by the dense-core or the
+    // factored-core launch of its entry, and the reduction reads live rows only;
+    // at config 3's level 5 the memset was 408 MB per step)
     z_out = h->fzbuf.as<double>();
     z_pair = 1;
     z_acc = 0;
@@ -492,6 +494,7 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     q.x = h->wt.as<double>(); q.x_ld = wt_ld; q.x_dc = dc;
     q.y = z_out; q.y_ld = z_ld; q.y_dc = dc;
     q.scale = 1.0; q.accumulate = z_acc; q.pair_out = z_pair;
+    q.no_step = g.any_fac_core ? 1 : 0;  // factored cores' entries carry no operator here: skipped per entry
     if (sa_full) {
       q.ft = 1;
       q.ft_rows = g.full_rows;

@@ -365,7 +365,7 @@ static bool step_persistent_ok(const std::vector<TileParams>& segs, const std::v
     const TileParams& q = segs[i];
     ++live;
     tiles += counts[i];
-    if (!q.ft || q.op_rows || q.op_klen || q.x_dc != 1 || q.y_dc != 1 || q.red_counter || q.b_block) return false;
+    if (q.no_step || !q.ft || q.op_rows || q.op_klen || q.x_dc != 1 || q.y_dc != 1 || q.red_counter || q.b_block) return false;
     if (q.nk > 1024 || q.nr != q0.nr || q.nk != q0.nk || q.ft_rows != q0.ft_rows || q.ft_opshift) return false;
     if (!q.code_is_op) {
       if (code_op && code_op != q.code_op) return false;
@@ -376,7 +376,10 @@ static bool step_persistent_ok(const std::vector<TileParams>& segs, const std::v
     // the row- and k-step-skipping kernel stays ahead there (measured on the config-2 tree:
     // l = 7 363.3 vs 367.5 ms, l = 6 147.2 vs 147.7 ms with skipping variants of this kernel;
     // its tiles are 2,000+ chunks long, so the per-CTA overhead this kernel removes is < 0.2%)
-    if (!q.y_rowblk && q.nk % 32 != 0 && q.nk % 32 <= 24) return false;
+    // ... but short tiles win far more from losing the per-CTA cost than the empty k-steps cost them
+    // (shared-basis cores, K = 203: 7-chunk entries, a dozen per tile)
+    const long long chunks_per_tile = (q.n_entries / std::max(q.n_tiles, 1)) * ((q.nk + 31) / 32);
+    if (!q.y_rowblk && q.nk % 32 != 0 && q.nk % 32 <= 24 && chunks_per_tile > 500) return false;
     // (dead m-tiles alone -- l = 9: 729 = 22 x 32 + 25 columns, 89-row last block -- run on the MPART variant)
     if (q.pair_out && (q.pipe_mp || q.pipe_loc || q.pipe_done)) return false;
     if (!q.pair_out && !q.accumulate) return false;

@@ -118,6 +118,8 @@ struct TileParams {
                       // tmap_b at column op_col[entry_code[e]]
   const int* seg_ksteps;  // seg_pair_gemm_kernel: live k-steps (0..4) per entry code (null: all 4)
   int l2_hints;     // TMA copies with L2 policies: operators evict_last, sources evict_first
+  int no_step;      // host-side: keep this list off the persistent step kernel (entries whose code has no
+                    // operator in this launch are skipped by tile_gemm_ws_kernel only)
   CUtensorMap tmap_a;
   // full-operator mode: 2-D map over the padded sources (x_ld x x_rows), box
   // (KC + 4) x 1, read by tile::gather4 copies (4 source rows per instruction)
