@@ -86,16 +86,17 @@ int64_t launch_pads(const std::vector<PadJob>& in, cudaStream_t s, int threads) 
 int64_t xpad_copy(cfm_handler* h, double* dst, int ld, const double* src, int64_t r0, int64_t r1, cudaStream_t s,
                       int threads, std::vector<PadJob>* batch) {
   if (r1 <= r0) return 0;
+  const int nsrc = h->n * h->f;  // doubles per source row (complex operators: interleaved re / im)
   if (is_device_ptr(src)) {
-    const PadJob J{dst + size_t(r0) * ld, src + size_t(r0) * h->n, (long long)(r1 - r0), 0, ld, h->n};
+    const PadJob J{dst + size_t(r0) * ld, src + size_t(r0) * nsrc, (long long)(r1 - r0), 0, ld, nsrc};
     if (batch) {
       batch->push_back(J);
       return 0;
     }
     return launch_pads({J}, s, threads);
   }
-  CUDA_CHECK(cudaMemcpy2DAsync(dst + size_t(r0) * ld, size_t(ld) * sizeof(double), src + size_t(r0) * h->n,
-                               size_t(h->n) * sizeof(double), size_t(h->n) * sizeof(double), size_t(r1 - r0),
+  CUDA_CHECK(cudaMemcpy2DAsync(dst + size_t(r0) * ld, size_t(ld) * sizeof(double), src + size_t(r0) * nsrc,
+                               size_t(nsrc) * sizeof(double), size_t(nsrc) * sizeof(double), size_t(r1 - r0),
                                cudaMemcpyDefault, s));
   return 0;
 }

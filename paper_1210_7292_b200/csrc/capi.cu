@@ -137,7 +137,7 @@ int cfm_set_lowrank_group(cfm_handler* h, int key, int n_transfers, const int8_t
     for (int i = 0; i < n_ops; ++i)
       if (ranks[i] < 0 || ranks[i] > h->n) throw Error(CFM_ERR_VALUE, "rank out of range");
     build_lowrank_stacks(h, g.left, g.right_h, n_ops, ranks, left, right, h->n, h->n);
-    if (use_full_ops(h)) build_lowrank_full(h, g, n_transfers, transfers, n_ops, ranks, left, right);
+    if (use_lowrank_full(h)) build_lowrank_full(h, g, n_transfers, transfers, n_ops, ranks, left, right);
     h->groups[key] = std::move(g);
     h->plans.clear();
     h->csr_cache.clear();

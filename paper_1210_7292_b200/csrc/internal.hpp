@@ -452,6 +452,7 @@ void build_two_stage_plan(const Group& g, LevelPlan& lp);
 inline bool full_mode(const Group& g, const LevelPlan& lp) { return g.kind == kDense && g.has_full && lp.dc == 1; }
 bool use_hybrid();
 bool use_two_stage();
+bool use_lowrank_full(const cfm_handler* h);
 int two_stage_mode();
 PFN_encodeTiled resolve_encode_tiled();
 void push_pair_plan(LevelPlan& lp);

@@ -277,6 +277,18 @@ bool use_full_ops(const cfm_handler* h) {
   return v != 0 && !h->op_complex && nf > 64 && nf <= 1024 && resolve_encode_tiled() != nullptr;
 }
 
+// Per-transfer permuted low-rank factors (fused kernel with contiguous padded
+// sources): also for complex operators (realified, CFM_LR_FULL_COMPLEX=0 disables).
+bool use_lowrank_full(const cfm_handler* h) {
+  if (!h->op_complex) return use_full_ops(h);
+  static int v = [] {
+    const char* e = getenv("CFM_LR_FULL_COMPLEX");
+    return e ? atoi(e) : 1;
+  }();
+  const int nf = h->n * h->f;
+  return v != 0 && nf > 64 && nf <= 1024;
+}
+
 template <int RP, int STAGES, bool VB, int KC = 16>
 static bool launch_lowrank_cfg(LowRankParams lp_, int64_t first, int64_t count, cudaStream_t s) {
   const int fixed = lr_smem_bytes<RP, KC, STAGES>() + 4 * 64 + 3 * 4 * 344 + 4 * kMaxTileEntries;

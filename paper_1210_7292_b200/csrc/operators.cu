@@ -371,33 +371,46 @@ void build_two_stage(cfm_handler* h, Group& g, int n_transfers, const int8_t* tr
 // Y[a] = sum_k right^H[a][k] x[inv[k]] = sum_j right^H[a][tab[j]] x[j]).
 void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t* transfers, int n_ops,
                                const int* ranks, const double* L, const double* R) {
-  const int n = h->n;
+  // Complex operators: the factors are realified first ([[Re, -Im], [Im, Re]] per
+  // element, rows / columns interleaved like a complex128 expansion row), and a
+  // permutation of the n coefficients moves the (re, im) row pairs together.
+  const int n = h->n, f = h->f;
+  const bool cplx = h->op_complex;
+  const int nf = n * f, sc = cplx ? 2 : 1;
   int rmax = 0;
   for (int i = 0; i < n_ops; ++i) rmax = std::max(rmax, ranks[i]);
   std::vector<size_t> off(n_ops + 1, 0);
-  for (int i = 0; i < n_ops; ++i) off[i + 1] = off[i] + size_t(n) * ranks[i];
-  make_stack(g.lrf_left, n_transfers, n, std::max(rmax, 1));
-  make_stack(g.lrf_right_h, n_transfers, std::max(rmax, 1), n);
+  for (int i = 0; i < n_ops; ++i) off[i + 1] = off[i] + size_t(n) * ranks[i] * sc;
+  make_stack(g.lrf_left, n_transfers, nf, std::max(rmax * f, 1));
+  make_stack(g.lrf_right_h, n_transfers, std::max(rmax * f, 1), nf);
   std::vector<int> ident(n), rk(n_transfers);
   std::iota(ident.begin(), ident.end(), 0);
   std::vector<double> bl(g.lrf_left.stride), br(g.lrf_right_h.stride);
+  std::vector<double> tl(g.lrf_left.stride), tr_(g.lrf_right_h.stride);
   std::vector<double> all_v(size_t(n_transfers) * g.lrf_right_h.stride);
   std::vector<double> all_u(size_t(n_transfers) * g.lrf_left.stride);
+  const int lld = g.lrf_left.ld, rld = g.lrf_right_h.ld;
   for (int k = 0; k < n_transfers; ++k) {
     const int c = tcode(transfers[3 * k], transfers[3 * k + 1], transfers[3 * k + 2]);
     const int o = g.main.op[c];
     const std::vector<int> tr = g.main.rperm[c] >= 0 ? permutation_table(g.main.rperm[c], h->order) : ident;
     const std::vector<int> tc = g.pass1.cperm[c] >= 0 ? permutation_table(g.pass1.cperm[c], h->order) : ident;
     const int r = ranks[o];
-    rk[k] = r;
+    rk[k] = r * f;
     std::fill(bl.begin(), bl.end(), 0.0);
     std::fill(br.begin(), br.end(), 0.0);
-    const double* Lo = L + off[o];
-    const double* Ro = R + off[o];
-    for (int i = 0; i < n; ++i)
-      for (int a = 0; a < r; ++a) bl[size_t(i) * g.lrf_left.ld + a] = Lo[size_t(tr[i]) * r + a];
-    for (int a = 0; a < r; ++a)
-      for (int j = 0; j < n; ++j) br[size_t(a) * g.lrf_right_h.ld + j] = Ro[size_t(tc[j]) * r + a];
+    if (r > 0) {
+      std::fill(tl.begin(), tl.end(), 0.0);
+      std::fill(tr_.begin(), tr_.end(), 0.0);
+      realify_into(L + off[o], n, r, cplx, tl.data(), lld);                       // left: (n f) x (r f)
+      realify_into(R + off[o], r, n, cplx, tr_.data(), rld, /*conj_t=*/true);      // right^H: (r f) x (n f)
+      for (int i = 0; i < n; ++i)
+        for (int q = 0; q < f; ++q)
+          std::copy_n(tl.begin() + size_t(tr[i] * f + q) * lld, r * f, bl.begin() + size_t(i * f + q) * lld);
+      for (int a = 0; a < r * f; ++a)
+        for (int j = 0; j < n; ++j)
+          for (int q = 0; q < f; ++q) br[size_t(a) * rld + j * f + q] = tr_[size_t(a) * rld + tc[j] * f + q];
+    }
     put_stack(g.lrf_left, k, bl);
     put_stack(g.lrf_right_h, k, br);
     std::copy(br.begin(), br.end(), all_v.begin() + size_t(k) * br.size());
@@ -408,7 +421,7 @@ void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t*
   set_per_op(g.lrf_left, {}, rk);
   set_per_op(g.lrf_right_h, rk, {});
   g.has_lrfull = true;
-  build_two_stage(h, g, n_transfers, transfers, rk, all_v, all_u);
+  if (!cplx) build_two_stage(h, g, n_transfers, transfers, rk, all_v, all_u);
 }
 
 }  // namespace cfm
