@@ -343,7 +343,16 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
   }
 
   if (g.kind == kLowRank) {
-    {
+    // Two passes on the full-operator kernels (CFM_LR_TWOPASS=1, default for complex
+    // operators): pass 1 Y[slot] = V_t^H x_src and pass 2 acc += U_t Y[slot] are short-tile
+    // GEMMs against the per-transfer permuted factors, which the persistent step kernel
+    // runs without per-CTA cost; the fused kernel (both phases in one CTA, Y in shared
+    // memory) pays about one shared-memory load per DMMA in its skinny phase 1.
+    const char* twopass_e = getenv("CFM_LR_TWOPASS");  // read per apply (tests switch it)
+    const int twopass_env = twopass_e ? atoi(twopass_e) : -1;
+    const bool ft2 = g.has_lrfull && g.has_lrmaps && dc == 1 &&
+                     (twopass_env >= 0 ? twopass_env != 0 : h->op_complex != 0);
+    if (!ft2) {
       LowRankParams q{};
       q.n_tiles = int(lp.hp.n_tiles);
       q.tile_col = lp.tile_col.as<int>();
@@ -403,7 +412,15 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
       }
     }
     // chunk tiles so the per-pair intermediate stays bounded
-    const int ldy = g.right_h.rows;  // rmax * f
+    const int ldy = ft2 ? round_up(g.lrf_right_h.rows, 2) : g.right_h.rows;  // rmax * f (16-B row pitch for TMA)
+    double* xp2 = nullptr;
+    int ldx2 = 0;
+    if (ft2) {
+      ldx2 = g.lrf_right_h.ld;
+      const auto xo = xpad_layout(h, {{lp.n_rows, ldx2}}, s);
+      xp2 = h->xpad.as<double>() + xo[0];
+      launches += xpad_copy(h, xp2, ldx2, d_x, 0, lp.n_rows, s);
+    }
     const size_t max_slots = std::max<size_t>(kBN, (size_t(1) << 30) / (sizeof(double) * std::max(ldy, 1)));
     const std::vector<int>& toff = lp.hp.tile_off;
     if (lp.mode == 1) ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
@@ -425,6 +442,14 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
         // runs of up to kPass1Run entries per CTA; each entry's Y written when it ends
         p1.tile_off = lp.runs.as<int>();
         p1.pair_out = 1;
+        if (ft2) {
+          fill_ops(p1, g.lrf_right_h, g.fullmap);
+          p1.op_rows = nullptr; p1.op_klen = nullptr;  // rows / columns past a rank are exact zeros
+          p1.rowtab = nullptr; p1.invtab = nullptr;
+          p1.ft = 1; p1.ft_rows = g.lrf_right_h.rows; p1.tmap_a = g.lrf_vmap;
+          p1.x = xp2; p1.x_ld = ldx2; p1.x_dc = 1; p1.x_rows = lp.n_rows;
+          p1.n_entries = E;
+        }
         launches += launch_range(p1, lp.run_start[t0], lp.run_start[t1] - lp.run_start[t0], s);
         // pass 2: acc += left[table] Y  (tiles = target tiles, sources = slots)
         TileParams p2 = p;
@@ -437,6 +462,15 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
         } else {
           p2.y = d_y; p2.y_ld = row_ld; p2.y_dc = dc;
           p2.scale = scale; p2.accumulate = 1;
+        }
+        if (ft2) {
+          fill_ops(p2, g.lrf_left, g.fullmap);
+          p2.op_rows = nullptr; p2.op_klen = nullptr;
+          p2.rowtab = nullptr; p2.invtab = nullptr;
+          p2.ft = 1; p2.ft_rows = g.lrf_left.rows; p2.tmap_a = g.lrf_umap;
+          p2.x_rows = e1 * kBN;
+          p2.n_entries = E;
+          if (lp.mode == 1) p2.entry_ncols = lp.entry_ncols.as<unsigned char>();
         }
         launches += launch_range(p2, t0, t1 - t0, s);
       }

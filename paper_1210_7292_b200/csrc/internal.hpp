@@ -161,6 +161,8 @@ struct Group {
   // columns permuted once), read with contiguous copies from padded sources
   bool has_lrfull = false;
   OpStack lrf_left, lrf_right_h;
+  CUtensorMap lrf_umap, lrf_vmap;  // box (KC + 4) x 128 over the two stacks (two-pass path on the persistent kernel)
+  bool has_lrmaps = false;
   // two-stage low-rank mode (real, dense levels): stage 1 Y = V_t^H x per
   // (source, transfer) for the whole transfer set of the source's class, as a
   // dense GEMM against a per-class stack of V_t^H rows; stage 2 sums U_t Y per

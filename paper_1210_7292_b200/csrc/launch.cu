@@ -257,12 +257,9 @@ bool use_concurrent_levels() {
   return v != 0;
 }
 
-bool use_fused_lowrank() {
-  static int v = [] {
-    const char* e = getenv("CFM_LOWRANK_FUSED");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
+bool use_fused_lowrank() {  // read per apply (tests switch it)
+  const char* e = getenv("CFM_LOWRANK_FUSED");
+  return !e || atoi(e) != 0;
 }
 
 

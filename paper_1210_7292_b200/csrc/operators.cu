@@ -421,6 +421,18 @@ void build_lowrank_full(cfm_handler* h, Group& g, int n_transfers, const int8_t*
   set_per_op(g.lrf_left, {}, rk);
   set_per_op(g.lrf_right_h, rk, {});
   g.has_lrfull = true;
+  if (PFN_encodeTiled enc = resolve_encode_tiled()) {
+    auto encode = [&](CUtensorMap* m, const OpStack& st) {
+      const cuuint64_t dims[2] = {cuuint64_t(st.ld), cuuint64_t((long long)st.n_ops * st.rows)};
+      const cuuint64_t strides[1] = {cuuint64_t(st.ld) * sizeof(double)};
+      const cuuint32_t box[2] = {cuuint32_t(kKC + 4), 128u};
+      const cuuint32_t estr[2] = {1u, 1u};
+      return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, st.d.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    g.has_lrmaps = encode(&g.lrf_umap, g.lrf_left) && encode(&g.lrf_vmap, g.lrf_right_h);
+  }
   if (!cplx) build_two_stage(h, g, n_transfers, transfers, rk, all_v, all_u);
 }
 

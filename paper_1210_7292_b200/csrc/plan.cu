@@ -566,27 +566,6 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
         }
     upload(lp.entry_ncols, nc);
   }
-  if (g.kind == kLowRank || (g.kind == kShared && g.any_fac_core)) {
-    std::vector<int> slots(size_t(E) * kBN), iota(E + 1);
-    for (int64_t e = 0; e < E; ++e)
-      for (int c = 0; c < kBN; ++c)
-        slots[size_t(e) * kBN + c] = lp.hp.entry_src[size_t(e) * kBN + c] >= 0 ? int(e * kBN + c) : -1;
-    std::iota(iota.begin(), iota.end(), 0);
-    upload(lp.slot_ids, slots);
-    upload(lp.iota, iota);
-    // runs of <= kPass1Run entries that never cross a tile boundary, so a tile
-    // range [t0, t1) maps to the run range [run_start[t0], run_start[t1])
-    std::vector<int> runs;
-    lp.run_start.assign(lp.hp.n_tiles + 1, 0);
-    for (int64_t t = 0; t < lp.hp.n_tiles; ++t) {
-      lp.run_start[t] = int64_t(runs.size());
-      for (int e = lp.hp.tile_off[t]; e < lp.hp.tile_off[t + 1]; e += kPass1Run) runs.push_back(e);
-    }
-    lp.run_start[lp.hp.n_tiles] = int64_t(runs.size());
-    runs.push_back(int(E));
-    lp.n_runs = int64_t(runs.size()) - 1;
-    upload(lp.runs, runs);
-  }
   // distinct targets / sources (SA transforms and accounting)
   {
     std::vector<char> seen_t(n_rows, 0), seen_s(n_rows, 0);
@@ -652,6 +631,31 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
           if (v >= 0) smax = std::max<int64_t>(smax, v / dc);
         }
     });
+  }
+  // per-entry slots and pass-1 runs of the two-pass paths -- built from the FINAL entry order (target-mode
+  // tiles were just re-ordered by row; building them before that dropped live columns on levels whose
+  // tile order changes, e.g. sphere levels forced to target tiles)
+  if (g.kind == kLowRank || (g.kind == kShared && g.any_fac_core)) {
+    const int64_t E = lp.hp.n_entries();
+    std::vector<int> slots(size_t(E) * kBN), iota(E + 1);
+    for (int64_t e = 0; e < E; ++e)
+      for (int c = 0; c < kBN; ++c)
+        slots[size_t(e) * kBN + c] = lp.hp.entry_src[size_t(e) * kBN + c] >= 0 ? int(e * kBN + c) : -1;
+    std::iota(iota.begin(), iota.end(), 0);
+    upload(lp.slot_ids, slots);
+    upload(lp.iota, iota);
+    // runs of <= kPass1Run entries that never cross a tile boundary, so a tile
+    // range [t0, t1) maps to the run range [run_start[t0], run_start[t1])
+    std::vector<int> runs;
+    lp.run_start.assign(lp.hp.n_tiles + 1, 0);
+    for (int64_t t = 0; t < lp.hp.n_tiles; ++t) {
+      lp.run_start[t] = int64_t(runs.size());
+      for (int e = lp.hp.tile_off[t]; e < lp.hp.tile_off[t + 1]; e += kPass1Run) runs.push_back(e);
+    }
+    lp.run_start[lp.hp.n_tiles] = int64_t(runs.size());
+    runs.push_back(int(E));
+    lp.n_runs = int64_t(runs.size()) - 1;
+    upload(lp.runs, runs);
   }
   if (g.kind == kLowRank && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) {
     bool done = false;

@@ -1156,3 +1156,42 @@ def test_persistent_step_kernel_matches_tile_kernel(torch_cuda, order, shape, mo
         assert O.rel_l2(out["1"][l] - 0.125, ref - 0.125) <= 1e-12
     assert O.rel_l2(single["1"], single["0"]) <= 1e-14
     assert O.rel_l2(single["1"], out["1"][4]) <= 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["twopass_ft", "twopass", "fused"])
+@pytest.mark.parametrize("mode", ["target", "pair"])
+def test_lowrank_paths_on_sparse_levels(torch_cuda, path, mode, monkeypatch):
+    """The three low-rank kernels paths on a sparse level (spherical shell at
+    level 4, iablk l = 5) as target tiles and as pair entries: the fused kernel,
+    the two-pass path on the permuted-gather kernels (what ranks above 64 take)
+    and the two-pass path on the full-operator kernels (per-transfer factors,
+    persistent step kernel; the default for complex operators), each vs the
+    oracle (<= 1e-10).  Target tiles of such a level are re-ordered by row after
+    they are built: the per-entry slots of the two-pass paths must follow that
+    order (regression: they were built before it and dropped live columns)."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, full_far_field_vectors, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_PLAN_MODE", mode)
+    monkeypatch.setenv("CFM_LR_TWOSTAGE", "0")
+    monkeypatch.setenv("CFM_LOWRANK_FUSED", "1" if path == "fused" else "0")
+    monkeypatch.setenv("CFM_LR_TWOPASS", "1" if path == "twopass_ft" else "0")
+    order, level, eps = 5, 4, 1e-5
+    cells = _full_level(level)
+    r = np.linalg.norm((cells + 0.5) / (1 << level) * 2 - 1, axis=1)
+    cells = cells[(r > 0.55) & (r < 0.95)]
+    tgt, off, src, t = O.far_lists(cells, level)
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: full_far_field_vectors()}, lw)
+    st = h.plan_level_cells(level, cells)
+    assert st["mode"] == mode
+    mp = torch.from_numpy(np.random.default_rng(37).uniform(-1, 1, (len(cells), order**3))).cuda()
+    loc = torch.full(mp.shape, 0.5, dtype=torch.float64, device="cuda")
+    h.apply_planned(level, mp, loc)
+    orc = O.OracleM2L("iablk", O.laplace_profile, np.float64, order, eps, -1.0).precompute(
+        {level: sorted({tuple(int(c) for c in v) for v in t})}, lw)
+    ref = np.full(mp.shape, 0.5)
+    orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert O.rel_l2(loc.cpu().numpy() - 0.5, ref - 0.5) <= 1e-10
