@@ -350,8 +350,9 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
     // memory) pays about one shared-memory load per DMMA in its skinny phase 1.
     const char* twopass_e = getenv("CFM_LR_TWOPASS");  // read per apply (tests switch it)
     const int twopass_env = twopass_e ? atoi(twopass_e) : -1;
+    // (also where the fused kernel cannot run: ranks above 64 realified rows)
     const bool ft2 = g.has_lrfull && g.has_lrmaps && dc == 1 &&
-                     (twopass_env >= 0 ? twopass_env != 0 : h->op_complex != 0);
+                     (twopass_env >= 0 ? twopass_env != 0 : (h->op_complex != 0 || g.lrf_right_h.rows > 64));
     if (!ft2) {
       LowRankParams q{};
       q.n_tiles = int(lp.hp.n_tiles);

@@ -1195,3 +1195,35 @@ def test_lowrank_paths_on_sparse_levels(torch_cuda, path, mode, monkeypatch):
     ref = np.full(mp.shape, 0.5)
     orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
     assert O.rel_l2(loc.cpu().numpy() - 0.5, ref - 0.5) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("twopass", ["1", "0"])
+def test_lowrank_ranks_above_64(torch_cuda, twopass, monkeypatch):
+    """ia at l = 7, eps = 1e-9: ranks above 64, which the fused kernel cannot
+    hold -- the level takes the two-pass path, on the full-operator kernels
+    (default) or on the permuted-gather kernels (CFM_LR_TWOPASS=0).  Full
+    level 3 (target tiles) vs the oracle (<= 1e-10), ranks equal."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_LR_TWOPASS", twopass)
+    monkeypatch.setenv("CFM_LR_TWOSTAGE", "0")
+    order, level, eps = 7, 3, 1e-9
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("ia", laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: transfers}, lw)
+    h.plan_level_cells(level, cells)
+    assert max(h.level_ranks(level)) > 64
+    mp = torch.from_numpy(np.random.default_rng(41).uniform(-1, 1, (len(cells), order**3))).cuda()
+    loc = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
+    flops = h.apply_planned(level, mp, loc)
+    orc = O.OracleM2L("ia", O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    assert orc.level_ranks(level) == h.level_ranks(level)
+    ref = np.zeros(mp.shape)
+    fr = orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert flops == fr
+    assert O.rel_l2(loc.cpu().numpy(), ref) <= 1e-10
