@@ -343,16 +343,13 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
   }
 
   if (g.kind == kLowRank) {
-    // Two passes on the full-operator kernels (CFM_LR_TWOPASS=1, default for complex
-    // operators): pass 1 Y[slot] = V_t^H x_src and pass 2 acc += U_t Y[slot] are short-tile
+    // Two passes on the full-operator kernels (CFM_LR_TWOPASS=0: the fused kernel): pass 1 Y[slot] = V_t^H x_src and pass 2 acc += U_t Y[slot] are short-tile
     // GEMMs against the per-transfer permuted factors, which the persistent step kernel
     // runs without per-CTA cost; the fused kernel (both phases in one CTA, Y in shared
     // memory) pays about one shared-memory load per DMMA in its skinny phase 1.
     const char* twopass_e = getenv("CFM_LR_TWOPASS");  // read per apply (tests switch it)
     const int twopass_env = twopass_e ? atoi(twopass_e) : -1;
-    // (also where the fused kernel cannot run: ranks above 64 realified rows)
-    const bool ft2 = g.has_lrfull && g.has_lrmaps && dc == 1 &&
-                     (twopass_env >= 0 ? twopass_env != 0 : (h->op_complex != 0 || g.lrf_right_h.rows > 64));
+    const bool ft2 = g.has_lrfull && g.has_lrmaps && dc == 1 && (twopass_env < 0 || twopass_env != 0);
     if (!ft2) {
       LowRankParams q{};
       q.n_tiles = int(lp.hp.n_tiles);
@@ -422,7 +419,9 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
       xp2 = h->xpad.as<double>() + xo[0];
       launches += xpad_copy(h, xp2, ldx2, d_x, 0, lp.n_rows, s);
     }
-    const size_t max_slots = std::max<size_t>(kBN, (size_t(1) << 30) / (sizeof(double) * std::max(ldy, 1)));
+    const char* ychunk_e = getenv("CFM_Y_CHUNK_MB");  // per-pair intermediate per chunk (default 1024 MB)
+    const size_t ychunk = (ychunk_e ? size_t(atoll(ychunk_e)) : size_t(1024)) << 20;
+    const size_t max_slots = std::max<size_t>(kBN, ychunk / (sizeof(double) * std::max(ldy, 1)));
     const std::vector<int>& toff = lp.hp.tile_off;
     if (lp.mode == 1) ensure(h->fbuf, size_t(lp.red.n_frows) * row_ld * sizeof(double));
     int64_t t0 = 0;
@@ -469,7 +468,11 @@ int64_t run_plan(cfm_handler* h, int level, LevelPlan& lp, const double* d_x, do
           p2.op_rows = nullptr; p2.op_klen = nullptr;
           p2.rowtab = nullptr; p2.invtab = nullptr;
           p2.ft = 1; p2.ft_rows = g.lrf_left.rows; p2.tmap_a = g.lrf_umap;
-          p2.x_rows = e1 * kBN;
+          // the Y map starts at the chunk's first slot (a TMA base below the
+          // allocation faults even when every touched row lies inside it)
+          p2.x = h->ybuf.as<double>();
+          p2.x_row0 = int(e0 * kBN);
+          p2.x_rows = (e1 - e0) * kBN;
           p2.n_entries = E;
           if (lp.mode == 1) p2.entry_ncols = lp.entry_ncols.as<unsigned char>();
         }

@@ -411,6 +411,7 @@ static int64_t launch_step_persistent(const std::vector<TileParams>& segs, const
     const int nrb = (q.nr + 127) / 128;
     g.start = int(work);
     g.tile_base = q.tile_base;
+    g.src_row0 = q.x_row0;
     g.mode = !q.pair_out ? 0 : (q.y_rowblk ? 2 : 1);
     g.tile_col = q.tile_col;
     g.tile_off = q.tile_off;

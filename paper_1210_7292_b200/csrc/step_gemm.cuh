@@ -44,7 +44,7 @@ struct StepSeg {
   int start;              // first work item of the segment in the launch
   int tile_base;          // plan tile of that item
   int mode;               // 0 target tiles, 1 pair entries, 2 Y_T scatter
-  int pad_;
+  int src_row0;           // subtracted from every source row id (tmap_b starts at that row)
   const int* tile_col;    // [tiles * 64] output columns (mode 2: the tile's source rows)
   const int* tile_off;    // [tiles + 1] entry range per tile (every tile has >= 1 entry)
   const int* entry_code;  // [E] transfer code (StepParams::code_op maps it) or operator id
@@ -149,6 +149,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) step_gemm_kernel(const __grid
         const int4* srow = reinterpret_cast<const int4*>(sg.entry_src + (long long)e * BN);
 #pragma unroll
         for (int j = 0; j < BN / 4; ++j) rows[j] = __ldg(srow + j);
+        if (sg.src_row0) {
+#pragma unroll
+          for (int j = 0; j < BN / 4; ++j) {
+            rows[j].x -= rows[j].x >= 0 ? sg.src_row0 : 0;
+            rows[j].y -= rows[j].y >= 0 ? sg.src_row0 : 0;
+            rows[j].z -= rows[j].z >= 0 ? sg.src_row0 : 0;
+            rows[j].w -= rows[j].w >= 0 ? sg.src_row0 : 0;
+          }
+        }
         int op = __ldg(sg.entry_code + e);
         if (!sg.code_is_op) op = __ldg(p.code_op + op);
         const int arow = op * p.a_rows + r0;

@@ -101,6 +101,7 @@ struct TileParams {
   const unsigned char* entry_ncols;  // pair plans: filled columns per entry (null: all BN)
   long long n_entries;               // host-side hint: entries of the plan (kernel choice)
   long long x_rows;                  // full-operator mode: rows of the padded source array x
+  int x_row0;                        // full-operator mode: subtracted from every source row id (tmap_b starts at that row)
   int ft_pipe;                       // full-operator target tiles: flat pipelined consumer loop
   int ft_skew;                       // flat loop: chunks the odd-wn consumer warps start behind the even ones (0: off)
   int ft_ktail;                      // flat loop: an entry's last k-step has one real column (DFMA rank-1)

@@ -262,6 +262,15 @@ __global__ void __launch_bounds__((WM * WN + 4) * 32, 1) tile_gemm_ws_kernel(con
       if (!p.b_block) {
 #pragma unroll
         for (int j = 0; j < BN / 4; ++j) rows[j] = __ldg(srow + j);
+        if (p.x_row0) {
+#pragma unroll
+          for (int j = 0; j < BN / 4; ++j) {
+            rows[j].x -= rows[j].x >= 0 ? p.x_row0 : 0;
+            rows[j].y -= rows[j].y >= 0 ? p.x_row0 : 0;
+            rows[j].z -= rows[j].z >= 0 ? p.x_row0 : 0;
+            rows[j].w -= rows[j].w >= 0 ? p.x_row0 : 0;
+          }
+        }
       }
       const int arow = (d.op >> p.ft_opshift) * p.ft_rows + r0;
       const int acol = (d.op & ((1 << p.ft_opshift) - 1)) * p.ft_colseg;

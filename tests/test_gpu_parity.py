@@ -1209,6 +1209,9 @@ def test_lowrank_ranks_above_64(torch_cuda, twopass, monkeypatch):
 
     monkeypatch.setenv("CFM_LR_TWOPASS", twopass)
     monkeypatch.setenv("CFM_LR_TWOSTAGE", "0")
+    # the per-pair intermediate in ~10 chunks of tiles (default 1 GB per chunk): later chunks
+    # address their slots relative to the chunk (a TMA map based below the buffer faults)
+    monkeypatch.setenv("CFM_Y_CHUNK_MB", "8")
     order, level, eps = 7, 3, 1e-9
     cells = _full_level(level)
     tgt, off, src, t = O.far_lists(cells, level)
