@@ -162,34 +162,61 @@ static bool build_two_stage_plan_T(const Group& g, LevelPlan& lp, int64_t n_targ
     tcode_decode(c, t0, t1, t2);
     tc[3 * c] = int8_t(t0), tc[3 * c + 1] = int8_t(t1), tc[3 * c + 2] = int8_t(t2);
   }
+  // pass over the pairs on host threads (46 M pairs at config 2's level 6): per target the range of
+  // its transfers, per source the same through per-thread arrays merged afterwards
   std::vector<int8_t> smn(size_t(n_rows) * 3, 127), smx(size_t(n_rows) * 3, -128);
   std::vector<int8_t> tcls(n_targets, -1);
   int64_t need_rows = 0;
-  for (int64_t i = 0; i < n_targets; ++i) {
-    if (tgt[i] < 0 || tgt[i] >= n_rows) return false;
-    int8_t mn[3] = {127, 127, 127}, mx[3] = {-128, -128, -128};
-    for (int64_t q = off[i]; q < off[i + 1]; ++q) {
-      const int c = codes[q];
-      const int k = g.fullmap.op[c];
-      if (k < 0 || k >= ntr || g.ts_rank[k] <= 0) return false;
-      need_rows += g.ts_rank[k];
-      const int64_t v = src[q];
-      if (v < 0 || v >= n_rows) return false;
-      for (int a = 0; a < 3; ++a) {
-        const int8_t t = tc[3 * c + a];
-        mn[a] = std::min(mn[a], t), mx[a] = std::max(mx[a], t);
-        smn[size_t(v) * 3 + a] = std::min(smn[size_t(v) * 3 + a], t);
-        smx[size_t(v) * 3 + a] = std::max(smx[size_t(v) * 3 + a], t);
+  const int nth = int(std::max<int64_t>(1, std::min<int64_t>(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())),
+                                                               n_targets / 4096)));
+  {
+    std::vector<std::vector<int8_t>> tmn(nth), tmx(nth);
+    std::vector<int64_t> tneed(nth, 0);
+    std::vector<char> bad(nth, 0);
+    auto work = [&](int w) {
+      std::vector<int8_t>& lmn = tmn[w];
+      std::vector<int8_t>& lmx = tmx[w];
+      lmn.assign(size_t(n_rows) * 3, 127);
+      lmx.assign(size_t(n_rows) * 3, -128);
+      for (int64_t i = n_targets * w / nth; i < n_targets * (w + 1) / nth; ++i) {
+        if (tgt[i] < 0 || tgt[i] >= n_rows) { bad[w] = 1; return; }
+        int8_t mn[3] = {127, 127, 127}, mx[3] = {-128, -128, -128};
+        for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+          const int c = codes[q];
+          const int k = (c >= 0 && c < kNumCodes) ? g.fullmap.op[c] : -1;
+          if (k < 0 || k >= ntr || g.ts_rank[k] <= 0) { bad[w] = 1; return; }
+          tneed[w] += g.ts_rank[k];
+          const int64_t v = src[q];
+          if (v < 0 || v >= n_rows) { bad[w] = 1; return; }
+          for (int a = 0; a < 3; ++a) {
+            const int8_t t = tc[3 * c + a];
+            mn[a] = std::min(mn[a], t), mx[a] = std::max(mx[a], t);
+            lmn[size_t(v) * 3 + a] = std::min(lmn[size_t(v) * 3 + a], t);
+            lmx[size_t(v) * 3 + a] = std::max(lmx[size_t(v) * 3 + a], t);
+          }
+        }
+        if (off[i + 1] == off[i]) continue;
+        int b = 0;
+        for (int a = 0; a < 3; ++a) {
+          if (mx[a] <= 2 && mn[a] >= -3) continue;
+          if (mn[a] >= -2 && mx[a] <= 3) b |= 1 << a;
+          else { bad[w] = 1; return; }  // not an octree far list
+        }
+        tcls[i] = int8_t(b);
+      }
+    };
+    std::vector<std::thread> th;
+    for (int w = 1; w < nth; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& t : th) t.join();
+    for (int w = 0; w < nth; ++w) {
+      if (bad[w]) return false;
+      need_rows += tneed[w];
+      for (size_t j = 0; j < smn.size(); ++j) {
+        smn[j] = std::min(smn[j], tmn[w][j]);
+        smx[j] = std::max(smx[j], tmx[w][j]);
       }
     }
-    if (off[i + 1] == off[i]) continue;
-    int b = 0;
-    for (int a = 0; a < 3; ++a) {
-      if (mx[a] <= 2 && mn[a] >= -3) continue;
-      if (mn[a] >= -2 && mx[a] <= 3) b |= 1 << a;
-      else return false;  // not an octree far list
-    }
-    tcls[i] = int8_t(b);
   }
   std::vector<int8_t> scls(n_rows, -1);
   std::vector<std::vector<int>> src_by(8);
@@ -209,22 +236,41 @@ static bool build_two_stage_plan_T(const Group& g, LevelPlan& lp, int64_t n_targ
   if (double(tiles1) * kBN * nb * 128 > 1.7 * double(need_rows)) return false;  // sparse level: fused kernel
   // per (source, class slot): where the pair's rank run lands in Y_T
   std::vector<int> nbr(size_t(n_rows) * nslots, -1);
-  std::vector<char> tseen(n_rows, 0);
-  for (int64_t i = 0; i < n_targets; ++i) {
-    if (off[i + 1] == off[i]) continue;
-    if (tseen[tgt[i]]) return false;  // a target listed twice: its Y_T row would be shared
-    tseen[tgt[i]] = 1;
-    const int ct = tcls[i];
-    for (int64_t q = off[i]; q < off[i + 1]; ++q) {
-      const int k = g.fullmap.op[codes[q]];
-      const int64_t v = src[q];
-      const int slot = g.tsT_slot[size_t(scls[v]) * ntr + k];
-      const int rho = g.tsT_rho[size_t(ct) * ntr + k];
-      if (slot < 0 || rho < 0) return false;
-      int& w = nbr[size_t(v) * nslots + slot];
-      if (w >= 0) return false;  // the same (source, transfer) twice: not an octree list
-      w = int(tgt[i] * ldy + rho);
+  {
+    std::vector<char> tseen(n_rows, 0);
+    for (int64_t i = 0; i < n_targets; ++i) {
+      if (off[i + 1] == off[i]) continue;
+      if (tseen[tgt[i]]) return false;  // a target listed twice: its Y_T row would be shared
+      tseen[tgt[i]] = 1;
     }
+    // (a (source, class slot) belongs to one pair of an octree list; a second pair on the same
+    // entry is not an octree list and refuses the plan)
+    std::vector<char> bad(nth, 0);
+    auto work = [&](int w) {
+      for (int64_t i = n_targets * w / nth; i < n_targets * (w + 1) / nth; ++i) {
+        if (off[i + 1] == off[i]) continue;
+        const int ct = tcls[i];
+        for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+          const int k = g.fullmap.op[codes[q]];
+          const int64_t v = src[q];
+          const int slot = g.tsT_slot[size_t(scls[v]) * ntr + k];
+          const int rho = g.tsT_rho[size_t(ct) * ntr + k];
+          if (slot < 0 || rho < 0) { bad[w] = 1; return; }
+          int expected = -1;  // (compare-exchange: a duplicate is caught also when two threads race for it)
+          if (!__atomic_compare_exchange_n(&nbr[size_t(v) * nslots + slot], &expected, int(tgt[i] * ldy + rho), false,
+                                           __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+            bad[w] = 1;
+            return;
+          }
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (int w = 1; w < nth; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& t : th) t.join();
+    for (int w = 0; w < nth; ++w)
+      if (bad[w]) return false;
   }
   // stage 1 plan: tiles of 64 same-class sources (ascending rows), ordered by their
   // first row, so a host-buffer apply can start on the first multipole slabs
@@ -552,7 +598,8 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
     for (int64_t q = 0; q < P; ++q) slo = std::min(slo, src[q]), shi = std::max(shi, src[q] + 1);
     lp.src_lo = std::min(slo, shi), lp.src_hi = shi, lp.tgt_lo = std::min(tlo, thi), lp.tgt_hi = thi;
   }
-  push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
+  if (lp.mode != 0 || lp.hp.n_tiles == 0)  // (target tiles are uploaded after their re-ordering below)
+    push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
   const int64_t E = lp.hp.n_entries();
   if (lp.mode == 1) {
     // filled columns per pair entry (slots are filled from column 0): the
@@ -618,7 +665,11 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
     }
     np_.tile_off[nt] = int(np_.entry_code.size());
     lp.hp = std::move(np_);
-    push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
+    // a low-rank level that takes the target-major two-stage path never runs the tile plan
+    // itself: no device copy of it, no two-pass slots (0.6 GB of uploads at config 2's level 6)
+    if (g.kind == kLowRank && dc == 1 && g.has_tsT && two_stage_mode() >= 2)
+      build_two_stage_plan_T(g, lp, n_targets, tgt, off, src, codes);
+    if (lp.ts != 2) push_plan(lp.hp, lp.tile_col, lp.tile_off, lp.entry_code, lp.entry_src);
     set_slab_plan(h, level, lp, [&](int64_t t, int64_t& tmin, int64_t& tmax, int64_t& smax) {
       tmin = INT64_MAX, tmax = -1, smax = -1;
       for (int c = 0; c < kBN; ++c) {
@@ -635,7 +686,7 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
   // per-entry slots and pass-1 runs of the two-pass paths -- built from the FINAL entry order (target-mode
   // tiles were just re-ordered by row; building them before that dropped live columns on levels whose
   // tile order changes, e.g. sphere levels forced to target tiles)
-  if (g.kind == kLowRank || (g.kind == kShared && g.any_fac_core)) {
+  if ((g.kind == kLowRank && lp.ts != 2) || (g.kind == kShared && g.any_fac_core)) {
     const int64_t E = lp.hp.n_entries();
     std::vector<int> slots(size_t(E) * kBN), iota(E + 1);
     for (int64_t e = 0; e < E; ++e)
@@ -657,11 +708,8 @@ LevelPlan build_level_plan(cfm_handler* h, int level, int64_t n_targets, const i
     lp.n_runs = int64_t(runs.size()) - 1;
     upload(lp.runs, runs);
   }
-  if (g.kind == kLowRank && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0) {
-    bool done = false;
-    if (g.has_tsT && two_stage_mode() >= 2) done = build_two_stage_plan_T(g, lp, n_targets, tgt, off, src, codes);
-    if (!done && g.has_ts) build_two_stage_plan(g, lp);
-  }
+  if (g.kind == kLowRank && lp.mode == 0 && dc == 1 && lp.hp.n_tiles > 0 && lp.ts != 2 && g.has_ts)
+    build_two_stage_plan(g, lp);
   if (use_hybrid() && full_mode(g, lp) && lp.mode == 0 && lp.hp.n_tiles > 0) {
     try {
       build_hybrid_plan(h, lp, n_targets, tgt, off, src, codes, key);
