@@ -1230,3 +1230,36 @@ def test_lowrank_ranks_above_64(torch_cuda, twopass, monkeypatch):
     fr = orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
     assert flops == fr
     assert O.rel_l2(loc.cpu().numpy(), ref) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("envs", [{"CFM_TS_KERNEL": "step"}, {"CFM_TS_PERSIST": "0"},
+                                  {"CFM_TS_PERSIST": "0", "CFM_STEP_PERSIST": "0"}, {"CFM_TS_SKEW": "0"}])
+def test_two_stage_target_major_kernel_variants(torch_cuda, envs, monkeypatch):
+    """The other kernels that can run the target-major two-stage path: the
+    dynamic-queue step kernel (its Y_T-scatter mode), the generic launch path
+    with and without the persistent step kernel (one CTA per tile on
+    tile_gemm_ws_kernel), and unskewed consumer halves.  Full level 4, iablk
+    l = 5, vs the oracle (<= 1e-10)."""
+    torch = torch_cuda
+    from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
+
+    monkeypatch.setenv("CFM_LR_TWOSTAGE", "2")
+    for k, v in envs.items():
+        monkeypatch.setenv(k, v)
+    order, level, eps = 5, 4, 1e-5
+    cells = _full_level(level)
+    tgt, off, src, t = O.far_lists(cells, level)
+    transfers = sorted({tuple(int(c) for c in v) for v in t})
+    lw = {level: 1.0 / (1 << level)}
+    h = make_handler("iablk", laplace_kernel(), ChebyshevGrid(order), eps)
+    h.precompute({level: transfers}, lw)
+    h.plan_level_cells(level, cells)
+    assert h.plan_stats(level)["two_stage"]
+    mp = torch.from_numpy(np.random.default_rng(43).uniform(-1, 1, (len(cells), order**3))).cuda()
+    loc = torch.full(mp.shape, 1.5, dtype=torch.float64, device="cuda")
+    h.apply_planned(level, mp, loc)
+    orc = O.OracleM2L("iablk", O.laplace_profile, np.float64, order, eps, -1.0).precompute({level: transfers}, lw)
+    ref = np.full(mp.shape, 1.5)
+    orc.apply_fast(level, tgt, off, src, t, mp.cpu().numpy(), ref)
+    assert O.rel_l2(loc.cpu().numpy() - 1.5, ref - 1.5) <= 1e-10
