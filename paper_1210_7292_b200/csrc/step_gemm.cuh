@@ -24,9 +24,9 @@
 //     waited for and its first fragments loaded before the current chunk's
 //     last k-step, also across tiles; no shared-memory tables, no CTA-wide
 //     barrier after the start;
-//   * the two consumer halves (wn = 0 / 1) start `skew` chunks apart, so the
-//     two consumer warps of an SM sub-partition reach their epilogues at
-//     different times and one of them keeps the pipe busy.
+//   * the two consumer halves (wn = 0 / 1) start `skew` chunks apart (measured
+//     neutral here: inside the 4-stage ring the halves drift apart on their own;
+//     worth 8% on the one-CTA-per-tile stage-1 kernel of the two-stage path).
 // Output modes per segment: 0 = target tiles (registers accumulate over the
 // tile's entries, one ordered read-modify-write of the targets' rows at the
 // end; a target column belongs to one tile: no atomics), 1 = pair entries
