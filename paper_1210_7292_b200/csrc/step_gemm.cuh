@@ -70,7 +70,7 @@ struct StepSeg {
   CUtensorMap tmap_b;  // its source rows
 };
 
-constexpr int kStepMaxSegs = 12;
+constexpr int kStepMaxSegs = 16;
 struct StepParams {
   int n_seg;
   int n_work;       // (tile, row block) items of the launch

@@ -142,7 +142,7 @@ constexpr int ws_ring_bytes() {
 // one launch: tiles [start[s], start[s+1]) of the launch belong to segment s.
 // CTA b works on tile b / nrb, row block b % nrb: the row blocks of a tile run
 // side by side and share its source columns in L2.
-constexpr int kMaxSegments = 12;
+constexpr int kMaxSegments = 16;  // (config 4: 6 levels + 4 short-tile lists + 4 hybrid pair lists + the merged pair plan = 15)
 struct MultiTileParams {
   int n_seg;
   int nrb;  // row blocks per tile
