@@ -1056,6 +1056,7 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
       off += L.bytes;
     }
   }
+  std::vector<size_t> late_order;  // late (ftl 2) levels in upload / launch order
   const int64_t pad_launches = launch_pads(pad_batch, s_in);
   if (any_piped) {
     // the kernel may start once the non-pipelined levels and the zeroed flags are in
@@ -1077,20 +1078,8 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
                                   reinterpret_cast<CUdeviceptr>(h->pipe_flags.as<unsigned>() + flag_off[i]), 1u, 0);
       if (r != CUDA_SUCCESS) throw Error(CFM_ERR_CUDA, "cuStreamWriteValue32 failed");
     }
-    bool any_late = false;
-    for (size_t i = 0; i < lv.size(); ++i)
-      if (ftl[i] == 2) {
-        CUDA_CHECK(cudaMemcpyAsync(const_cast<double*>(staged_x[i]), host_x[i], lv[i].bytes, cudaMemcpyHostToDevice,
-                                   s_in));
-        any_late = true;
-      }
-    if (any_late) {
-      if (!h->ev_x) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming));
-      CUDA_CHECK(cudaEventRecord(h->ev_x, s_in));
-    }
     unsigned* flags = h->pipe_flags.as<unsigned>();
-    for (size_t i = 0; i < lv.size(); ++i) {
-      if (!piped[i]) continue;
+    auto upload_slabs = [&](size_t i) {  // the row slabs of pipelined level i (locals; multipoles unless resident)
       const LevelPlan& P = *lv[i].lp;
       const int S = P.n_slabs;
       const size_t row_b = lv[i].bytes / size_t(P.n_rows);
@@ -1142,7 +1131,29 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
       }
       slab_copy(lv[i].host_y, lv[i].y, S - 1, cudaMemcpyHostToDevice, s_in);
       write_flag(loc_ready, unsigned(S));
+    };
+    // late levels, smallest first, each with its own "multipoles resident" event: a smaller
+    // late level is launched (and keeps the GPU busy) while a larger one still crosses PCIe
+    // (config 4: level 6's 0.7 GB arrive 105 ms before level 7's 5.75 GB)
+    late_order.clear();
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (ftl[i] == 2) late_order.push_back(i);
+    std::stable_sort(late_order.begin(), late_order.end(), [&](size_t a, size_t b) { return lv[a].bytes < lv[b].bytes; });
+    while (h->ev_late_x.size() < late_order.size()) {
+      cudaEvent_t e;
+      CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->ev_late_x.push_back(e);
     }
+    for (size_t j = 0; j < late_order.size(); ++j) {
+      const size_t i = late_order[j];
+      CUDA_CHECK(cudaMemcpyAsync(const_cast<double*>(staged_x[i]), host_x[i], lv[i].bytes, cudaMemcpyHostToDevice, s_in));
+      CUDA_CHECK(cudaEventRecord(h->ev_late_x[j], s_in));
+      // ... and its locals slabs right behind, before the next late level's multipoles: its
+      // epilogues would otherwise hold the SMs until that (much longer) upload is over
+      if (piped[i]) upload_slabs(i);
+    }
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (piped[i] && ftl[i] != 2) upload_slabs(i);
   }
   CUDA_CHECK(cudaEventRecord(h->ev0, s));
   const auto t_host1 = std::chrono::steady_clock::now();
@@ -1403,13 +1414,20 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
     // soon as its sources are in and its CTAs fill the SMs that the first
     // group's tail leaves idle (levels are independent in M2L); the caller's
     // stream joins it after the launches.
-    // Groups: 0 = first launch, 1 = middle (ftl 4, e2e only), 2 = late (ftl 2).
-    std::vector<std::vector<size_t>> groups(3);
+    // Groups: 0 = first launch, 1 = middle (ftl 4, e2e only), 2.. = the late levels (ftl 2),
+    // one group each in upload order.
+    std::vector<std::vector<size_t>> groups(2 + std::max<size_t>(late_order.size(), 1));
     for (size_t i = 0; i < lv.size(); ++i)
-      if (counts[i]) groups[ftl[i] == 2 ? 2 : ftl[i] == 4 ? 1 : 0].push_back(i);
+      if (counts[i] && ftl[i] != 2) groups[ftl[i] == 4 ? 1 : 0].push_back(i);
+    for (size_t j = 0; j < late_order.size(); ++j)
+      if (counts[late_order[j]]) groups[2 + j].push_back(late_order[j]);
     for (size_t k : short_segs) groups[0].push_back(k);
     if (mp_plan) groups[0].push_back(merged_seg);
-    const bool side = use_late_stream() && !groups[0].empty() && (!groups[1].empty() || !groups[2].empty());
+    bool any_late_grp = false;
+    size_t last_late = 0;
+    for (size_t gi = 2; gi < groups.size(); ++gi)
+      if (!groups[gi].empty()) any_late_grp = true, last_late = gi;
+    const bool side = use_late_stream() && !groups[0].empty() && (!groups[1].empty() || any_late_grp);
     if (side) {
       if (!h->s_late) CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_late, cudaStreamNonBlocking));
       if (!h->ev_late0) CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_late0, cudaEventDisableTiming));
@@ -1434,9 +1452,9 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
                                        lv[i].lp->n_rows, sg, 256, &pj);
         launches += launch_pads(pj, sg);
       }
-      if (gi == 2) {
+      if (gi >= 2) {
         if (side) sg = h->s_late;
-        CUDA_CHECK(cudaStreamWaitEvent(sg, h->ev_x, 0));
+        CUDA_CHECK(cudaStreamWaitEvent(sg, h->ev_late_x[gi - 2], 0));
         for (size_t i : grp)
           launches += xpad_copy(h, const_cast<double*>(lv[i].x), lay[lay_idx[i]].second, staged_x[i], 0,
                                 lv[i].lp->n_rows, sg);
@@ -1499,7 +1517,7 @@ void apply_levels_impl(cfm_handler* h, int n_levels, const int* levels, const do
             }
         }
       }
-      if (gi == 2 && side) {
+      if (gi >= 2 && gi == last_late && side) {
         CUDA_CHECK(cudaEventRecord(h->ev_late1, sg));
         CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_late1, 0));
       }

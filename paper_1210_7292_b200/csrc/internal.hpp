@@ -343,6 +343,7 @@ struct cfm_handler {
   int ts_chunks = 1;
   std::function<void(int64_t)> ts_after_chunk;
   std::vector<cudaEvent_t> ev_pool;  // events of the host-buffer low-rank pipeline
+  std::vector<cudaEvent_t> ev_late_x;  // per late level: its multipoles are resident (dense host-buffer pipeline)
   bool last_csr_hit = false;  // the last cfm_apply_level_csr reused a cached plan
   int last_csr_mode = -1, last_csr_two_stage = 0;  // and that plan's mode / two-stage flag
   uint64_t last_csr_gen = 0;                        // and its id (unique per built plan)

@@ -490,10 +490,8 @@ void set_slab_plan(cfm_handler* h, int level, LevelPlan& lp,
     const char* e = getenv("CFM_MAX_SLABS");
     return e ? std::max<int64_t>(2, atoll(e)) : int64_t(16);
   }();
-  static const int64_t min_rows = [] {  // levels with fewer rows are not host-pipelined
-    const char* e = getenv("CFM_PIPE_MIN_ROWS");
-    return e ? atoll(e) : int64_t(0);
-  }();
+  const char* min_rows_e = getenv("CFM_PIPE_MIN_ROWS");  // levels with fewer rows are not host-pipelined
+  const int64_t min_rows = min_rows_e ? atoll(min_rows_e) : int64_t(0);  // (read per plan: a test pipelines small levels)
   int S = int(std::min<int64_t>(max_slabs, std::max<int64_t>(1, n_rows / slab_rows)));
   if (min_rows > 0) S = n_rows >= min_rows ? std::max(S, 2) : 1;
   // the last slab's download cannot start before the kernel's last wave

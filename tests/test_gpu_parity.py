@@ -579,7 +579,7 @@ def test_sharded_plans_equal_single_gpu(torch_cuda, golden, mode, monkeypatch):
     assert torch.equal(out, ref)
 
 
-@pytest.mark.parametrize("order,hybrid", [(4, "0"), (5, "0"), (5, "1")])
+@pytest.mark.parametrize("order,hybrid", [(4, "0"), (5, "0"), (5, "1"), (5, "late3")])
 def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, hybrid, monkeypatch):
     """Host buffers on a large level go through the slab copy pipeline
     (multipole/locals slabs streamed while the kernel runs, gated by device
@@ -595,6 +595,11 @@ def test_copy_pipeline_host_buffers_bitwise(torch_cuda, order, hybrid, monkeypat
     torch = torch_cuda
     from paper_1210_7292_b200 import ChebyshevGrid, laplace_kernel, make_handler
 
+    if hybrid == "late3":
+        # levels 4, 5 and 6 all host-pipelined: three late levels, each launched when its own
+        # multipoles are in (smallest first), its locals slabs uploaded right behind them
+        monkeypatch.setenv("CFM_PIPE_MIN_ROWS", "4096")
+        hybrid = "0"
     monkeypatch.setenv("CFM_HYBRID", hybrid)
     lv = (3, 4, 5, 6)  # l = 5: level 5 runs as the middle launch group (uploaded during the first launch)
     cells = {l: _full_level(l) for l in lv}
